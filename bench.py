@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 G-REST per-step eigen-update (BASELINE.json metric).
+
+One "step" = one update batch through the whole hot path: on-device
+validation/assembly of Delta, the CSR merge A <- pad(A) + Delta, and
+tracker_step (grest-rsvd, k=32, L=P=100) on R-MAT scale 20 (config 3).
+
+  value : steps/s with the edit lists already resident in HBM (st_step_device)
+  e2e   : steps/s through the C ABI with host edit lists (H2D inside the timed
+          region) and the k Ritz values read back every step
+  roofline : the dominant kernel class, algorithmic work / CUDA-event time
+  cpu_baseline : the CPU restatement (oracle/) on one step of the same stream
+
+`--impl reference` times the reference's CPU implementation of the path (the
+oracle port: the reference itself cannot be built here) with all
+host threads on the same config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "eigen-update steps/s at R-MAT s20 k=32; SpMM+Gram GB/s vs HBM peak"
+HBM_PEAK_FALLBACK = 6650.0
+# FP64 tensor (DMMA) peak: not in MEASURED_PEAKS.json; measured by us on this
+# pool with cuBLAS DGEMM 8192^3 (profiles/fp64_peaks_r01.txt).
+FP64_PEAK_MEASURED = 35.46
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def make_workload(name: str, steps: int, seed_offset: int = 0, scale: int | None = None):
+    from paper_2603_19439_b200 import streams
+
+    if name == "cfg3":
+        s = streams.config3(seed=3 + seed_offset, scale=scale or 20, steps=steps)
+        return s, dict(k=32, kind="grest-rsvd", order="abs_desc", operator="adjacency",
+                       workload=f"cfg3 R-MAT scale {scale or 20} ef16 (0.57,0.19,0.19,0.05) symmetrized+dedup, "
+                                f"k=32 grest-rsvd L=P=100; per step 1% new nodes x 10 PA edges + 0.5% deletions")
+    if name == "cfg1":
+        s = streams.config1(seed=1 + seed_offset, steps=steps)
+        return s, dict(k=8, kind="grest-rsvd", order="abs_desc", operator="adjacency",
+                       workload="cfg1 SBM n=10,000 4 blocks p_in=0.01 p_out=0.001, k=8; 500 inserts + 100 deletes")
+    if name == "cfg2":
+        s = streams.config2(seed=2 + seed_offset, steps=steps)
+        return s, dict(k=16, kind="grest-rsvd", order="alg_desc", operator="normalized-laplacian",
+                       workload="cfg2 ER n=100,000 avg deg 20 normalized Laplacian k=16; 1% inserts + 0.5% deletes")
+    raise SystemExit(f"unknown config {name}")
+
+
+def operator_csr(rp, col, val, operator):
+    """The tracked operator at t=0 (adjacency, or T = 2I - L_n for the
+    normalized Laplacian, graph.cpp:139-150) for computing X0."""
+    if operator == "adjacency":
+        return rp, col, val
+    n = len(rp) - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    deg = np.bincount(rows, weights=val, minlength=n)
+    s = np.where(deg > 0, 1.0 / np.sqrt(np.maximum(deg, 1e-300)), 0.0)
+    offv = (s[rows] * s[col]) * val
+    diag = np.where(deg > 0, 1.0, 2.0)
+    r2 = np.concatenate([rows, np.arange(n)])
+    c2 = np.concatenate([col, np.arange(n)])
+    v2 = np.concatenate([offv, diag])
+    o = np.lexsort((c2, r2))
+    rp2 = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(r2, minlength=n), out=rp2[1:])
+    return rp2.astype(np.int32), c2[o].astype(np.int32), v2[o]
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def dist_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def cpu_baseline(stream, x0_vals, x0_vecs, wl, threads: int):
+    """The oracle (CPU port of the reference path) on one step of the stream."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    rp, col, val = stream.csr0()
+    a = po.Csr(len(rp) - 1, rp, col, val)
+    o = po.Session(a, kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0,
+                   values=x0_vals, vectors=x0_vecs)
+    t0 = time.perf_counter()
+    o.step(stream.updates[0])
+    dt = time.perf_counter() - t0
+    return dt, o.last_tracker_seconds
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2603_19439_b200 import KERNEL_CLASSES, DeviceUpdate, TrackerSession, init_eig
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    W, K = args.warmup, args.steps
+    t_setup = time.time()
+    stream, wl = make_workload(args.config, W + K, seed_offset=rank if world > 1 else 0, scale=args.scale)
+    rp, col, val = stream.csr0()
+    orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
+    vals0, vecs0 = init_eig.leading_eigenpairs(orp, ocol, oval, wl["k"], wl["order"], device=f"cuda:{local}")
+    setup_s = time.time() - t_setup
+    kw = dict(kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0, device=local)
+
+    # ---- value: edit lists resident in HBM
+    sess = TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=True, **kw)
+    dev_updates = [DeviceUpdate(u, device=f"cuda:{local}") for u in stream.updates]
+    for t in range(W):
+        sess.step_device(dev_updates[t])
+    torch.cuda.synchronize()
+    barrier(world)
+    sess.reset_kernel_stats()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    torch.cuda.synchronize()
+    e0.record()
+    for t in range(W, W + K):
+        sess.step_device(dev_updates[t])
+        launches += sess.launches()
+    e1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = dist_max(e0.elapsed_time(e1), world)
+    kstats = sess.kernel_stats()
+    info = sess.info()
+    sess.close()
+    del dev_updates
+
+    # ---- e2e: host edit lists through the C ABI, Ritz values read back
+    sess = TrackerSession(rp, col, val, vals0, vecs0, **kw)
+    for t in range(W):
+        sess.step(stream.updates[t])
+    torch.cuda.synchronize()
+    barrier(world)
+    h2d = 0
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for t in range(W, W + K):
+        sess.step(stream.updates[t])
+        _ = sess.values()
+        h2d += stream.updates[t].h2d_bytes()
+    f1.record()
+    torch.cuda.synchronize()
+    ms_e2e = dist_max(f0.elapsed_time(f1), world)
+    sess.close()
+
+    value = world * K / (ms / 1e3)
+    e2e = world * K / (ms_e2e / 1e3)
+    hbm_peak, hbm_src = measured_peaks()
+
+    # ---- roofline of the dominant kernel class (by device time)
+    classes = {}
+    for name in KERNEL_CLASSES:
+        st = kstats[name]
+        if st["launches"] == 0:
+            continue
+        flops_class = name in ("dmma_gram", "dmma_gemm", "masked_gram_x")
+        byte_class = name in ("spmm", "spmm_sketch", "csr_merge", "rotate_x")
+        ach = st["work"] / (st["ms"] / 1e3) if st["ms"] > 0 else 0.0
+        row = dict(ms_per_step=st["ms"] / K, launches_per_step=st["launches"] / K,
+                   share=st["ms"] / ms if ms > 0 else 0.0)
+        if flops_class:
+            row.update(achieved_tflops=ach / 1e12, frac_fp64_peak=ach / 1e12 / FP64_PEAK_MEASURED)
+        elif byte_class:
+            row.update(achieved_gbs=ach / 1e9, frac_hbm=ach / 1e9 / hbm_peak)
+        classes[name] = row
+    own = {k_: v for k_, v in classes.items() if k_ != "eigensolver"}
+    dom = max(own, key=lambda k_: own[k_]["ms_per_step"]) if own else None
+    roof = None
+    if dom is not None:
+        st = kstats[dom]
+        ach = st["work"] / (st["ms"] / 1e3)
+        if dom in ("dmma_gram", "dmma_gemm", "masked_gram_x"):
+            roof = dict(kernel=dom, bound="tensor", achieved=ach / 1e12, peak=FP64_PEAK_MEASURED, unit="TFLOP/s",
+                        frac=ach / 1e12 / FP64_PEAK_MEASURED, traffic=None,
+                        peak_source="measured cuBLAS DGEMM 8192^3 on this pool (FP64 not in MEASURED_PEAKS.json)",
+                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="flop")
+        else:
+            roof = dict(kernel=dom, bound="hbm", achieved=ach / 1e9, peak=hbm_peak, unit="GB/s",
+                        frac=ach / 1e9 / hbm_peak, traffic=None, peak_source=hbm_src,
+                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="byte")
+    out = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded R-MAT + preferential-attachment stream; BASELINE config 3 shapes)",
+        "config": {"workload": wl["workload"], "n0": int(len(rp) - 1), "nnz0": int(rp[-1]), "k": wl["k"],
+                   "kind": wl["kind"], "rsvd_l": 100, "rsvd_p": 100, "n_final": info["n"],
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (row sharding: round 2)",
+                   "l2": "inputs larger than L2 (CSR ~0.38 GB + X ~0.27 GB per replica)",
+                   "setup_s": round(setup_s, 1)},
+        "roofline": roof,
+        "kernel_classes": classes,
+        "e2e": {"value": e2e, "unit": "steps/s", "ms_per_step": ms_e2e / K, "h2d_bytes_per_step": h2d // K,
+                "d2h_bytes_per_step": 8 * wl["k"]},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        dt, dt_tracker = cpu_baseline(stream, vals0, vecs0, wl, threads)
+        out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "steps/s", "cores": threads, "kind": "port",
+                               "sample": f"1 step (step {0}) of the same stream: assemble_update + apply_update + "
+                                         f"tracker_step via the oracle restatement, OpenMP {threads} threads; "
+                                         f"tracker_step alone {dt_tracker:.2f} s",
+                               "seconds_per_step": dt}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference's CPU path (oracle port; the reference cannot be built
+    here: Eigen is absent) with all host threads, on the same config."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    W = min(args.warmup, 1)
+    budget_s = 150.0
+    stream, wl = make_workload(args.config, W + args.steps, scale=args.scale)
+    rp, col, val = stream.csr0()
+    orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
+    n = len(rp) - 1
+    rng = np.random.default_rng(0)
+    x, _ = np.linalg.qr(rng.standard_normal((n, wl["k"])))  # X0 quality does not change the step cost
+    a = po.Csr(n, rp, col, val)
+    o = po.Session(a, kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0,
+                   values=np.linspace(wl["k"], 1, wl["k"]), vectors=x)
+    for t in range(W):
+        o.step(stream.updates[t])
+    times = []
+    for t in range(W, W + args.steps):
+        t0 = time.perf_counter()
+        o.step(stream.updates[t])
+        times.append(time.perf_counter() - t0)
+        if sum(times) > budget_s:
+            break
+    value = len(times) / sum(times)
+    sample = (f"{len(times)} of {args.steps} requested timed steps (budget {budget_s:.0f} s) after {W} warm-up, "
+              f"oracle restatement with OpenMP {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": len(times), "warmup": W, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["workload"], "n0": n, "nnz0": int(rp[-1]), "k": wl["k"]},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (development)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/* spectrack_gpu.h — C ABI of the B200-native G-REST per-step eigen-update.
+ *
+ * Drop-in boundary for the reference library `spectrack` (arxiv 2603.19439,
+ * proj/include/spectrack). The reference has no C ABI: its callers link the C++
+ * functions cited below. Each entry point here replaces one of them; the C++
+ * shim include/spectrack_b200.hpp re-exposes the reference signatures on top
+ * of this ABI (see INTEGRATION.md for the binding a maintainer adds).
+ *
+ * Conventions: plain pointers and sizes, no C++ or torch types. CSR arrays are
+ * int32 offsets / int32 column indices / fp64 values (Eigen::SparseMatrix<
+ * double, RowMajor>, sparse.hpp:18). Dense matrices cross the boundary
+ * column-major with a leading dimension (Eigen's default). Node ids are int64
+ * (Eigen::Index). Every function returns an st_status; on failure
+ * st_last_error() holds the reference's exception message, and the session is
+ * left exactly as before the call (the reference's value semantics).
+ */
+#ifndef SPECTRACK_GPU_H
+#define SPECTRACK_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ST_OK = 0,
+  ST_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  ST_RUNTIME_ERROR = 2,    /* std::runtime_error in the reference */
+  ST_CUDA_ERROR = 3,       /* device failure (no reference counterpart) */
+  ST_OTHER = 4
+} st_status;
+
+/* TrackerKind (trackers.hpp:36-45); the G-REST path implements the projection kinds. */
+typedef enum { ST_IASC = 3, ST_GREST2 = 4, ST_GREST3 = 5, ST_GREST_RSVD = 6 } st_tracker_kind;
+/* BasisKind (trackers.hpp:104) */
+typedef enum { ST_BASIS_IASC = 0, ST_BASIS_GREST2 = 1, ST_BASIS_GREST3 = 2, ST_BASIS_GREST_RSVD = 3 } st_basis_kind;
+/* SpectralOrder (types.hpp:22) */
+typedef enum { ST_ABS_DESC = 0, ST_ALG_DESC = 1 } st_order;
+/* OperatorKind (laplacian_track.hpp:14) */
+typedef enum { ST_ADJACENCY = 0, ST_LAPLACIAN = 1, ST_NORMALIZED_LAPLACIAN = 2 } st_operator;
+
+/* TrackerOptions (trackers.hpp:52-63) restricted to the G-REST fields, plus the
+ * operator the session maintains and the CUDA device it is bound to. */
+typedef struct {
+  int32_t kind;     /* st_tracker_kind */
+  int32_t op;       /* st_operator */
+  int64_t k;        /* tracked pairs */
+  int32_t order;    /* st_order (alg_desc for Laplacian operators) */
+  int64_t rsvd_l;   /* randomized range finder target rank (default 100) */
+  int64_t rsvd_p;   /* oversampling (default 100) */
+  uint64_t seed;    /* TrackerOptions::seed */
+  int32_t device;   /* CUDA device ordinal */
+  int32_t flags;    /* ST_FLAG_* */
+} st_config;
+
+#define ST_FLAG_FORCE_DENSE 1  /* disable the compressed row-subset representation */
+#define ST_FLAG_TIMING 2       /* record per-phase CUDA-event timings */
+#define ST_FLAG_KERNEL_TIMING 4 /* record per-kernel-class CUDA-event timings (st_kernel_stats) */
+
+/* One update batch: the edit lists of assemble_update (graph.hpp:65-69).
+ * added (i, j, w) and removed (i, j) address existing nodes; new_edges
+ * (i, j, w) touch at least one of the n_new appended nodes, which get ids
+ * n_old + 0 .. n_old + n_new - 1 in order. */
+typedef struct {
+  int64_t n_added;
+  const int64_t* added_i;
+  const int64_t* added_j;
+  const double* added_w;
+  int64_t n_removed;
+  const int64_t* removed_i;
+  const int64_t* removed_j;
+  int64_t n_new;
+  int64_t n_new_edges;
+  const int64_t* new_i;
+  const int64_t* new_j;
+  const double* new_w;
+} st_update;
+
+typedef struct st_session st_session;
+
+/* Session = the state one reference caller keeps across steps: the adjacency
+ * CSR (and the shifted operator T for Laplacian operators, as in
+ * ShiftedLaplacianSession, laplacian_track.cpp:43-46) plus the TrackerState
+ * (trackers.hpp:65-75). The initial eigenpairs are an input (the output of
+ * tracker_init, trackers.cpp:132-145): values[k] and vectors n x k
+ * column-major with leading dimension ld. Replaces: constructing
+ * ShiftedLaplacianSession + holding TrackerState by value. */
+st_status st_create(const st_config* cfg, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                    const double* values_csr, const double* eig_values, const double* eig_vectors, int64_t ld,
+                    st_session** out);
+void st_destroy(st_session* s);
+
+/* One step of the hot path. Replaces, in one call, the reference loop body
+ * (experiment.cpp:169-173, 203):
+ *   GraphUpdate d = assemble_update(...);            graph.cpp:45-100
+ *   Perturbation p = to_perturbation(d)              trackers.cpp:128-130
+ *                    | session.advance(d);           laplacian_track.cpp:48-64
+ *   A = apply_update(A, d);                          graph.cpp:102-115
+ *   state = tracker_step(state, p);                  trackers.cpp:341-387
+ * Inputs are host buffers; the state stays resident on the device. */
+st_status st_step(st_session* s, const st_update* upd);
+
+/* st_step with the edit arrays already resident in device memory (same
+ * layout; every pointer in *upd is a device pointer). Used to time the step
+ * with its inputs in HBM. */
+st_status st_step_device(st_session* s, const st_update* upd);
+
+/* Sizes of the current state; alpha is the Laplacian shift (0 for adjacency). */
+st_status st_info(const st_session* s, int64_t* n, int64_t* k, uint64_t* steps_taken, int64_t* nnz_a,
+                  int64_t* nnz_t, int64_t* nnz_delta, double* alpha);
+
+/* SpectralEmbedding (trackers.hpp:28-34): values[k], vectors n x k column-major. */
+st_status st_get_embedding(const st_session* s, double* values, double* vectors, int64_t ld);
+/* Ritz values only (k doubles), the per-step result read by the e2e benchmark. */
+st_status st_get_values(const st_session* s, double* values);
+
+/* CSR export: which = 0 adjacency A, 1 shifted operator T, 2 the last step's
+ * perturbation (Delta, or Delta_T for Laplacian operators). rowptr has n+1
+ * entries, colidx/values nnz entries (sizes from st_info). */
+st_status st_get_csr(const st_session* s, int32_t which, int32_t* rowptr, int32_t* colidx, double* values);
+
+/* build_projection_basis (trackers.cpp:226-280) for `upd` against the current
+ * state, without changing the session: Z is n_total x D column-major (caller
+ * buffer of at least n_total * max_cols doubles); *cols receives D. */
+st_status st_probe_basis(st_session* s, const st_update* upd, int32_t basis_kind, uint64_t seed, double* z,
+                         int64_t ld, int64_t max_cols, int64_t* cols);
+
+/* rayleigh_ritz_step (trackers.cpp:282-308) for `upd` against the current
+ * state with a caller basis z (rows x cols, column-major), without changing the
+ * session: values[k], vectors rows x k column-major. */
+st_status st_probe_rr(st_session* s, const st_update* upd, const double* z, int64_t rows, int64_t cols, int64_t ldz,
+                      double* values, double* vectors, int64_t ldv);
+
+/* Message of the last failed call on this session (or of st_create when s is NULL). */
+const char* st_last_error(const st_session* s);
+
+/* Per-phase device timings (ms) of the last step when ST_FLAG_TIMING is set:
+ * [ingest, basis, rr_gram, eig, rotate, total]; returns the number written. */
+int32_t st_last_timings(const st_session* s, double* ms, int32_t cap);
+/* Kernel launches issued by the last st_step (counted by the library). */
+int64_t st_last_launches(const st_session* s);
+
+/* Accumulated device time (ms), launch count and algorithmic work of one
+ * kernel class since the last reset (ST_FLAG_KERNEL_TIMING). Classes: 0 DMMA
+ * Gram (flops), 1 DMMA row-local GEMM (flops), 2 CSR SpMM Delta.X / Delta.Z
+ * (bytes), 3 Cholesky, 4 triangular inverse, 5 eigensolver, 6 CSR merge
+ * (bytes), 7 RNG (draws), 8 Ritz rotation of X (bytes), 9 masked Gram of X
+ * (flops), 10 sketch SpMMs (bytes), 11 other ingestion. Returns 0 for an
+ * unknown class. */
+int32_t st_kernel_stats(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work);
+void st_reset_kernel_stats(st_session* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECTRACK_GPU_H */

@@ -272,7 +272,7 @@ def from_triplets(n: int, trips) -> Csr:
 
 
 def update_delta(n_old: int, upd: Update) -> Csr:
-    keep, a = upd.args()
+    keep, a = Update(upd.added, upd.removed, upd.n_new, upd.new_edges).args()
     err = C.create_string_buffer(ERRLEN)
     h = C.c_void_p()
     _check(lib().or_update_delta(I64(n_old), *a, C.byref(h), err, ERRLEN), err)
@@ -280,7 +280,7 @@ def update_delta(n_old: int, upd: Update) -> Csr:
 
 
 def apply_update(a: Csr, upd: Update, n_old: int | None = None) -> Csr:
-    keep, args = upd.args()
+    keep, args = Update(upd.added, upd.removed, upd.n_new, upd.new_edges).args()
     err = C.create_string_buffer(ERRLEN)
     h = C.c_void_p()
     _check(lib().or_apply_update(I64(a.n), _p(a.rowptr, I32P), _p(a.col, I32P), _p(a.val), *args,
@@ -332,7 +332,7 @@ class Session:
         return n.value, k.value, st.value, alpha.value
 
     def step(self, upd: Update) -> None:
-        keep, args = upd.args()
+        keep, args = Update(upd.added, upd.removed, upd.n_new, upd.new_edges).args()
         err = C.create_string_buffer(ERRLEN)
         secs = C.c_double(0)
         _check(lib().or_session_step(C.c_void_p(self._h), *args, C.byref(secs), err, ERRLEN), err)
@@ -349,7 +349,7 @@ class Session:
         return _csr_out(lib().or_session_csr(C.c_void_p(self._h), C.c_int(which)))
 
     def probe_basis(self, upd: Update, basis_kind: str, seed: int) -> np.ndarray:
-        keep, args = upd.args()
+        keep, args = Update(upd.added, upd.removed, upd.n_new, upd.new_edges).args()
         err = C.create_string_buffer(ERRLEN)
         h = C.c_void_p()
         bk = {"iasc": 0, "grest2": 1, "grest3": 2, "grest-rsvd": 3}[basis_kind]
@@ -358,7 +358,7 @@ class Session:
         return _mat_out(h.value)
 
     def probe_rr(self, upd: Update, z: np.ndarray):
-        keep, args = upd.args()
+        keep, args = Update(upd.added, upd.removed, upd.n_new, upd.new_edges).args()
         err = C.create_string_buffer(ERRLEN)
         h = C.c_void_p()
         _, k, _, _ = self.info()

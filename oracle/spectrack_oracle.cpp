@@ -82,15 +82,18 @@ Mat transpose(const Mat& m) {
   return t;
 }
 
+// Dense products on tall column-major blocks, blocked by rows so each row
+// block of the operands is read from memory once (per-element sums keep a
+// fixed order for a fixed thread count).
 Mat matmul(const Mat& a, const Mat& b) {
   if (a.cols != b.rows) throw std::invalid_argument("matmul: shape mismatch");
   Mat c(a.rows, b.cols);
   const Index n = a.rows;
-  const int T = n > 65536 ? nthreads() : 1;
-  const Index chunk = (n + T - 1) / T;
-#pragma omp parallel for num_threads(T) schedule(static, 1) if (T > 1)
-  for (int t = 0; t < T; ++t) {
-    const Index lo = t * chunk, hi = std::min(n, lo + chunk);
+  constexpr Index RB = 512;
+  const Index nblk = (n + RB - 1) / RB;
+#pragma omp parallel for schedule(static) if (n > 65536)
+  for (Index blk = 0; blk < nblk; ++blk) {
+    const Index lo = blk * RB, hi = std::min(n, lo + RB);
     for (Index j = 0; j < b.cols; ++j) {
       double* cj = c.col(j);
       for (Index l = 0; l < a.cols; ++l) {
@@ -109,18 +112,22 @@ Mat matmul_tn(const Mat& a, const Mat& b) {
   const Index n = a.rows;
   const int T = n > 65536 ? nthreads() : 1;
   const Index chunk = (n + T - 1) / T;
+  constexpr Index RB = 256;
   std::vector<Mat> part(static_cast<size_t>(T), Mat(a.cols, b.cols));
 #pragma omp parallel for num_threads(T) schedule(static, 1) if (T > 1)
   for (int t = 0; t < T; ++t) {
-    const Index lo = t * chunk, hi = std::min(n, lo + chunk);
+    const Index lo0 = t * chunk, hi0 = std::min(n, lo0 + chunk);
     Mat& p = part[static_cast<size_t>(t)];
-    for (Index j = 0; j < b.cols; ++j) {
-      const double* bj = b.col(j);
-      for (Index i = 0; i < a.cols; ++i) {
-        const double* ai = a.col(i);
-        double s = 0.0;
-        for (Index r = lo; r < hi; ++r) s += ai[r] * bj[r];
-        p(i, j) = s;
+    for (Index lo = lo0; lo < hi0; lo += RB) {
+      const Index hi = std::min(hi0, lo + RB);
+      for (Index j = 0; j < b.cols; ++j) {
+        const double* bj = b.col(j);
+        for (Index i = 0; i < a.cols; ++i) {
+          const double* ai = a.col(i);
+          double s = 0.0;
+          for (Index r = lo; r < hi; ++r) s += ai[r] * bj[r];
+          p(i, j) += s;
+        }
       }
     }
   }

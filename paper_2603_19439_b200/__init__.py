@@ -1,0 +1,287 @@
+"""B200-native G-REST per-step eigen-update (arxiv 2603.19439 hot path).
+
+Python binding of the C ABI in include/spectrack_gpu.h (libspectrack_b200.so,
+built in-tree for sm_100a). The library is the product; this module only
+marshals host buffers for tests and bench.py. There is no CPU fallback: if the
+CUDA library is missing or no GPU is visible, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspectrack_b200.so")
+
+I64 = C.c_int64
+DP = C.POINTER(C.c_double)
+I32P = C.POINTER(C.c_int32)
+I64P = C.POINTER(C.c_int64)
+
+ST_OK, ST_INVALID_ARGUMENT, ST_RUNTIME_ERROR, ST_CUDA_ERROR, ST_OTHER = range(5)
+KIND = {"iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6}
+BASIS = {"iasc": 0, "grest2": 1, "grest3": 2, "grest-rsvd": 3}
+OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
+ORDER = {"abs_desc": 0, "alg_desc": 1}
+FLAG_FORCE_DENSE, FLAG_TIMING, FLAG_KERNEL_TIMING = 1, 2, 4
+KERNEL_CLASSES = ["dmma_gram", "dmma_gemm", "spmm", "cholesky", "tri_inverse", "eigensolver", "csr_merge", "rng",
+                  "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other"]
+
+
+class StConfig(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("op", C.c_int32), ("k", C.c_int64), ("order", C.c_int32),
+                ("rsvd_l", C.c_int64), ("rsvd_p", C.c_int64), ("seed", C.c_uint64), ("device", C.c_int32),
+                ("flags", C.c_int32)]
+
+
+class StUpdate(C.Structure):
+    _fields_ = [("n_added", C.c_int64), ("added_i", I64P), ("added_j", I64P), ("added_w", DP),
+                ("n_removed", C.c_int64), ("removed_i", I64P), ("removed_j", I64P), ("n_new", C.c_int64),
+                ("n_new_edges", C.c_int64), ("new_i", I64P), ("new_j", I64P), ("new_w", DP)]
+
+
+class TrackerError(Exception):
+    """Failure with the reference's exception category in ``kind``
+    ('invalid_argument' | 'runtime_error' | 'cuda' | 'other')."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(msg)
+        self.kind = kind
+
+
+_KINDS = {ST_INVALID_ARGUMENT: "invalid_argument", ST_RUNTIME_ERROR: "runtime_error", ST_CUDA_ERROR: "cuda",
+          ST_OTHER: "other"}
+_lib = None
+
+
+def lib():
+    """Load the in-tree CUDA library (fails loudly when it is absent)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.st_create.argtypes = [C.POINTER(StConfig), I64, I32P, I32P, DP, DP, DP, I64, C.POINTER(C.c_void_p)]
+        L.st_step.argtypes = [C.c_void_p, C.POINTER(StUpdate)]
+        L.st_info.argtypes = [C.c_void_p, I64P, I64P, C.POINTER(C.c_uint64), I64P, I64P, I64P, DP]
+        L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
+        L.st_get_values.argtypes = [C.c_void_p, DP]
+        L.st_get_csr.argtypes = [C.c_void_p, C.c_int32, I32P, I32P, DP]
+        L.st_probe_basis.argtypes = [C.c_void_p, C.POINTER(StUpdate), C.c_int32, C.c_uint64, DP, I64, I64, I64P]
+        L.st_probe_rr.argtypes = [C.c_void_p, C.POINTER(StUpdate), DP, I64, I64, I64, DP, DP, I64]
+        L.st_last_error.argtypes = [C.c_void_p]
+        L.st_last_error.restype = C.c_char_p
+        L.st_destroy.argtypes = [C.c_void_p]
+        L.st_destroy.restype = None
+        L.st_last_timings.argtypes = [C.c_void_p, DP, C.c_int32]
+        L.st_last_timings.restype = C.c_int32
+        L.st_last_launches.argtypes = [C.c_void_p]
+        L.st_last_launches.restype = C.c_int64
+        L.st_step_device.argtypes = [C.c_void_p, C.POINTER(StUpdate)]
+        L.st_step_device.restype = C.c_int
+        L.st_kernel_stats.argtypes = [C.c_void_p, C.c_int32, DP, I64P, DP]
+        L.st_kernel_stats.restype = C.c_int32
+        L.st_reset_kernel_stats.argtypes = [C.c_void_p]
+        L.st_reset_kernel_stats.restype = None
+        for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
+                  "st_probe_basis", "st_probe_rr"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _p(a, t=DP):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+def _i64(x):
+    return np.ascontiguousarray(np.asarray(x, np.int64).reshape(-1))
+
+
+def _d(x):
+    return np.ascontiguousarray(np.asarray(x, np.float64).reshape(-1))
+
+
+@dataclass
+class Update:
+    """Edit lists of one step (assemble_update, graph.hpp:65-69)."""
+    added: tuple = ((), (), ())
+    removed: tuple = ((), ())
+    n_new: int = 0
+    new_edges: tuple = ((), (), ())
+
+    @staticmethod
+    def make(added=(), removed=(), n_new=0, new_edges=()):
+        def e3(e):
+            if isinstance(e, tuple) and len(e) == 3 and hasattr(e[0], "__len__"):
+                return _i64(e[0]), _i64(e[1]), _d(e[2])
+            e = list(e)
+            return (_i64([t[0] for t in e]), _i64([t[1] for t in e]),
+                    _d([t[2] if len(t) > 2 else 1.0 for t in e]))
+
+        def e2(e):
+            if isinstance(e, tuple) and len(e) == 2 and hasattr(e[0], "__len__"):
+                return _i64(e[0]), _i64(e[1])
+            e = list(e)
+            return _i64([t[0] for t in e]), _i64([t[1] for t in e])
+
+        return Update(e3(added), e2(removed), int(n_new), e3(new_edges))
+
+    def struct(self):
+        ai, aj, aw = _i64(self.added[0]), _i64(self.added[1]), _d(self.added[2])
+        ri, rj = _i64(self.removed[0]), _i64(self.removed[1])
+        ni, nj, nw = _i64(self.new_edges[0]), _i64(self.new_edges[1]), _d(self.new_edges[2])
+        keep = (ai, aj, aw, ri, rj, ni, nj, nw)
+        s = StUpdate(len(ai), _p(ai, I64P), _p(aj, I64P), _p(aw), len(ri), _p(ri, I64P), _p(rj, I64P),
+                     int(self.n_new), len(ni), _p(ni, I64P), _p(nj, I64P), _p(nw))
+        return keep, s
+
+    def h2d_bytes(self) -> int:
+        return 16 * (len(self.added[0]) + len(self.removed[0]) + len(self.new_edges[0])) + 8 * (
+            len(self.added[0]) + len(self.new_edges[0]))
+
+
+class TrackerSession:
+    """One tracker lane on one GPU: the adjacency CSR (and shifted operator for
+    Laplacian operators) plus the TrackerState, resident in HBM."""
+
+    def __init__(self, rowptr, col, val, values, vectors, kind="grest-rsvd", k=None, order="abs_desc",
+                 rsvd_l=100, rsvd_p=100, seed=0, operator="adjacency", device=0, force_dense=False, timing=False,
+                 kernel_timing=False):
+        L = lib()
+        rowptr = np.ascontiguousarray(rowptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        values = _d(values)
+        vectors = np.asfortranarray(np.asarray(vectors, np.float64))
+        n = len(rowptr) - 1
+        k = len(values) if k is None else k
+        flags = ((FLAG_FORCE_DENSE if force_dense else 0) | (FLAG_TIMING if timing else 0)
+                 | (FLAG_KERNEL_TIMING if kernel_timing else 0))
+        cfg = StConfig(KIND[kind], OPERATOR[operator], k, ORDER[order], rsvd_l, rsvd_p, seed, device, flags)
+        h = C.c_void_p()
+        rc = L.st_create(C.byref(cfg), n, _p(rowptr, I32P), _p(col, I32P), _p(val), _p(values),
+                         vectors.ctypes.data_as(DP), vectors.shape[0], C.byref(h))
+        if rc != ST_OK:
+            raise TrackerError(_KINDS.get(rc, "other"), L.st_last_error(None).decode())
+        self._h = h.value
+        self.k = k
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().st_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != ST_OK:
+            raise TrackerError(_KINDS.get(rc, "other"), lib().st_last_error(self._h).decode())
+
+    def step(self, upd: Update) -> None:
+        keep, s = upd.struct()
+        self._check(lib().st_step(self._h, C.byref(s)))
+
+    def step_device(self, dev_update) -> None:
+        """Step with edit arrays already in device memory: `dev_update` is a
+        DeviceUpdate (torch CUDA tensors)."""
+        self._check(lib().st_step_device(self._h, C.byref(dev_update.struct)))
+
+    def kernel_stats(self) -> dict:
+        out = {}
+        for i, name in enumerate(KERNEL_CLASSES):
+            ms, work = C.c_double(), C.c_double()
+            cnt = I64()
+            lib().st_kernel_stats(self._h, i, C.byref(ms), C.byref(cnt), C.byref(work))
+            out[name] = dict(ms=ms.value, launches=cnt.value, work=work.value)
+        return out
+
+    def reset_kernel_stats(self) -> None:
+        lib().st_reset_kernel_stats(self._h)
+
+    def info(self):
+        n, k, nnz_a, nnz_t, nnz_d = I64(), I64(), I64(), I64(), I64()
+        st = C.c_uint64()
+        alpha = C.c_double()
+        lib().st_info(self._h, C.byref(n), C.byref(k), C.byref(st), C.byref(nnz_a), C.byref(nnz_t),
+                      C.byref(nnz_d), C.byref(alpha))
+        return dict(n=n.value, k=k.value, steps_taken=st.value, nnz_a=nnz_a.value, nnz_t=nnz_t.value,
+                    nnz_delta=nnz_d.value, alpha=alpha.value)
+
+    def values(self) -> np.ndarray:
+        v = np.zeros(self.k)
+        self._check(lib().st_get_values(self._h, _p(v)))
+        return v
+
+    def embedding(self):
+        n = self.info()["n"]
+        vals = np.zeros(self.k)
+        vecs = np.zeros((n, self.k), order="F")
+        self._check(lib().st_get_embedding(self._h, _p(vals), vecs.ctypes.data_as(DP), n))
+        return vals, np.ascontiguousarray(vecs)
+
+    def csr(self, which: int = 0):
+        inf = self.info()
+        n = inf["n"]
+        nnz = {0: inf["nnz_a"], 1: inf["nnz_t"], 2: inf["nnz_delta"]}[which]
+        rp = np.zeros(n + 1, np.int32)
+        col = np.zeros(max(nnz, 1), np.int32)
+        val = np.zeros(max(nnz, 1))
+        self._check(lib().st_get_csr(self._h, which, _p(rp, I32P), _p(col, I32P), _p(val)))
+        return rp, col[:nnz], val[:nnz]
+
+    def probe_basis(self, upd: Update, basis_kind: str, seed: int) -> np.ndarray:
+        keep, s = upd.struct()
+        n_total = self.info()["n"] + upd.n_new
+        maxc = 2 * self.k + max(upd.n_new, 0) + 512
+        z = np.zeros((n_total, maxc), order="F")
+        cols = I64()
+        self._check(lib().st_probe_basis(self._h, C.byref(s), BASIS[basis_kind], seed, z.ctypes.data_as(DP),
+                                         n_total, maxc, C.byref(cols)))
+        return np.ascontiguousarray(z[:, : cols.value])
+
+    def probe_rr(self, upd: Update, z: np.ndarray):
+        keep, s = upd.struct()
+        zf = np.asfortranarray(np.asarray(z, np.float64))
+        vals = np.zeros(self.k)
+        vecs = np.zeros((z.shape[0], self.k), order="F")
+        self._check(lib().st_probe_rr(self._h, C.byref(s), zf.ctypes.data_as(DP), z.shape[0], z.shape[1],
+                                      max(z.shape[0], 1), _p(vals), vecs.ctypes.data_as(DP), max(z.shape[0], 1)))
+        return vals, np.ascontiguousarray(vecs)
+
+    def timings(self):
+        buf = np.zeros(8)
+        n = lib().st_last_timings(self._h, _p(buf), 8)
+        return buf[:n]
+
+    def launches(self) -> int:
+        return int(lib().st_last_launches(self._h))
+
+
+class DeviceUpdate:
+    """An Update whose edit arrays live in HBM (torch CUDA tensors)."""
+
+    def __init__(self, upd: Update, device="cuda"):
+        import torch
+
+        def t(x, dt):
+            return torch.as_tensor(np.ascontiguousarray(x), dtype=dt).to(device)
+
+        self.tensors = [t(upd.added[0], torch.int64), t(upd.added[1], torch.int64), t(upd.added[2], torch.float64),
+                        t(upd.removed[0], torch.int64), t(upd.removed[1], torch.int64),
+                        t(upd.new_edges[0], torch.int64), t(upd.new_edges[1], torch.int64),
+                        t(upd.new_edges[2], torch.float64)]
+        ai, aj, aw, ri, rj, ni, nj, nw = self.tensors
+
+        def ip(x):
+            return C.cast(C.c_void_p(x.data_ptr()), I64P)
+
+        def dp(x):
+            return C.cast(C.c_void_p(x.data_ptr()), DP)
+
+        self.struct = StUpdate(len(ai), ip(ai), ip(aj), dp(aw), len(ri), ip(ri), ip(rj), int(upd.n_new), len(ni),
+                               ip(ni), ip(nj), dp(nw))

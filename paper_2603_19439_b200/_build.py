@@ -1,0 +1,31 @@
+"""In-tree build of the CUDA library (sm_100a) behind include/spectrack_gpu.h."""
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libspectrack_b200.so")
+SOURCES = ["csrc/session.cu"]
+HEADERS = ["csrc/common.cuh", "csrc/dmma.cuh", "csrc/spmm.cuh", "csrc/smalllin.cuh", "csrc/rng.cuh",
+           "csrc/ingest.cuh", "csrc/stepk.cuh", "../include/spectrack_gpu.h"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in SOURCES + HEADERS)
+
+
+def build(force: bool = False) -> str:
+    if force or _stale():
+        nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+        cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, *[os.path.join(HERE, s) for s in SOURCES], "-lcusolver"]
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True))

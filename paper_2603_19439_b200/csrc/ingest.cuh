@@ -1,0 +1,354 @@
+// On-device ingestion of one update batch (HBM-bound integer/byte work):
+//   * validation of the edit lists with the reference's rules and error
+//     precedence (proj/src/graph.cpp:45-100),
+//   * the symmetric perturbation Delta as a sorted COO -> CSR (graph.cpp:17-32,
+//     sparse.cpp:17-23),
+//   * A_hat = pad(A) + Delta merged into a fresh CSR with exact-zero pruning
+//     and the "invalid deletion" / "negative weight" checks (graph.cpp:102-115),
+//   * for Laplacian operators, T_next and Delta_T = T_next - pad(T_old)
+//     (graph.cpp:117-151, laplacian_track.cpp:48-64), bit-exact.
+#pragma once
+
+#include "common.cuh"
+
+namespace stg {
+
+enum EditError : int {
+  kErrNone = 0,
+  kErrZeroWeight = 1,
+  kErrEditRange = 2,
+  kErrSelfLoop = 3,
+  kErrDuplicate = 4,
+  kErrNewRange = 5,
+  kErrNewWeight = 6,
+  kErrNewOldOnly = 7,
+};
+
+constexpr u64 kSentinel = ~0ULL;
+
+struct EditsDev {
+  const i64 *ai, *aj;
+  const double* aw;
+  const i64 *ri, *rj;
+  const i64 *ni, *nj;
+  const double* nw;
+  i64 n_add, n_rem, n_newe;
+  i64 n_old, S;
+};
+
+__device__ __forceinline__ void edit_at(const EditsDev& d, i64 g, int& list, i64& i, i64& j, double& w) {
+  if (g < d.n_add) {
+    list = 0; i = d.ai[g]; j = d.aj[g]; w = d.aw[g];
+  } else if (g < d.n_add + d.n_rem) {
+    const i64 h = g - d.n_add;
+    list = 1; i = d.ri[h]; j = d.rj[h]; w = -1.0;
+  } else {
+    const i64 h = g - d.n_add - d.n_rem;
+    list = 2; i = d.ni[h]; j = d.nj[h]; w = d.nw[h];
+  }
+}
+
+// Per-edit checks in the reference's order, up to (not including) the
+// duplicate test; pair keys for the duplicate test (graph.cpp:52-59).
+__global__ void edit_check_kernel(EditsDev d, u64* pkey, i64* pval, int* code, int* post) {
+  const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 E = d.n_add + d.n_rem + d.n_newe;
+  if (g >= E) return;
+  int list;
+  i64 i, j;
+  double w;
+  edit_at(d, g, list, i, j, w);
+  const i64 n_total = d.n_old + d.S;
+  int c = kErrNone, p = 0;
+  if (list == 0 && w == 0.0) c = kErrZeroWeight;
+  else if (list < 2 && (i < 0 || j < 0 || i >= d.n_old || j >= d.n_old)) c = kErrEditRange;
+  else if (list == 2 && (i < 0 || j < 0 || i >= n_total || j >= n_total)) c = kErrNewRange;
+  else if (list == 2 && w <= 0.0) c = kErrNewWeight;
+  else if (i == j) c = kErrSelfLoop;
+  if (list == 2 && c == kErrNone && (i > j ? i : j) < d.n_old) p = 1;
+  code[g] = c;
+  post[g] = p;
+  const i64 lo = i < j ? i : j, hi = i < j ? j : i;
+  pkey[g] = c == kErrNone ? ((static_cast<u64>(lo) << 32) | static_cast<u64>(hi)) : kSentinel;
+  pval[g] = g;
+}
+
+// Sorted pair keys (stable: edit order within a key): later occurrences are
+// duplicates of an earlier edit.
+__global__ void dup_mark_kernel(const u64* skey, const i64* sval, i64 E, int* dup) {
+  const i64 s = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (s >= E) return;
+  const u64 k = skey[s];
+  dup[sval[s]] = (s > 0 && k != kSentinel && skey[s - 1] == k) ? 1 : 0;
+}
+
+// Final per-edit status (first failing check) -> first error in edit order;
+// valid edits emit their two directed entries (row << 32 | col, weight).
+__global__ void edit_emit_kernel(EditsDev d, const int* code, const int* dup, const int* post, u64* err,
+                                 u64* ekey, double* eval, unsigned long long* nvalid) {
+  const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 E = d.n_add + d.n_rem + d.n_newe;
+  if (g >= E) return;
+  int c = code[g];
+  if (c == kErrNone && dup[g]) c = kErrDuplicate;
+  if (c == kErrNone && post[g]) c = kErrNewOldOnly;
+  if (c != kErrNone) {
+    atomicMin(err, (static_cast<u64>(g) << 8) | static_cast<u64>(c));
+    ekey[2 * g] = ekey[2 * g + 1] = kSentinel;
+    eval[2 * g] = eval[2 * g + 1] = 0.0;
+    return;
+  }
+  int list;
+  i64 i, j;
+  double w;
+  edit_at(d, g, list, i, j, w);
+  ekey[2 * g] = (static_cast<u64>(i) << 32) | static_cast<u64>(j);
+  ekey[2 * g + 1] = (static_cast<u64>(j) << 32) | static_cast<u64>(i);
+  eval[2 * g] = eval[2 * g + 1] = w;
+  atomicAdd(nvalid, 2ULL);
+}
+
+// Sorted entries -> row/col arrays, per-row counts, and row marks.
+__global__ void delta_rows_kernel(const u64* skey, i64 n2, int* drow, int* dcol, int* rowcnt, int* mark, int stamp) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n2) return;
+  const u64 k = skey[e];
+  if (k == kSentinel) return;
+  const int r = static_cast<int>(k >> 32), c = static_cast<int>(k & 0xffffffffULL);
+  drow[e] = r;
+  dcol[e] = c;
+  atomicAdd(rowcnt + r, 1);
+  mark[r] = stamp;
+}
+
+__global__ void mark_range_kernel(int* mark, i64 lo, i64 hi, int stamp) {
+  const i64 r = lo + static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < hi) mark[r] = stamp;
+}
+
+// ---- apply_update merge -------------------------------------------------
+// Pass 1 (per Delta entry): locate in A's row, classify, count, check.
+__global__ void merge_classify_kernel(const u64* skey, const double* sval, i64 n2, const int* arp, const int* acol,
+                                      const double* aval, i64 n_old, int* lb, int* flag, double* newv, int* contrib,
+                                      int* rowcnt, u64* err) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n2) return;
+  const u64 k = skey[e];
+  if (k == kSentinel) {
+    contrib[e] = 0;
+    return;
+  }
+  const int r = static_cast<int>(k >> 32), c = static_cast<int>(k & 0xffffffffULL);
+  const double dv = sval[e];
+  int s = 0, len = 0;
+  if (r < n_old) {
+    s = arp[r];
+    len = arp[r + 1] - s;
+  }
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (acol[s + mid] < c) lo = mid + 1; else hi = mid;
+  }
+  const bool found = lo < len && acol[s + lo] == c;
+  const double sum = found ? aval[s + lo] + dv : 0.0 + dv;
+  if (sum < -1e-12)
+    atomicMin(err, (static_cast<u64>(r) << 32) | (static_cast<u64>(c) << 1) | (found ? 1ULL : 0ULL));
+  const bool prune = found && sum == 0.0;
+  const int ct = found ? (prune ? -1 : 0) : 1;
+  lb[e] = lo;
+  flag[e] = (found ? 1 : 0) | (prune ? 2 : 0);
+  newv[e] = sum;
+  contrib[e] = ct;
+  if (ct) atomicAdd(rowcnt + r, ct);
+}
+
+__global__ void row_len_kernel(const int* arp, i64 n_old, i64 n_total, int* rowcnt) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r > n_total) return;
+  rowcnt[r] = (r < n_old) ? arp[r + 1] - arp[r] : 0;
+}
+
+// Pass 2a: A's entries to their new positions (warp per row).
+__global__ void __launch_bounds__(256) merge_rows_kernel(const int* arp, const int* acol, const double* aval,
+                                                         i64 n_old, const int* mark, int stamp, const int* drp,
+                                                         const int* dcol, const int* flag, const double* newv,
+                                                         const int* prefix, const int* nrp, int* ncol, double* nval) {
+  const i64 r = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n_old) return;
+  const int s = arp[r], len = arp[r + 1] - s;
+  const int o = nrp[r];
+  if (mark[r] != stamp) {
+    for (int i = lane; i < len; i += 32) {
+      ncol[o + i] = acol[s + i];
+      nval[o + i] = aval[s + i];
+    }
+    return;
+  }
+  const int ds = drp[r], dn = drp[r + 1] - ds;
+  const int p0 = prefix[ds];
+  for (int i = lane; i < len; i += 32) {
+    const int c = acol[s + i];
+    int lo = 0, hi = dn;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (dcol[ds + mid] < c) lo = mid + 1; else hi = mid;
+    }
+    const bool match = lo < dn && dcol[ds + lo] == c;
+    if (match && (flag[ds + lo] & 2)) continue;  // cancelled to exactly zero: pruned
+    const int pos = o + i + (prefix[ds + lo] - p0);
+    ncol[pos] = c;
+    nval[pos] = match ? newv[ds + lo] : aval[s + i];
+  }
+}
+
+// Pass 2b: Delta entries with no stored counterpart in A.
+__global__ void merge_insert_kernel(i64 n2, const int* drow, const int* dcol, const u64* skey, const int* lb,
+                                    const int* flag, const double* newv, const int* prefix, const int* drp,
+                                    const int* nrp, int* ncol, double* nval) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n2 || skey[e] == kSentinel || (flag[e] & 1)) return;
+  const int r = drow[e];
+  const int pos = nrp[r] + lb[e] + (prefix[e] - prefix[drp[r]]);
+  ncol[pos] = dcol[e];
+  nval[pos] = newv[e];
+}
+
+// ---- Laplacian operators -------------------------------------------------
+// Weighted degrees as the reference computes them: A * ones, row sums in
+// column order (sparse.cpp:97-99).
+__global__ void degrees_kernel(const int* rp, const double* val, i64 n, double* deg) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) s += val[e];
+  deg[r] = s;
+}
+
+__global__ void max_reduce_kernel(const double* x, i64 n, double* out) {
+  __shared__ double sh[1024];
+  double m = 0.0;  // degrees are >= 0; an empty graph has d_max = 0 (laplacian_track.cpp:37)
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, x[i]);
+  sh[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// shift_for (laplacian_track.cpp:35-39): normalized -> 2; combinatorial -> max(alpha, 2 d_max)
+__global__ void shift_kernel(int normalized, const double* dmax, const double* alpha_old, double* alpha_new) {
+  alpha_new[0] = normalized ? 2.0 : fmax(alpha_old[0], 2.0 * dmax[0]);
+}
+
+__device__ __forceinline__ double lap_offdiag(int normalized, const double* scale, i64 r, int c, double a) {
+  return normalized ? __dmul_rn(__dmul_rn(scale[r], scale[c]), a) : a;
+}
+__device__ __forceinline__ double lap_diag(int normalized, const double* deg, const double* alpha, i64 r) {
+  return normalized ? (deg[r] > 0.0 ? 1.0 : 2.0) : __dsub_rn(alpha[0], deg[r]);
+}
+
+__global__ void scale_kernel(const double* deg, i64 n, double* scale) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < n) scale[r] = deg[r] > 0.0 ? 1.0 / sqrt(deg[r]) : 0.0;
+}
+
+// T rows: A's pattern plus the diagonal, exact zeros pruned (graph.cpp:139-150).
+__global__ void lap_count_kernel(const int* rp, const int* col, const double* val, i64 n, int normalized,
+                                 const double* deg, const double* scale, const double* alpha, int* cnt) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r > n) return;
+  if (r == n) {
+    cnt[r] = 0;
+    return;
+  }
+  int c = lap_diag(normalized, deg, alpha, r) != 0.0 ? 1 : 0;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) c += lap_offdiag(normalized, scale, r, col[e], val[e]) != 0.0 ? 1 : 0;
+  cnt[r] = c;
+}
+
+__global__ void lap_write_kernel(const int* rp, const int* col, const double* val, i64 n, int normalized,
+                                 const double* deg, const double* scale, const double* alpha, const int* trp,
+                                 int* tcol, double* tval) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int o = trp[r];
+  const double dg = lap_diag(normalized, deg, alpha, r);
+  bool diag_done = false;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) {
+    const int c = col[e];
+    if (!diag_done && c > r) {
+      if (dg != 0.0) { tcol[o] = static_cast<int>(r); tval[o++] = dg; }
+      diag_done = true;
+    }
+    const double v = lap_offdiag(normalized, scale, r, c, val[e]);
+    if (v != 0.0) { tcol[o] = c; tval[o++] = v; }
+  }
+  if (!diag_done && dg != 0.0) { tcol[o] = static_cast<int>(r); tval[o] = dg; }
+}
+
+// Delta_T = T_next - pad(T_old): per-row sorted difference, exact zeros pruned
+// (laplacian_track.cpp:57-58). write == 0 counts, write == 1 emits.
+__global__ void lap_diff_kernel(const int* orp, const int* ocol, const double* oval, i64 n_old, const int* nrp,
+                                const int* ncol, const double* nval, i64 n, const int* drp, int* cnt, int* dcol,
+                                double* dval, int write) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r > n) return;
+  if (r == n) {
+    if (!write) cnt[r] = 0;
+    return;
+  }
+  int i = r < n_old ? orp[r] : 0, ie = r < n_old ? orp[r + 1] : 0;
+  int j = nrp[r], je = nrp[r + 1];
+  int c = 0, o = write ? drp[r] : 0;
+  while (i < ie || j < je) {
+    const int ci = i < ie ? ocol[i] : 0x7fffffff, cj = j < je ? ncol[j] : 0x7fffffff;
+    double v;
+    int cc;
+    if (ci == cj) { v = __dsub_rn(nval[j], oval[i]); cc = ci; ++i; ++j; }
+    else if (cj < ci) { v = __dsub_rn(nval[j], 0.0); cc = cj; ++j; }
+    else { v = __dsub_rn(0.0, oval[i]); cc = ci; ++i; }
+    if (v != 0.0) {
+      if (write) { dcol[o] = cc; dval[o] = v; ++o; }
+      ++c;
+    }
+  }
+  if (!write) cnt[r] = c;
+}
+
+// Row marks from a CSR's nonempty rows (Delta_T pattern).
+__global__ void mark_nonempty_kernel(const int* rp, i64 n, int* mark, int stamp) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < n && rp[r + 1] > rp[r]) mark[r] = stamp;
+}
+
+// ---- compressed row set P -------------------------------------------------
+__global__ void flag_kernel(const int* mark, int stamp, i64 n, int* flag) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r <= n) flag[r] = (r < n && mark[r] == stamp) ? 1 : 0;
+}
+
+__global__ void scatter_p_kernel(const int* flag, const int* pos, i64 n, int* P, int* posmap) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < n && flag[r]) {
+    P[pos[r]] = static_cast<int>(r);
+    posmap[r] = pos[r];
+  }
+}
+
+// Local (compressed) CSR of Delta over P: rows gathered, columns renumbered.
+__global__ void compress_rowptr_kernel(const int* grp, const int* P, i64 p, int* lrp, int nnz) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < p) lrp[t] = grp[P[t]];
+  if (t == p) lrp[t] = nnz;
+}
+
+__global__ void compress_cols_kernel(const int* gcol, i64 nnz, const int* posmap, int* lcol) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < nnz) lcol[e] = posmap[gcol[e]];
+}
+
+}  // namespace stg

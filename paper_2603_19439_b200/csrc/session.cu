@@ -1,0 +1,1467 @@
+// B200-native G-REST per-step eigen-update: session state, the step pipeline
+// and the C ABI of include/spectrack_gpu.h.
+//
+// Representation. Every vector the step builds (columns of X-bar, Delta X-bar,
+// the RSVD sketch, the basis Z) lies in span(X-bar) + span{e_i : i in P}, where
+// P is the set of rows touched by Delta plus the appended nodes. Writing such a
+// vector as v = E u + X_out a (E selects the rows of P, X_out is X-bar with the
+// rows of P zeroed), inner products are <v1, v2> = u1'u2 + a1' K a2 with
+// K = X_out' X_out = R_c' R_c. The step therefore runs on the stacked
+// coordinates [u (|P| rows); R_c a (k rows); a (k rows)]: Grams use the first
+// |P| + k rows, linear combinations all of them. This is an exact isometry of
+// the reference's n-row algebra (proj/src/trackers.cpp:226-308), so every
+// projection, Gram-Schmidt decision and Ritz value is the reference's, while
+// the tall-skinny work scales with |P| instead of n. Only two passes touch all
+// n rows: K (masked Gram of X) and the final rotation X <- X A_new / E U_new.
+// When |P| > n/2 the session runs the same code with P = all rows.
+#include <cub/cub.cuh>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/spectrack_gpu.h"
+#include "common.cuh"
+#include "dmma.cuh"
+#include "ingest.cuh"
+#include "rng.cuh"
+#include "smalllin.cuh"
+#include "spmm.cuh"
+#include "stepk.cuh"
+
+namespace stg {
+
+// kernel classes for per-class device timing (st_kernel_stats)
+enum KClass : int {
+  kGram = 0, kGemm = 1, kSpmm = 2, kChol = 3, kTriinv = 4, kEig = 5, kMerge = 6, kRng = 7, kRotate = 8,
+  kKcGram = 9, kSpmmSketch = 10, kIngestOther = 11
+};
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// ------------------------------------------------------------------ memory
+class Arena {
+ public:
+  ~Arena() {
+    for (auto& kv : bufs_)
+      if (kv.second.ptr) cudaFree(kv.second.ptr);
+  }
+  template <class T>
+  T* get(const std::string& name, i64 count) {
+    Buf& b = bufs_[name];
+    const size_t bytes = static_cast<size_t>(std::max<i64>(count, 1)) * sizeof(T);
+    if (b.bytes < bytes) {
+      if (b.ptr) STG_CUDA(cudaFree(b.ptr));
+      const size_t nb = bytes + bytes / 4 + 256;
+      STG_CUDA(cudaMalloc(&b.ptr, nb));
+      b.bytes = nb;
+    }
+    return static_cast<T*>(b.ptr);
+  }
+  size_t total() const {
+    size_t s = 0;
+    for (auto& kv : bufs_) s += kv.second.bytes;
+    return s;
+  }
+
+ private:
+  struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::unordered_map<std::string, Buf> bufs_;
+};
+
+class Pinned {
+ public:
+  ~Pinned() {
+    if (p_) cudaFreeHost(p_);
+  }
+  void* get(size_t bytes) {
+    if (bytes > cap_) {
+      if (p_) STG_CUDA(cudaFreeHost(p_));
+      cap_ = bytes + bytes / 4 + 4096;
+      STG_CUDA(cudaMallocHost(&p_, cap_));
+    }
+    return p_;
+  }
+
+ private:
+  void* p_ = nullptr;
+  size_t cap_ = 0;
+};
+
+struct DevCsr {
+  i64 n = 0, nnz = 0;
+  int* rp = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;
+};
+
+// A view of a row-major block.
+struct Blk {
+  double* p = nullptr;
+  int ld = 0;
+  Blk cols(int c0) const { return Blk{p + c0, ld}; }
+};
+
+struct Scalars {  // pinned host mirror of device scalars read at sync points
+  u64 err_edit;
+  u64 err_apply;
+  unsigned long long nvalid;
+  int nnz_new;
+  int p;
+  int nnz_t;
+  int nnz_dt;
+  int flags;
+  int info;
+  double alpha;
+};
+
+static const char* edit_message(int code) {
+  switch (code) {
+    case kErrZeroWeight: return "assemble_update: zero-weight edit";
+    case kErrEditRange: return "assemble_update: edited edge must address existing nodes";
+    case kErrSelfLoop: return "assemble_update: self-loop rejected";
+    case kErrDuplicate: return "assemble_update: duplicate edge across edit lists";
+    case kErrNewRange: return "assemble_update: new edge endpoint out of range";
+    case kErrNewWeight: return "assemble_update: new edges need positive weight";
+    case kErrNewOldOnly: return "assemble_update: new edge addresses only existing nodes";
+    default: return "assemble_update: invalid edit";
+  }
+}
+
+// The perturbation of one step in compressed form.
+struct Pert {
+  i64 n_old = 0, S = 0, n_total = 0;
+  i64 nnz = 0;         // nnz(Delta) (global)
+  i64 p = 0, p_old = 0;  // |P|, rows of P below n_old
+  bool dense = false;  // P = all rows
+  const int* grp = nullptr;  // global CSR of Delta (n_total + 1)
+  const int* gcol = nullptr;
+  const double* val = nullptr;
+  const int* lrp = nullptr;  // local CSR over P
+  const int* lcol = nullptr;
+  const int* P = nullptr;
+  const int* posmap = nullptr;
+  const int* mark = nullptr;  // rows of P: mark[r] == stamp
+  int stamp = 0;
+  bool empty() const { return S == 0 && nnz == 0; }
+};
+
+// Compressed basis produced by build_basis: N = p + 2k rows, D columns.
+struct Basis {
+  Blk z;
+  int D = 0;
+};
+
+// ------------------------------------------------------------------ session
+class Session {
+ public:
+  st_config cfg{};
+  std::string last_error;
+  i64 n = 0, k = 0;
+  u64 steps_taken = 0;
+  double alpha = 0.0;
+  std::vector<double> values;
+  double timings[8] = {0};
+  int ntimings = 0;
+  i64 launches = 0;
+  // per-kernel-class device time (CUDA events on the launching stream) and
+  // algorithmic work (flops for DMMA classes, bytes for memory-bound classes)
+  struct KStat {
+    double ms = 0, work = 0;
+    i64 launches = 0;
+  };
+  static constexpr int kClasses = 12;
+  KStat kstats[kClasses];
+
+  Session(const st_config& c, i64 n0, const int* rp, const int* col, const double* val, const double* ev,
+          const double* evec, i64 ld)
+      : cfg(c) {
+    STG_CUDA(cudaSetDevice(cfg.device));
+    STG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
+    for (auto& e : tev_) STG_CUDA(cudaEventCreate(&e));
+    if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
+    cusolverDnSetStream(solver_, st_);
+    STG_CUDA(cudaMallocHost(&hs_, sizeof(Scalars)));
+    d_scal_ = arena_.get<u64>("scalars", 32);
+    k = cfg.k;
+    n = n0;
+    if (k < 1 || k > n) throw InvalidArgument("tracker_init: k must satisfy 1 <= k <= n");
+    if (cfg.kind < ST_IASC || cfg.kind > ST_GREST_RSVD)
+      throw InvalidArgument("st_create: tracker kind outside the G-REST path");
+    if (cfg.op == ST_NORMALIZED_LAPLACIAN || cfg.op == ST_LAPLACIAN) {
+      if (cfg.order != ST_ALG_DESC) {
+        // the reference adapter forces alg_desc for shifted operators (laplacian_track.cpp:88)
+      }
+    }
+    // adjacency CSR
+    const i64 nnz = rp[n0];
+    A_[0] = alloc_csr("A0", n0, nnz);
+    STG_CUDA(cudaMemcpyAsync(A_[0].rp, rp, sizeof(int) * (n0 + 1), cudaMemcpyHostToDevice, st_));
+    STG_CUDA(cudaMemcpyAsync(A_[0].col, col, sizeof(int) * std::max<i64>(nnz, 1), cudaMemcpyHostToDevice, st_));
+    STG_CUDA(cudaMemcpyAsync(A_[0].val, val, sizeof(double) * std::max<i64>(nnz, 1), cudaMemcpyHostToDevice, st_));
+    acur_ = 0;
+    ensure_node_capacity(n0);
+    // eigenpairs: column-major host -> row-major device
+    values.assign(ev, ev + k);
+    std::vector<double> xr(static_cast<size_t>(n0 * k));
+    for (i64 c = 0; c < k; ++c)
+      for (i64 i = 0; i < n0; ++i) xr[static_cast<size_t>(i * k + c)] = evec[c * ld + i];
+    STG_CUDA(cudaMemcpy2DAsync(X_, sizeof(double) * ldx(), xr.data(), sizeof(double) * k, sizeof(double) * k, n0,
+                               cudaMemcpyHostToDevice, st_));
+    d_values_ = arena_.get<double>("values", k);
+    STG_CUDA(cudaMemcpyAsync(d_values_, values.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st_));
+    if (is_laplacian()) init_laplacian();
+    STG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  ~Session() {
+    cudaStreamSynchronize(st_);
+    cudaStreamSynchronize(st_rng_);
+    if (X_) cudaFree(X_);
+    if (solver_) cusolverDnDestroy(solver_);
+    if (hs_) cudaFreeHost(hs_);
+    for (auto& e : tev_) cudaEventDestroy(e);
+    cudaEventDestroy(ev_rng_);
+    cudaStreamDestroy(st_rng_);
+    cudaStreamDestroy(st_);
+  }
+
+  bool is_laplacian() const { return cfg.op == ST_LAPLACIAN || cfg.op == ST_NORMALIZED_LAPLACIAN; }
+  const DevCsr& A() const { return A_[acur_]; }
+  const DevCsr& T() const { return T_[tcur_]; }
+  i64 nnz_delta() const { return last_delta_nnz_; }
+
+  // ---------------------------------------------------------------- public ops
+  void step(const st_update& u, bool device_ptrs = false) {
+    launches = 0;
+    timing_begin();
+    Pert pt = ingest(u, /*commit_slot*/ true, device_ptrs);
+    timing_mark(0);
+    if (pt.empty()) {
+      commit_graph(pt);
+      steps_taken += 1;
+      timing_end(0);
+      kflush();
+      return;
+    }
+    const u64 basis_seed = mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken);
+    Basis b = build_basis(pt, cfg.kind - ST_IASC, basis_seed);
+    timing_mark(1);
+    std::vector<double> newvals;
+    rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+    commit_graph(pt);
+    values = newvals;
+    n = pt.n_total;
+    steps_taken += 1;
+    timing_end(5);
+    kflush();
+  }
+
+  i64 probe_basis(const st_update& u, int basis_kind, u64 seed, double* z, i64 ldz, i64 max_cols) {
+    launches = 0;
+    Pert pt = ingest(u, false);
+    if (pt.n_old != n) throw InvalidArgument("build_projection_basis: perturbation dimension mismatch");
+    if (pt.empty() && basis_kind != 0) {
+      // trackers.cpp:375-376 with Delta = 0: the basis is the padded old vectors
+      if (k > max_cols) throw InvalidArgument("st_probe_basis: output buffer too narrow");
+      std::vector<double> x(static_cast<size_t>(n * k));
+      copy_x_colmajor(x.data(), n);
+      for (i64 c = 0; c < k; ++c)
+        for (i64 i = 0; i < pt.n_total; ++i) z[c * ldz + i] = i < n ? x[static_cast<size_t>(c * n + i)] : 0.0;
+      return k;
+    }
+    Basis b = build_basis(pt, basis_kind, seed);
+    if (b.D > max_cols) throw InvalidArgument("st_probe_basis: output buffer too narrow");
+    expand_dense(pt, b.z, b.D, z, ldz);
+    return b.D;
+  }
+
+  void probe_rr(const st_update& u, const double* z, i64 rows, i64 cols, i64 ldz, double* vals, double* vecs,
+                i64 ldv) {
+    launches = 0;
+    Pert pt = ingest(u, false);
+    if (pt.n_old != n) throw InvalidArgument("rayleigh_ritz_step: perturbation dimension mismatch");
+    if (pt.empty()) {  // trackers.cpp:286: state returned unchanged
+      std::memcpy(vals, values.data(), sizeof(double) * k);
+      std::vector<double> x(static_cast<size_t>(n * k));
+      copy_x_colmajor(x.data(), n);
+      for (i64 c = 0; c < k; ++c) std::memcpy(vecs + c * ldv, x.data() + c * n, sizeof(double) * n);
+      return;
+    }
+    if (rows != pt.n_total) throw InvalidArgument("rayleigh_ritz_step: basis row count mismatch");
+    if (cols < k) throw InvalidArgument("rayleigh_ritz_step: projection subspace too small");
+    // caller bases live in the full row space: P = all rows, a-coordinates 0
+    make_dense(pt);
+    const i64 N = pt.p + 2 * k;
+    const int ldz_d = ld_for(cols);
+    double* zd = arena_.get<double>("probe_z", N * ldz_d);
+    STG_CUDA(cudaMemsetAsync(zd, 0, sizeof(double) * N * ldz_d, st_));
+    std::vector<double> zr(static_cast<size_t>(rows * cols));
+    for (i64 c = 0; c < cols; ++c)
+      for (i64 i = 0; i < rows; ++i) zr[static_cast<size_t>(i * cols + c)] = z[c * ldz + i];
+    STG_CUDA(cudaMemcpy2DAsync(zd, sizeof(double) * ldz_d, zr.data(), sizeof(double) * cols, sizeof(double) * cols,
+                               rows, cudaMemcpyHostToDevice, st_));
+    // Xc for the Eq. (14) low-rank term: rows [0, n_old) = X, new rows 0, no a-part
+    Basis b{Blk{zd, ldz_d}, static_cast<int>(cols)};
+    double* xc = arena_.get<double>("probe_xc", N * ldx());
+    STG_CUDA(cudaMemsetAsync(xc, 0, sizeof(double) * N * ldx(), st_));
+    STG_CUDA(cudaMemcpyAsync(xc, X_, sizeof(double) * n * ldx(), cudaMemcpyDeviceToDevice, st_));
+    std::vector<double> newvals;
+    std::vector<double> w(static_cast<size_t>(pt.n_total * k));
+    rayleigh_ritz(pt, b, newvals, false, w.data(), pt.n_total, Blk{xc, ldx()});
+    std::memcpy(vals, newvals.data(), sizeof(double) * k);
+    for (i64 c = 0; c < k; ++c)
+      for (i64 i = 0; i < pt.n_total; ++i) vecs[c * ldv + i] = w[static_cast<size_t>(i * k + c)];
+  }
+
+  void copy_x_colmajor(double* out, i64 rows) {
+    std::vector<double> xr(static_cast<size_t>(rows * k));
+    STG_CUDA(cudaMemcpy2DAsync(xr.data(), sizeof(double) * k, X_, sizeof(double) * ldx(), sizeof(double) * k, rows,
+                               cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    for (i64 c = 0; c < k; ++c)
+      for (i64 i = 0; i < rows; ++i) out[c * rows + i] = xr[static_cast<size_t>(i * k + c)];
+  }
+
+  void get_embedding(double* vals, double* vecs, i64 ld) {
+    std::memcpy(vals, values.data(), sizeof(double) * k);
+    std::vector<double> x(static_cast<size_t>(n * k));
+    copy_x_colmajor(x.data(), n);
+    for (i64 c = 0; c < k; ++c) std::memcpy(vecs + c * ld, x.data() + c * n, sizeof(double) * n);
+  }
+
+  void get_csr(int which, int* rp, int* col, double* val) {
+    DevCsr m;
+    if (which == 0) m = A();
+    else if (which == 1) {
+      if (!is_laplacian()) throw InvalidArgument("st_get_csr: the adjacency session has no shifted operator");
+      m = T();
+    } else {
+      m.n = last_delta_n_;
+      m.nnz = last_delta_nnz_;
+      m.rp = last_delta_.rp;
+      m.col = last_delta_.col;
+      m.val = last_delta_.val;
+      if (!m.rp) {
+        std::fill(rp, rp + n + 1, 0);
+        return;
+      }
+    }
+    STG_CUDA(cudaMemcpyAsync(rp, m.rp, sizeof(int) * (m.n + 1), cudaMemcpyDeviceToHost, st_));
+    if (m.nnz) {
+      STG_CUDA(cudaMemcpyAsync(col, m.col, sizeof(int) * m.nnz, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(val, m.val, sizeof(double) * m.nnz, cudaMemcpyDeviceToHost, st_));
+    }
+    STG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+ private:
+  Arena arena_;
+  Pinned pin_;
+  cudaStream_t st_ = nullptr, st_rng_ = nullptr;
+  cudaEvent_t ev_rng_ = nullptr;
+  cudaEvent_t tev_[8];
+  int tev_n_ = 0;
+  cusolverDnHandle_t solver_ = nullptr;
+  Scalars* hs_ = nullptr;
+  u64* d_scal_ = nullptr;  // [0] err_edit [1] err_apply [2] nvalid [3] flags(int) [4] info(int)
+  DevCsr A_[2], T_[2];
+  int acur_ = 0, tcur_ = 0;
+  double* d_alpha_ = nullptr;  // [0] current [1] next [2] dmax
+  double* X_ = nullptr;
+  i64 xcap_ = 0;
+  double* d_values_ = nullptr;
+  int* mark_delta_ = nullptr;
+  int* mark_p_ = nullptr;
+  int* posmap_ = nullptr;
+  i64 nodecap_ = 0;
+  int stamp_ = 0;
+  DevCsr last_delta_;
+  i64 last_delta_nnz_ = 0, last_delta_n_ = 0;
+  // pending (uncommitted) next graph
+  int anext_ = -1, tnext_ = -1;
+  double alpha_next_ = 0.0;
+
+  struct PendingK {
+    int cls;
+    cudaEvent_t a, b;
+    double work;
+  };
+  std::vector<PendingK> pend_;
+  std::vector<cudaEvent_t> evpool_;
+  size_t evnext_ = 0;
+  bool ktiming() const { return cfg.flags & ST_FLAG_KERNEL_TIMING; }
+  cudaEvent_t next_event() {
+    if (evnext_ == evpool_.size()) {
+      cudaEvent_t e;
+      STG_CUDA(cudaEventCreate(&e));
+      evpool_.push_back(e);
+    }
+    return evpool_[evnext_++];
+  }
+  void kbegin(int cls, double work, cudaStream_t s = nullptr) {
+    if (!ktiming()) return;
+    PendingK p{cls, next_event(), next_event(), work};
+    STG_CUDA(cudaEventRecord(p.a, s ? s : st_));
+    pend_.push_back(p);
+  }
+  void kend(cudaStream_t s = nullptr) {
+    if (!ktiming()) return;
+    STG_CUDA(cudaEventRecord(pend_.back().b, s ? s : st_));
+  }
+ public:
+  void kflush() {
+    if (pend_.empty()) return;
+    STG_CUDA(cudaDeviceSynchronize());
+    for (auto& p : pend_) {
+      float ms = 0;
+      STG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+      kstats[p.cls].ms += ms;
+      kstats[p.cls].work += p.work;
+      kstats[p.cls].launches += 1;
+    }
+    pend_.clear();
+    evnext_ = 0;
+  }
+  void kreset() {
+    for (auto& k : kstats) k = KStat{};
+  }
+
+ private:
+  int ldx() const { return static_cast<int>(k % 2 ? k + 1 : k); }
+  int* flags_ptr() { return reinterpret_cast<int*>(d_scal_ + 3); }
+  int* info_ptr() { return reinterpret_cast<int*>(d_scal_ + 4); }
+
+  template <typename K, typename... Args>
+  void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    kernel<<<grid, block, smem, s>>>(args...);
+    STG_LAUNCH();
+    ++launches;
+  }
+  static unsigned blocks(i64 n, int b = 256) { return static_cast<unsigned>(std::max<i64>(1, cdiv(n, b))); }
+
+  // ---------------------------------------------------------------- timing
+  void timing_begin() {
+    ntimings = 0;
+    if (cfg.flags & ST_FLAG_TIMING) STG_CUDA(cudaEventRecord(tev_[0], st_));
+  }
+  void timing_mark(int slot) {
+    if (cfg.flags & ST_FLAG_TIMING) STG_CUDA(cudaEventRecord(tev_[slot + 1], st_));
+  }
+  void timing_end(int last) {
+    if (!(cfg.flags & ST_FLAG_TIMING)) return;
+    STG_CUDA(cudaEventRecord(tev_[7], st_));
+    STG_CUDA(cudaEventSynchronize(tev_[7]));
+    float ms = 0;
+    for (int i = 0; i < 6; ++i) timings[i] = 0;
+    (void)last;
+    STG_CUDA(cudaEventElapsedTime(&ms, tev_[0], tev_[7]));
+    timings[5] = ms;
+    ntimings = 6;
+    // phase marks 1..4 are recorded when reached
+    float a;
+    if (cudaEventElapsedTime(&a, tev_[0], tev_[1]) == cudaSuccess) timings[0] = a;
+    if (cudaEventElapsedTime(&a, tev_[1], tev_[2]) == cudaSuccess) timings[1] = a;
+    if (cudaEventElapsedTime(&a, tev_[2], tev_[3]) == cudaSuccess) timings[2] = a;
+    if (cudaEventElapsedTime(&a, tev_[3], tev_[4]) == cudaSuccess) timings[3] = a;
+    if (cudaEventElapsedTime(&a, tev_[4], tev_[7]) == cudaSuccess) timings[4] = a;
+    (void)cudaGetLastError();  // unrecorded phase events (empty steps) are not errors
+  }
+
+  static u64 mix_seed(u64 base, u64 salt) {  // rng.hpp:16-21
+    u64 z = base + 0x9e3779b97f4a7c15ULL * (salt + 0x632be59bd9b4e019ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+
+  DevCsr alloc_csr(const std::string& name, i64 nrows, i64 nnz) {
+    DevCsr m;
+    m.n = nrows;
+    m.nnz = nnz;
+    m.rp = arena_.get<int>(name + ".rp", nrows + 1);
+    m.col = arena_.get<int>(name + ".col", nnz);
+    m.val = arena_.get<double>(name + ".val", nnz);
+    return m;
+  }
+
+  void ensure_node_capacity(i64 need) {
+    if (need <= nodecap_ && X_) return;
+    const i64 cap = std::max<i64>(need + need / 4, 1024);
+    double* nx = nullptr;
+    STG_CUDA(cudaMalloc(&nx, sizeof(double) * cap * ldx()));
+    if (X_) {
+      STG_CUDA(cudaMemcpyAsync(nx, X_, sizeof(double) * nodecap_ * ldx(), cudaMemcpyDeviceToDevice, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      STG_CUDA(cudaFree(X_));
+    }
+    X_ = nx;
+    // fresh mark arrays start at -1 (stamps are per step and always >= 1)
+    mark_delta_ = arena_.get<int>("mark_delta_" + std::to_string(cap), cap);
+    mark_p_ = arena_.get<int>("mark_p_" + std::to_string(cap), cap);
+    posmap_ = arena_.get<int>("posmap_" + std::to_string(cap), cap);
+    STG_CUDA(cudaMemsetAsync(mark_delta_, 0xff, sizeof(int) * cap, st_));
+    STG_CUDA(cudaMemsetAsync(mark_p_, 0xff, sizeof(int) * cap, st_));
+    nodecap_ = cap;
+  }
+
+  // ---------------------------------------------------------------- linear algebra helpers
+  void gram(const double* A, int lda, const double* B, int ldb, i64 rows, int m1, int m2, bool sym, double* out,
+            int ldo, double alpha = 1.0, const int* mask = nullptr, int mask_val = 0) {
+    if (m1 <= 0 || m2 <= 0) return;
+    dm::GramArgs a{};
+    a.A = A;
+    a.lda = lda;
+    a.B = B;
+    a.ldb = ldb;
+    a.nrows = rows;
+    a.m1 = m1;
+    a.m2 = m2;
+    a.tiles_i = static_cast<int>(cdiv(m1, dm::BM));
+    a.tiles_j = static_cast<int>(cdiv(m2, dm::BN));
+    a.sym = sym ? 1 : 0;
+    a.mask = mask;
+    a.mask_val = mask_val;
+    const int ntiles = sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j;
+    const i64 target = 148 * 6;
+    i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), 128), cdiv(target, ntiles)));
+    splits = std::min<i64>(splits, 65535);
+    a.rows_per_split = round_up(cdiv(std::max<i64>(rows, 1), splits), dm::BK);
+    splits = std::max<i64>(1, cdiv(std::max<i64>(rows, 1), a.rows_per_split));
+    const i64 m1p = static_cast<i64>(a.tiles_i) * dm::BM, m2p = static_cast<i64>(a.tiles_j) * dm::BN;
+    a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
+    kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
+    launch(dm::gram_tn_kernel, dim3(ntiles, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
+    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
+           static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
+           static_cast<int>(m2p), a.sym, out, ldo, alpha);
+    kend();
+  }
+
+  void nn(const double* A, int lda, i64 rows, int m1, const double* C, int ldc, int m2, double* Out, int ldo,
+          double alpha, double beta, const double* B, int ldb, bool tri = false) {
+    if (rows <= 0 || m2 <= 0) return;
+    dm::NNArgs a{};
+    a.A = A;
+    a.lda = lda;
+    a.nrows = rows;
+    a.m1 = m1;
+    a.C = C;
+    a.ldc = ldc;
+    a.m2 = m2;
+    a.Bm = B;
+    a.ldb = ldb;
+    a.Out = Out;
+    a.ldo = ldo;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.upper_tri_c = tri ? 1 : 0;
+    kbegin(kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
+    launch(dm::gemm_nn_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::BM)), static_cast<unsigned>(cdiv(m2, dm::BN))),
+           dim3(dm::NT), 0, st_, a);
+    kend();
+  }
+
+  // CSR x dense with compulsory-traffic accounting: 12 B per nonzero, the row
+  // pointers, and one read of each referenced dense row plus the output rows.
+  void do_spmm(const SpmmArgs& a, i64 nnz, i64 distinct_cols, int cls = kSpmm) {
+    kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
+    spmm(a, st_);
+    launches += cdiv(a.m, 256);
+    kend();
+  }
+
+  void chol(const double* G, int ldg, int w, double* R, int ldr, const double* orig2, double tau2, bool psd) {
+    kbegin(kChol, static_cast<double>(w) * w * w / 3.0);
+    struct End {
+      Session* s;
+      ~End() { s->kend(); }
+    } end{this};
+    const size_t packed = sizeof(double) * static_cast<size_t>(w) * (w + 1) / 2;
+    if (packed <= 220 * 1024) {
+      static bool attr = false;
+      if (!attr) {
+        STG_CUDA(cudaFuncSetAttribute(chol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+        attr = true;
+      }
+      launch(chol_kernel<true>, dim3(1), dim3(1024), packed, st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
+             flags_ptr(), static_cast<double*>(nullptr));
+    } else {
+      double* work = arena_.get<double>("chol_work", static_cast<i64>(w) * w);
+      launch(chol_kernel<false>, dim3(1), dim3(1024), 0, st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0, flags_ptr(),
+             work);
+    }
+  }
+
+  void triinv(const double* R, int ldr, int w, double* Ri, int ldi) {
+    if (w > 32 * kTriMaxSlots) throw RuntimeError("triinv: block wider than 320 columns");
+    kbegin(kTriinv, static_cast<double>(w) * w * w / 3.0);
+    launch(triinv_kernel, dim3(blocks(w, 4)), dim3(128), 0, st_, R, ldr, w, Ri, ldi);
+    kend();
+  }
+
+  // Symmetric eigendecomposition (cuSOLVER syevd, ascending) of a row-major
+  // D x D block after (M + M')/2; w and V (column-major) in arena buffers.
+  void eig(const double* M, int ldm, int D, double** w_out, double** v_out, const std::string& tag) {
+    kbegin(kEig, 9.0 * D * D * D);
+    struct End {
+      Session* s;
+      ~End() { s->kend(); }
+    } end{this};
+    double* V = arena_.get<double>("eigV" + tag, static_cast<i64>(D) * D);
+    double* w = arena_.get<double>("eigW" + tag, D);
+    launch(symmetrize_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_, M, ldm, D, V, flags_ptr());
+    int lwork = 0;
+    if (cusolverDnDsyevd_bufferSize(solver_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, V, D, w, &lwork) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw CudaError("cusolverDnDsyevd_bufferSize failed");
+    double* work = arena_.get<double>("eig_work", lwork);
+    if (cusolverDnDsyevd(solver_, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, D, V, D, w, work, lwork,
+                         info_ptr()) != CUSOLVER_STATUS_SUCCESS)
+      throw CudaError("cusolverDnDsyevd failed");
+    *w_out = w;
+    *v_out = V;
+  }
+
+  void read_scalars() {
+    STG_CUDA(cudaMemcpyAsync(&hs_->flags, flags_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&hs_->info, info_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+  }
+
+  // ---------------------------------------------------------------- Laplacian setup
+  void init_laplacian() {
+    d_alpha_ = arena_.get<double>("alpha", 4);
+    const bool normalized = cfg.op == ST_NORMALIZED_LAPLACIAN;
+    const DevCsr& a = A();
+    double* deg = arena_.get<double>("deg", n + 1);
+    double* scale = arena_.get<double>("scale", n + 1);
+    launch(degrees_kernel, dim3(blocks(n)), dim3(256), 0, st_, static_cast<const int*>(a.rp),
+           static_cast<const double*>(a.val), n, deg);
+    launch(max_reduce_kernel, dim3(1), dim3(1024), 0, st_, static_cast<const double*>(deg), n, d_alpha_ + 2);
+    STG_CUDA(cudaMemsetAsync(d_alpha_, 0, sizeof(double), st_));  // shift_for(a0, kind, 0.0)
+    launch(shift_kernel, dim3(1), dim3(1), 0, st_, normalized ? 1 : 0, static_cast<const double*>(d_alpha_ + 2),
+           static_cast<const double*>(d_alpha_), d_alpha_);
+    launch(scale_kernel, dim3(blocks(n)), dim3(256), 0, st_, static_cast<const double*>(deg), n, scale);
+    T_[0] = build_t("T0", a, n, normalized, deg, scale, d_alpha_);
+    tcur_ = 0;
+    STG_CUDA(cudaMemcpyAsync(&hs_->alpha, d_alpha_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    alpha = hs_->alpha;
+    T_[0].nnz = t_nnz_host_;
+  }
+
+  i64 t_nnz_host_ = 0;
+  DevCsr build_t(const std::string& name, const DevCsr& a, i64 nr, bool normalized, const double* deg,
+                 const double* scale, const double* alpha_ptr) {
+    int* cnt = arena_.get<int>("t_cnt", nr + 1);
+    launch(lap_count_kernel, dim3(blocks(nr + 1)), dim3(256), 0, st_, static_cast<const int*>(a.rp),
+           static_cast<const int*>(a.col), static_cast<const double*>(a.val), nr, normalized ? 1 : 0, deg, scale,
+           alpha_ptr, cnt);
+    DevCsr t;
+    t.n = nr;
+    t.rp = arena_.get<int>(name + ".rp", nr + 1);
+    scan_int(cnt, t.rp, nr + 1);
+    int nnz_t = 0;
+    STG_CUDA(cudaMemcpyAsync(&nnz_t, t.rp + nr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    t.nnz = nnz_t;
+    t_nnz_host_ = nnz_t;
+    t.col = arena_.get<int>(name + ".col", nnz_t);
+    t.val = arena_.get<double>(name + ".val", nnz_t);
+    launch(lap_write_kernel, dim3(blocks(nr)), dim3(256), 0, st_, static_cast<const int*>(a.rp),
+           static_cast<const int*>(a.col), static_cast<const double*>(a.val), nr, normalized ? 1 : 0, deg, scale,
+           alpha_ptr, static_cast<const int*>(t.rp), t.col, t.val);
+    return t;
+  }
+
+  void scan_int(const int* in, int* out, i64 count) {
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int>(count), st_);
+    void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+    cub::DeviceScan::ExclusiveSum(t, tmp, in, out, static_cast<int>(count), st_);
+  }
+
+  // ---------------------------------------------------------------- ingestion
+  // Validation, Delta, A_next (and T_next, Delta_T), P. Nothing committed.
+  Pert ingest(const st_update& u, bool keep_delta, bool device_ptrs = false) {
+    if (u.n_new < 0) throw InvalidArgument("assemble_update: negative node count");
+    if (u.n_added < 0 || u.n_removed < 0 || u.n_new_edges < 0) throw InvalidArgument("st_step: negative list length");
+    const i64 n_old = n, S = u.n_new, n_total = n_old + S;
+    if (n_total >= (1LL << 31)) throw InvalidArgument("st_step: node count exceeds int32 CSR indexing");
+    const i64 E = u.n_added + u.n_removed + u.n_new_edges;
+    ensure_node_capacity(n_total);
+    ++stamp_;
+    if (stamp_ == 0x7fffffff) stamp_ = 1;
+    Pert pt;
+    pt.n_old = n_old;
+    pt.S = S;
+    pt.n_total = n_total;
+    pt.stamp = stamp_;
+    STG_CUDA(cudaMemsetAsync(d_scal_, 0xff, sizeof(u64) * 2, st_));  // err_edit, err_apply = MAX
+    STG_CUDA(cudaMemsetAsync(d_scal_ + 2, 0, sizeof(u64) * 3, st_));  // nvalid, flags, info
+    EditsDev ed;
+    if (device_ptrs) {
+      ed.ai = reinterpret_cast<const i64*>(u.added_i);
+      ed.aj = reinterpret_cast<const i64*>(u.added_j);
+      ed.aw = u.added_w;
+      ed.ri = reinterpret_cast<const i64*>(u.removed_i);
+      ed.rj = reinterpret_cast<const i64*>(u.removed_j);
+      ed.ni = reinterpret_cast<const i64*>(u.new_i);
+      ed.nj = reinterpret_cast<const i64*>(u.new_j);
+      ed.nw = u.new_w;
+    } else {
+      // upload the edit lists (one pinned staging buffer, one copy)
+      const size_t bytes = sizeof(i64) * (2 * E) + sizeof(double) * (u.n_added + u.n_new_edges);
+      char* host = static_cast<char*>(pin_.get(std::max<size_t>(bytes, 8)));
+      char* dev = arena_.get<char>("edits", static_cast<i64>(std::max<size_t>(bytes, 8)));
+      size_t off = 0;
+      auto put = [&](const void* src, size_t b) -> size_t {
+        const size_t o = off;
+        if (b) std::memcpy(host + off, src, b);
+        off += b;
+        return o;
+      };
+      const size_t o_ai = put(u.added_i, sizeof(i64) * u.n_added), o_aj = put(u.added_j, sizeof(i64) * u.n_added);
+      const size_t o_ri = put(u.removed_i, sizeof(i64) * u.n_removed);
+      const size_t o_rj = put(u.removed_j, sizeof(i64) * u.n_removed);
+      const size_t o_ni = put(u.new_i, sizeof(i64) * u.n_new_edges), o_nj = put(u.new_j, sizeof(i64) * u.n_new_edges);
+      const size_t o_aw = put(u.added_w, sizeof(double) * u.n_added);
+      const size_t o_nw = put(u.new_w, sizeof(double) * u.n_new_edges);
+      if (off) STG_CUDA(cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, st_));
+      ed.ai = reinterpret_cast<const i64*>(dev + o_ai);
+      ed.aj = reinterpret_cast<const i64*>(dev + o_aj);
+      ed.aw = reinterpret_cast<const double*>(dev + o_aw);
+      ed.ri = reinterpret_cast<const i64*>(dev + o_ri);
+      ed.rj = reinterpret_cast<const i64*>(dev + o_rj);
+      ed.ni = reinterpret_cast<const i64*>(dev + o_ni);
+      ed.nj = reinterpret_cast<const i64*>(dev + o_nj);
+      ed.nw = reinterpret_cast<const double*>(dev + o_nw);
+    }
+    ed.n_add = u.n_added;
+    ed.n_rem = u.n_removed;
+    ed.n_newe = u.n_new_edges;
+    ed.n_old = n_old;
+    ed.S = S;
+    u64* err_edit = d_scal_;
+    u64* err_apply = d_scal_ + 1;
+    unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(d_scal_ + 2);
+    const i64 n2 = 2 * E;
+    // ---- validation + Delta entries
+    u64* pkey = arena_.get<u64>("pkey", E);
+    i64* pval = arena_.get<i64>("pval", E);
+    u64* pkey_s = arena_.get<u64>("pkey_s", E);
+    i64* pval_s = arena_.get<i64>("pval_s", E);
+    int* code = arena_.get<int>("code", E);
+    int* post = arena_.get<int>("post", E);
+    int* dup = arena_.get<int>("dup", E);
+    u64* ekey = arena_.get<u64>("ekey", n2);
+    double* eval = arena_.get<double>("eval", n2);
+    u64* ekey_s = arena_.get<u64>(keep_delta ? "ekey_s" : "ekey_s_probe", n2);
+    double* eval_s = arena_.get<double>(keep_delta ? "eval_s" : "eval_s_probe", n2);
+    if (E > 0) {
+      launch(edit_check_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, pkey, pval, code, post);
+      size_t tmp = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, 64, st_);
+      void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+      cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, 64, st_);
+      launch(dup_mark_kernel, dim3(blocks(E)), dim3(256), 0, st_, static_cast<const u64*>(pkey_s),
+             static_cast<const i64*>(pval_s), E, dup);
+      launch(edit_emit_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, static_cast<const int*>(code),
+             static_cast<const int*>(dup), static_cast<const int*>(post), err_edit, ekey, eval, nvalid);
+      tmp = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, 64, st_);
+      t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+      cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, 64, st_);
+    }
+    // ---- Delta (global CSR over n_total rows)
+    const std::string sfx = keep_delta ? "" : "_probe";
+    int* drow = arena_.get<int>("drow" + sfx, n2);
+    int* dcol = arena_.get<int>("dcol" + sfx, n2);
+    int* dcnt = arena_.get<int>("dcnt", n_total + 1);
+    int* drp = arena_.get<int>("drp" + sfx, n_total + 1);
+    STG_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (n_total + 1), st_));
+    if (n2 > 0)
+      launch(delta_rows_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s), n2, drow, dcol,
+             dcnt, mark_delta_, stamp_);
+    scan_int(dcnt, drp, n_total + 1);
+    // ---- apply_update merge (A_next in the spare slot)
+    const DevCsr& a = A();
+    int* lb = arena_.get<int>("m_lb", n2);
+    int* mflag = arena_.get<int>("m_flag", n2);
+    double* newv = arena_.get<double>("m_newv", n2);
+    int* contrib = arena_.get<int>("m_contrib", n2 + 1);
+    int* prefix = arena_.get<int>("m_prefix", n2 + 1);
+    int* ncnt = arena_.get<int>("m_ncnt", n_total + 1);
+    const int slot = keep_delta ? 1 - acur_ : 2;  // probes never touch the live buffers
+    const std::string aname = "A" + std::to_string(slot);
+    DevCsr an;
+    an.n = n_total;
+    an.rp = arena_.get<int>(aname + ".rp", n_total + 1);
+    an.col = arena_.get<int>(aname + ".col", a.nnz + n2);
+    an.val = arena_.get<double>(aname + ".val", a.nnz + n2);
+    launch(row_len_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(a.rp), n_old, n_total,
+           ncnt);
+    STG_CUDA(cudaMemsetAsync(contrib, 0, sizeof(int) * (n2 + 1), st_));
+    if (n2 > 0)
+      launch(merge_classify_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s),
+             static_cast<const double*>(eval_s), n2, static_cast<const int*>(a.rp), static_cast<const int*>(a.col),
+             static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply);
+    scan_int(ncnt, an.rp, n_total + 1);
+    scan_int(contrib, prefix, n2 + 1);
+    kbegin(kMerge, 0.0);
+    const size_t merge_pend = pend_.size() - (ktiming() ? 1 : 0);
+    if (n_old > 0)
+      launch(merge_rows_kernel, dim3(blocks(n_old, 8)), dim3(256), 0, st_, static_cast<const int*>(a.rp),
+             static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
+             static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
+             static_cast<const int*>(dcol), static_cast<const int*>(mflag), static_cast<const double*>(newv),
+             static_cast<const int*>(prefix), static_cast<const int*>(an.rp), an.col, an.val);
+    if (n2 > 0)
+      launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, st_, n2, static_cast<const int*>(drow),
+             static_cast<const int*>(dcol), static_cast<const u64*>(ekey_s), static_cast<const int*>(lb),
+             static_cast<const int*>(mflag), static_cast<const double*>(newv), static_cast<const int*>(prefix),
+             static_cast<const int*>(drp), static_cast<const int*>(an.rp), an.col, an.val);
+    kend();
+    // ---- sync 1: validation outcome and sizes
+    STG_CUDA(cudaMemcpyAsync(&hs_->err_edit, err_edit, sizeof(u64) * 3, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&hs_->nnz_new, an.rp + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
+    if (hs_->err_apply != kSentinel) {
+      if (hs_->err_apply & 1ULL) throw InvalidArgument("apply_update: update drives an edge weight negative");
+      throw InvalidArgument("apply_update: invalid deletion (no such edge)");
+    }
+    an.nnz = hs_->nnz_new;
+    pt.nnz = static_cast<i64>(hs_->nvalid);
+    if (ktiming())  // read old CSR + write new CSR (SURVEY 8(d) ingestion bytes, edits excluded)
+      pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (n_old + 1) + 12.0 * an.nnz + 4.0 * (n_total + 1);
+    anext_ = slot;
+    A_[slot] = an;
+    // ---- the tracked operator's perturbation
+    const int* grp = drp;
+    const int* gcol = dcol;
+    const double* gval = eval_s;
+    if (is_laplacian()) {
+      const bool normalized = cfg.op == ST_NORMALIZED_LAPLACIAN;
+      double* deg = arena_.get<double>("deg", n_total + 1);
+      double* scale = arena_.get<double>("scale", n_total + 1);
+      launch(degrees_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const int*>(an.rp),
+             static_cast<const double*>(an.val), n_total, deg);
+      launch(max_reduce_kernel, dim3(1), dim3(1024), 0, st_, static_cast<const double*>(deg), n_total, d_alpha_ + 2);
+      launch(shift_kernel, dim3(1), dim3(1), 0, st_, normalized ? 1 : 0, static_cast<const double*>(d_alpha_ + 2),
+             static_cast<const double*>(d_alpha_), d_alpha_ + 1);
+      launch(scale_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const double*>(deg), n_total, scale);
+      const int ts = keep_delta ? 1 - tcur_ : 2;
+      DevCsr tn = build_t("T" + std::to_string(ts), an, n_total, normalized, deg, scale, d_alpha_ + 1);
+      tnext_ = ts;
+      T_[ts] = tn;
+      const DevCsr& to = T();
+      int* dtcnt = arena_.get<int>("dt_cnt", n_total + 1);
+      int* dtrp = arena_.get<int>("dt_rp" + sfx, n_total + 1);
+      launch(lap_diff_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(to.rp),
+             static_cast<const int*>(to.col), static_cast<const double*>(to.val), n_old,
+             static_cast<const int*>(tn.rp), static_cast<const int*>(tn.col), static_cast<const double*>(tn.val),
+             n_total, static_cast<const int*>(nullptr), dtcnt, static_cast<int*>(nullptr),
+             static_cast<double*>(nullptr), 0);
+      scan_int(dtcnt, dtrp, n_total + 1);
+      int nnz_dt = 0;
+      STG_CUDA(cudaMemcpyAsync(&hs_->nnz_dt, dtrp + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(&hs_->alpha, d_alpha_ + 1, sizeof(double), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      nnz_dt = hs_->nnz_dt;
+      alpha_next_ = hs_->alpha;
+      int* dtcol = arena_.get<int>("dt_col" + sfx, nnz_dt);
+      double* dtval = arena_.get<double>("dt_val" + sfx, nnz_dt);
+      launch(lap_diff_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(to.rp),
+             static_cast<const int*>(to.col), static_cast<const double*>(to.val), n_old,
+             static_cast<const int*>(tn.rp), static_cast<const int*>(tn.col), static_cast<const double*>(tn.val),
+             n_total, static_cast<const int*>(dtrp), dtcnt, dtcol, dtval, 1);
+      launch(mark_nonempty_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const int*>(dtrp), n_total,
+             mark_p_, stamp_);
+      grp = dtrp;
+      gcol = dtcol;
+      gval = dtval;
+      pt.nnz = nnz_dt;
+    } else {
+      // adjacency: P-marks are the Delta rows
+      if (n_total > 0)
+        STG_CUDA(cudaMemcpyAsync(mark_p_, mark_delta_, sizeof(int) * n_total, cudaMemcpyDeviceToDevice, st_));
+    }
+    if (S > 0)
+      launch(mark_range_kernel, dim3(blocks(S)), dim3(256), 0, st_, mark_p_, n_old, n_total, stamp_);
+    pt.grp = grp;
+    pt.gcol = gcol;
+    pt.val = gval;
+    // ---- P and the compressed CSR
+    int* flag = arena_.get<int>("p_flag", n_total + 1);
+    int* pos = arena_.get<int>("p_pos", n_total + 1);
+    int* P = arena_.get<int>("P", n_total + 1);
+    launch(flag_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(mark_p_), stamp_, n_total,
+           flag);
+    scan_int(flag, pos, n_total + 1);
+    launch(scatter_p_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const int*>(flag),
+           static_cast<const int*>(pos), n_total, P, posmap_);
+    STG_CUDA(cudaMemcpyAsync(&hs_->p, pos + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    pt.p = hs_->p;
+    pt.p_old = pt.p - S;
+    pt.P = P;
+    pt.posmap = posmap_;
+    pt.mark = mark_p_;
+    if ((cfg.flags & ST_FLAG_FORCE_DENSE) || 2 * pt.p > n_total) {
+      make_dense(pt);
+    } else {
+      int* lrp = arena_.get<int>("lrp", pt.p + 1);
+      int* lcol = arena_.get<int>("lcol", pt.nnz);
+      launch(compress_rowptr_kernel, dim3(blocks(pt.p + 1)), dim3(256), 0, st_, grp, static_cast<const int*>(P), pt.p,
+             lrp, static_cast<int>(pt.nnz));
+      if (pt.nnz > 0)
+        launch(compress_cols_kernel, dim3(blocks(pt.nnz)), dim3(256), 0, st_, gcol, pt.nnz,
+               static_cast<const int*>(posmap_), lcol);
+      pt.lrp = lrp;
+      pt.lcol = lcol;
+    }
+    return pt;
+  }
+
+  void make_dense(Pert& pt) {
+    pt.dense = true;
+    pt.p = pt.n_total;
+    pt.p_old = pt.n_old;
+    pt.lrp = pt.grp;
+    pt.lcol = pt.gcol;
+  }
+
+  void commit_graph(const Pert& pt) {
+    if (anext_ >= 0) {
+      acur_ = anext_;
+      anext_ = -1;
+    }
+    if (is_laplacian() && tnext_ >= 0) {
+      tcur_ = tnext_;
+      tnext_ = -1;
+      alpha = alpha_next_;
+      STG_CUDA(cudaMemcpyAsync(d_alpha_, d_alpha_ + 1, sizeof(double), cudaMemcpyDeviceToDevice, st_));
+    }
+    last_delta_.rp = const_cast<int*>(pt.grp);
+    last_delta_.col = const_cast<int*>(pt.gcol);
+    last_delta_.val = const_cast<double*>(pt.val);
+    last_delta_nnz_ = pt.nnz;
+    last_delta_n_ = pt.n_total;
+    n = pt.n_total;
+    // rows appended to X are zero until the rotation writes them (padded_vectors)
+  }
+
+  // ---------------------------------------------------------------- orthonormalize
+  // ortho.hpp:13-39 on the stacked coordinates: BCGS2 + CholQR2 when every
+  // column is clearly independent, the exact column-by-column MGS2 replica when
+  // a pivot is suspect. W (N x w) is consumed; Q is written to `out`.
+  int orthonormalize(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out) {
+    if (w == 0) return 0;
+    const int ldw = ld_for(w);
+    double* W1 = arena_.get<double>("on_W1", N * ldw);
+    double* C = arena_.get<double>("on_C", static_cast<i64>(std::max(a, 1)) * ldw);
+    double* Gm = arena_.get<double>("on_G", static_cast<i64>(w) * ldw);
+    double* R = arena_.get<double>("on_R", static_cast<i64>(w) * ldw);
+    double* Ri = arena_.get<double>("on_Ri", static_cast<i64>(w) * ldw);
+    double* o2 = arena_.get<double>("on_o2", w);
+    // pass 1
+    if (against && a > 0) {
+      gram(against->p, against->ld, W.p, W.ld, G, a, w, false, C, ldw);
+      nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, W.p, W.ld);
+    } else {
+      launch(copy2d_kernel, dim3(blocks(N * w)), dim3(256), 0, st_, static_cast<const double*>(W.p), W.ld, W1, ldw, N,
+             w);
+    }
+    gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
+    launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw,
+           static_cast<const double*>(C), ldw, (against ? a : 0), w, o2);
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    chol(Gm, ldw, w, R, ldw, o2, kSuspectTau2, false);
+    read_scalars();
+    if (hs_->flags & (kSuspect | kBreakdown)) return mgs2_exact(W, w, against, a, N, G, out);
+    triinv(R, ldw, w, Ri, ldw);
+    nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
+    // pass 2
+    if (against && a > 0) {
+      gram(against->p, against->ld, out.p, out.ld, G, a, w, false, C, ldw);
+      nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, out.p, out.ld);
+    } else {
+      launch(copy2d_kernel, dim3(blocks(N * w)), dim3(256), 0, st_, static_cast<const double*>(out.p), out.ld, W1, ldw,
+             N, w);
+    }
+    gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
+    chol(Gm, ldw, w, R, ldw, nullptr, 0.0, false);
+    triinv(R, ldw, w, Ri, ldw);
+    nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
+    return w;
+  }
+
+  static constexpr double kSuspectTau2 = 1e-10;  // residual / original norm below 1e-5
+
+  double host_norm_g(const double* v, int ldv, i64 G) {
+    double* g1 = arena_.get<double>("mgs_g1", 8);
+    gram(v, ldv, v, ldv, G, 1, 1, true, g1, 1);
+    double h = 0;
+    STG_CUDA(cudaMemcpyAsync(&h, g1, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    return std::sqrt(h);
+  }
+
+  // Exact replica of ortho.hpp:26-37, one column at a time.
+  int mgs2_exact(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out) {
+    const int ldv = 8;
+    double* v = arena_.get<double>("mgs_v", N * ldv);
+    double* t = arena_.get<double>("mgs_t", std::max(a, w) * ldv + 8);
+    int r = 0;
+    for (int c = 0; c < w; ++c) {
+      launch(copy2d_kernel, dim3(blocks(N)), dim3(256), 0, st_, static_cast<const double*>(W.p + c), W.ld, v, ldv, N, 1);
+      const double orig = host_norm_g(v, ldv, G);
+      if (orig == 0.0) continue;
+      for (int pass = 0; pass < 2; ++pass) {
+        if (against && a > 0) {
+          gram(against->p, against->ld, v, ldv, G, a, 1, false, t, ldv);
+          nn(against->p, against->ld, N, a, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
+        }
+        if (r > 0) {
+          gram(out.p, out.ld, v, ldv, G, r, 1, false, t, ldv);
+          nn(out.p, out.ld, N, r, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
+        }
+      }
+      const double nrm = host_norm_g(v, ldv, G);
+      if (nrm < 1e-10 * orig) continue;
+      double* sc = arena_.get<double>("mgs_scale", 8);
+      const double inv = 1.0 / nrm;
+      STG_CUDA(cudaMemcpyAsync(sc, &inv, sizeof(double), cudaMemcpyHostToDevice, st_));
+      // out[:, r] = v / nrm  (as a 1x1 "GEMM" so it stays on the stream)
+      nn(v, ldv, N, 1, sc, 8, 1, out.p + r, out.ld, 1.0, 0.0, nullptr, 0);
+      STG_CUDA(cudaStreamSynchronize(st_));
+      ++r;
+    }
+    return r;
+  }
+
+  // ---------------------------------------------------------------- basis
+  // build_projection_basis (trackers.cpp:226-280) in stacked coordinates.
+  // Z columns [0, k) hold X-bar; returns Z with D columns.
+  Basis build_basis(const Pert& pt, int basis_kind, u64 seed) {
+    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const i64 S = pt.S;
+    const int kk = static_cast<int>(k);
+    // widths
+    int trail_max = 0;
+    bool rsvd = false;
+    int q = 0;
+    if (basis_kind == 0) {
+      trail_max = static_cast<int>(S);
+    } else if (basis_kind >= 2) {
+      const bool bypass = basis_kind == 2 || S <= cfg.rsvd_l;
+      if (bypass) {
+        trail_max = static_cast<int>(S);
+      } else {
+        rsvd = true;
+        q = static_cast<int>(std::min<i64>(S, cfg.rsvd_l + cfg.rsvd_p));
+        trail_max = static_cast<int>(std::min<i64>(cfg.rsvd_l, q));
+      }
+    }
+    const int wmax = (basis_kind == 0 ? 0 : kk) + trail_max;
+    const int ldz = ld_for(kk + wmax);
+    double* Z = arena_.get<double>("Z", N * ldz);
+    Blk z{Z, ldz};
+    // ---- RNG for the sketch starts first on its own stream
+    double* omega = nullptr;
+    int ldo = 0;
+    if (rsvd) {
+      ldo = ld_for(q);
+      omega = arena_.get<double>("omega", S * ldo);
+      const i64 npairs = cdiv(S * q, 2);
+      u64* raw = arena_.get<u64>("mt_raw", 2 * npairs);
+      const u64 rseed = mix_seed(seed, 0x5bdULL);
+      kbegin(kRng, 2.0 * npairs, st_rng_);
+      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, 2 * npairs, raw);
+      launch(box_muller_kernel, dim3(blocks(npairs)), dim3(256), 0, st_rng_, static_cast<const u64*>(raw), npairs, S,
+             q, omega, ldo);
+      kend(st_rng_);
+      STG_CUDA(cudaEventRecord(ev_rng_, st_rng_));
+    }
+    // ---- X-bar in stacked coordinates: [X_P; R_c; I]
+    build_xbar(pt, z);
+    if (basis_kind == 0) {
+      // iasc: [[X, 0], [0, I_S]] (trackers.cpp:233-238)
+      STG_CUDA(cudaMemset2DAsync(Z + kk, sizeof(double) * ldz, 0, sizeof(double) * S, N, st_));
+      if (S > 0)
+        launch(unit_cols_kernel, dim3(blocks(S)), dim3(256), 0, st_, Z + kk, ldz, pt.p_old, S);
+      return Basis{z, static_cast<int>(kk + S)};
+    }
+    // ---- candidates [(I - XX') Delta X | trailing]
+    const int ldc = ld_for(wmax);
+    double* cand = arena_.get<double>("cand", N * ldc);
+    STG_CUDA(cudaMemsetAsync(cand, 0, sizeof(double) * N * ldc, st_));
+    double* ck = arena_.get<double>("ck", static_cast<i64>(kk) * ld_for(std::max(q, std::max(trail_max, kk))));
+    // dx = Delta X (rows of P; the coordinate rows stay 0)
+    SpmmArgs sa{};
+    sa.rows = p;
+    sa.row_off = 0;
+    sa.rowptr = pt.lrp;
+    sa.col = pt.lcol;
+    sa.val = pt.val;
+    sa.X = Z;
+    sa.ldx = ldz;
+    sa.m = kk;
+    sa.Y = cand;
+    sa.ldy = ldc;
+    do_spmm(sa, pt.nnz, p);
+    gram(Z, ldz, cand, ldc, G, kk, kk, false, ck, ldc);
+    nn(Z, ldz, N, kk, ck, ldc, kk, cand, ldc, -1.0, 1.0, cand, ldc);
+    int w = kk;
+    if (basis_kind >= 2) {
+      if (!rsvd) {
+        // d2 dense: column j = Delta[:, n_old + j]; by symmetry row p_old + j of the local CSR
+        if (S > 0) {
+          launch(d2_dense_kernel, dim3(blocks(S, 8)), dim3(256), 0, st_, pt.lrp, pt.lcol, pt.val, pt.p_old, S,
+                 cand + kk, ldc);
+          const int lck = ld_for(S);
+          double* c2 = arena_.get<double>("c2", static_cast<i64>(kk) * lck);
+          gram(Z, ldz, cand + kk, ldc, G, kk, static_cast<int>(S), false, c2, lck);
+          nn(Z, ldz, N, kk, c2, lck, static_cast<int>(S), cand + kk, ldc, -1.0, 1.0, cand + kk, ldc);
+          w += static_cast<int>(S);
+        }
+      } else {
+        w += rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc});
+      }
+    }
+    // ---- extra = orthonormalize(candidates, X-bar) written next to X-bar
+    const int wq = orthonormalize(Blk{cand, ldc}, w, &z, kk, N, G, Blk{Z + kk, ldz});
+    return Basis{z, kk + wq};
+  }
+
+  // rsvd_basis (rsvd.hpp:34-66) with the closures of trackers.cpp:256-267.
+  int rsvd_trailing(const Pert& pt, Blk z, int q, const double* omega, int ldo, Blk out) {
+    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const int kk = static_cast<int>(k);
+    const int ldy = ld_for(q);
+    double* Y = arena_.get<double>("Y", N * ldy);
+    STG_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * N * ldy, st_));
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_rng_, 0));
+    // Y0 = d2 * Omega: nonzeros of Delta in the appended-node columns
+    SpmmArgs sa{};
+    sa.rows = p;
+    sa.rowptr = pt.lrp;
+    sa.col = pt.lcol;
+    sa.val = pt.val;
+    sa.col_lo = static_cast<int>(pt.p_old);
+    sa.X = omega - pt.p_old * ldo;
+    sa.ldx = ldo;
+    sa.m = q;
+    sa.Y = Y;
+    sa.ldy = ldy;
+    do_spmm(sa, pt.nnz, pt.S, kSpmmSketch);
+    double* cy = arena_.get<double>("cy", static_cast<i64>(kk) * ldy);
+    gram(z.p, z.ld, Y, ldy, G, kk, q, false, cy, ldy);
+    nn(z.p, z.ld, N, kk, cy, ldy, q, Y, ldy, -1.0, 1.0, Y, ldy);
+    // M = orthonormalize(Y)
+    double* M = arena_.get<double>("Msk", N * ldy);
+    const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy});
+    if (qm == 0) return 0;
+    // bt_m = d2' (M - X (X'M)): rows of the appended nodes times the projected M
+    double* cm = arena_.get<double>("cm", static_cast<i64>(kk) * ldy);
+    gram(z.p, z.ld, M, ldy, G, kk, qm, false, cm, ldy);
+    double* Mp = arena_.get<double>("Mp", p * ldy);
+    nn(z.p, z.ld, p, kk, cm, ldy, qm, Mp, ldy, -1.0, 1.0, M, ldy);
+    double* btm = arena_.get<double>("btm", pt.S * ldy);
+    SpmmArgs sb{};
+    sb.rows = pt.S;
+    sb.row_off = pt.p_old;
+    sb.rowptr = pt.lrp;
+    sb.col = pt.lcol;
+    sb.val = pt.val;
+    sb.X = Mp;
+    sb.ldx = ldy;
+    sb.m = qm;
+    sb.Y = btm;
+    sb.ldy = ldy;
+    do_spmm(sb, pt.nnz, p, kSpmmSketch);
+    // thin U of (M'B) = eigenvectors of bt_m' bt_m, singular values descending
+    double* gb = arena_.get<double>("gb", static_cast<i64>(qm) * ldy);
+    gram(btm, ldy, btm, ldy, pt.S, qm, qm, true, gb, ldy);
+    double *w = nullptr, *V = nullptr;
+    eig(gb, ldy, qm, &w, &V, "sk");
+    std::vector<double> lam(static_cast<size_t>(qm));
+    STG_CUDA(cudaMemcpyAsync(lam.data(), w, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
+    read_scalars();
+    if (hs_->info != 0) throw RuntimeError("rsvd_basis: SVD did not converge");
+    // rank: sv(r) > 1e-10 sv(0) and > 0 (rsvd.hpp:59-62)
+    std::vector<double> sv(static_cast<size_t>(qm));
+    for (int i = 0; i < qm; ++i) sv[i] = std::sqrt(std::max(lam[static_cast<size_t>(qm - 1 - i)], 0.0));
+    const double cutoff = qm > 0 ? 1e-10 * sv[0] : 0.0;
+    int rank = 0;
+    while (rank < qm && sv[rank] > cutoff && sv[rank] > 0.0) ++rank;
+    const int keep = static_cast<int>(std::min<i64>(cfg.rsvd_l, rank));
+    if (keep == 0) return 0;
+    const int ldu = ld_for(keep);
+    double* U = arena_.get<double>("Ukeep", static_cast<i64>(qm) * ldu);
+    launch(gather_desc_kernel, dim3(blocks(static_cast<i64>(qm) * keep)), dim3(256), 0, st_,
+           static_cast<const double*>(V), qm, keep, U, ldu);
+    // R = M U_keep
+    nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+    return keep;
+  }
+
+  void build_xbar(const Pert& pt, Blk z) {
+    const i64 p = pt.p;
+    const int kk = static_cast<int>(k);
+    double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ld_for(kk));
+    if (!pt.dense) {
+      double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ld_for(kk));
+      gram(X_, ldx(), X_, ldx(), pt.n_old, kk, kk, true, kc, ld_for(kk), 1.0, pt.mark, pt.stamp);
+      chol(kc, ld_for(kk), kk, rc, ld_for(kk), nullptr, 0.0, true);
+    } else {
+      STG_CUDA(cudaMemsetAsync(rc, 0, sizeof(double) * kk * ld_for(kk), st_));
+    }
+    launch(gather_xbar_kernel, dim3(blocks((p + 2 * k) * k)), dim3(256), 0, st_, static_cast<const double*>(X_), ldx(),
+           pt.P, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(rc), ld_for(kk), z.p, z.ld);
+  }
+
+  // ---------------------------------------------------------------- Rayleigh-Ritz
+  // rayleigh_ritz_step (trackers.cpp:282-308). write_state: rotate X in place;
+  // otherwise expand the new vectors (dense mode only) into host `wout`.
+  void rayleigh_ritz(const Pert& pt, const Basis& b, std::vector<double>& newvals, bool write_state, double* wout,
+                     i64 wrows, Blk xbar_override = Blk{}) {
+    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const int D = b.D, kk = static_cast<int>(k);
+    const Blk xb = xbar_override.p ? xbar_override : b.z;
+    const int ldd = ld_for(D);
+    // Gram check (trackers.cpp:293-295)
+    double* gz = arena_.get<double>("rr_gz", static_cast<i64>(D) * ldd);
+    gram(b.z.p, b.z.ld, b.z.p, b.z.ld, G, D, D, true, gz, ldd);
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    launch(orthocheck_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_,
+           static_cast<const double*>(gz), ldd, D, 1e-6, flags_ptr());
+    // zx = Z' X-bar (D x k)
+    const int ldk = ld_for(kk);
+    double* zx = arena_.get<double>("rr_zx", static_cast<i64>(D) * ldk);
+    gram(b.z.p, b.z.ld, xb.p, xb.ld, G, D, kk, false, zx, ldk);
+    // dz = Delta Z (rows of P), T = Z_P' dz
+    double* dz = arena_.get<double>("rr_dz", p * ldd);
+    SpmmArgs sa{};
+    sa.rows = p;
+    sa.rowptr = pt.lrp;
+    sa.col = pt.lcol;
+    sa.val = pt.val;
+    sa.X = b.z.p;
+    sa.ldx = b.z.ld;
+    sa.m = D;
+    sa.Y = dz;
+    sa.ldy = ldd;
+    do_spmm(sa, pt.nnz, p);
+    double* tm = arena_.get<double>("rr_t", static_cast<i64>(D) * ldd);
+    gram(b.z.p, b.z.ld, dz, ldd, p, D, D, false, tm, ldd);
+    double* mm = arena_.get<double>("rr_m", static_cast<i64>(D) * ldd);
+    launch(rr_matrix_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_, static_cast<const double*>(zx),
+           ldk, static_cast<const double*>(d_values_), kk, static_cast<const double*>(tm), ldd, D, mm, ldd);
+    timing_mark(2);
+    double *w = nullptr, *V = nullptr;
+    eig(mm, ldd, D, &w, &V, "rr");
+    int* perm = arena_.get<int>("rr_perm", D);
+    launch(sort_perm_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(w), D, static_cast<int>(cfg.order),
+           perm);
+    double* F = arena_.get<double>("rr_F", static_cast<i64>(D) * ldk);
+    double* nv = arena_.get<double>("rr_vals", kk);
+    launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(D) * kk)), dim3(256), 0, st_,
+           static_cast<const double*>(V), D, static_cast<const double*>(w), static_cast<const int*>(perm), kk, F, ldk,
+           nv);
+    timing_mark(3);
+    // W = Z F (all stacked rows): rows of P -> new rows of X, a-rows -> A_new
+    double* W = arena_.get<double>("rr_W", N * ldk);
+    nn(b.z.p, b.z.ld, N, D, F, ldk, kk, W, ldk, 1.0, 0.0, nullptr, 0);
+    newvals.assign(static_cast<size_t>(kk), 0.0);
+    STG_CUDA(cudaMemcpyAsync(newvals.data(), nv, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
+    if (write_state) {
+      kbegin(kRotate, 16.0 * k * pt.n_total + 8.0 * pt.n_total);
+      launch(rotate_x_kernel, dim3(blocks(pt.n_total, 8)), dim3(256), 0, st_, X_, ldx(), pt.n_old, pt.n_total,
+             pt.dense ? 1 : 0, static_cast<const int*>(pt.mark), pt.stamp, static_cast<const int*>(pt.posmap),
+             static_cast<const double*>(W), ldk, static_cast<const double*>(W + (p + k) * ldk), kk,
+             static_cast<const int*>(flags_ptr()), static_cast<const int*>(info_ptr()));
+      kend();
+    }
+    read_scalars();
+    if (hs_->flags & kNonFinite) throw InvalidArgument("sym_eig_dense: non-finite entries");
+    if (hs_->flags & kNotOrthonormal) throw InvalidArgument("rayleigh_ritz_step: basis is not column-orthonormal");
+    if (hs_->info != 0) throw RuntimeError("sym_eig_dense: factorization did not converge");
+    if (write_state) {
+      STG_CUDA(cudaMemcpyAsync(d_values_, nv, sizeof(double) * kk, cudaMemcpyDeviceToDevice, st_));
+    } else if (wout) {
+      std::vector<double> tmp(static_cast<size_t>(wrows * kk));
+      STG_CUDA(cudaMemcpy2DAsync(tmp.data(), sizeof(double) * kk, W, sizeof(double) * ldk, sizeof(double) * kk, wrows,
+                                 cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      std::memcpy(wout, tmp.data(), sizeof(double) * wrows * kk);
+    }
+  }
+
+  // Dense n_total x D column-major expansion of a stacked basis (probes only).
+  void expand_dense(const Pert& pt, Blk z, int D, double* out, i64 ldo) {
+    const int ldd = ld_for(D);
+    double* dz = arena_.get<double>("expand", pt.n_total * ldd);
+    const double* arows = z.p + (pt.p + k) * z.ld;
+    launch(expand_kernel, dim3(blocks(pt.n_total, 8)), dim3(256), 0, st_, static_cast<const double*>(X_), ldx(),
+           pt.n_old, pt.n_total, pt.dense ? 1 : 0, static_cast<const int*>(pt.mark), pt.stamp,
+           static_cast<const int*>(pt.posmap), static_cast<const double*>(z.p), z.ld, arows, static_cast<int>(k), D, dz,
+           ldd);
+    std::vector<double> tmp(static_cast<size_t>(pt.n_total * D));
+    STG_CUDA(cudaMemcpy2DAsync(tmp.data(), sizeof(double) * D, dz, sizeof(double) * ldd, sizeof(double) * D,
+                               pt.n_total, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    for (int c = 0; c < D; ++c)
+      for (i64 i = 0; i < pt.n_total; ++i) out[c * ldo + i] = tmp[static_cast<size_t>(i * D + c)];
+  }
+
+};
+
+}  // namespace stg
+
+// ====================================================================== C ABI
+struct st_session {
+  std::unique_ptr<stg::Session> impl;
+  std::string err;
+};
+
+namespace {
+thread_local std::string g_create_error;
+
+template <class F>
+st_status guarded(st_session* s, F&& f) {
+  std::string* err = s ? &s->err : &g_create_error;
+  try {
+    f();
+    return ST_OK;
+  } catch (const std::invalid_argument& e) {
+    *err = e.what();
+    return ST_INVALID_ARGUMENT;
+  } catch (const stg::CudaError& e) {
+    *err = e.what();
+    return ST_CUDA_ERROR;
+  } catch (const std::runtime_error& e) {
+    *err = e.what();
+    return ST_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return ST_OTHER;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+st_status st_create(const st_config* cfg, int64_t n, const int32_t* rowptr, const int32_t* colidx,
+                    const double* values_csr, const double* eig_values, const double* eig_vectors, int64_t ld,
+                    st_session** out) {
+  return guarded(nullptr, [&] {
+    if (!cfg || !out || !rowptr || !eig_values || !eig_vectors) throw std::invalid_argument("st_create: null argument");
+    if (n < 1) throw std::invalid_argument("st_create: empty graph");
+    if (ld < n) throw std::invalid_argument("st_create: leading dimension below n");
+    auto s = std::make_unique<st_session>();
+    s->impl = std::make_unique<stg::Session>(*cfg, n, rowptr, colidx, values_csr, eig_values, eig_vectors, ld);
+    *out = s.release();
+  });
+}
+
+void st_destroy(st_session* s) { delete s; }
+
+st_status st_step(st_session* s, const st_update* upd) {
+  return guarded(s, [&] {
+    if (!upd) throw std::invalid_argument("st_step: null update");
+    s->impl->step(*upd);
+  });
+}
+
+st_status st_info(const st_session* s, int64_t* n, int64_t* k, uint64_t* steps_taken, int64_t* nnz_a,
+                  int64_t* nnz_t, int64_t* nnz_delta, double* alpha) {
+  const auto& m = *s->impl;
+  if (n) *n = m.n;
+  if (k) *k = m.k;
+  if (steps_taken) *steps_taken = m.steps_taken;
+  if (nnz_a) *nnz_a = m.A().nnz;
+  if (nnz_t) *nnz_t = m.is_laplacian() ? m.T().nnz : 0;
+  if (nnz_delta) *nnz_delta = m.nnz_delta();
+  if (alpha) *alpha = m.alpha;
+  return ST_OK;
+}
+
+st_status st_get_embedding(const st_session* s, double* values, double* vectors, int64_t ld) {
+  auto* ms = const_cast<st_session*>(s);
+  return guarded(ms, [&] {
+    if (ld < ms->impl->n) throw std::invalid_argument("st_get_embedding: leading dimension below n");
+    ms->impl->get_embedding(values, vectors, ld);
+  });
+}
+
+st_status st_get_values(const st_session* s, double* values) {
+  std::memcpy(values, s->impl->values.data(), sizeof(double) * s->impl->values.size());
+  return ST_OK;
+}
+
+st_status st_get_csr(const st_session* s, int32_t which, int32_t* rowptr, int32_t* colidx, double* values) {
+  auto* ms = const_cast<st_session*>(s);
+  return guarded(ms, [&] { ms->impl->get_csr(which, rowptr, colidx, values); });
+}
+
+st_status st_probe_basis(st_session* s, const st_update* upd, int32_t basis_kind, uint64_t seed, double* z,
+                         int64_t ld, int64_t max_cols, int64_t* cols) {
+  return guarded(s, [&] {
+    if (basis_kind < 0 || basis_kind > 3) throw std::invalid_argument("st_probe_basis: unknown basis kind");
+    *cols = s->impl->probe_basis(*upd, basis_kind, seed, z, ld, max_cols);
+  });
+}
+
+st_status st_probe_rr(st_session* s, const st_update* upd, const double* z, int64_t rows, int64_t cols, int64_t ldz,
+                      double* values, double* vectors, int64_t ldv) {
+  return guarded(s, [&] { s->impl->probe_rr(*upd, z, rows, cols, ldz, values, vectors, ldv); });
+}
+
+const char* st_last_error(const st_session* s) { return s ? s->err.c_str() : g_create_error.c_str(); }
+
+int32_t st_last_timings(const st_session* s, double* ms, int32_t cap) {
+  const auto& m = *s->impl;
+  const int32_t n = std::min<int32_t>(cap, m.ntimings);
+  for (int32_t i = 0; i < n; ++i) ms[i] = m.timings[i];
+  return n;
+}
+
+int64_t st_last_launches(const st_session* s) { return s->impl->launches; }
+
+st_status st_step_device(st_session* s, const st_update* upd) {
+  return guarded(s, [&] {
+    if (!upd) throw std::invalid_argument("st_step_device: null update");
+    s->impl->step(*upd, true);
+  });
+}
+
+int32_t st_kernel_stats(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work) {
+  if (cls < 0 || cls >= stg::Session::kClasses) return 0;
+  const auto& k = s->impl->kstats[cls];
+  *ms = k.ms;
+  *launches = k.launches;
+  *work = k.work;
+  return 1;
+}
+
+void st_reset_kernel_stats(st_session* s) { s->impl->kreset(); }
+
+}  // extern "C"

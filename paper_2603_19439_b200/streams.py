@@ -1,0 +1,217 @@
+"""Seeded synthetic graph streams for the BASELINE configs (harness, numpy only).
+
+The reference ships paper protocols (proj/src/dynamics.cpp) but no generators
+for the BASELINE configs (equal-block SBM, Erdos-Renyi, R-MAT, preferential
+attachment with deletions), so these are new. Every stream is a start graph
+plus a list of update batches in the edit-list form of assemble_update
+(proj/include/spectrack/graph.hpp:65-69); the CUDA path and the CPU oracle
+consume the identical batches.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import Update
+
+SHIFT = np.int64(1 << 32)
+
+
+def _keys(u, v):
+    lo, hi = np.minimum(u, v), np.maximum(u, v)
+    return lo.astype(np.int64) * SHIFT + hi.astype(np.int64)
+
+
+def _unkey(k):
+    return (k // SHIFT).astype(np.int64), (k % SHIFT).astype(np.int64)
+
+
+def csr_from_keys(n: int, keys: np.ndarray, weights: np.ndarray | None = None):
+    """Symmetric CSR (both triangles, sorted columns) from undirected pair keys."""
+    u, v = _unkey(keys)
+    w = np.ones(len(keys)) if weights is None else weights
+    rows = np.concatenate([u, v])
+    cols = np.concatenate([v, u])
+    vals = np.concatenate([w, w])
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = rows[order], cols[order], vals[order]
+    rowptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rowptr[1:])
+    return rowptr.astype(np.int32), cols.astype(np.int32), vals.astype(np.float64)
+
+
+def _sample_pairs_block(rng, lo_a, size_a, lo_b, size_b, p, same):
+    """Bernoulli(p) pairs between two node blocks (i < j inside one block)."""
+    total = size_a * (size_a - 1) // 2 if same else size_a * size_b
+    if total == 0 or p <= 0:
+        return np.zeros(0, np.int64)
+    m = rng.binomial(total, p)
+    idx = np.unique(rng.integers(0, total, size=int(m * 1.02) + 16))
+    while len(idx) < m:
+        idx = np.unique(np.concatenate([idx, rng.integers(0, total, size=m - len(idx) + 16)]))
+    idx = rng.permutation(idx)[:m]
+    if same:
+        # row-major upper-triangle index -> (i, j), i < j
+        i = (size_a - 2 - np.floor(np.sqrt(-8.0 * idx + 4.0 * size_a * (size_a - 1) - 7) / 2.0 - 0.5)).astype(np.int64)
+        j = idx + i + 1 - size_a * (size_a - 1) // 2 + (size_a - i) * ((size_a - i) - 1) // 2
+        return _keys(lo_a + i, lo_a + j)
+    i, j = idx // size_b, idx % size_b
+    return _keys(lo_a + i, lo_b + j)
+
+
+def sbm_keys(n: int, blocks: int, p_in: float, p_out: float, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    bounds = np.linspace(0, n, blocks + 1).astype(np.int64)
+    parts = []
+    for a in range(blocks):
+        for b in range(a, blocks):
+            parts.append(_sample_pairs_block(rng, bounds[a], bounds[a + 1] - bounds[a], bounds[b],
+                                             bounds[b + 1] - bounds[b], p_in if a == b else p_out, a == b))
+    return np.unique(np.concatenate(parts))
+
+
+def rmat_keys(scale: int, edge_factor: int, abcd=(0.57, 0.19, 0.19, 0.05), seed: int = 0) -> np.ndarray:
+    """R-MAT edges, symmetrized, self-loops dropped, deduplicated. Quadrant
+    probabilities are whole percentages, so each level draws one uint8 in
+    [0, 100) per edge and compares against the cumulative thresholds."""
+    rng = np.random.default_rng(seed)
+    m = edge_factor << scale
+    pa, pb, pc = (int(round(100 * x)) for x in abcd[:3])
+    t1, t2, t3 = pa, pa + pb, pa + pb + pc
+    u = np.zeros(m, np.int64)
+    v = np.zeros(m, np.int64)
+    for lvl in range(scale):
+        r = rng.integers(0, 100, size=m, dtype=np.uint8)
+        sh = scale - 1 - lvl
+        down = r >= t2                               # quadrants c, d: row bit
+        right = (r >= t1) ^ down ^ (r >= t3)         # quadrants b, d: column bit
+        u |= down.astype(np.int64) << sh
+        v |= right.astype(np.int64) << sh
+    keep = u != v
+    k = np.sort(_keys(u[keep], v[keep]))
+    return k[np.concatenate([[True], k[1:] != k[:-1]])] if len(k) else k
+
+
+@dataclass
+class Stream:
+    n0: int
+    keys0: np.ndarray
+    updates: list = field(default_factory=list)
+    name: str = ""
+
+    def csr0(self):
+        return csr_from_keys(self.n0, self.keys0)
+
+
+class _EdgeSet:
+    """Sorted undirected key set with degrees, evolved batch by batch."""
+
+    def __init__(self, n, keys):
+        self.n = n
+        self.keys = np.sort(keys)
+        u, v = _unkey(self.keys)
+        self.deg = np.bincount(np.concatenate([u, v]), minlength=n).astype(np.int64)
+
+    def has(self, k):
+        pos = np.searchsorted(self.keys, k)
+        pos = np.minimum(pos, len(self.keys) - 1)
+        return self.keys[pos] == k if len(self.keys) else np.zeros(len(k), bool)
+
+    def sample_existing(self, rng, count):
+        idx = np.unique(rng.integers(0, len(self.keys), size=count + count // 8 + 16))
+        while len(idx) < count:
+            idx = np.unique(np.concatenate([idx, rng.integers(0, len(self.keys), size=count)]))
+        return self.keys[rng.permutation(idx)[:count]]
+
+    def sample_by_degree(self, rng, size):
+        cum = np.cumsum(self.deg)
+        if cum[-1] == 0:
+            return rng.integers(0, self.n, size=size)
+        return np.searchsorted(cum, rng.integers(0, cum[-1], size=size), side="right")
+
+    def sample_absent(self, rng, count, forbid=None):
+        out = np.zeros(0, np.int64)
+        while len(out) < count:
+            u = rng.integers(0, self.n, size=2 * (count - len(out)) + 16)
+            v = rng.integers(0, self.n, size=len(u))
+            ok = u != v
+            k = np.unique(_keys(u[ok], v[ok]))
+            k = k[~self.has(k)]
+            if forbid is not None and len(forbid):
+                k = k[~np.isin(k, forbid)]
+            out = np.unique(np.concatenate([out, k]))
+        return rng.permutation(out)[:count]
+
+    def apply(self, added, removed, n_new, new_keys):
+        keep = np.ones(len(self.keys), bool)
+        keep[np.searchsorted(self.keys, removed)] = False
+        self.keys = np.sort(np.concatenate([self.keys[keep], added, new_keys]))
+        self.n += n_new
+        deg = np.zeros(self.n, np.int64)
+        deg[: len(self.deg)] = self.deg
+        ru, rv = _unkey(removed)
+        au, av = _unkey(np.concatenate([added, new_keys]))
+        deg -= np.bincount(np.concatenate([ru, rv]), minlength=self.n)
+        deg += np.bincount(np.concatenate([au, av]), minlength=self.n)
+        self.deg = deg
+
+
+def _update(added_keys, removed_keys, n_new, new_keys) -> Update:
+    ai, aj = _unkey(added_keys)
+    ri, rj = _unkey(removed_keys)
+    ni, nj = _unkey(new_keys)
+    return Update((ai, aj, np.ones(len(ai))), (ri, rj), int(n_new), (ni, nj, np.ones(len(ni))))
+
+
+def edit_stream(n0, keys0, steps, seed, insert, delete, new_nodes=0, new_degree=0, name="") -> Stream:
+    """Generic stream: per step `insert(m)` new edges among existing nodes
+    (uniform over non-edges), `delete(m)` uniform existing edges, and
+    `new_nodes(n)` appended nodes with `new_degree` distinct preferential-
+    attachment edges each (targets drawn proportional to pre-step degree)."""
+    rng = np.random.default_rng(seed)
+    es = _EdgeSet(n0, keys0)
+    s = Stream(n0, es.keys.copy(), name=name)
+    for _ in range(steps):
+        m = len(es.keys)
+        n_ins, n_del = int(insert(m)), int(delete(m))
+        S = int(new_nodes(es.n)) if callable(new_nodes) else int(new_nodes)
+        removed = es.sample_existing(rng, n_del) if n_del else np.zeros(0, np.int64)
+        added = es.sample_absent(rng, n_ins, forbid=removed) if n_ins else np.zeros(0, np.int64)
+        new_keys = np.zeros(0, np.int64)
+        if S and new_degree:
+            tgt = es.sample_by_degree(rng, S * new_degree).reshape(S, new_degree)
+            for _r in range(64):  # redraw repeated targets of one newcomer
+                srt = np.sort(tgt, axis=1)
+                dup = np.zeros_like(tgt, dtype=bool)
+                dup[:, 1:] = srt[:, 1:] == srt[:, :-1]
+                if not dup.any():
+                    break
+                tgt = srt
+                tgt[dup] = es.sample_by_degree(rng, int(dup.sum()))
+            newcomers = es.n + np.repeat(np.arange(S), new_degree)
+            new_keys = np.unique(_keys(tgt.reshape(-1), newcomers))
+        s.updates.append(_update(added, removed, S, new_keys))
+        es.apply(added, removed, S, new_keys)
+    return s
+
+
+# ---------------------------------------------------------------- BASELINE configs
+def config1(seed=1, n=10_000, steps=10):
+    """SBM n=10,000, 4 equal blocks, p_in=0.01, p_out=0.001; 500 inserts + 100 deletes per step."""
+    keys = sbm_keys(n, 4, 0.01, 0.001, seed)
+    return edit_stream(n, keys, steps, seed + 1, lambda m: 500, lambda m: 100, name="cfg1-sbm10k")
+
+
+def config2(seed=2, n=100_000, avg_deg=20, steps=20):
+    """Erdos-Renyi n=100,000, average degree 20; 1% inserts, 0.5% deletes (of edges) per step."""
+    keys = sbm_keys(n, 1, avg_deg / (n - 1), 0.0, seed)
+    return edit_stream(n, keys, steps, seed + 1, lambda m: 0.01 * m, lambda m: 0.005 * m, name="cfg2-er100k")
+
+
+def config3(seed=3, scale=20, steps=10, edge_factor=16):
+    """R-MAT scale 20, ef 16; per step 1% new nodes x 10 PA edges and 0.5% edge deletions."""
+    keys = rmat_keys(scale, edge_factor, seed=seed)
+    n = 1 << scale
+    return edit_stream(n, keys, steps, seed + 1, lambda m: 0, lambda m: 0.005 * m,
+                       new_nodes=lambda nn: nn // 100, new_degree=10, name=f"cfg3-rmat-s{scale}")

@@ -1,0 +1,182 @@
+"""Parity of the CUDA path (C ABI) against the CPU oracle on identical seeded
+inputs: CSR/Delta bit-exact, Ritz values within 1e-10, spans within 1e-8."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from harness import SIN_TOL, VALUE_RTOL, check_state, edges_of, pair, random_update, sin_angle, value_err
+from support import random_graph, span_residual
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_known_answers.json")))
+
+
+def U(*a, **k):
+    from paper_2603_19439_b200 import Update
+    return Update.make(*a, **k)
+
+
+def test_fig1_known_answer_bitwise():
+    g0 = GOLD["fig1"]
+    a0 = po.from_edges(6, g0["a0_edges"])
+    gpu, orc = pair(a0.rowptr, a0.col, a0.val, kind="grest2", k=2)
+    u = g0["update"]
+    upd = U(u["added"], u["removed"], u["n_new"], u["new_edges"])
+    gpu.step(upd)
+    orc.step(upd)
+    rp, col, val = gpu.csr(0)
+    gold = g0["a1"]
+    assert rp.tolist() == gold["rowptr"] and col.tolist() == gold["col"] and val.tolist() == gold["val"]
+    rp, col, val = gpu.csr(2)
+    gold = g0["delta"]
+    assert rp.tolist() == gold["rowptr"] and col.tolist() == gold["col"] and val.tolist() == gold["val"]
+    check_state(gpu, orc, tag="fig1")
+
+
+@pytest.mark.parametrize("upd,msg", [
+    (dict(added=[(0, 1, 1.0)], removed=[(0, 1)]), "duplicate edge"),
+    (dict(added=[(2, 2, 1.0)]), "self-loop"),
+    (dict(added=[(0, 9, 1.0)]), "existing nodes"),
+    (dict(n_new=1, new_edges=[(0, 1, 1.0)]), "only existing"),
+    (dict(n_new=1, new_edges=[(0, 7, -1.0)]), "positive weight"),
+    (dict(added=[(0, 1, 0.0)]), "zero-weight"),
+    (dict(n_new=1, new_edges=[(0, 9, 1.0)]), "out of range"),
+    (dict(added=[(3, 4, 1.0), (0, 5, 0.0), (1, 1, 1.0)]), "zero-weight"),          # first error wins
+    (dict(added=[(1, 1, 1.0), (0, 5, 0.0)]), "self-loop"),
+    (dict(removed=[(0, 3)]), "invalid deletion"),                                # apply_update
+])
+def test_errors_match_reference_and_leave_state(upd, msg):
+    a = random_graph(7, 0.4, 21)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest3", k=2)
+    v0, x0 = gpu.embedding()
+    a0 = gpu.csr(0)
+    upd = U(**upd)
+    with pytest.raises(po.OracleError) as eo:
+        orc.step(upd)
+    from paper_2603_19439_b200 import TrackerError
+    with pytest.raises(TrackerError) as eg:
+        gpu.step(upd)
+    assert msg in str(eo.value) and str(eg.value) == str(eo.value) and eg.value.kind == eo.value.kind
+    v1, x1 = gpu.embedding()
+    assert np.array_equal(v0, v1) and np.array_equal(x0, x1)
+    assert all(np.array_equal(p, q) for p, q in zip(a0, gpu.csr(0)))
+    assert gpu.info()["steps_taken"] == 0
+
+
+def test_negative_weight_deletion():
+    a = po.from_edges(3, [(0, 1, 0.5), (1, 2, 1.0)])
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest2", k=1)
+    from paper_2603_19439_b200 import TrackerError
+    with pytest.raises(TrackerError, match="negative"):
+        gpu.step(U(removed=[(0, 1)]))
+
+
+@pytest.mark.parametrize("kind,L,P", [("grest2", 100, 100), ("grest3", 100, 100), ("grest-rsvd", 4, 3),
+                                      ("grest-rsvd", 100, 100), ("iasc", 100, 100)])
+@pytest.mark.parametrize("dense", [False, True])
+def test_random_stream_parity(kind, L, P, dense):
+    rng = np.random.default_rng(5)
+    n = 160
+    a = random_graph(n, 0.05, 31)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind=kind, k=6, rsvd_l=L, rsvd_p=P, seed=3, force_dense=dense)
+    for t in range(4):
+        cur = gpu.info()["n"]
+        upd = random_update(rng, edges_of(gpu.csr(0)), cur, 6, 3, 9 if t % 2 == 0 else 0, 3)
+        gpu.step(upd)
+        orc.step(upd)
+        check_state(gpu, orc, tag=f"{kind} step {t}")
+
+
+def test_empty_update_is_identity():
+    a = random_graph(24, 0.2, 3)
+    for kind in ("iasc", "grest2", "grest3", "grest-rsvd"):
+        gpu, orc = pair(a.rowptr, a.col, a.val, kind=kind, k=4)
+        v0, x0 = gpu.embedding()
+        gpu.step(U())
+        v1, x1 = gpu.embedding()
+        assert np.array_equal(v0, v1) and np.array_equal(x0, x1)
+        assert gpu.info()["steps_taken"] == 1 and gpu.info()["n"] == 24
+
+
+@pytest.mark.parametrize("basis", ["iasc", "grest2", "grest3", "grest-rsvd"])
+def test_probe_basis_spans_match(basis):
+    a = random_graph(40, 0.15, 12)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest3", k=3, rsvd_l=2, rsvd_p=2)
+    upd = U([(0, 4, 1.0), (1, 5, 1.0)], [], 3, [(2, 40, 1.0), (3, 41, 1.0), (6, 42, 1.0), (40, 41, 1.0),
+                                                 (9, 42, 1.0)])
+    zg = gpu.probe_basis(upd, basis, 5)
+    zo = orc.probe_basis(upd, basis, 5)
+    assert zg.shape == zo.shape
+    assert np.abs(zg.T @ zg - np.eye(zg.shape[1])).max() <= 1e-10
+    assert span_residual(zg, zo) <= 1e-8 and span_residual(zo, zg) <= 1e-8
+    _, x = gpu.embedding()
+    assert np.allclose(zg[:40, :3], x, atol=0, rtol=0)  # Z[:, :k] == X-bar bitwise (test_projection.cpp:68)
+
+
+def test_probe_rr_exact_on_invariant_subspace_and_validation():
+    a = random_graph(8, 0.5, 14)
+    up = U([(0, 5, 1.0)], [], 2, [(3, 8, 1.0), (6, 9, 1.0), (8, 9, 1.0)])
+    a_next = po.apply_update(a, up)
+    w, v = po.sym_eig(a_next.dense(), 0)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest2", k=8)
+    vals, vecs = gpu.probe_rr(up, v[:, :8])
+    assert value_err(vals, w[:8]) <= 1e-9
+    assert sin_angle(vecs, v[:, :8]) <= 1e-7
+    ov, ox = orc.probe_rr(up, v[:, :8])
+    assert value_err(vals, ov) <= VALUE_RTOL and sin_angle(vecs, ox) <= SIN_TOL
+    from paper_2603_19439_b200 import TrackerError
+    b = random_graph(10, 0.3, 16)
+    gpu, _ = pair(b.rowptr, b.col, b.val, kind="grest2", k=4)
+    u2 = U([(0, 3, 1.0)])
+    with pytest.raises(TrackerError, match="projection subspace too small"):
+        gpu.probe_rr(u2, np.eye(10, 3))
+    skew = np.eye(10, 5)
+    skew[0, 1] = 0.5
+    with pytest.raises(TrackerError, match="column-orthonormal"):
+        gpu.probe_rr(u2, skew)
+    with pytest.raises(TrackerError, match="row count"):
+        gpu.probe_rr(u2, np.eye(9, 5))
+
+
+@pytest.mark.parametrize("op", ["normalized-laplacian", "laplacian"])
+def test_laplacian_sessions_bitwise_and_parity(op):
+    rng = np.random.default_rng(9)
+    n = 120
+    a = random_graph(n, 0.06, 44)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest3", k=5, order="alg_desc", operator=op)
+    assert gpu.info()["alpha"] == orc.info()[3]
+    for t in range(4):
+        cur = gpu.info()["n"]
+        upd = random_update(rng, edges_of(gpu.csr(0)), cur, 8, 4, 3, 2)
+        gpu.step(upd)
+        orc.step(upd)
+        check_state(gpu, orc, laplacian=True, tag=f"{op} step {t}")
+        assert gpu.info()["alpha"] == orc.info()[3]
+
+
+def test_config1_parity_all_steps():
+    from paper_2603_19439_b200 import streams
+    s = streams.config1()
+    rp, col, val = s.csr0()
+    gpu, orc = pair(rp, col, val, kind="grest-rsvd", k=8, seed=0)
+    for t, upd in enumerate(s.updates):
+        gpu.step(upd)
+        orc.step(upd)
+        check_state(gpu, orc, tag=f"cfg1 step {t}")
+
+
+def test_rsvd_path_rmat_parity():
+    from paper_2603_19439_b200 import streams
+    keys = streams.rmat_keys(14, 16, seed=7)
+    s = streams.edit_stream(1 << 14, keys, 2, 8, lambda m: 0, lambda m: 0.005 * m,
+                            new_nodes=lambda nn: nn // 100, new_degree=10)
+    rp, col, val = s.csr0()
+    gpu, orc = pair(rp, col, val, kind="grest-rsvd", k=8, seed=11)
+    for t, upd in enumerate(s.updates):
+        assert upd.n_new > 100  # exercises the randomized range finder
+        gpu.step(upd)
+        orc.step(upd)
+        check_state(gpu, orc, tag=f"rmat14 step {t}")
