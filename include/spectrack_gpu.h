@@ -141,6 +141,15 @@ int32_t st_last_timings(const st_session* s, double* ms, int32_t cap);
 /* Kernel launches issued by the last st_step (counted by the library). */
 int64_t st_last_launches(const st_session* s);
 
+/* Standalone device replacements for two reference kernels (no session):
+ * sym_eig_dense (eig.hpp:37-50): eigenvalues of (S + S')/2 in spectral order
+ * and the leading `want` eigenvectors (n x want column-major), n <= 232;
+ * GaussianSampler(seed).gaussian_matrix(rows, cols) (rng.hpp:64-69),
+ * column-major. */
+st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, int32_t order, int64_t want,
+                           double* values, double* vectors);
+st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_t cols, double* out_colmajor);
+
 /* Accumulated device time (ms), launch count and algorithmic work of one
  * kernel class since the last reset (ST_FLAG_KERNEL_TIMING). Classes: 0 DMMA
  * Gram (flops), 1 DMMA row-local GEMM (flops), 2 CSR SpMM Delta.X / Delta.Z

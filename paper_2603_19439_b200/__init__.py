@@ -86,6 +86,10 @@ def lib():
         L.st_kernel_stats.restype = C.c_int32
         L.st_reset_kernel_stats.argtypes = [C.c_void_p]
         L.st_reset_kernel_stats.restype = None
+        L.st_sym_eig_dense.argtypes = [C.c_int32, I64, DP, C.c_int32, I64, DP, DP]
+        L.st_sym_eig_dense.restype = C.c_int
+        L.st_gaussian_matrix.argtypes = [C.c_int32, C.c_uint64, I64, I64, DP]
+        L.st_gaussian_matrix.restype = C.c_int
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
                   "st_probe_basis", "st_probe_rr"):
             getattr(L, f).restype = C.c_int
@@ -260,6 +264,30 @@ class TrackerSession:
 
     def launches(self) -> int:
         return int(lib().st_last_launches(self._h))
+
+
+def sym_eig_dense(s: np.ndarray, order: str = "abs_desc", want: int | None = None, device: int = 0):
+    """Device sym_eig_dense (eig.hpp:37-50): eigenvalues of (S + S')/2 in
+    spectral order and the leading `want` eigenvectors (columns)."""
+    n = s.shape[0]
+    want = n if want is None else want
+    sf = np.asfortranarray(np.asarray(s, np.float64))
+    vals = np.zeros(n)
+    vecs = np.zeros((n, max(want, 1)), order="F")
+    rc = lib().st_sym_eig_dense(device, n, sf.ctypes.data_as(DP), ORDER[order], want, _p(vals),
+                                vecs.ctypes.data_as(DP))
+    if rc != ST_OK:
+        raise TrackerError(_KINDS.get(rc, "other"), lib().st_last_error(None).decode())
+    return vals, np.ascontiguousarray(vecs[:, :want])
+
+
+def gaussian_matrix(seed: int, rows: int, cols: int, device: int = 0) -> np.ndarray:
+    """Device GaussianSampler(seed).gaussian_matrix(rows, cols) (rng.hpp:64-69)."""
+    out = np.zeros((rows, cols), order="F")
+    rc = lib().st_gaussian_matrix(device, seed, rows, cols, out.ctypes.data_as(DP))
+    if rc != ST_OK:
+        raise TrackerError(_KINDS.get(rc, "other"), lib().st_last_error(None).decode())
+    return np.ascontiguousarray(out)
 
 
 class DeviceUpdate:

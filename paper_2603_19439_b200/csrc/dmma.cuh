@@ -59,7 +59,100 @@ __device__ __forceinline__ void load_k_tile(double (*s)[SST], const double* g, i
   }
 }
 
-__global__ void __launch_bounds__(NT) gram_tn_kernel(GramArgs a) {
+// 32 rows per stage (8 DMMA k-steps between barriers), double-buffered in
+// dynamic shared memory. Tiles entirely inside the matrix take the FULL path
+// with no per-subtile predicates, so the unrolled k-loop schedules freely.
+constexpr int BK2 = 32;
+constexpr size_t kGramSmem = sizeof(double) * 2 * 2 * BK2 * SST;
+
+__device__ __forceinline__ void load_k_tile32r(double* s, const double* g, int ld, i64 r, i64 rend, int c0, int m,
+                                               const int* mask, int mask_val) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = threadIdx.x + NT * q;  // 1024 chunks: 32 rows x 32 pairs
+    const int row = c >> 5, col = (c & 31) * 2;
+    i64 gr = r + row;
+    const int gc = c0 + col;
+    double* dst = s + row * SST + col;
+    if (mask && gr < rend && mask[gr] == mask_val) gr = rend;
+    if (gr < rend && gc + 2 <= m) {
+      cp_async_pair(dst, g + gr * ld + gc);
+    } else {
+      dst[0] = (gr < rend && gc < m) ? g[gr * ld + gc] : 0.0;
+      dst[1] = (gr < rend && gc + 1 < m) ? g[gr * ld + gc + 1] : 0.0;
+    }
+  }
+}
+
+template <bool FULL>
+__device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64 r0, i64 r1, double* smem) {
+  double* sA = smem;                   // [2][BK2][SST]
+  double* sB = smem + 2 * BK2 * SST;   // [2][BK2][SST]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int ibase = ti * BM + wm * 32, jbase = tj * BN + wn * 32;
+  bool vi[4], vj[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    vi[x] = FULL || ibase + x * 8 < a.m1;
+    vj[x] = FULL || jbase + x * 8 < a.m2;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const i64 nchunks = r1 > r0 ? cdiv(r1 - r0, BK2) : 0;
+  if (nchunks > 0) {
+    load_k_tile32r(sA, a.A, a.lda, r0, r1, ti * BM, a.m1, a.mask, a.mask_val);
+    load_k_tile32r(sB, a.B, a.ldb, r0, r1, tj * BN, a.m2, a.mask, a.mask_val);
+    cp_async_commit();
+  }
+  for (i64 c = 0; c < nchunks; ++c) {
+    const int s = c & 1;
+    if (c + 1 < nchunks) {
+      load_k_tile32r(sA + (s ^ 1) * BK2 * SST, a.A, a.lda, r0 + (c + 1) * BK2, r1, ti * BM, a.m1, a.mask,
+                     a.mask_val);
+      load_k_tile32r(sB + (s ^ 1) * BK2 * SST, a.B, a.ldb, r0 + (c + 1) * BK2, r1, tj * BN, a.m2, a.mask,
+                     a.mask_val);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* pa = sA + s * BK2 * SST + t * SST + wm * 32 + g;
+    const double* pb = sB + s * BK2 * SST + t * SST + wn * 32 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK2; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = pa[kk * SST + x * 8];
+        fb[x] = pb[kk * SST + x * 8];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (FULL || (vi[x] && vj[y])) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+    }
+    __syncthreads();
+  }
+  const i64 m1p = static_cast<i64>(a.tiles_i) * BM, m2p = static_cast<i64>(a.tiles_j) * BN;
+  double* out = a.partial + static_cast<i64>(blockIdx.y) * m1p * m2p;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const i64 i = ibase + x * 8 + g, j = jbase + y * 8 + 2 * t;
+      *reinterpret_cast<double2*>(out + i * m2p + j) = make_double2(acc[x][y][0], acc[x][y][1]);
+    }
+}
+
+__global__ void __launch_bounds__(NT, 3) gram_tn_kernel(GramArgs a) {
+  extern __shared__ __align__(16) double dsm[];
   int ti, tj;
   if (a.sym) {
     int t = blockIdx.x;
@@ -75,67 +168,10 @@ __global__ void __launch_bounds__(NT) gram_tn_kernel(GramArgs a) {
   }
   const i64 r0 = static_cast<i64>(blockIdx.y) * a.rows_per_split;
   const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
-  __shared__ __align__(16) double sA[2][BK][SST];
-  __shared__ __align__(16) double sB[2][BK][SST];
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int ibase = ti * BM + wm * 32, jbase = tj * BN + wn * 32;
-  bool vi[4], vj[4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    vi[x] = ibase + x * 8 < a.m1;
-    vj[x] = jbase + x * 8 < a.m2;
-  }
-  double acc[4][4][2];
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-
-  const i64 nchunks = r1 > r0 ? cdiv(r1 - r0, BK) : 0;
-  if (nchunks > 0) {
-    load_k_tile(sA[0], a.A, a.lda, r0, r1, ti * BM, a.m1, a.mask, a.mask_val);
-    load_k_tile(sB[0], a.B, a.ldb, r0, r1, tj * BN, a.m2, a.mask, a.mask_val);
-    cp_async_commit();
-  }
-  for (i64 c = 0; c < nchunks; ++c) {
-    const int s = c & 1;
-    if (c + 1 < nchunks) {
-      load_k_tile(sA[s ^ 1], a.A, a.lda, r0 + (c + 1) * BK, r1, ti * BM, a.m1, a.mask, a.mask_val);
-      load_k_tile(sB[s ^ 1], a.B, a.ldb, r0 + (c + 1) * BK, r1, tj * BN, a.m2, a.mask, a.mask_val);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double fa[4], fb[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        fa[x] = sA[s][kk + t][wm * 32 + x * 8 + g];
-        fb[x] = sB[s][kk + t][wn * 32 + x * 8 + g];
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-          if (vi[x] && vj[y]) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
-    }
-    __syncthreads();
-  }
-  const i64 m1p = static_cast<i64>(a.tiles_i) * BM, m2p = static_cast<i64>(a.tiles_j) * BN;
-  double* out = a.partial + static_cast<i64>(blockIdx.y) * m1p * m2p;
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      const i64 i = ibase + x * 8 + g, j = jbase + y * 8 + 2 * t;
-      *reinterpret_cast<double2*>(out + i * m2p + j) = make_double2(acc[x][y][0], acc[x][y][1]);
-    }
+  if ((ti + 1) * BM <= a.m1 && (tj + 1) * BN <= a.m2)
+    gram_tile<true>(a, ti, tj, r0, r1, dsm);
+  else
+    gram_tile<false>(a, ti, tj, r0, r1, dsm);
 }
 
 // Deterministic split reduction; for sym the (min, max) element is read so the
@@ -154,10 +190,115 @@ __global__ void gram_reduce_kernel(const double* partial, int splits, int m1, in
     jj = i;
   }
   const i64 stride = static_cast<i64>(m1p) * m2p;
+  const double* src = partial + static_cast<i64>(ii) * m2p + jj;
+  // fixed summation order; eight independent loads in flight per thread
   double s = 0.0;
-  for (int sp = 0; sp < splits; ++sp) s += partial[sp * stride + static_cast<i64>(ii) * m2p + jj];
+  int sp = 0;
+  for (; sp + 8 <= splits; sp += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = src[(sp + u) * stride];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
+  }
+  for (; sp < splits; ++sp) s += src[sp * stride];
   out[static_cast<i64>(i) * ldo + j] = alpha * s;
 }
+
+
+// ---- narrow variants (all dims <= 32): one 32 x 32 output tile per CTA,
+// the four warps split the rows of each stage (gram) or the output rows (nn),
+// so no warp idles on out-of-range subtiles.
+constexpr int SBK = 32;      // rows per gram stage
+constexpr int SS = 36;       // [*][32] tiles: stride == 4 (mod 16)
+
+__device__ __forceinline__ void load_k_tile32(double (*s)[SS], const double* g, int ld, i64 r, i64 rend, int m,
+                                              const int* mask, int mask_val) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = threadIdx.x + NT * q;  // 512 chunks: 32 rows x 16 pairs
+    const int row = c >> 4, col = (c & 15) * 2;
+    i64 gr = r + row;
+    double* dst = &s[row][col];
+    if (mask && gr < rend && mask[gr] == mask_val) gr = rend;
+    if (gr < rend && col + 2 <= m) {
+      cp_async_pair(dst, g + gr * ld + col);
+    } else {
+      dst[0] = (gr < rend && col < m) ? g[gr * ld + col] : 0.0;
+      dst[1] = 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) gram_tn_small_kernel(GramArgs a) {
+  const i64 r0 = static_cast<i64>(blockIdx.y) * a.rows_per_split;
+  const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
+  __shared__ __align__(16) double sA[2][SBK][SS];
+  __shared__ __align__(16) double sB[2][SBK][SS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  bool vi[4], vj[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    vi[x] = x * 8 < a.m1;
+    vj[x] = x * 8 < a.m2;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const i64 nchunks = r1 > r0 ? cdiv(r1 - r0, SBK) : 0;
+  if (nchunks > 0) {
+    load_k_tile32(sA[0], a.A, a.lda, r0, r1, a.m1, a.mask, a.mask_val);
+    load_k_tile32(sB[0], a.B, a.ldb, r0, r1, a.m2, a.mask, a.mask_val);
+    cp_async_commit();
+  }
+  for (i64 c = 0; c < nchunks; ++c) {
+    const int s = c & 1;
+    if (c + 1 < nchunks) {
+      load_k_tile32(sA[s ^ 1], a.A, a.lda, r0 + (c + 1) * SBK, r1, a.m1, a.mask, a.mask_val);
+      load_k_tile32(sB[s ^ 1], a.B, a.ldb, r0 + (c + 1) * SBK, r1, a.m2, a.mask, a.mask_val);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = warp * 8; kk < warp * 8 + 8; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = sA[s][kk + t][x * 8 + g];
+        fb[x] = sB[s][kk + t][x * 8 + g];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (vi[x] && vj[y]) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+    }
+    __syncthreads();
+  }
+  // reduce the four warps' tiles through shared memory (fixed order)
+  double* red = &sA[0][0][0];  // 4 x 32 x 32 doubles fit in sA + sB
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = x * 8 + g, j = y * 8 + 2 * t;
+      red[warp * 1024 + i * 32 + j] = acc[x][y][0];
+      red[warp * 1024 + i * 32 + j + 1] = acc[x][y][1];
+    }
+  __syncthreads();
+  double* out = a.partial + static_cast<i64>(blockIdx.y) * 1024;
+  for (int e = threadIdx.x; e < 1024; e += NT)
+    out[e] = ((red[e] + red[1024 + e]) + red[2048 + e]) + red[3072 + e];
+}
+
+constexpr int NBM = 128, NBK = 8, NSAR = 12;  // narrow nn: 128 rows x 32 cols, K chunks of 8
+
 
 struct NNArgs {
   const double* A;
@@ -173,35 +314,154 @@ struct NNArgs {
   int ldo;
   double alpha, beta;
   int upper_tri_c;  // C upper triangular (zeros stored below): skip K chunks past the column tile
+  const int* skip_flags;  // optional: do nothing when (*skip_flags & skip_mask) or *skip_info != 0
+  int skip_mask;
+  const int* skip_info;
 };
 
-__global__ void __launch_bounds__(NT) gemm_nn_kernel(NNArgs a) {
-  __shared__ __align__(16) double sA[2][BM][SAR];
-  __shared__ __align__(16) double sC[2][BK][SST];
-  const i64 row0 = static_cast<i64>(blockIdx.x) * BM;
-  const int tj = blockIdx.y;
+__device__ __forceinline__ bool nn_skipped(const NNArgs& a) {
+  return a.skip_flags && ((*a.skip_flags & a.skip_mask) || *a.skip_info != 0);
+}
+
+constexpr int SAR2 = BK2 + 4;  // [64][32] A tiles: stride 36 == 4 (mod 16)
+constexpr size_t kNNSmem = sizeof(double) * 2 * (BM * SAR2 + BK2 * SST);
+
+template <bool FULL>
+__device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, double* smem) {
+  double* sA = smem;                  // [2][BM][SAR2]
+  double* sC = smem + 2 * BM * SAR2;  // [2][BK2][SST]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
   const int kmax = a.upper_tri_c ? min(a.m1, (tj + 1) * BN) : a.m1;
-  const int nk = static_cast<int>(cdiv(kmax, BK));
+  const int nk = static_cast<int>(cdiv(kmax, BK2));
   bool vi[4], vj[4];
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
-    vi[x] = row0 + wm * 32 + x * 8 < a.nrows;
-    vj[x] = tj * BN + wn * 32 + x * 8 < a.m2;
+    vi[x] = FULL || row0 + wm * 32 + x * 8 < a.nrows;
+    vj[x] = FULL || tj * BN + wn * 32 + x * 8 < a.m2;
   }
   double acc[4][4][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  auto load = [&](int s, int k0) {
+    double* A_s = sA + s * BM * SAR2;
+    double* C_s = sC + s * BK2 * SST;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // A: 64 rows x 32 cols = 1024 pairs
+      const int c = threadIdx.x + NT * q;
+      const int row = c >> 4, col = (c & 15) * 2;
+      const i64 gr = row0 + row;
+      const int gk = k0 + col;
+      double* dst = A_s + row * SAR2 + col;
+      if (gr < a.nrows && gk + 2 <= a.m1) {
+        cp_async_pair(dst, a.A + gr * a.lda + gk);
+      } else {
+        dst[0] = (gr < a.nrows && gk < a.m1) ? a.A[gr * a.lda + gk] : 0.0;
+        dst[1] = (gr < a.nrows && gk + 1 < a.m1) ? a.A[gr * a.lda + gk + 1] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // C: 32 rows x 64 cols = 1024 pairs
+      const int c = threadIdx.x + NT * q;
+      const int row = c >> 5, col = (c & 31) * 2;
+      const int gk = k0 + row, gc = tj * BN + col;
+      double* dst = C_s + row * SST + col;
+      if (gk < a.m1 && gc + 2 <= a.m2) {
+        cp_async_pair(dst, a.C + static_cast<i64>(gk) * a.ldc + gc);
+      } else {
+        dst[0] = (gk < a.m1 && gc < a.m2) ? a.C[static_cast<i64>(gk) * a.ldc + gc] : 0.0;
+        dst[1] = (gk < a.m1 && gc + 1 < a.m2) ? a.C[static_cast<i64>(gk) * a.ldc + gc + 1] : 0.0;
+      }
+    }
+  };
+  if (nk > 0) {
+    load(0, 0);
+    cp_async_commit();
+  }
+  for (int c = 0; c < nk; ++c) {
+    const int s = c & 1;
+    if (c + 1 < nk) {
+      load(s ^ 1, (c + 1) * BK2);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* pa = sA + s * BM * SAR2 + (wm * 32 + g) * SAR2 + t;
+    const double* pc = sC + s * BK2 * SST + t * SST + wn * 32 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK2; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = pa[x * 8 * SAR2 + kk];
+        fb[x] = pc[kk * SST + x * 8];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (FULL || (vi[x] && vj[y])) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const i64 r = row0 + wm * 32 + x * 8 + g;
+      const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
+      if (!FULL && r >= a.nrows) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!FULL && col + h >= a.m2) continue;
+        double v = a.alpha * acc[x][y][h];
+        if (a.beta != 0.0) v += a.beta * a.Bm[r * a.ldb + col + h];
+        a.Out[r * a.ldo + col + h] = v;
+      }
+    }
+}
 
+__global__ void __launch_bounds__(NT, 3) gemm_nn_kernel(NNArgs a) {
+  if (nn_skipped(a)) return;
+  extern __shared__ __align__(16) double dsm[];
+  const i64 row0 = static_cast<i64>(blockIdx.x) * BM;
+  const int tj = blockIdx.y;
+  if (row0 + BM <= a.nrows && (tj + 1) * BN <= a.m2)
+    nn_tile<true>(a, row0, tj, dsm);
+  else
+    nn_tile<false>(a, row0, tj, dsm);
+}
+
+__global__ void __launch_bounds__(NT) gemm_nn_small_kernel(NNArgs a) {
+  if (nn_skipped(a)) return;
+  __shared__ __align__(16) double sA[2][NBM][NSAR];
+  __shared__ __align__(16) double sC[2][NBK][SS];
+  const i64 row0 = static_cast<i64>(blockIdx.x) * NBM;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int kmax = a.m1;
+  const int nk = static_cast<int>(cdiv(kmax, NBK));
+  bool vi[4], vj[4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    vi[x] = row0 + warp * 32 + x * 8 < a.nrows;
+    vj[x] = x * 8 < a.m2;
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   auto load = [&](int s, int k0) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {  // A: 64 rows x 16 cols
+    for (int q = 0; q < 4; ++q) {  // A: 128 rows x 8 cols = 512 pairs
       const int c = threadIdx.x + NT * q;
-      const int row = c >> 3, col = (c & 7) * 2;
+      const int row = c >> 2, col = (c & 3) * 2;
       const i64 gr = row0 + row;
       const int gk = k0 + col;
       double* dst = &sA[s][row][col];
@@ -212,21 +472,19 @@ __global__ void __launch_bounds__(NT) gemm_nn_kernel(NNArgs a) {
         dst[1] = 0.0;
       }
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // C: 16 rows x 64 cols
-      const int c = threadIdx.x + NT * q;
-      const int row = c >> 5, col = (c & 31) * 2;
-      const int gk = k0 + row, gc = tj * BN + col;
+    {  // C: 8 rows x 32 cols = 128 pairs
+      const int c = threadIdx.x;
+      const int row = c >> 4, col = (c & 15) * 2;
+      const int gk = k0 + row;
       double* dst = &sC[s][row][col];
-      if (gk < a.m1 && gc + 2 <= a.m2) {
-        cp_async_pair(dst, a.C + static_cast<i64>(gk) * a.ldc + gc);
+      if (gk < a.m1 && col + 2 <= a.m2) {
+        cp_async_pair(dst, a.C + static_cast<i64>(gk) * a.ldc + col);
       } else {
-        dst[0] = (gk < a.m1 && gc < a.m2) ? a.C[static_cast<i64>(gk) * a.ldc + gc] : 0.0;
+        dst[0] = (gk < a.m1 && col < a.m2) ? a.C[static_cast<i64>(gk) * a.ldc + col] : 0.0;
         dst[1] = 0.0;
       }
     }
   };
-
   if (nk > 0) {
     load(0, 0);
     cp_async_commit();
@@ -234,7 +492,7 @@ __global__ void __launch_bounds__(NT) gemm_nn_kernel(NNArgs a) {
   for (int c = 0; c < nk; ++c) {
     const int s = c & 1;
     if (c + 1 < nk) {
-      load(s ^ 1, (c + 1) * BK);
+      load(s ^ 1, (c + 1) * NBK);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -242,12 +500,12 @@ __global__ void __launch_bounds__(NT) gemm_nn_kernel(NNArgs a) {
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < NBK; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
-        fa[x] = sA[s][wm * 32 + x * 8 + g][kk + t];
-        fb[x] = sC[s][kk + t][wn * 32 + x * 8 + g];
+        fa[x] = sA[s][warp * 32 + x * 8 + g][kk + t];
+        fb[x] = sC[s][kk + t][x * 8 + g];
       }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
@@ -261,8 +519,8 @@ __global__ void __launch_bounds__(NT) gemm_nn_kernel(NNArgs a) {
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      const i64 r = row0 + wm * 32 + x * 8 + g;
-      const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
+      const i64 r = row0 + warp * 32 + x * 8 + g;
+      const int col = y * 8 + 2 * t;
       if (r >= a.nrows) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {

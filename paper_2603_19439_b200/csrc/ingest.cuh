@@ -169,37 +169,83 @@ __global__ void row_len_kernel(const int* arp, i64 n_old, i64 n_total, int* rowc
   rowcnt[r] = (r < n_old) ? arp[r + 1] - arp[r] : 0;
 }
 
-// Pass 2a: A's entries to their new positions (warp per row).
-__global__ void __launch_bounds__(256) merge_rows_kernel(const int* arp, const int* acol, const double* aval,
-                                                         i64 n_old, const int* mark, int stamp, const int* drp,
-                                                         const int* dcol, const int* flag, const double* newv,
-                                                         const int* prefix, const int* nrp, int* ncol, double* nval) {
-  const i64 r = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+// Pass 2a: A's entries to their new positions. Work is split into fixed
+// chunks of A's nonzeros (one warp per kMergeChunk entries), so hub rows with
+// tens of thousands of entries are spread over many warps. A warp walks the
+// rows its chunk intersects: untouched rows are shifted copies; in rows of P
+// each entry counts the Delta entries with smaller column from a 32-wide
+// window of the (short, sorted) Delta row, broadcast by shuffles and advanced
+// monotonically.
+constexpr int kMergeChunk = 512;
+
+__global__ void __launch_bounds__(256) merge_chunks_kernel(const int* arp, const int* acol, const double* aval,
+                                                           i64 n_old, const int* mark, int stamp, const int* drp,
+                                                           const int* dcol, const int* flag, const double* newv,
+                                                           const int* prefix, const int* nrp, int* ncol,
+                                                           double* nval) {
+  const i64 w = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (r >= n_old) return;
-  const int s = arp[r], len = arp[r + 1] - s;
-  const int o = nrp[r];
-  if (mark[r] != stamp) {
-    for (int i = lane; i < len; i += 32) {
-      ncol[o + i] = acol[s + i];
-      nval[o + i] = aval[s + i];
-    }
-    return;
+  const i64 nnz = arp[n_old];
+  const i64 e0 = w * kMergeChunk;
+  if (e0 >= nnz) return;
+  const i64 e1 = min(nnz, e0 + kMergeChunk);
+  // row holding entry e0: the largest r < n_old with arp[r] <= e0
+  i64 lo = 0, hi = n_old - 1;
+  while (lo < hi) {
+    const i64 mid = (lo + hi + 1) >> 1;
+    if (arp[mid] <= e0) lo = mid; else hi = mid - 1;
   }
-  const int ds = drp[r], dn = drp[r + 1] - ds;
-  const int p0 = prefix[ds];
-  for (int i = lane; i < len; i += 32) {
-    const int c = acol[s + i];
-    int lo = 0, hi = dn;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (dcol[ds + mid] < c) lo = mid + 1; else hi = mid;
+  i64 r = lo;
+  i64 pos = e0;
+  while (pos < e1) {
+    const int s = arp[r], e = arp[r + 1];
+    const i64 seg_end = min(static_cast<i64>(e), e1);
+    if (seg_end > pos) {
+      const int o = nrp[r];
+      if (mark[r] != stamp) {
+        for (i64 q = pos + lane; q < seg_end; q += 32) {
+          ncol[o + (q - s)] = acol[q];
+          nval[o + (q - s)] = aval[q];
+        }
+      } else {
+        const int ds = drp[r], dn = drp[r + 1] - ds;
+        const int p0 = prefix[ds];
+        // Delta entries with column below the segment's first column
+        const int cfirst = acol[pos];
+        int a0 = 0, a1 = dn;
+        while (a0 < a1) {
+          const int mid = (a0 + a1) >> 1;
+          if (dcol[ds + mid] < cfirst) a0 = mid + 1; else a1 = mid;
+        }
+        int dbase = a0;
+        for (i64 base = pos; base < seg_end; base += 32) {
+          const i64 q = base + lane;
+          const bool valid = q < seg_end;
+          const int c = valid ? acol[q] : 0x7fffffff;
+          const int last = static_cast<int>(min(static_cast<i64>(31), seg_end - base - 1));
+          const int cmax = __shfl_sync(0xffffffffu, c, last);
+          int cnt = dbase, hit = -1;
+          for (int w0 = dbase; w0 < dn; w0 += 32) {
+            const int dc = w0 + lane < dn ? dcol[ds + w0 + lane] : 0x7fffffff;
+            if (__shfl_sync(0xffffffffu, dc, 0) > cmax) break;  // window entirely past the chunk
+            for (int j = 0; j < 32; ++j) {
+              const int dj = __shfl_sync(0xffffffffu, dc, j);
+              cnt += dj < c ? 1 : 0;
+              if (dj == c) hit = w0 + j;
+            }
+            if (__shfl_sync(0xffffffffu, dc, 31) >= cmax) break;
+          }
+          dbase = __shfl_sync(0xffffffffu, cnt, last);
+          if (!valid) continue;
+          if (hit >= 0 && (flag[ds + hit] & 2)) continue;  // cancelled to exactly zero: pruned
+          const int out = o + static_cast<int>(q - s) + (prefix[ds + cnt] - p0);
+          ncol[out] = c;
+          nval[out] = hit >= 0 ? newv[ds + hit] : aval[q];
+        }
+      }
+      pos = seg_end;
     }
-    const bool match = lo < dn && dcol[ds + lo] == c;
-    if (match && (flag[ds + lo] & 2)) continue;  // cancelled to exactly zero: pruned
-    const int pos = o + i + (prefix[ds + lo] - p0);
-    ncol[pos] = c;
-    nval[pos] = match ? newv[ds + lo] : aval[s + i];
+    ++r;
   }
 }
 

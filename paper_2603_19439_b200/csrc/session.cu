@@ -28,6 +28,7 @@
 #include "../../include/spectrack_gpu.h"
 #include "common.cuh"
 #include "dmma.cuh"
+#include "eigsolve.cuh"
 #include "ingest.cuh"
 #include "rng.cuh"
 #include "smalllin.cuh"
@@ -197,6 +198,10 @@ class Session {
     if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
     cusolverDnSetStream(solver_, st_);
     STG_CUDA(cudaMallocHost(&hs_, sizeof(Scalars)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kGramSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kNNSmem)));
     d_scal_ = arena_.get<u64>("scalars", 32);
     k = cfg.k;
     n = n0;
@@ -249,7 +254,18 @@ class Session {
   // ---------------------------------------------------------------- public ops
   void step(const st_update& u, bool device_ptrs = false) {
     launches = 0;
+    kdiscard();  // a failed or probe call may have left unflushed entries
     timing_begin();
+    const u64 basis_seed = mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken);
+    omega_S_ = -1;  // a sketch from an earlier call is never reused
+    if (cfg.kind == ST_GREST_RSVD && u.n_new > cfg.rsvd_l && u.n_new > 0) {
+      // the sketch's seed and shape are known before ingestion: overlap the
+      // sequential mt19937_64 recurrence with it (trackers.cpp:362, rsvd.hpp:42-44)
+      const int q = static_cast<int>(std::min<i64>(u.n_new, cfg.rsvd_l + cfg.rsvd_p));
+      double* om;
+      int ldo;
+      prepare_omega(basis_seed, u.n_new, q, &om, &ldo);
+    }
     Pert pt = ingest(u, /*commit_slot*/ true, device_ptrs);
     timing_mark(0);
     if (pt.empty()) {
@@ -259,7 +275,6 @@ class Session {
       kflush();
       return;
     }
-    const u64 basis_seed = mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken);
     Basis b = build_basis(pt, cfg.kind - ST_IASC, basis_seed);
     timing_mark(1);
     std::vector<double> newvals;
@@ -274,6 +289,7 @@ class Session {
 
   i64 probe_basis(const st_update& u, int basis_kind, u64 seed, double* z, i64 ldz, i64 max_cols) {
     launches = 0;
+    omega_S_ = -1;
     Pert pt = ingest(u, false);
     if (pt.n_old != n) throw InvalidArgument("build_projection_basis: perturbation dimension mismatch");
     if (pt.empty() && basis_kind != 0) {
@@ -327,6 +343,54 @@ class Session {
     std::memcpy(vals, newvals.data(), sizeof(double) * k);
     for (i64 c = 0; c < k; ++c)
       for (i64 i = 0; i < pt.n_total; ++i) vecs[c * ldv + i] = w[static_cast<size_t>(i * k + c)];
+  }
+
+  // Kernel microbenchmark on synthetic operands (development / profiling):
+  // which = 0 gram (sym if flag&1), 1 nn (tri if flag&1), 2 chol, 3 triinv,
+  // 4 on-device eigensolver (want = m2), 5 masked gram over N rows.
+  double bench_kernel(int which, i64 N, int m1, int m2, int flag, int iters) {
+    const int ld1 = ld_for(m1), ld2 = ld_for(m2);
+    double* A = arena_.get<double>("bk_A", N * ld1);
+    double* B = arena_.get<double>("bk_B", N * ld2);
+    double* C = arena_.get<double>("bk_C", static_cast<i64>(ld1) * ld2 + static_cast<i64>(m1) * ld1);
+    double* O = arena_.get<double>("bk_O", std::max<i64>(N * ld2, static_cast<i64>(m1) * ld2));
+    launch(fill_kernel, dim3(blocks(N * ld1)), dim3(256), 0, st_, A, N * ld1, 1e-3);
+    launch(fill_kernel, dim3(blocks(N * ld2)), dim3(256), 0, st_, B, N * ld2, 2e-3);
+    // SPD-ish small matrix for chol/eig: I + small
+    std::vector<double> h(static_cast<size_t>(m1) * ld1, 0.0);
+    for (int i = 0; i < m1; ++i)
+      for (int j = 0; j < m1; ++j) h[static_cast<size_t>(i) * ld1 + j] = (i == j ? 2.0 + i : 0.0) + 0.01 * std::sin(i * 7.0 + j * 3.0 + (i + j));
+    for (int i = 0; i < m1; ++i)
+      for (int j = 0; j < i; ++j) h[static_cast<size_t>(i) * ld1 + j] = h[static_cast<size_t>(j) * ld1 + i];
+    STG_CUDA(cudaMemcpyAsync(C, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st_));
+    cudaEvent_t a, b;
+    STG_CUDA(cudaEventCreate(&a));
+    STG_CUDA(cudaEventCreate(&b));
+    auto run = [&]() {
+      switch (which) {
+        case 0: gram(A, ld1, (flag & 1) ? A : B, (flag & 1) ? ld1 : ld2, N, m1, (flag & 1) ? m1 : m2, flag & 1, O, ld2); break;
+        case 1: nn(A, ld1, N, m1, C, ld1, m2, O, ld2, 1.0, 0.0, nullptr, 0, flag & 1); break;
+        case 2: chol(C, ld1, m1, O, ld1, nullptr, 0.0, true); break;
+        case 3: triinv(C, ld1, m1, O, ld1); break;
+        case 4: {
+          double* w = arena_.get<double>("bk_w", m1);
+          eig_fast(C, ld1, m1, 0, m2, w, O, ld2);
+          break;
+        }
+        case 5: gram(A, ld1, A, ld1, N, m1, m1, true, O, ld2, 1.0, mark_p_, -12345); break;
+      }
+    };
+    for (int i = 0; i < 2; ++i) run();
+    STG_CUDA(cudaEventRecord(a, st_));
+    for (int i = 0; i < iters; ++i) run();
+    STG_CUDA(cudaEventRecord(b, st_));
+    STG_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    STG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    kdiscard();
+    return ms / iters;
   }
 
   void copy_x_colmajor(double* out, i64 rows) {
@@ -414,15 +478,18 @@ class Session {
     }
     return evpool_[evnext_++];
   }
+  std::vector<size_t> open_;  // kbegin/kend nest (e.g. the rotation contains a GEMM)
   void kbegin(int cls, double work, cudaStream_t s = nullptr) {
     if (!ktiming()) return;
     PendingK p{cls, next_event(), next_event(), work};
     STG_CUDA(cudaEventRecord(p.a, s ? s : st_));
+    open_.push_back(pend_.size());
     pend_.push_back(p);
   }
   void kend(cudaStream_t s = nullptr) {
     if (!ktiming()) return;
-    STG_CUDA(cudaEventRecord(pend_.back().b, s ? s : st_));
+    STG_CUDA(cudaEventRecord(pend_[open_.back()].b, s ? s : st_));
+    open_.pop_back();
   }
  public:
   void kflush() {
@@ -436,6 +503,12 @@ class Session {
       kstats[p.cls].launches += 1;
     }
     pend_.clear();
+    open_.clear();
+    evnext_ = 0;
+  }
+  void kdiscard() {
+    pend_.clear();
+    open_.clear();
     evnext_ = 0;
   }
   void kreset() {
@@ -537,16 +610,23 @@ class Session {
     a.sym = sym ? 1 : 0;
     a.mask = mask;
     a.mask_val = mask_val;
-    const int ntiles = sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j;
+    const bool narrow = m1 <= 32 && m2 <= 32;
+    if (narrow) a.tiles_i = a.tiles_j = 1;
+    const int ntiles = narrow ? 1 : (sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j);
     const i64 target = 148 * 6;
-    i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), 128), cdiv(target, ntiles)));
+    const i64 rows_min = narrow ? 256 : 128;
+    i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
     splits = std::min<i64>(splits, 65535);
-    a.rows_per_split = round_up(cdiv(std::max<i64>(rows, 1), splits), dm::BK);
+    a.rows_per_split = round_up(cdiv(std::max<i64>(rows, 1), splits), narrow ? dm::SBK : dm::BK2);
     splits = std::max<i64>(1, cdiv(std::max<i64>(rows, 1), a.rows_per_split));
-    const i64 m1p = static_cast<i64>(a.tiles_i) * dm::BM, m2p = static_cast<i64>(a.tiles_j) * dm::BN;
+    const i64 m1p = narrow ? 32 : static_cast<i64>(a.tiles_i) * dm::BM;
+    const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * dm::BN;
     a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
     kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
-    launch(dm::gram_tn_kernel, dim3(ntiles, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
+    if (narrow)
+      launch(dm::gram_tn_small_kernel, dim3(1, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
+    else
+      launch(dm::gram_tn_kernel, dim3(ntiles, static_cast<unsigned>(splits)), dim3(dm::NT), dm::kGramSmem, st_, a);
     launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
            static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
            static_cast<int>(m2p), a.sym, out, ldo, alpha);
@@ -554,7 +634,7 @@ class Session {
   }
 
   void nn(const double* A, int lda, i64 rows, int m1, const double* C, int ldc, int m2, double* Out, int ldo,
-          double alpha, double beta, const double* B, int ldb, bool tri = false) {
+          double alpha, double beta, const double* B, int ldb, bool tri = false, bool gated = false) {
     if (rows <= 0 || m2 <= 0) return;
     dm::NNArgs a{};
     a.A = A;
@@ -571,9 +651,18 @@ class Session {
     a.alpha = alpha;
     a.beta = beta;
     a.upper_tri_c = tri ? 1 : 0;
+    if (gated) {  // skip when the step has already failed (keeps a failed step side-effect free)
+      a.skip_flags = flags_ptr();
+      a.skip_mask = kNonFinite | kNotOrthonormal;
+      a.skip_info = info_ptr();
+    }
     kbegin(kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
-    launch(dm::gemm_nn_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::BM)), static_cast<unsigned>(cdiv(m2, dm::BN))),
-           dim3(dm::NT), 0, st_, a);
+    if (m2 <= 32)
+      launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
+    else
+      launch(dm::gemm_nn_kernel,
+             dim3(static_cast<unsigned>(cdiv(rows, dm::BM)), static_cast<unsigned>(cdiv(m2, dm::BN))), dim3(dm::NT),
+             dm::kNNSmem, st_, a);
     kend();
   }
 
@@ -636,6 +725,36 @@ class Session {
       throw CudaError("cusolverDnDsyevd failed");
     *w_out = w;
     *v_out = V;
+  }
+
+  // On-device eigensolver (one CTA) for order <= kEigMaxN: all eigenvalues in
+  // spectral order (w_sorted) and the leading `want` eigenvectors (F, row-major).
+  bool eig_fast(const double* M, int ldm, int D, int order, int want, double* w_sorted, double* F, int ldf,
+                double ortol = 1e-3) {
+    if (D > kEigMaxN || want > kEigMaxWant) return false;
+    static bool attr = false;
+    if (!attr) {
+      STG_CUDA(cudaFuncSetAttribute(syev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(syev_smem_bytes(kEigMaxN))));
+      attr = true;
+    }
+    EigArgs ea{};
+    ea.M = M;
+    ea.ldm = ldm;
+    ea.n = D;
+    ea.order = order;
+    ea.want = want;
+    ea.w_sorted = w_sorted;
+    ea.F = F;
+    ea.ldf = ldf;
+    ea.work = arena_.get<double>("eig_work_inv", static_cast<i64>(std::max(want, 1)) * 6 * D);
+    ea.flags = flags_ptr();
+    ea.info = info_ptr();
+    ea.ortol = ortol;
+    kbegin(kEig, 4.0 * D * D * D / 3.0);
+    launch(syev_kernel, dim3(1), dim3(1024), syev_smem_bytes(D), st_, ea);
+    kend();
+    return true;
   }
 
   void read_scalars() {
@@ -826,9 +945,9 @@ class Session {
     scan_int(contrib, prefix, n2 + 1);
     kbegin(kMerge, 0.0);
     const size_t merge_pend = pend_.size() - (ktiming() ? 1 : 0);
-    if (n_old > 0)
-      launch(merge_rows_kernel, dim3(blocks(n_old, 8)), dim3(256), 0, st_, static_cast<const int*>(a.rp),
-             static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
+    if (a.nnz > 0)
+      launch(merge_chunks_kernel, dim3(blocks(cdiv(a.nnz, kMergeChunk), 8)), dim3(256), 0, st_,
+             static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
              static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
              static_cast<const int*>(dcol), static_cast<const int*>(mflag), static_cast<const double*>(newv),
              static_cast<const int*>(prefix), static_cast<const int*>(an.rp), an.col, an.val);
@@ -1084,22 +1203,10 @@ class Session {
     const int ldz = ld_for(kk + wmax);
     double* Z = arena_.get<double>("Z", N * ldz);
     Blk z{Z, ldz};
-    // ---- RNG for the sketch starts first on its own stream
+    // ---- RNG for the sketch (normally already launched at the start of the step)
     double* omega = nullptr;
     int ldo = 0;
-    if (rsvd) {
-      ldo = ld_for(q);
-      omega = arena_.get<double>("omega", S * ldo);
-      const i64 npairs = cdiv(S * q, 2);
-      u64* raw = arena_.get<u64>("mt_raw", 2 * npairs);
-      const u64 rseed = mix_seed(seed, 0x5bdULL);
-      kbegin(kRng, 2.0 * npairs, st_rng_);
-      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, 2 * npairs, raw);
-      launch(box_muller_kernel, dim3(blocks(npairs)), dim3(256), 0, st_rng_, static_cast<const u64*>(raw), npairs, S,
-             q, omega, ldo);
-      kend(st_rng_);
-      STG_CUDA(cudaEventRecord(ev_rng_, st_rng_));
-    }
+    if (rsvd) prepare_omega(seed, S, q, &omega, &ldo);
     // ---- X-bar in stacked coordinates: [X_P; R_c; I]
     build_xbar(pt, z);
     if (basis_kind == 0) {
@@ -1200,11 +1307,25 @@ class Session {
     // thin U of (M'B) = eigenvectors of bt_m' bt_m, singular values descending
     double* gb = arena_.get<double>("gb", static_cast<i64>(qm) * ldy);
     gram(btm, ldy, btm, ldy, pt.S, qm, qm, true, gb, ldy);
-    double *w = nullptr, *V = nullptr;
-    eig(gb, ldy, qm, &w, &V, "sk");
+    const int wantu = static_cast<int>(std::min<i64>(cfg.rsvd_l, qm));
+    const int ldu = ld_for(wantu);
+    double* U = arena_.get<double>("Ukeep", static_cast<i64>(qm) * ldu);
+    double* lamd = arena_.get<double>("sk_lam", qm);
     std::vector<double> lam(static_cast<size_t>(qm));
-    STG_CUDA(cudaMemcpyAsync(lam.data(), w, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
-    read_scalars();
+    // only span(U_keep) matters here (R is re-orthonormalized with the basis),
+    // so clusters are re-orthogonalized only when nearly degenerate
+    if (eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10)) {
+      STG_CUDA(cudaMemcpyAsync(lam.data(), lamd, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
+      read_scalars();
+      std::reverse(lam.begin(), lam.end());  // ascending like the cuSOLVER path
+    } else {
+      double *w = nullptr, *V = nullptr;
+      eig(gb, ldy, qm, &w, &V, "sk");
+      STG_CUDA(cudaMemcpyAsync(lam.data(), w, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
+      read_scalars();
+      launch(gather_desc_kernel, dim3(blocks(static_cast<i64>(qm) * wantu)), dim3(256), 0, st_,
+             static_cast<const double*>(V), qm, wantu, U, ldu);
+    }
     if (hs_->info != 0) throw RuntimeError("rsvd_basis: SVD did not converge");
     // rank: sv(r) > 1e-10 sv(0) and > 0 (rsvd.hpp:59-62)
     std::vector<double> sv(static_cast<size_t>(qm));
@@ -1214,13 +1335,35 @@ class Session {
     while (rank < qm && sv[rank] > cutoff && sv[rank] > 0.0) ++rank;
     const int keep = static_cast<int>(std::min<i64>(cfg.rsvd_l, rank));
     if (keep == 0) return 0;
-    const int ldu = ld_for(keep);
-    double* U = arena_.get<double>("Ukeep", static_cast<i64>(qm) * ldu);
-    launch(gather_desc_kernel, dim3(blocks(static_cast<i64>(qm) * keep)), dim3(256), 0, st_,
-           static_cast<const double*>(V), qm, keep, U, ldu);
     // R = M U_keep
     nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
     return keep;
+  }
+
+  // Omega (S x q, rng.hpp:64-69 fill order) generated on the side stream; the
+  // consumer waits on ev_rng_. Launched once per (seed, S, q).
+  u64 omega_seed_ = 0;
+  i64 omega_S_ = -1;
+  int omega_q_ = -1;
+  void prepare_omega(u64 seed, i64 S, int q, double** omega, int* ldo_out) {
+    const int ldo = ld_for(q);
+    double* om = arena_.get<double>("omega", S * ldo);
+    if (!(omega_seed_ == seed && omega_S_ == S && omega_q_ == q)) {
+      const i64 npairs = cdiv(S * q, 2);
+      u64* raw = arena_.get<u64>("mt_raw", 2 * npairs);
+      const u64 rseed = mix_seed(seed, 0x5bdULL);
+      kbegin(kRng, 2.0 * npairs, st_rng_);
+      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, 2 * npairs, raw);
+      launch(box_muller_kernel, dim3(blocks(npairs)), dim3(256), 0, st_rng_, static_cast<const u64*>(raw), npairs, S,
+             q, om, ldo);
+      kend(st_rng_);
+      STG_CUDA(cudaEventRecord(ev_rng_, st_rng_));
+      omega_seed_ = seed;
+      omega_S_ = S;
+      omega_q_ = q;
+    }
+    *omega = om;
+    *ldo_out = ldo;
   }
 
   void build_xbar(const Pert& pt, Blk z) {
@@ -1271,21 +1414,25 @@ class Session {
     sa.ldy = ldd;
     do_spmm(sa, pt.nnz, p);
     double* tm = arena_.get<double>("rr_t", static_cast<i64>(D) * ldd);
-    gram(b.z.p, b.z.ld, dz, ldd, p, D, D, false, tm, ldd);
+    // Z'(Delta Z) is symmetric (Delta is): compute tile pairs ti <= tj and mirror;
+    // the reference symmetrizes the projected matrix anyway (eig.hpp:47)
+    gram(b.z.p, b.z.ld, dz, ldd, p, D, D, true, tm, ldd);
     double* mm = arena_.get<double>("rr_m", static_cast<i64>(D) * ldd);
     launch(rr_matrix_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_, static_cast<const double*>(zx),
            ldk, static_cast<const double*>(d_values_), kk, static_cast<const double*>(tm), ldd, D, mm, ldd);
     timing_mark(2);
-    double *w = nullptr, *V = nullptr;
-    eig(mm, ldd, D, &w, &V, "rr");
-    int* perm = arena_.get<int>("rr_perm", D);
-    launch(sort_perm_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(w), D, static_cast<int>(cfg.order),
-           perm);
     double* F = arena_.get<double>("rr_F", static_cast<i64>(D) * ldk);
-    double* nv = arena_.get<double>("rr_vals", kk);
-    launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(D) * kk)), dim3(256), 0, st_,
-           static_cast<const double*>(V), D, static_cast<const double*>(w), static_cast<const int*>(perm), kk, F, ldk,
-           nv);
+    double* nv = arena_.get<double>("rr_vals", std::max(D, kk));
+    if (!eig_fast(mm, ldd, D, static_cast<int>(cfg.order), kk, nv, F, ldk)) {
+      double *w = nullptr, *V = nullptr;
+      eig(mm, ldd, D, &w, &V, "rr");
+      int* perm = arena_.get<int>("rr_perm", D);
+      launch(sort_perm_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(w), D,
+             static_cast<int>(cfg.order), perm);
+      launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(D) * kk)), dim3(256), 0, st_,
+             static_cast<const double*>(V), D, static_cast<const double*>(w), static_cast<const int*>(perm), kk, F,
+             ldk, nv);
+    }
     timing_mark(3);
     // W = Z F (all stacked rows): rows of P -> new rows of X, a-rows -> A_new
     double* W = arena_.get<double>("rr_W", N * ldk);
@@ -1293,11 +1440,20 @@ class Session {
     newvals.assign(static_cast<size_t>(kk), 0.0);
     STG_CUDA(cudaMemcpyAsync(newvals.data(), nv, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
     if (write_state) {
+      // X <- X A_new on the rows outside P (in place, DMMA, single column tile),
+      // then the rows of P take W's rows. Both are skipped if the step failed.
       kbegin(kRotate, 16.0 * k * pt.n_total + 8.0 * pt.n_total);
-      launch(rotate_x_kernel, dim3(blocks(pt.n_total, 8)), dim3(256), 0, st_, X_, ldx(), pt.n_old, pt.n_total,
-             pt.dense ? 1 : 0, static_cast<const int*>(pt.mark), pt.stamp, static_cast<const int*>(pt.posmap),
-             static_cast<const double*>(W), ldk, static_cast<const double*>(W + (p + k) * ldk), kk,
-             static_cast<const int*>(flags_ptr()), static_cast<const int*>(info_ptr()));
+      if (!pt.dense && k <= 64)
+        nn(X_, ldx(), pt.n_old, kk, W + (p + k) * ldk, ldk, kk, X_, ldx(), 1.0, 0.0, nullptr, 0, false, true);
+      if (pt.dense || k <= 64)
+        launch(scatter_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, X_, ldx(), pt.P, pt.dense ? 1 : 0, p,
+               static_cast<const double*>(W), ldk, kk, static_cast<const int*>(flags_ptr()),
+               static_cast<const int*>(info_ptr()));
+      else
+        launch(rotate_x_kernel, dim3(blocks(pt.n_total, 8)), dim3(256), 0, st_, X_, ldx(), pt.n_old, pt.n_total,
+               pt.dense ? 1 : 0, static_cast<const int*>(pt.mark), pt.stamp, static_cast<const int*>(pt.posmap),
+               static_cast<const double*>(W), ldk, static_cast<const double*>(W + (p + k) * ldk), kk,
+               static_cast<const int*>(flags_ptr()), static_cast<const int*>(info_ptr()));
       kend();
     }
     read_scalars();
@@ -1445,6 +1601,107 @@ int32_t st_last_timings(const st_session* s, double* ms, int32_t cap) {
 }
 
 int64_t st_last_launches(const st_session* s) { return s->impl->launches; }
+
+st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, int32_t order, int64_t want,
+                           double* values, double* vectors) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || want < 0 || want > n) throw std::invalid_argument("sym_eig_dense: bad sizes");
+    for (int64_t i = 0; i < n * n; ++i)
+      if (!std::isfinite(s_colmajor[i])) throw std::invalid_argument("sym_eig_dense: non-finite entries");
+    if (n == 0) return;
+    if (n > stg::kEigMaxN) throw std::invalid_argument("st_sym_eig_dense: order above the on-device solver limit");
+    STG_CUDA(cudaSetDevice(device));
+    static bool attr = false;
+    if (!attr) {
+      STG_CUDA(cudaFuncSetAttribute(stg::syev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(stg::syev_smem_bytes(stg::kEigMaxN))));
+      attr = true;
+    }
+    // row-major copy of S' (the kernel symmetrizes (S + S')/2 itself)
+    std::vector<double> rm(static_cast<size_t>(n * n));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) rm[static_cast<size_t>(i * n + j)] = s_colmajor[j * n + i];
+    double *dm, *dw, *df, *work;
+    int* di;
+    const int64_t wv = std::max<int64_t>(want, 1);
+    STG_CUDA(cudaMalloc(&dm, sizeof(double) * n * n));
+    STG_CUDA(cudaMalloc(&dw, sizeof(double) * n));
+    STG_CUDA(cudaMalloc(&df, sizeof(double) * n * wv));
+    STG_CUDA(cudaMalloc(&work, sizeof(double) * 6 * n * wv));
+    STG_CUDA(cudaMalloc(&di, sizeof(int) * 2));
+    STG_CUDA(cudaMemset(di, 0, sizeof(int) * 2));
+    STG_CUDA(cudaMemcpy(dm, rm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    stg::EigArgs ea{};
+    ea.M = dm;
+    ea.ldm = static_cast<int>(n);
+    ea.n = static_cast<int>(n);
+    ea.order = order;
+    ea.want = static_cast<int>(want);
+    ea.w_sorted = dw;
+    ea.F = df;
+    ea.ldf = static_cast<int>(wv);
+    ea.work = work;
+    ea.flags = di;
+    ea.info = di + 1;
+    ea.ortol = 1e-3;
+    long long* prof = nullptr;
+    if (getenv("STG_EIG_PROF")) {
+      STG_CUDA(cudaMalloc(&prof, sizeof(long long) * 8));
+      ea.prof = prof;
+    }
+    stg::syev_kernel<<<1, 1024, stg::syev_smem_bytes(static_cast<int>(n))>>>(ea);
+    STG_LAUNCH();
+    STG_CUDA(cudaDeviceSynchronize());
+    if (prof) {
+      long long hp[8];
+      STG_CUDA(cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "syev n=%lld want=%lld cycles: sym %lld tridiag %lld bisect %lld order %lld invit %lld back %lld\n",
+              static_cast<long long>(n), static_cast<long long>(want), hp[1] - hp[0], hp[2] - hp[1], hp[3] - hp[2],
+              hp[4] - hp[3], hp[5] - hp[4], hp[6] - hp[5]);
+      cudaFree(prof);
+    }
+    std::vector<double> f(static_cast<size_t>(n * wv));
+    STG_CUDA(cudaMemcpy(values, dw, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    STG_CUDA(cudaMemcpy(f.data(), df, sizeof(double) * n * wv, cudaMemcpyDeviceToHost));
+    for (int64_t c = 0; c < want; ++c)
+      for (int64_t i = 0; i < n; ++i) vectors[c * n + i] = f[static_cast<size_t>(i * wv + c)];
+    cudaFree(dm);
+    cudaFree(dw);
+    cudaFree(df);
+    cudaFree(work);
+    cudaFree(di);
+  });
+}
+
+st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_t cols, double* out_colmajor) {
+  return guarded(nullptr, [&] {
+    if (rows < 0 || cols < 0) throw std::invalid_argument("gaussian_matrix: negative size");
+    if (rows * cols == 0) return;
+    STG_CUDA(cudaSetDevice(device));
+    const int64_t npairs = (rows * cols + 1) / 2;
+    stg::u64* raw;
+    double* om;
+    const int ld = static_cast<int>(cols);
+    STG_CUDA(cudaMalloc(&raw, sizeof(stg::u64) * 2 * npairs));
+    STG_CUDA(cudaMalloc(&om, sizeof(double) * rows * cols));
+    stg::mt19937_64_kernel<<<1, 160>>>(seed, 2 * npairs, raw);
+    STG_LAUNCH();
+    stg::box_muller_kernel<<<static_cast<unsigned>((npairs + 255) / 256), 256>>>(raw, npairs, rows,
+                                                                                 static_cast<int>(cols), om, ld);
+    STG_LAUNCH();
+    std::vector<double> rm(static_cast<size_t>(rows * cols));
+    STG_CUDA(cudaMemcpy(rm.data(), om, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost));
+    for (int64_t c = 0; c < cols; ++c)
+      for (int64_t r = 0; r < rows; ++r) out_colmajor[c * rows + r] = rm[static_cast<size_t>(r * cols + c)];
+    cudaFree(raw);
+    cudaFree(om);
+  });
+}
+
+st_status st_debug_bench(st_session* s, int32_t which, int64_t N, int32_t m1, int32_t m2, int32_t flag,
+                         int32_t iters, double* ms) {
+  return guarded(s, [&] { *ms = s->impl->bench_kernel(which, N, m1, m2, flag, iters); });
+}
 
 st_status st_step_device(st_session* s, const st_update* upd) {
   return guarded(s, [&] {

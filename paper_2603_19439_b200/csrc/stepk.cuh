@@ -80,6 +80,18 @@ __global__ void __launch_bounds__(256) rotate_x_kernel(double* X, int ldx, i64 n
   if (lane + 32 < k) xr[lane + 32] = a1;
 }
 
+// Rows of P take the rotated stacked rows W[t] (row P[t], or t in dense mode).
+__global__ void __launch_bounds__(256) scatter_rows_kernel(double* X, int ldx, const int* P, int dense, i64 p,
+                                                           const double* W, int ldw, int k, const int* flags,
+                                                           const int* info) {
+  if ((*flags & (kNonFinite | kNotOrthonormal)) || *info != 0) return;
+  const i64 t = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= p) return;
+  const i64 row = dense ? t : static_cast<i64>(P[t]);
+  for (int c = lane; c < k; c += 32) X[row * ldx + c] = W[t * ldw + c];
+}
+
 // Dense expansion of a stacked basis (probe API only).
 __global__ void __launch_bounds__(256) expand_kernel(const double* X, int ldx, i64 n_old, i64 n_total, int dense,
                                                      const int* mark, int stamp, const int* posmap, const double* z,

@@ -1,0 +1,80 @@
+"""Device replacements of two reference kernels checked against the oracle:
+sym_eig_dense (eig.hpp:37-50, test_linalg.cpp:30-96) and the GaussianSampler
+stream (rng.hpp:27-75) that feeds the RSVD sketch."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from harness import sin_angle
+
+pytestmark = pytest.mark.gpu
+
+
+def dev():
+    import paper_2603_19439_b200 as m
+    return m
+
+
+def test_sym_eig_reference_cases():
+    m = dev()
+    w, v = m.sym_eig_dense(np.diag([3.0, 1.0, 2.0]), "abs_desc")
+    assert np.allclose(w, [3, 2, 1], rtol=0, atol=1e-14)
+    assert abs(v[0, 0]) == pytest.approx(1) and abs(v[2, 1]) == pytest.approx(1) and abs(v[1, 2]) == pytest.approx(1)
+    w, v = m.sym_eig_dense(np.array([[-7.5]]), "alg_desc")
+    assert w[0] == pytest.approx(-7.5) and abs(v[0, 0]) == pytest.approx(1.0)
+    w, _ = m.sym_eig_dense(np.diag([-3.0, 1.0, 2.0]), "abs_desc")
+    assert np.allclose(w[:2], [-3, 2])
+    w, _ = m.sym_eig_dense(np.diag([-3.0, 1.0, 2.0]), "alg_desc")
+    assert np.allclose(w[[0, 2]], [2, -3])
+    w, _ = m.sym_eig_dense(np.array([[0.0, 2.0], [2.0, 0.0]]), "abs_desc")
+    assert np.allclose(w, [2, -2])  # magnitude tie broken toward the algebraic maximum
+    nan2 = np.zeros((2, 2))
+    nan2[0, 0] = np.nan
+    with pytest.raises(m.TrackerError, match="non-finite"):
+        m.sym_eig_dense(nan2)
+
+
+@pytest.mark.parametrize("n", [2, 8, 33, 64, 164, 200, 232])
+@pytest.mark.parametrize("order", ["abs_desc", "alg_desc"])
+def test_sym_eig_random_matches_oracle(n, order):
+    m = dev()
+    g = po.gaussian_matrix(100 + n, n, n)
+    s = 0.5 * (g + g.T)
+    s[0, 1] += 1e-13  # slightly asymmetric input is symmetrized (test_linalg.cpp:80-88)
+    w, v = m.sym_eig_dense(s, order, want=min(n, 40))
+    wo, vo = po.sym_eig(s, {"abs_desc": 0, "alg_desc": 1}[order])
+    scale = np.abs(wo).max()
+    assert np.abs(w - wo).max() <= 1e-12 * scale
+    sym = 0.5 * (s + s.T)
+    resid = np.abs(sym @ v - v * w[: v.shape[1]]).max()
+    assert resid <= 1e-11 * scale
+    assert np.abs(v.T @ v - np.eye(v.shape[1])).max() <= 1e-12
+    # compare spans over groups of separated eigenvalues
+    k = v.shape[1]
+    if k < n and abs(abs(wo[k - 1]) - abs(wo[k])) > 1e-6 * scale:
+        assert sin_angle(v, vo[:, :k]) <= 1e-9
+
+
+def test_sym_eig_clustered_and_repeated():
+    m = dev()
+    rng = np.random.default_rng(4)
+    n = 120
+    q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    d = np.concatenate([np.full(5, 7.0), np.full(3, -7.0 + 1e-13), np.linspace(-3, 3, n - 8)])
+    s = (q * d) @ q.T
+    w, v = m.sym_eig_dense(s, "abs_desc", want=8)
+    assert np.abs(np.abs(w[:8]) - 7.0).max() <= 1e-12 * 7
+    assert np.abs(v.T @ v - np.eye(8)).max() <= 1e-11
+    top = q[:, :8]
+    assert sin_angle(v, top) <= 1e-9
+
+
+@pytest.mark.parametrize("seed,rows,cols", [(0, 10, 3), (5489, 1000, 7), (12345, 10485, 200), (7, 3, 3)])
+def test_gaussian_stream_matches_reference_sampler(seed, rows, cols):
+    m = dev()
+    g = m.gaussian_matrix(seed, rows, cols)
+    o = po.gaussian_matrix(seed, rows, cols)
+    # identical mt19937_64 words and uniforms; log/sincos may differ by an ulp
+    rel = np.abs(g - o) / np.maximum(1.0, np.abs(o))
+    assert rel.max() <= 4e-16 * 8
+    assert (g == o).mean() > 0.5
