@@ -374,7 +374,10 @@ class Session {
         case 3: triinv(C, ld1, m1, O, ld1); break;
         case 4: {
           double* w = arena_.get<double>("bk_w", m1);
+          const int saved = cfg.flags;
+          cfg.flags |= ST_FLAG_DEVICE_EIG;
           eig_fast(C, ld1, m1, 0, m2, w, O, ld2);
+          cfg.flags = saved;
           break;
         }
         case 5: gram(A, ld1, A, ld1, N, m1, m1, true, O, ld2, 1.0, mark_p_, -12345); break;
@@ -731,6 +734,9 @@ class Session {
   // spectral order (w_sorted) and the leading `want` eigenvectors (F, row-major).
   bool eig_fast(const double* M, int ldm, int D, int order, int want, double* w_sorted, double* F, int ldf,
                 double ortol = 1e-3) {
+    // The one-CTA solver is still slower than cuSOLVER syevd at the step's
+    // orders, so the step uses it only on request.
+    if (!(cfg.flags & ST_FLAG_DEVICE_EIG)) return false;
     if (D > kEigMaxN || want > kEigMaxWant) return false;
     static bool attr = false;
     if (!attr) {

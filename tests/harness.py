@@ -25,7 +25,7 @@ def value_err(va, vb) -> float:
 
 
 def pair(rowptr, col, val, kind="grest-rsvd", k=8, order="abs_desc", rsvd_l=100, rsvd_p=100, seed=0,
-         operator="adjacency", force_dense=False):
+         operator="adjacency", force_dense=False, **kw):
     """(gpu, oracle) sessions from the same initial state: the oracle runs the
     reference tracker_init (Lanczos) and the GPU session takes its output."""
     from paper_2603_19439_b200 import TrackerSession
@@ -35,7 +35,7 @@ def pair(rowptr, col, val, kind="grest-rsvd", k=8, order="abs_desc", rsvd_l=100,
     o = po.Session(a, kind=kind, k=k, order=order, rsvd_l=rsvd_l, rsvd_p=rsvd_p, seed=seed, operator=operator)
     vals, vecs = o.embedding()
     g = TrackerSession(a.rowptr, a.col, a.val, vals, vecs, kind=kind, k=k, order=order, rsvd_l=rsvd_l,
-                       rsvd_p=rsvd_p, seed=seed, operator=operator, force_dense=force_dense)
+                       rsvd_p=rsvd_p, seed=seed, operator=operator, force_dense=force_dense, **kw)
     return g, o
 
 
