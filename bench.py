@@ -124,7 +124,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def dist_setup():
+def dist_setup(backend: str | None = None):
+    """One process per GPU (torchrun env); NCCL on GPUs, gloo for CPU tests."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -132,18 +133,22 @@ def dist_setup():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        backend = backend or os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
     return world, rank, local
 
 
 def dist_max(x: float, world: int) -> float:
+    """Max over ranks of a per-rank device time (the job's time is the slowest rank's)."""
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -1,0 +1,267 @@
+// spectrack_b200.hpp — header-only C++17 shim that re-exposes the reference
+// `spectrack` update API (proj/include/spectrack/{trackers,graph,
+// laplacian_track}.hpp) on top of the C ABI in spectrack_gpu.h, without Eigen.
+//
+// Mapping (reference -> here):
+//   assemble_update(n_old, added, removed, S, new_edges)   graph.hpp:65-69
+//       -> EditLists (the same four arguments, validated on the device with
+//          the reference's rules and messages)
+//   tracker_init(a0, kind, opts)                           trackers.hpp:92
+//       -> GpuTracker(a0, kind, opts, op, initial)  (X0, Lambda0 are an input:
+//          the north-star API takes the initial eigenpairs)
+//   tracker_step(state, GraphUpdate)                       trackers.hpp:132-133
+//   apply_update(A, d)                                     graph.hpp:74
+//   ShiftedLaplacianSession::advance(d)                    laplacian_track.hpp:34
+//       -> tracker_step(tracker, edits): one call performs all three on the
+//          device-resident state
+//   build_projection_basis / rayleigh_ritz_step            trackers.hpp:112-118
+//       -> GpuTracker::projection_basis / rayleigh_ritz (no state change)
+//   sym_eig_dense (eig.hpp:37-50), GaussianSampler::gaussian_matrix (rng.hpp:64-69)
+//       -> sym_eig_dense / gaussian_matrix below
+// Errors are rethrown as the reference's exception types with its messages:
+// std::invalid_argument and std::runtime_error.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+#include "spectrack_gpu.h"
+
+namespace spectrack_b200 {
+
+using Index = std::int64_t;
+
+enum class TrackerKind { iasc = ST_IASC, grest2 = ST_GREST2, grest3 = ST_GREST3, grest_rsvd = ST_GREST_RSVD };
+enum class BasisKind { iasc = 0, grest2 = 1, grest3 = 2, grest_rsvd = 3 };
+enum class SpectralOrder { abs_desc = ST_ABS_DESC, alg_desc = ST_ALG_DESC };
+enum class OperatorKind {
+  adjacency = ST_ADJACENCY,
+  laplacian = ST_LAPLACIAN,
+  normalized_laplacian = ST_NORMALIZED_LAPLACIAN
+};
+
+// TrackerOptions (trackers.hpp:52-63), G-REST fields.
+struct TrackerOptions {
+  Index k = 8;
+  SpectralOrder order = SpectralOrder::abs_desc;
+  Index rsvd_l = 100;
+  Index rsvd_p = 100;
+  std::uint64_t seed = 0;
+};
+
+// Symmetric CSR in the layout of SymSparseMatrix (sparse.hpp:18, 46-48).
+struct Csr {
+  Index n = 0;
+  std::vector<std::int32_t> row_offsets{0};
+  std::vector<std::int32_t> col_indices;
+  std::vector<double> values;
+  Index nnz() const { return static_cast<Index>(values.size()); }
+};
+
+// SpectralEmbedding (trackers.hpp:28-34): vectors column-major n x k.
+struct SpectralEmbedding {
+  std::vector<double> values;
+  std::vector<double> vectors;
+  Index n = 0;
+  Index k() const { return static_cast<Index>(values.size()); }
+};
+
+// The arguments of assemble_update (graph.cpp:45-100).
+struct EditLists {
+  std::vector<std::tuple<Index, Index, double>> added_edges;
+  std::vector<std::pair<Index, Index>> removed_edges;
+  Index new_node_count = 0;
+  std::vector<std::tuple<Index, Index, double>> new_edges;
+};
+
+namespace detail {
+inline void rethrow(st_status s, const char* msg) {
+  switch (s) {
+    case ST_OK: return;
+    case ST_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case ST_RUNTIME_ERROR: throw std::runtime_error(msg);
+    default: throw std::runtime_error(std::string("spectrack_b200 device failure: ") + msg);
+  }
+}
+
+struct PackedUpdate {  // SoA copies of the edit lists backing an st_update
+  std::vector<std::int64_t> ai, aj, ri, rj, ni, nj;
+  std::vector<double> aw, nw;
+  st_update u{};
+  explicit PackedUpdate(const EditLists& e) {
+    for (const auto& [i, j, w] : e.added_edges) {
+      ai.push_back(i);
+      aj.push_back(j);
+      aw.push_back(w);
+    }
+    for (const auto& [i, j] : e.removed_edges) {
+      ri.push_back(i);
+      rj.push_back(j);
+    }
+    for (const auto& [i, j, w] : e.new_edges) {
+      ni.push_back(i);
+      nj.push_back(j);
+      nw.push_back(w);
+    }
+    u.n_added = static_cast<std::int64_t>(ai.size());
+    u.added_i = ai.data();
+    u.added_j = aj.data();
+    u.added_w = aw.data();
+    u.n_removed = static_cast<std::int64_t>(ri.size());
+    u.removed_i = ri.data();
+    u.removed_j = rj.data();
+    u.n_new = e.new_node_count;
+    u.n_new_edges = static_cast<std::int64_t>(ni.size());
+    u.new_i = ni.data();
+    u.new_j = nj.data();
+    u.new_w = nw.data();
+  }
+};
+}  // namespace detail
+
+// One tracker lane resident on one GPU: the adjacency (and, for Laplacian
+// operators, the shifted operator T of ShiftedLaplacianSession) plus the
+// TrackerState. Unlike the reference's value-semantics TrackerState, the state
+// lives in HBM and is updated in place; a failed step leaves it unchanged,
+// which is what the reference's `state = tracker_step(state, ...)` assignment
+// observes when the call throws.
+class GpuTracker {
+ public:
+  GpuTracker(const Csr& a0, TrackerKind kind, const TrackerOptions& opts, OperatorKind op,
+             const SpectralEmbedding& initial, int device = 0, int flags = 0) {
+    st_config cfg{};
+    cfg.kind = static_cast<std::int32_t>(kind);
+    cfg.op = static_cast<std::int32_t>(op);
+    cfg.k = opts.k;
+    cfg.order = static_cast<std::int32_t>(opts.order);
+    cfg.rsvd_l = opts.rsvd_l;
+    cfg.rsvd_p = opts.rsvd_p;
+    cfg.seed = opts.seed;
+    cfg.device = device;
+    cfg.flags = flags;
+    if (initial.k() != opts.k || initial.n != a0.n || static_cast<Index>(initial.vectors.size()) != a0.n * opts.k)
+      throw std::invalid_argument("tracker_init: initial embedding does not match n x k");
+    detail::rethrow(st_create(&cfg, a0.n, a0.row_offsets.data(), a0.col_indices.data(), a0.values.data(),
+                              initial.values.data(), initial.vectors.data(), a0.n, &s_),
+                    st_last_error(nullptr));
+  }
+  GpuTracker(const GpuTracker&) = delete;
+  GpuTracker& operator=(const GpuTracker&) = delete;
+  GpuTracker(GpuTracker&& o) noexcept : s_(o.s_) { o.s_ = nullptr; }
+  ~GpuTracker() {
+    if (s_) st_destroy(s_);
+  }
+
+  // assemble_update + to_perturbation/advance + apply_update + tracker_step
+  void step(const EditLists& edits) {
+    detail::PackedUpdate pu(edits);
+    detail::rethrow(st_step(s_, &pu.u), st_last_error(s_));
+  }
+
+  Index n() const { return info().n; }
+  std::uint64_t steps_taken() const { return info().steps; }
+  double alpha() const { return info().alpha; }  // Laplacian shift (laplacian_track.hpp:40)
+
+  SpectralEmbedding embedding() const {
+    const Info in = info();
+    SpectralEmbedding e;
+    e.n = in.n;
+    e.values.resize(static_cast<size_t>(in.k));
+    e.vectors.resize(static_cast<size_t>(in.n * in.k));
+    detail::rethrow(st_get_embedding(s_, e.values.data(), e.vectors.data(), in.n), st_last_error(s_));
+    return e;
+  }
+
+  // laplacian_view (laplacian_track.cpp:66-71): nu = alpha - mu
+  SpectralEmbedding laplacian_view() const {
+    SpectralEmbedding e = embedding();
+    const double a = alpha();
+    for (double& v : e.values) v = a - v;
+    return e;
+  }
+
+  // which: 0 adjacency, 1 shifted operator T, 2 last perturbation (Delta or Delta_T)
+  Csr csr(int which) const {
+    const Info in = info();
+    const Index nnz = which == 0 ? in.nnz_a : which == 1 ? in.nnz_t : in.nnz_delta;
+    Csr m;
+    m.n = in.n;
+    m.row_offsets.resize(static_cast<size_t>(in.n + 1));
+    m.col_indices.resize(static_cast<size_t>(nnz));
+    m.values.resize(static_cast<size_t>(nnz));
+    detail::rethrow(st_get_csr(s_, which, m.row_offsets.data(), m.col_indices.data(), m.values.data()),
+                    st_last_error(s_));
+    return m;
+  }
+
+  // build_projection_basis (trackers.cpp:226-280) for `edits`, column-major n_total x D
+  std::vector<double> projection_basis(const EditLists& edits, BasisKind kind, std::uint64_t seed,
+                                       Index* cols) const {
+    detail::PackedUpdate pu(edits);
+    const Index n_total = n() + edits.new_node_count;
+    const Index maxc = 2 * info().k + edits.new_node_count + 512;
+    std::vector<double> z(static_cast<size_t>(n_total * maxc));
+    std::int64_t d = 0;
+    detail::rethrow(st_probe_basis(s_, &pu.u, static_cast<std::int32_t>(kind), seed, z.data(), n_total, maxc, &d),
+                    st_last_error(s_));
+    z.resize(static_cast<size_t>(n_total * d));
+    if (cols) *cols = d;
+    return z;
+  }
+
+  // rayleigh_ritz_step (trackers.cpp:282-308) against a caller basis (column-major)
+  SpectralEmbedding rayleigh_ritz(const EditLists& edits, const std::vector<double>& z, Index rows, Index cols) const {
+    detail::PackedUpdate pu(edits);
+    const Index k = info().k;
+    SpectralEmbedding e;
+    e.n = rows;
+    e.values.resize(static_cast<size_t>(k));
+    e.vectors.resize(static_cast<size_t>(rows * k));
+    detail::rethrow(st_probe_rr(s_, &pu.u, z.data(), rows, cols, rows, e.values.data(), e.vectors.data(), rows),
+                    st_last_error(s_));
+    return e;
+  }
+
+ private:
+  struct Info {
+    Index n, k, nnz_a, nnz_t, nnz_delta;
+    std::uint64_t steps;
+    double alpha;
+  };
+  Info info() const {
+    Info in{};
+    st_info(s_, &in.n, &in.k, &in.steps, &in.nnz_a, &in.nnz_t, &in.nnz_delta, &in.alpha);
+    return in;
+  }
+  st_session* s_ = nullptr;
+};
+
+// tracker_step (trackers.hpp:132-133) in the reference's call shape.
+inline GpuTracker& tracker_step(GpuTracker& t, const EditLists& edits) {
+  t.step(edits);
+  return t;
+}
+
+// sym_eig_dense (eig.hpp:37-50): values in spectral order, leading `want`
+// eigenvectors column-major.
+inline std::pair<std::vector<double>, std::vector<double>> sym_eig_dense(const std::vector<double>& s, Index n,
+                                                                         SpectralOrder order, Index want,
+                                                                         int device = 0) {
+  std::vector<double> w(static_cast<size_t>(n)), v(static_cast<size_t>(n * want));
+  detail::rethrow(st_sym_eig_dense(device, n, s.data(), static_cast<std::int32_t>(order), want, w.data(), v.data()),
+                  st_last_error(nullptr));
+  return {w, v};
+}
+
+// GaussianSampler(seed).gaussian_matrix(rows, cols) (rng.hpp:64-69), column-major.
+inline std::vector<double> gaussian_matrix(std::uint64_t seed, Index rows, Index cols, int device = 0) {
+  std::vector<double> out(static_cast<size_t>(rows * cols));
+  detail::rethrow(st_gaussian_matrix(device, seed, rows, cols, out.data()), st_last_error(nullptr));
+  return out;
+}
+
+}  // namespace spectrack_b200
