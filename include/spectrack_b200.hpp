@@ -79,7 +79,11 @@ struct EditLists {
 };
 
 namespace detail {
-inline void rethrow(st_status s, const char* msg) {
+// The message is fetched after the call returns (st_last_error's buffer is
+// rewritten by every failing call).
+inline void rethrow(st_status s, const st_session* session) {
+  if (s == ST_OK) return;
+  const char* msg = st_last_error(session);
   switch (s) {
     case ST_OK: return;
     case ST_INVALID_ARGUMENT: throw std::invalid_argument(msg);
@@ -147,7 +151,7 @@ class GpuTracker {
       throw std::invalid_argument("tracker_init: initial embedding does not match n x k");
     detail::rethrow(st_create(&cfg, a0.n, a0.row_offsets.data(), a0.col_indices.data(), a0.values.data(),
                               initial.values.data(), initial.vectors.data(), a0.n, &s_),
-                    st_last_error(nullptr));
+                    nullptr);
   }
   GpuTracker(const GpuTracker&) = delete;
   GpuTracker& operator=(const GpuTracker&) = delete;
@@ -159,7 +163,7 @@ class GpuTracker {
   // assemble_update + to_perturbation/advance + apply_update + tracker_step
   void step(const EditLists& edits) {
     detail::PackedUpdate pu(edits);
-    detail::rethrow(st_step(s_, &pu.u), st_last_error(s_));
+    detail::rethrow(st_step(s_, &pu.u), s_);
   }
 
   Index n() const { return info().n; }
@@ -172,7 +176,7 @@ class GpuTracker {
     e.n = in.n;
     e.values.resize(static_cast<size_t>(in.k));
     e.vectors.resize(static_cast<size_t>(in.n * in.k));
-    detail::rethrow(st_get_embedding(s_, e.values.data(), e.vectors.data(), in.n), st_last_error(s_));
+    detail::rethrow(st_get_embedding(s_, e.values.data(), e.vectors.data(), in.n), s_);
     return e;
   }
 
@@ -194,7 +198,7 @@ class GpuTracker {
     m.col_indices.resize(static_cast<size_t>(nnz));
     m.values.resize(static_cast<size_t>(nnz));
     detail::rethrow(st_get_csr(s_, which, m.row_offsets.data(), m.col_indices.data(), m.values.data()),
-                    st_last_error(s_));
+                    s_);
     return m;
   }
 
@@ -207,7 +211,7 @@ class GpuTracker {
     std::vector<double> z(static_cast<size_t>(n_total * maxc));
     std::int64_t d = 0;
     detail::rethrow(st_probe_basis(s_, &pu.u, static_cast<std::int32_t>(kind), seed, z.data(), n_total, maxc, &d),
-                    st_last_error(s_));
+                    s_);
     z.resize(static_cast<size_t>(n_total * d));
     if (cols) *cols = d;
     return z;
@@ -222,7 +226,7 @@ class GpuTracker {
     e.values.resize(static_cast<size_t>(k));
     e.vectors.resize(static_cast<size_t>(rows * k));
     detail::rethrow(st_probe_rr(s_, &pu.u, z.data(), rows, cols, rows, e.values.data(), e.vectors.data(), rows),
-                    st_last_error(s_));
+                    s_);
     return e;
   }
 
@@ -253,14 +257,14 @@ inline std::pair<std::vector<double>, std::vector<double>> sym_eig_dense(const s
                                                                          int device = 0) {
   std::vector<double> w(static_cast<size_t>(n)), v(static_cast<size_t>(n * want));
   detail::rethrow(st_sym_eig_dense(device, n, s.data(), static_cast<std::int32_t>(order), want, w.data(), v.data()),
-                  st_last_error(nullptr));
+                  nullptr);
   return {w, v};
 }
 
 // GaussianSampler(seed).gaussian_matrix(rows, cols) (rng.hpp:64-69), column-major.
 inline std::vector<double> gaussian_matrix(std::uint64_t seed, Index rows, Index cols, int device = 0) {
   std::vector<double> out(static_cast<size_t>(rows * cols));
-  detail::rethrow(st_gaussian_matrix(device, seed, rows, cols, out.data()), st_last_error(nullptr));
+  detail::rethrow(st_gaussian_matrix(device, seed, rows, cols, out.data()), nullptr);
   return out;
 }
 

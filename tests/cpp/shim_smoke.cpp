@@ -65,6 +65,9 @@ int main() {
     tracker_step(t, bad);
   } catch (const std::invalid_argument& e) {
     threw = std::string(e.what()).find("invalid deletion") != std::string::npos;
+    if (!threw) std::fprintf(stderr, "unexpected message: %s\n", e.what());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "unexpected exception: %s\n", e.what());
   }
   CHECK(threw);
   CHECK(t.steps_taken() == 0 && t.n() == 6);
