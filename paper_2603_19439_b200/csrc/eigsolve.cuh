@@ -29,7 +29,7 @@
 namespace stg {
 
 constexpr int kEigMaxN = 232;   // packed lower triangle + vectors fit in 227 KB of shared memory
-constexpr int kEigFullN = 160;  // full square storage up to here
+constexpr int kEigFullN = 165;  // full square storage up to here (covers D <= 164 at config 3)
 constexpr int kEigMaxWant = 256;
 
 struct EigArgs {

@@ -171,81 +171,120 @@ __global__ void row_len_kernel(const int* arp, i64 n_old, i64 n_total, int* rowc
 
 // Pass 2a: A's entries to their new positions. Work is split into fixed
 // chunks of A's nonzeros (one warp per kMergeChunk entries), so hub rows with
-// tens of thousands of entries are spread over many warps. A warp walks the
-// rows its chunk intersects: untouched rows are shifted copies; in rows of P
-// each entry counts the Delta entries with smaller column from a 32-wide
-// window of the (short, sorted) Delta row, broadcast by shuffles and advanced
-// monotonically.
-constexpr int kMergeChunk = 512;
+// tens of thousands of entries are spread over many warps. A warp loads the
+// metadata of 32 consecutive rows at once (row starts, shifts, P marks) into
+// lanes; entries of untouched rows are then copied 32 at a time, each lane
+// finding its entry's row by a 5-step shuffle search (no dependent memory
+// loads), and rows of P are merged with a 32-wide window of the (short,
+// sorted) Delta row broadcast by shuffles and advanced monotonically.
+constexpr int kMergeChunk = 1024;
 
-__global__ void __launch_bounds__(256) merge_chunks_kernel(const int* arp, const int* acol, const double* aval,
-                                                           i64 n_old, const int* mark, int stamp, const int* drp,
-                                                           const int* dcol, const int* flag, const double* newv,
-                                                           const int* prefix, const int* nrp, int* ncol,
-                                                           double* nval) {
+__device__ __forceinline__ void merge_p_segment(i64 pos, i64 seg_end, int s, int o, int ds, int dn, int lane,
+                                                const int* __restrict__ acol, const double* __restrict__ aval,
+                                                const int* __restrict__ dcol, const int* __restrict__ flag,
+                                                const double* __restrict__ newv, const int* __restrict__ prefix,
+                                                int* __restrict__ ncol, double* __restrict__ nval) {
+  const int p0 = prefix[ds];
+  const int cfirst = acol[pos];
+  int a0 = 0, a1 = dn;  // Delta entries with column below the segment's first column
+  while (a0 < a1) {
+    const int mid = (a0 + a1) >> 1;
+    if (dcol[ds + mid] < cfirst) a0 = mid + 1; else a1 = mid;
+  }
+  int dbase = a0;
+  for (i64 base = pos; base < seg_end; base += 32) {
+    const i64 q = base + lane;
+    const bool valid = q < seg_end;
+    const int c = valid ? acol[q] : 0x7fffffff;
+    const int last = static_cast<int>(min(static_cast<i64>(31), seg_end - base - 1));
+    const int cmax = __shfl_sync(0xffffffffu, c, last);
+    int cnt = dbase, hit = -1;
+    for (int w0 = dbase; w0 < dn; w0 += 32) {
+      const int dc = w0 + lane < dn ? dcol[ds + w0 + lane] : 0x7fffffff;
+      if (__shfl_sync(0xffffffffu, dc, 0) > cmax) break;  // window entirely past the chunk
+      for (int j = 0; j < 32; ++j) {
+        const int dj = __shfl_sync(0xffffffffu, dc, j);
+        cnt += dj < c ? 1 : 0;
+        if (dj == c) hit = w0 + j;
+      }
+      if (__shfl_sync(0xffffffffu, dc, 31) >= cmax) break;
+    }
+    dbase = __shfl_sync(0xffffffffu, cnt, last);
+    if (!valid) continue;
+    if (hit >= 0 && (flag[ds + hit] & 2)) continue;  // cancelled to exactly zero: pruned
+    const int out = o + static_cast<int>(q - s) + (prefix[ds + cnt] - p0);
+    ncol[out] = c;
+    nval[out] = hit >= 0 ? newv[ds + hit] : aval[q];
+  }
+}
+
+__global__ void __launch_bounds__(256) merge_chunks_kernel(const int* __restrict__ arp, const int* __restrict__ acol,
+                                                           const double* __restrict__ aval, i64 n_old,
+                                                           const int* __restrict__ mark, int stamp,
+                                                           const int* __restrict__ drp, const int* __restrict__ dcol,
+                                                           const int* __restrict__ flag,
+                                                           const double* __restrict__ newv,
+                                                           const int* __restrict__ prefix,
+                                                           const int* __restrict__ nrp, int* __restrict__ ncol,
+                                                           double* __restrict__ nval) {
   const i64 w = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const i64 nnz = arp[n_old];
   const i64 e0 = w * kMergeChunk;
   if (e0 >= nnz) return;
   const i64 e1 = min(nnz, e0 + kMergeChunk);
-  // row holding entry e0: the largest r < n_old with arp[r] <= e0
-  i64 lo = 0, hi = n_old - 1;
+  i64 lo = 0, hi = n_old - 1;  // row holding entry e0
   while (lo < hi) {
     const i64 mid = (lo + hi + 1) >> 1;
     if (arp[mid] <= e0) lo = mid; else hi = mid - 1;
   }
-  i64 r = lo;
-  i64 pos = e0;
+  i64 r = lo, pos = e0;
   while (pos < e1) {
-    const int s = arp[r], e = arp[r + 1];
-    const i64 seg_end = min(static_cast<i64>(e), e1);
-    if (seg_end > pos) {
-      const int o = nrp[r];
-      if (mark[r] != stamp) {
-        for (i64 q = pos + lane; q < seg_end; q += 32) {
-          ncol[o + (q - s)] = acol[q];
-          nval[o + (q - s)] = aval[q];
-        }
-      } else {
-        const int ds = drp[r], dn = drp[r + 1] - ds;
-        const int p0 = prefix[ds];
-        // Delta entries with column below the segment's first column
-        const int cfirst = acol[pos];
-        int a0 = 0, a1 = dn;
-        while (a0 < a1) {
-          const int mid = (a0 + a1) >> 1;
-          if (dcol[ds + mid] < cfirst) a0 = mid + 1; else a1 = mid;
-        }
-        int dbase = a0;
-        for (i64 base = pos; base < seg_end; base += 32) {
-          const i64 q = base + lane;
-          const bool valid = q < seg_end;
-          const int c = valid ? acol[q] : 0x7fffffff;
-          const int last = static_cast<int>(min(static_cast<i64>(31), seg_end - base - 1));
-          const int cmax = __shfl_sync(0xffffffffu, c, last);
-          int cnt = dbase, hit = -1;
-          for (int w0 = dbase; w0 < dn; w0 += 32) {
-            const int dc = w0 + lane < dn ? dcol[ds + w0 + lane] : 0x7fffffff;
-            if (__shfl_sync(0xffffffffu, dc, 0) > cmax) break;  // window entirely past the chunk
-            for (int j = 0; j < 32; ++j) {
-              const int dj = __shfl_sync(0xffffffffu, dc, j);
-              cnt += dj < c ? 1 : 0;
-              if (dj == c) hit = w0 + j;
-            }
-            if (__shfl_sync(0xffffffffu, dc, 31) >= cmax) break;
-          }
-          dbase = __shfl_sync(0xffffffffu, cnt, last);
-          if (!valid) continue;
-          if (hit >= 0 && (flag[ds + hit] & 2)) continue;  // cancelled to exactly zero: pruned
-          const int out = o + static_cast<int>(q - s) + (prefix[ds + cnt] - p0);
-          ncol[out] = c;
-          nval[out] = hit >= 0 ? newv[ds + hit] : aval[q];
-        }
+    // metadata of rows r .. r + 31 (one per lane)
+    const i64 rr = r + lane;
+    const bool in = rr < n_old;
+    const int rs = in ? arp[rr] : static_cast<int>(nnz);
+    const int re = in ? arp[rr + 1] : static_cast<int>(nnz);
+    const int o = in ? nrp[rr] : 0;
+    const bool pm = in && mark[rr] == stamp;
+    const i64 gend = min(static_cast<i64>(__shfl_sync(0xffffffffu, re, 31)), e1);
+    // untouched rows: entry-parallel shifted copy
+    for (i64 base = pos; base < gend; base += 32) {
+      const i64 q = base + lane;
+      int idx = 0;  // last lane whose row starts at or before q
+#pragma unroll
+      for (int st = 16; st > 0; st >>= 1) {
+        const int cand = idx + st;
+        const int rsc = __shfl_sync(0xffffffffu, rs, cand);
+        if (rsc <= q) idx = cand;
       }
-      pos = seg_end;
+      const int rs_i = __shfl_sync(0xffffffffu, rs, idx);
+      const int o_i = __shfl_sync(0xffffffffu, o, idx);
+      const bool p_i = __shfl_sync(0xffffffffu, pm ? 1 : 0, idx);
+      if (q < gend && !p_i) {
+        const i64 dst = o_i + (q - rs_i);
+        ncol[dst] = acol[q];
+        nval[dst] = aval[q];
+      }
     }
-    ++r;
+    // rows of P overlapping [pos, gend)
+    unsigned todo = __ballot_sync(0xffffffffu, pm && re > pos && rs < gend);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int s_l = __shfl_sync(0xffffffffu, rs, l);
+      const int e_l = __shfl_sync(0xffffffffu, re, l);
+      const int o_l = __shfl_sync(0xffffffffu, o, l);
+      const i64 row = r + l;
+      const int ds = drp[row], dn = drp[row + 1] - ds;
+      merge_p_segment(max(pos, static_cast<i64>(s_l)), min(static_cast<i64>(e_l), gend), s_l, o_l, ds, dn, lane,
+                      acol, aval, dcol, flag, newv, prefix, ncol, nval);
+    }
+    // next group starts at the row holding gend
+    if (gend >= e1) break;
+    const unsigned before = __ballot_sync(0xffffffffu, rs <= gend);
+    r += 31 - __clz(before);
+    pos = gend;
   }
 }
 

@@ -468,11 +468,14 @@ class Session {
     int cls;
     cudaEvent_t a, b;
     double work;
+    char tag[48];
   };
+  char ktag_[48] = {0};  // optional shape tag for the next kbegin (STG_KLOG)
   std::vector<PendingK> pend_;
   std::vector<cudaEvent_t> evpool_;
   size_t evnext_ = 0;
   bool ktiming() const { return cfg.flags & ST_FLAG_KERNEL_TIMING; }
+  const bool klog_ = getenv("STG_KLOG") != nullptr;
   cudaEvent_t next_event() {
     if (evnext_ == evpool_.size()) {
       cudaEvent_t e;
@@ -484,7 +487,9 @@ class Session {
   std::vector<size_t> open_;  // kbegin/kend nest (e.g. the rotation contains a GEMM)
   void kbegin(int cls, double work, cudaStream_t s = nullptr) {
     if (!ktiming()) return;
-    PendingK p{cls, next_event(), next_event(), work};
+    PendingK p{cls, next_event(), next_event(), work, {0}};
+    std::memcpy(p.tag, ktag_, sizeof(p.tag));
+    ktag_[0] = 0;
     STG_CUDA(cudaEventRecord(p.a, s ? s : st_));
     open_.push_back(pend_.size());
     pend_.push_back(p);
@@ -504,6 +509,8 @@ class Session {
       kstats[p.cls].ms += ms;
       kstats[p.cls].work += p.work;
       kstats[p.cls].launches += 1;
+      if (klog_) fprintf(stderr, "klog cls=%d %-40s %9.1f us  work=%.3g  rate=%.3g/s\n", p.cls, p.tag, 1e3 * ms,
+                         p.work, ms > 0 ? p.work / (ms * 1e-3) : 0.0);
     }
     pend_.clear();
     open_.clear();
@@ -625,6 +632,7 @@ class Session {
     const i64 m1p = narrow ? 32 : static_cast<i64>(a.tiles_i) * dm::BM;
     const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * dm::BN;
     a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "gram %lldx%dx%d%s", rows, m1, m2, sym ? " sym" : "");
     kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
     if (narrow)
       launch(dm::gram_tn_small_kernel, dim3(1, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
@@ -659,6 +667,7 @@ class Session {
       a.skip_mask = kNonFinite | kNotOrthonormal;
       a.skip_info = info_ptr();
     }
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "nn %lldx%dx%d%s", rows, m1, m2, tri ? " tri" : "");
     kbegin(kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
     if (m2 <= 32)
       launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
@@ -672,6 +681,7 @@ class Session {
   // CSR x dense with compulsory-traffic accounting: 12 B per nonzero, the row
   // pointers, and one read of each referenced dense row plus the output rows.
   void do_spmm(const SpmmArgs& a, i64 nnz, i64 distinct_cols, int cls = kSpmm) {
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "spmm %lld rows m=%d", a.rows, a.m);
     kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
     spmm(a, st_);
     launches += cdiv(a.m, 256);
@@ -679,25 +689,18 @@ class Session {
   }
 
   void chol(const double* G, int ldg, int w, double* R, int ldr, const double* orig2, double tau2, bool psd) {
+    if (w > kCholMaxW) throw RuntimeError("chol: block wider than 238 columns");
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "chol w=%d", w);
     kbegin(kChol, static_cast<double>(w) * w * w / 3.0);
-    struct End {
-      Session* s;
-      ~End() { s->kend(); }
-    } end{this};
-    const size_t packed = sizeof(double) * static_cast<size_t>(w) * (w + 1) / 2;
-    if (packed <= 220 * 1024) {
-      static bool attr = false;
-      if (!attr) {
-        STG_CUDA(cudaFuncSetAttribute(chol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
-        attr = true;
-      }
-      launch(chol_kernel<true>, dim3(1), dim3(1024), packed, st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
-             flags_ptr(), static_cast<double*>(nullptr));
-    } else {
-      double* work = arena_.get<double>("chol_work", static_cast<i64>(w) * w);
-      launch(chol_kernel<false>, dim3(1), dim3(1024), 0, st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0, flags_ptr(),
-             work);
+    static bool attr = false;
+    if (!attr) {
+      STG_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(chol_smem_bytes(kCholMaxW))));
+      attr = true;
     }
+    launch(chol_kernel, dim3(1), dim3(1024), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
+           flags_ptr());
+    kend();
   }
 
   void triinv(const double* R, int ldr, int w, double* Ri, int ldi) {
@@ -710,6 +713,7 @@ class Session {
   // Symmetric eigendecomposition (cuSOLVER syevd, ascending) of a row-major
   // D x D block after (M + M')/2; w and V (column-major) in arena buffers.
   void eig(const double* M, int ldm, int D, double** w_out, double** v_out, const std::string& tag) {
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "syevd D=%d", D);
     kbegin(kEig, 9.0 * D * D * D);
     struct End {
       Session* s;

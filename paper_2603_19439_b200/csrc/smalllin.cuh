@@ -21,58 +21,55 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Upper Cholesky G = R'R of a symmetric w x w block (row-major), single CTA.
-// PACKED keeps the upper triangle in shared memory (w <= 238). When orig2 is
-// given, pivot d_j <= tau2 * orig2[j] raises kSuspect: the column's residual is
-// within sqrt(tau2) of its original norm, where the reference's per-column
-// drop test (ortho.hpp:34-35) must be re-evaluated exactly. With psd != 0 a
+// Upper Cholesky G = R'R of a symmetric w x w block (row-major), one CTA,
+// the upper triangle in shared memory (rows packed: row i holds columns i..w-1).
+// Right-looking with ONE barrier per column: after the barrier every thread
+// reads the pivot U(j,j) (broadcast) and derives 1/r itself; row j of R is
+// written to global scaled, while the trailing update uses the raw row j with
+// the factor 1/d: U(i,c) -= U(j,i) U(j,c) / d. When orig2 is given, a pivot
+// d_j <= tau2 * orig2[j] raises kSuspect: the column's residual is within
+// sqrt(tau2) of its original norm, where the reference's per-column drop test
+// (ortho.hpp:34-35) must be re-evaluated exactly. With psd != 0 a
 // non-positive pivot zeroes the row (semidefinite factor) instead of failing.
-template <bool PACKED>
+constexpr int kCholMaxW = 238;
+
 __global__ void __launch_bounds__(1024) chol_kernel(const double* G, int ldg, int w, double* R, int ldr,
-                                                    const double* orig2, double tau2, int psd, int* flags,
-                                                    double* gwork) {
+                                                    const double* orig2, double tau2, int psd, int* flags) {
   extern __shared__ double sm[];
-  double* U = PACKED ? sm : gwork;
-  auto at = [&](int i, int c) -> double& {
-    return PACKED ? U[static_cast<i64>(i) * w - (static_cast<i64>(i) * (i - 1)) / 2 + (c - i)]
-                  : U[static_cast<i64>(i) * w + c];
-  };
+  int* rowoff = reinterpret_cast<int*>(sm + static_cast<i64>(w) * (w + 1) / 2);
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
+  for (int i = tid; i < w; i += nth) rowoff[i] = i * w - (i * (i - 1)) / 2 - i;  // + c for c >= i
+  __syncthreads();
   for (i64 idx = tid; idx < static_cast<i64>(w) * w; idx += nth) {
     const int i = static_cast<int>(idx / w), c = static_cast<int>(idx % w);
-    if (c >= i) at(i, c) = G[static_cast<i64>(i) * ldg + c];
+    if (c >= i) sm[rowoff[i] + c] = G[static_cast<i64>(i) * ldg + c];
+    else R[static_cast<i64>(i) * ldr + c] = 0.0;
   }
-  __shared__ double s_r;
   __syncthreads();
   for (int j = 0; j < w; ++j) {
+    const double* uj = sm + rowoff[j];
+    const double d = uj[j];
+    const bool bad = !(d > 0.0) || !isfinite(d);
     if (tid == 0) {
-      const double d = at(j, j);
-      const bool bad = !(d > 0.0) || !isfinite(d);
       if (orig2 && !(d > tau2 * orig2[j])) atomicOr(flags, kSuspect);
-      double r = 0.0;
-      if (bad) {
-        if (!psd) atomicOr(flags, kBreakdown);
-      } else {
-        r = sqrt(d);
-      }
-      at(j, j) = r;
-      s_r = r;
+      if (bad && !psd) atomicOr(flags, kBreakdown);
     }
-    __syncthreads();
-    const double inv = s_r > 0.0 ? 1.0 / s_r : 0.0;
-    for (int c = j + 1 + tid; c < w; c += nth) at(j, c) *= inv;
-    __syncthreads();
+    const double inv_r = bad ? 0.0 : 1.0 / sqrt(d);
+    const double inv_d = bad ? 0.0 : 1.0 / d;
+    for (int c = j + tid; c < w; c += nth) R[static_cast<i64>(j) * ldr + c] = c == j ? (bad ? 0.0 : sqrt(d)) : uj[c] * inv_r;
+    // trailing update, warp per row i > j, lanes over columns c >= i
     for (int i = j + 1 + warp; i < w; i += nw) {
-      const double rji = at(j, i);
-      for (int c = i + lane; c < w; c += 32) at(i, c) -= rji * at(j, c);
+      const double f = uj[i] * inv_d;
+      double* ui = sm + rowoff[i];
+      for (int c = i + lane; c < w; c += 32) ui[c] -= f * uj[c];
     }
     __syncthreads();
   }
-  for (i64 idx = tid; idx < static_cast<i64>(w) * w; idx += nth) {
-    const int i = static_cast<int>(idx / w), c = static_cast<int>(idx % w);
-    R[static_cast<i64>(i) * ldr + c] = c >= i ? at(i, c) : 0.0;
-  }
+}
+
+inline size_t chol_smem_bytes(int w) {
+  return sizeof(double) * static_cast<size_t>(w) * (w + 1) / 2 + sizeof(int) * static_cast<size_t>(w);
 }
 
 // Inverse of an upper-triangular R (row-major): one warp per column j of R^-1,
