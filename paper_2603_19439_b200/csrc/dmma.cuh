@@ -174,35 +174,27 @@ __global__ void __launch_bounds__(NT, 3) gram_tn_kernel(GramArgs a) {
     gram_tile<false>(a, ti, tj, r0, r1, dsm);
 }
 
-// Deterministic split reduction; for sym the (min, max) element is read so the
-// result is exactly symmetric.
-__global__ void gram_reduce_kernel(const double* partial, int splits, int m1, int m2, int m1p, int m2p, int sym,
-                                   double* out, int ldo, double alpha) {
-  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Deterministic split reduction, one warp per output element: lane l sums
+// splits l, l+32, ... in order, then a fixed butterfly combines the lanes. For
+// sym the (min, max) element is read so the result is exactly symmetric.
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const double* partial, int splits, int m1, int m2, int m1p,
+                                                          int m2p, int sym, double* out, int ldo, double alpha) {
+  const i64 idx = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (idx >= static_cast<i64>(m1) * m2) return;
   const int i = static_cast<int>(idx / m2), j = static_cast<int>(idx % m2);
   int ii = i, jj = j;
-  if (sym && (i / BM) > (j / BN)) {
-    ii = j;
-    jj = i;
-  } else if (sym && i > j && (i / BM) == (j / BN)) {
+  if (sym && ((i / BM) > (j / BN) || (i > j && (i / BM) == (j / BN)))) {
     ii = j;
     jj = i;
   }
   const i64 stride = static_cast<i64>(m1p) * m2p;
   const double* src = partial + static_cast<i64>(ii) * m2p + jj;
-  // fixed summation order; eight independent loads in flight per thread
   double s = 0.0;
-  int sp = 0;
-  for (; sp + 8 <= splits; sp += 8) {
-    double v[8];
+  for (int sp = lane; sp < splits; sp += 32) s += src[sp * stride];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = src[(sp + u) * stride];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s += v[u];
-  }
-  for (; sp < splits; ++sp) s += src[sp * stride];
-  out[static_cast<i64>(i) * ldo + j] = alpha * s;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[static_cast<i64>(i) * ldo + j] = alpha * s;
 }
 
 
@@ -249,16 +241,17 @@ __global__ void __launch_bounds__(NT) gram_tn_small_kernel(GramArgs a) {
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const i64 nchunks = r1 > r0 ? cdiv(r1 - r0, SBK) : 0;
+  const bool same = a.A == a.B && a.lda == a.ldb;  // A'A: stage the block once
   if (nchunks > 0) {
     load_k_tile32(sA[0], a.A, a.lda, r0, r1, a.m1, a.mask, a.mask_val);
-    load_k_tile32(sB[0], a.B, a.ldb, r0, r1, a.m2, a.mask, a.mask_val);
+    if (!same) load_k_tile32(sB[0], a.B, a.ldb, r0, r1, a.m2, a.mask, a.mask_val);
     cp_async_commit();
   }
   for (i64 c = 0; c < nchunks; ++c) {
     const int s = c & 1;
     if (c + 1 < nchunks) {
       load_k_tile32(sA[s ^ 1], a.A, a.lda, r0 + (c + 1) * SBK, r1, a.m1, a.mask, a.mask_val);
-      load_k_tile32(sB[s ^ 1], a.B, a.ldb, r0 + (c + 1) * SBK, r1, a.m2, a.mask, a.mask_val);
+      if (!same) load_k_tile32(sB[s ^ 1], a.B, a.ldb, r0 + (c + 1) * SBK, r1, a.m2, a.mask, a.mask_val);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -271,7 +264,7 @@ __global__ void __launch_bounds__(NT) gram_tn_small_kernel(GramArgs a) {
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
         fa[x] = sA[s][kk + t][x * 8 + g];
-        fb[x] = sB[s][kk + t][x * 8 + g];
+        fb[x] = same ? fa[x] : sB[s][kk + t][x * 8 + g];
       }
 #pragma unroll
       for (int x = 0; x < 4; ++x)

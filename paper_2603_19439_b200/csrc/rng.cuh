@@ -23,20 +23,28 @@ __device__ __forceinline__ u64 mt_temper(u64 y) {
   return y;
 }
 
-__global__ void __launch_bounds__(160) mt19937_64_kernel(u64 seed, i64 count, u64* out) {
+// Generates tempered outputs [156 b_begin, 156 b_end) of the stream seeded with
+// `seed`. With init the ring is seeded; otherwise it resumes from `state`
+// (the 468-word ring saved by the previous launch), so a speculative prefix
+// can be extended when more words turn out to be needed.
+__global__ void __launch_bounds__(160) mt19937_64_kernel(u64 seed, i64 b_begin, i64 b_end, int init, u64* state,
+                                                         u64* out) {
   __shared__ u64 ring[kMtRing];
   const int i = threadIdx.x;
-  if (i == 0) {  // std::mersenne_twister_engine::seed: x_j = f (x_{j-1} ^ (x_{j-1} >> 62)) + j
-    u64 x = seed;
-    ring[0] = x;
-    for (int j = 1; j < kMtN; ++j) {
-      x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<u64>(j);
-      ring[j] = x;
+  if (init) {
+    if (i == 0) {  // std::mersenne_twister_engine::seed: x_j = f (x_{j-1} ^ (x_{j-1} >> 62)) + j
+      u64 x = seed;
+      ring[0] = x;
+      for (int j = 1; j < kMtN; ++j) {
+        x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<u64>(j);
+        ring[j] = x;
+      }
     }
+  } else {
+    for (int j = i; j < kMtRing; j += blockDim.x) ring[j] = state[j];
   }
   __syncthreads();
-  const i64 blocks = cdiv(count, kMtM);
-  for (i64 b = 0; b < blocks; ++b) {
+  for (i64 b = b_begin; b < b_end; ++b) {
     // new word J + 312 + i from x[J+i], x[J+i+1], x[J+156+i], J = 156 b
     if (i < kMtM) {
       const i64 J = b * kMtM;
@@ -46,11 +54,11 @@ __global__ void __launch_bounds__(160) mt19937_64_kernel(u64 seed, i64 count, u6
       const u64 y = (xi & 0xFFFFFFFF80000000ULL) | (xi1 & 0x7FFFFFFFULL);
       const u64 v = xm ^ (y >> 1) ^ ((y & 1ULL) ? 0xB5026F5AA96619E9ULL : 0ULL);
       ring[(J + kMtN + i) % kMtRing] = v;
-      const i64 o = J + i;
-      if (o < count) out[o] = mt_temper(v);
+      out[J + i] = mt_temper(v);
     }
     __syncthreads();
   }
+  for (int j = i; j < kMtRing; j += blockDim.x) state[j] = ring[j];
 }
 
 // Omega(r, c) = normal #(c * S + r); normals come in (cos, sin) pairs from

@@ -275,10 +275,17 @@ class Session {
       kflush();
       return;
     }
-    Basis b = build_basis(pt, cfg.kind - ST_IASC, basis_seed);
-    timing_mark(1);
     std::vector<double> newvals;
-    rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+    try {
+      Basis b = build_basis(pt, cfg.kind - ST_IASC, basis_seed);
+      timing_mark(1);
+      rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+    } catch (...) {
+      restore_x();
+      cudaStreamSynchronize(st_);
+      throw;
+    }
+    xrestore_.active = false;  // the rotation rewrote the rows of P
     commit_graph(pt);
     values = newvals;
     n = pt.n_total;
@@ -301,6 +308,13 @@ class Session {
         for (i64 i = 0; i < pt.n_total; ++i) z[c * ldz + i] = i < n ? x[static_cast<size_t>(c * n + i)] : 0.0;
       return k;
     }
+    struct Restore {
+      Session* s;
+      ~Restore() {
+        s->restore_x();
+        cudaStreamSynchronize(s->st_);
+      }
+    } restore{this};
     Basis b = build_basis(pt, basis_kind, seed);
     if (b.D > max_cols) throw InvalidArgument("st_probe_basis: output buffer too narrow");
     expand_dense(pt, b.z, b.D, z, ldz);
@@ -638,7 +652,7 @@ class Session {
       launch(dm::gram_tn_small_kernel, dim3(1, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
     else
       launch(dm::gram_tn_kernel, dim3(ntiles, static_cast<unsigned>(splits)), dim3(dm::NT), dm::kGramSmem, st_, a);
-    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
+    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2, 8)), dim3(256), 0, st_,
            static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
            static_cast<int>(m2p), a.sym, out, ldo, alpha);
     kend();
@@ -1351,44 +1365,110 @@ class Session {
   }
 
   // Omega (S x q, rng.hpp:64-69 fill order) generated on the side stream; the
-  // consumer waits on ev_rng_. Launched once per (seed, S, q).
+  // consumer waits on ev_rng_. The raw mt19937_64 words depend only on the
+  // seed, and the next step's seed is known (trackers.cpp:362), so after each
+  // sketch the side stream speculatively generates a prefix of the next
+  // step's stream; a step that needs more words resumes it from the saved ring.
   u64 omega_seed_ = 0;
   i64 omega_S_ = -1;
   int omega_q_ = -1;
+  u64 pre_seed_ = 0;      // seed of the raw words in mt_raw (rseed)
+  i64 pre_blocks_ = -1;   // 156-word blocks already generated for pre_seed_
+  i64 raw_cap_ = 0;       // capacity of mt_raw in words
+  u64* raw_ = nullptr;
+  u64* ring_state_ = nullptr;
+
+  void ensure_raw(i64 words) {
+    if (words <= raw_cap_) return;
+    STG_CUDA(cudaStreamSynchronize(st_rng_));
+    raw_cap_ = round_up(words + words / 2, kMtM);
+    raw_ = arena_.get<u64>("mt_raw", raw_cap_);
+    pre_blocks_ = -1;  // contents lost
+  }
+
+  void generate_raw(u64 rseed, i64 blocks_needed) {
+    if (!ring_state_) ring_state_ = arena_.get<u64>("mt_ring", kMtRing);
+    ensure_raw(blocks_needed * kMtM);
+    if (pre_seed_ == rseed && pre_blocks_ >= 0) {
+      if (pre_blocks_ >= blocks_needed) return;
+      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, pre_blocks_, blocks_needed, 0, ring_state_, raw_);
+    } else {
+      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, static_cast<i64>(0), blocks_needed, 1,
+             ring_state_, raw_);
+    }
+    pre_seed_ = rseed;
+    pre_blocks_ = blocks_needed;
+  }
+
   void prepare_omega(u64 seed, i64 S, int q, double** omega, int* ldo_out) {
     const int ldo = ld_for(q);
     double* om = arena_.get<double>("omega", S * ldo);
     if (!(omega_seed_ == seed && omega_S_ == S && omega_q_ == q)) {
       const i64 npairs = cdiv(S * q, 2);
-      u64* raw = arena_.get<u64>("mt_raw", 2 * npairs);
       const u64 rseed = mix_seed(seed, 0x5bdULL);
       kbegin(kRng, 2.0 * npairs, st_rng_);
-      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, rseed, 2 * npairs, raw);
-      launch(box_muller_kernel, dim3(blocks(npairs)), dim3(256), 0, st_rng_, static_cast<const u64*>(raw), npairs, S,
+      generate_raw(rseed, cdiv(2 * npairs, kMtM));
+      launch(box_muller_kernel, dim3(blocks(npairs)), dim3(256), 0, st_rng_, static_cast<const u64*>(raw_), npairs, S,
              q, om, ldo);
       kend(st_rng_);
       STG_CUDA(cudaEventRecord(ev_rng_, st_rng_));
       omega_seed_ = seed;
       omega_S_ = S;
       omega_q_ = q;
+      // speculative prefix of the next step's stream (runs behind this step)
+      const u64 next = mix_seed(mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken + 1), 0x5bdULL);
+      const i64 guess = cdiv(2 * npairs + 2 * npairs / 8, kMtM);
+      pre_seed_ = 0;
+      pre_blocks_ = -1;
+      ensure_raw(guess * kMtM);
+      launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_rng_, next, static_cast<i64>(0), guess, 1, ring_state_,
+             raw_);
+      pre_seed_ = next;
+      pre_blocks_ = guess;
     }
     *omega = om;
     *ldo_out = ldo;
   }
 
+  // X-bar in stacked coordinates [X_P; R_c; I]. K = X_out' X_out is a plain
+  // Gram of X after the rows of P (already copied into Z) are zeroed in place;
+  // restore_x() writes them back if the step fails, and the final rotation
+  // overwrites them on success.
+  struct XRestore {
+    bool active = false;
+    const int* P = nullptr;
+    i64 p_old = 0;
+    const double* z = nullptr;
+    int ldz = 0;
+  } xrestore_;
+
+  void restore_x() {
+    if (!xrestore_.active) return;
+    launch(restore_rows_kernel, dim3(blocks(xrestore_.p_old, 8)), dim3(256), 0, st_, X_, ldx(), xrestore_.P,
+           xrestore_.p_old, xrestore_.z, xrestore_.ldz, static_cast<int>(k));
+    xrestore_.active = false;
+  }
+
   void build_xbar(const Pert& pt, Blk z) {
     const i64 p = pt.p;
     const int kk = static_cast<int>(k);
-    double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ld_for(kk));
-    if (!pt.dense) {
-      double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ld_for(kk));
-      gram(X_, ldx(), X_, ldx(), pt.n_old, kk, kk, true, kc, ld_for(kk), 1.0, pt.mark, pt.stamp);
-      chol(kc, ld_for(kk), kk, rc, ld_for(kk), nullptr, 0.0, true);
-    } else {
-      STG_CUDA(cudaMemsetAsync(rc, 0, sizeof(double) * kk * ld_for(kk), st_));
-    }
+    const int ldr = ld_for(kk);
+    double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ldr);
     launch(gather_xbar_kernel, dim3(blocks((p + 2 * k) * k)), dim3(256), 0, st_, static_cast<const double*>(X_), ldx(),
-           pt.P, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(rc), ld_for(kk), z.p, z.ld);
+           pt.P, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(nullptr), ldr, z.p, z.ld);
+    if (!pt.dense) {
+      if (pt.p_old > 0) {
+        launch(zero_rows_kernel, dim3(blocks(pt.p_old, 8)), dim3(256), 0, st_, X_, ldx(), pt.P, pt.p_old, kk);
+        xrestore_ = XRestore{true, pt.P, pt.p_old, z.p, z.ld};
+      }
+      double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ldr);
+      gram(X_, ldx(), X_, ldx(), pt.n_old, kk, kk, true, kc, ldr);
+      chol(kc, ldr, kk, rc, ldr, nullptr, 0.0, true);
+      launch(copy2d_kernel, dim3(blocks(k * k)), dim3(256), 0, st_, static_cast<const double*>(rc), ldr, z.p + p * z.ld,
+             z.ld, k, kk);
+    } else {  // dense mode: no rows outside P, K = 0
+      STG_CUDA(cudaMemset2DAsync(z.p + p * z.ld, sizeof(double) * z.ld, 0, sizeof(double) * kk, k, st_));
+    }
   }
 
   // ---------------------------------------------------------------- Rayleigh-Ritz
@@ -1689,12 +1769,14 @@ st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_
     if (rows * cols == 0) return;
     STG_CUDA(cudaSetDevice(device));
     const int64_t npairs = (rows * cols + 1) / 2;
-    stg::u64* raw;
+    const int64_t nblocks = (2 * npairs + stg::kMtM - 1) / stg::kMtM;
+    stg::u64 *raw, *ring;
     double* om;
     const int ld = static_cast<int>(cols);
-    STG_CUDA(cudaMalloc(&raw, sizeof(stg::u64) * 2 * npairs));
+    STG_CUDA(cudaMalloc(&raw, sizeof(stg::u64) * nblocks * stg::kMtM));
+    STG_CUDA(cudaMalloc(&ring, sizeof(stg::u64) * stg::kMtRing));
     STG_CUDA(cudaMalloc(&om, sizeof(double) * rows * cols));
-    stg::mt19937_64_kernel<<<1, 160>>>(seed, 2 * npairs, raw);
+    stg::mt19937_64_kernel<<<1, 160>>>(seed, 0, nblocks, 1, ring, raw);
     STG_LAUNCH();
     stg::box_muller_kernel<<<static_cast<unsigned>((npairs + 255) / 256), 256>>>(raw, npairs, rows,
                                                                                  static_cast<int>(cols), om, ld);
@@ -1704,6 +1786,7 @@ st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_
     for (int64_t c = 0; c < cols; ++c)
       for (int64_t r = 0; r < rows; ++r) out_colmajor[c * rows + r] = rm[static_cast<size_t>(r * cols + c)];
     cudaFree(raw);
+    cudaFree(ring);
     cudaFree(om);
   });
 }

@@ -20,11 +20,30 @@ __global__ void gather_xbar_kernel(const double* X, int ldx, const int* P, int d
     if (t < p_old) v = X[(dense ? t : static_cast<i64>(P[t])) * ldx + c];
     else v = 0.0;
   } else if (t < p + k) {
+    if (!rc) return;  // written later (K from the zeroed-row Gram)
     v = rc[(t - p) * ldrc + c];
   } else {
     v = (t - p - k == c) ? 1.0 : 0.0;
   }
   z[t * ldz + c] = v;
+}
+
+// X rows of P (old nodes) zeroed in place / restored from the stacked copy.
+__global__ void __launch_bounds__(256) zero_rows_kernel(double* X, int ldx, const int* P, i64 p_old, int k) {
+  const i64 t = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= p_old) return;
+  double* xr = X + static_cast<i64>(P[t]) * ldx;
+  for (int c = lane; c < k; c += 32) xr[c] = 0.0;
+}
+
+__global__ void __launch_bounds__(256) restore_rows_kernel(double* X, int ldx, const int* P, i64 p_old,
+                                                           const double* z, int ldz, int k) {
+  const i64 t = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= p_old) return;
+  double* xr = X + static_cast<i64>(P[t]) * ldx;
+  for (int c = lane; c < k; c += 32) xr[c] = z[t * ldz + c];
 }
 
 // iasc: unit vectors of the appended nodes (z points at column k).
