@@ -60,20 +60,25 @@ __device__ __forceinline__ void load_k_tile(double (*s)[SST], const double* g, i
 }
 
 // 32 rows per stage (8 DMMA k-steps between barriers), double-buffered in
-// dynamic shared memory. Tiles entirely inside the matrix take the FULL path
-// with no per-subtile predicates, so the unrolled k-loop schedules freely.
+// dynamic shared memory. The CTA tile is (32 WM) x (32 WN) with WM * WN = 4
+// warps: 64 x 64 for square Grams, 32 x 128 / 128 x 32 when one side is the
+// k = 32 tracked block, so no warp idles on an empty half-tile. Tiles entirely
+// inside the matrix take the FULL path with no per-subtile predicates.
 constexpr int BK2 = 32;
-constexpr size_t kGramSmem = sizeof(double) * 2 * 2 * BK2 * SST;
+constexpr size_t gram_smem(int WM, int WN) { return sizeof(double) * 2 * BK2 * ((32 * WM + 4) + (32 * WN + 4)); }
+constexpr size_t kGramSmem = gram_smem(1, 4);  // the largest layout
 
-__device__ __forceinline__ void load_k_tile32r(double* s, const double* g, int ld, i64 r, i64 rend, int c0, int m,
-                                               const int* mask, int mask_val) {
+template <int TW>
+__device__ __forceinline__ void load_k_tile_w(double* s, const double* g, int ld, i64 r, i64 rend, int c0, int m,
+                                              const int* mask, int mask_val) {
+  constexpr int STR = TW + 4, PAIRS = TW / 2, CH = BK2 * PAIRS / NT;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const int c = threadIdx.x + NT * q;  // 1024 chunks: 32 rows x 32 pairs
-    const int row = c >> 5, col = (c & 31) * 2;
+  for (int q = 0; q < CH; ++q) {
+    const int c = threadIdx.x + NT * q;
+    const int row = c / PAIRS, col = (c % PAIRS) * 2;
     i64 gr = r + row;
     const int gc = c0 + col;
-    double* dst = s + row * SST + col;
+    double* dst = s + row * STR + col;
     if (mask && gr < rend && mask[gr] == mask_val) gr = rend;
     if (gr < rend && gc + 2 <= m) {
       cp_async_pair(dst, g + gr * ld + gc);
@@ -84,14 +89,15 @@ __device__ __forceinline__ void load_k_tile32r(double* s, const double* g, int l
   }
 }
 
-template <bool FULL>
+template <bool FULL, int WM, int WN>
 __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64 r0, i64 r1, double* smem) {
-  double* sA = smem;                   // [2][BK2][SST]
-  double* sB = smem + 2 * BK2 * SST;   // [2][BK2][SST]
+  constexpr int TA = 32 * WM, TB = 32 * WN, SA = TA + 4, SB = TB + 4;
+  double* sA = smem;                   // [2][BK2][SA]
+  double* sB = smem + 2 * BK2 * SA;    // [2][BK2][SB]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int ibase = ti * BM + wm * 32, jbase = tj * BN + wn * 32;
+  const int wm = warp % WM, wn = warp / WM;
+  const int ibase = ti * TA + wm * 32, jbase = tj * TB + wn * 32;
   bool vi[4], vj[4];
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
@@ -105,32 +111,32 @@ __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const i64 nchunks = r1 > r0 ? cdiv(r1 - r0, BK2) : 0;
   if (nchunks > 0) {
-    load_k_tile32r(sA, a.A, a.lda, r0, r1, ti * BM, a.m1, a.mask, a.mask_val);
-    load_k_tile32r(sB, a.B, a.ldb, r0, r1, tj * BN, a.m2, a.mask, a.mask_val);
+    load_k_tile_w<TA>(sA, a.A, a.lda, r0, r1, ti * TA, a.m1, a.mask, a.mask_val);
+    load_k_tile_w<TB>(sB, a.B, a.ldb, r0, r1, tj * TB, a.m2, a.mask, a.mask_val);
     cp_async_commit();
   }
   for (i64 c = 0; c < nchunks; ++c) {
     const int s = c & 1;
     if (c + 1 < nchunks) {
-      load_k_tile32r(sA + (s ^ 1) * BK2 * SST, a.A, a.lda, r0 + (c + 1) * BK2, r1, ti * BM, a.m1, a.mask,
-                     a.mask_val);
-      load_k_tile32r(sB + (s ^ 1) * BK2 * SST, a.B, a.ldb, r0 + (c + 1) * BK2, r1, tj * BN, a.m2, a.mask,
-                     a.mask_val);
+      load_k_tile_w<TA>(sA + (s ^ 1) * BK2 * SA, a.A, a.lda, r0 + (c + 1) * BK2, r1, ti * TA, a.m1, a.mask,
+                        a.mask_val);
+      load_k_tile_w<TB>(sB + (s ^ 1) * BK2 * SB, a.B, a.ldb, r0 + (c + 1) * BK2, r1, tj * TB, a.m2, a.mask,
+                        a.mask_val);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* pa = sA + s * BK2 * SST + t * SST + wm * 32 + g;
-    const double* pb = sB + s * BK2 * SST + t * SST + wn * 32 + g;
+    const double* pa = sA + s * BK2 * SA + t * SA + wm * 32 + g;
+    const double* pb = sB + s * BK2 * SB + t * SB + wn * 32 + g;
 #pragma unroll
     for (int kk = 0; kk < BK2; kk += 4) {
       double fa[4], fb[4];
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
-        fa[x] = pa[kk * SST + x * 8];
-        fb[x] = pb[kk * SST + x * 8];
+        fa[x] = pa[kk * SA + x * 8];
+        fb[x] = pb[kk * SB + x * 8];
       }
 #pragma unroll
       for (int x = 0; x < 4; ++x)
@@ -140,7 +146,7 @@ __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64
     }
     __syncthreads();
   }
-  const i64 m1p = static_cast<i64>(a.tiles_i) * BM, m2p = static_cast<i64>(a.tiles_j) * BN;
+  const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
   double* out = a.partial + static_cast<i64>(blockIdx.y) * m1p * m2p;
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -151,7 +157,8 @@ __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) gram_tn_kernel(GramArgs a) {
+template <int WM, int WN>
+__global__ void __launch_bounds__(NT, WM == WN ? 3 : 2) gram_tn_kernel(GramArgs a) {
   extern __shared__ __align__(16) double dsm[];
   int ti, tj;
   if (a.sym) {
@@ -168,10 +175,10 @@ __global__ void __launch_bounds__(NT, 3) gram_tn_kernel(GramArgs a) {
   }
   const i64 r0 = static_cast<i64>(blockIdx.y) * a.rows_per_split;
   const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
-  if ((ti + 1) * BM <= a.m1 && (tj + 1) * BN <= a.m2)
-    gram_tile<true>(a, ti, tj, r0, r1, dsm);
+  if ((ti + 1) * 32 * WM <= a.m1 && (tj + 1) * 32 * WN <= a.m2)
+    gram_tile<true, WM, WN>(a, ti, tj, r0, r1, dsm);
   else
-    gram_tile<false>(a, ti, tj, r0, r1, dsm);
+    gram_tile<false, WM, WN>(a, ti, tj, r0, r1, dsm);
 }
 
 // Deterministic split reduction, one warp per output element: lane l sums
@@ -339,6 +346,21 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  // beta * B for the epilogue: issued before the K loop so its latency
+  // overlaps the operand loads (the short-K projections are memory bound)
+  double bpre[4][4][2];
+  if (FULL && a.beta != 0.0) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const i64 r = row0 + wm * 32 + x * 8 + g;
+        const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
+        const double2 v = *reinterpret_cast<const double2*>(a.Bm + r * a.ldb + col);
+        bpre[x][y][0] = v.x;
+        bpre[x][y][1] = v.y;
+      }
+  }
   auto load = [&](int s, int k0) {
     double* A_s = sA + s * BM * SAR2;
     double* C_s = sC + s * BK2 * SST;
@@ -408,10 +430,19 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
     for (int y = 0; y < 4; ++y) {
       const i64 r = row0 + wm * 32 + x * 8 + g;
       const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
-      if (!FULL && r >= a.nrows) continue;
+      if (FULL) {
+        double2 v = make_double2(a.alpha * acc[x][y][0], a.alpha * acc[x][y][1]);
+        if (a.beta != 0.0) {
+          v.x += a.beta * bpre[x][y][0];
+          v.y += a.beta * bpre[x][y][1];
+        }
+        *reinterpret_cast<double2*>(a.Out + r * a.ldo + col) = v;
+        continue;
+      }
+      if (r >= a.nrows) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (!FULL && col + h >= a.m2) continue;
+        if (col + h >= a.m2) continue;
         double v = a.alpha * acc[x][y][h];
         if (a.beta != 0.0) v += a.beta * a.Bm[r * a.ldb + col + h];
         a.Out[r * a.ldo + col + h] = v;

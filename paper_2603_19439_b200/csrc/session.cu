@@ -198,8 +198,12 @@ class Session {
     if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
     cusolverDnSetStream(solver_, st_);
     STG_CUDA(cudaMallocHost(&hs_, sizeof(Scalars)));
-    STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(dm::kGramSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_smem(2, 2))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_smem(1, 4))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_smem(4, 1))));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
     d_scal_ = arena_.get<u64>("scalars", 32);
@@ -629,29 +633,38 @@ class Session {
     a.nrows = rows;
     a.m1 = m1;
     a.m2 = m2;
-    a.tiles_i = static_cast<int>(cdiv(m1, dm::BM));
-    a.tiles_j = static_cast<int>(cdiv(m2, dm::BN));
+    // layout: 64 x 64 tiles, or 32 x 128 / 128 x 32 when one side is <= 32 wide
+    const bool narrow = m1 <= 32 && m2 <= 32;
+    const int layout = narrow ? -1 : (!sym && m1 <= 32) ? 1 : (!sym && m2 <= 32) ? 2 : 0;
+    const int TA = layout == 1 ? 32 : layout == 2 ? 128 : 64;
+    const int TB = layout == 1 ? 128 : layout == 2 ? 32 : 64;
+    a.tiles_i = static_cast<int>(cdiv(m1, TA));
+    a.tiles_j = static_cast<int>(cdiv(m2, TB));
     a.sym = sym ? 1 : 0;
     a.mask = mask;
     a.mask_val = mask_val;
-    const bool narrow = m1 <= 32 && m2 <= 32;
     if (narrow) a.tiles_i = a.tiles_j = 1;
     const int ntiles = narrow ? 1 : (sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j);
-    const i64 target = 148 * 6;
+    const i64 target = 148 * (layout == 0 ? 6 : 4);
     const i64 rows_min = narrow ? 256 : 128;
     i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
     splits = std::min<i64>(splits, 65535);
     a.rows_per_split = round_up(cdiv(std::max<i64>(rows, 1), splits), narrow ? dm::SBK : dm::BK2);
     splits = std::max<i64>(1, cdiv(std::max<i64>(rows, 1), a.rows_per_split));
-    const i64 m1p = narrow ? 32 : static_cast<i64>(a.tiles_i) * dm::BM;
-    const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * dm::BN;
+    const i64 m1p = narrow ? 32 : static_cast<i64>(a.tiles_i) * TA;
+    const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * TB;
     a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "gram %lldx%dx%d%s", rows, m1, m2, sym ? " sym" : "");
     kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
+    const dim3 grid(ntiles, static_cast<unsigned>(splits));
     if (narrow)
-      launch(dm::gram_tn_small_kernel, dim3(1, static_cast<unsigned>(splits)), dim3(dm::NT), 0, st_, a);
+      launch(dm::gram_tn_small_kernel, grid, dim3(dm::NT), 0, st_, a);
+    else if (layout == 1)
+      launch(dm::gram_tn_kernel<1, 4>, grid, dim3(dm::NT), dm::gram_smem(1, 4), st_, a);
+    else if (layout == 2)
+      launch(dm::gram_tn_kernel<4, 1>, grid, dim3(dm::NT), dm::gram_smem(4, 1), st_, a);
     else
-      launch(dm::gram_tn_kernel, dim3(ntiles, static_cast<unsigned>(splits)), dim3(dm::NT), dm::kGramSmem, st_, a);
+      launch(dm::gram_tn_kernel<2, 2>, grid, dim3(dm::NT), dm::gram_smem(2, 2), st_, a);
     launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2, 8)), dim3(256), 0, st_,
            static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
            static_cast<int>(m2p), a.sym, out, ldo, alpha);
