@@ -57,7 +57,7 @@ typedef struct {
 #define ST_FLAG_FORCE_DENSE 1  /* disable the compressed row-subset representation */
 #define ST_FLAG_TIMING 2       /* record per-phase CUDA-event timings */
 #define ST_FLAG_KERNEL_TIMING 4 /* record per-kernel-class CUDA-event timings (st_kernel_stats) */
-#define ST_FLAG_DEVICE_EIG 8    /* projected eigensolves with the one-CTA solver instead of cuSOLVER syevd */
+#define ST_FLAG_CUSOLVER_EIG 8  /* projected eigensolves with cuSOLVER syevd instead of the on-device solver */
 
 /* One update batch: the edit lists of assemble_update (graph.hpp:65-69).
  * added (i, j, w) and removed (i, j) address existing nodes; new_edges

@@ -26,7 +26,7 @@ KIND = {"iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6}
 BASIS = {"iasc": 0, "grest2": 1, "grest3": 2, "grest-rsvd": 3}
 OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
 ORDER = {"abs_desc": 0, "alg_desc": 1}
-FLAG_FORCE_DENSE, FLAG_TIMING, FLAG_KERNEL_TIMING, FLAG_DEVICE_EIG = 1, 2, 4, 8
+FLAG_FORCE_DENSE, FLAG_TIMING, FLAG_KERNEL_TIMING, FLAG_CUSOLVER_EIG = 1, 2, 4, 8
 KERNEL_CLASSES = ["dmma_gram", "dmma_gemm", "spmm", "cholesky", "tri_inverse", "eigensolver", "csr_merge", "rng",
                   "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other"]
 
@@ -154,7 +154,7 @@ class TrackerSession:
 
     def __init__(self, rowptr, col, val, values, vectors, kind="grest-rsvd", k=None, order="abs_desc",
                  rsvd_l=100, rsvd_p=100, seed=0, operator="adjacency", device=0, force_dense=False, timing=False,
-                 kernel_timing=False, device_eig=False):
+                 kernel_timing=False, cusolver_eig=False):
         L = lib()
         rowptr = np.ascontiguousarray(rowptr, np.int32)
         col = np.ascontiguousarray(col, np.int32)
@@ -164,7 +164,7 @@ class TrackerSession:
         n = len(rowptr) - 1
         k = len(values) if k is None else k
         flags = ((FLAG_FORCE_DENSE if force_dense else 0) | (FLAG_TIMING if timing else 0)
-                 | (FLAG_KERNEL_TIMING if kernel_timing else 0) | (FLAG_DEVICE_EIG if device_eig else 0))
+                 | (FLAG_KERNEL_TIMING if kernel_timing else 0) | (FLAG_CUSOLVER_EIG if cusolver_eig else 0))
         cfg = StConfig(KIND[kind], OPERATOR[operator], k, ORDER[order], rsvd_l, rsvd_p, seed, device, flags)
         h = C.c_void_p()
         rc = L.st_create(C.byref(cfg), n, _p(rowptr, I32P), _p(col, I32P), _p(val), _p(values),

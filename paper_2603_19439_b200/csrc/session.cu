@@ -393,7 +393,7 @@ class Session {
         case 4: {
           double* w = arena_.get<double>("bk_w", m1);
           const int saved = cfg.flags;
-          cfg.flags |= ST_FLAG_DEVICE_EIG;
+          cfg.flags &= ~ST_FLAG_CUSOLVER_EIG;
           eig_fast(C, ld1, m1, 0, m2, w, O, ld2);
           cfg.flags = saved;
           break;
@@ -765,31 +765,27 @@ class Session {
   // spectral order (w_sorted) and the leading `want` eigenvectors (F, row-major).
   bool eig_fast(const double* M, int ldm, int D, int order, int want, double* w_sorted, double* F, int ldf,
                 double ortol = 1e-3) {
-    // The one-CTA solver is still slower than cuSOLVER syevd at the step's
-    // orders, so the step uses it only on request.
-    if (!(cfg.flags & ST_FLAG_DEVICE_EIG)) return false;
+    // cuSOLVER syevd on request (ST_FLAG_CUSOLVER_EIG) or above the one-CTA
+    // tridiagonalization's shared-memory limit
+    if (cfg.flags & ST_FLAG_CUSOLVER_EIG) return false;
     if (D > kEigMaxN || want > kEigMaxWant) return false;
     static bool attr = false;
     if (!attr) {
-      STG_CUDA(cudaFuncSetAttribute(syev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(syev_smem_bytes(kEigMaxN))));
+      STG_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(std::max(tridiag_smem_bytes(kEigMaxN),
+                                                              tridiag_smem_bytes(kEigFullN)))));
+      STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(invit_smem_bytes(kEigMaxN))));
       attr = true;
     }
-    EigArgs ea{};
-    ea.M = M;
-    ea.ldm = ldm;
-    ea.n = D;
-    ea.order = order;
-    ea.want = want;
-    ea.w_sorted = w_sorted;
-    ea.F = F;
-    ea.ldf = ldf;
-    ea.work = arena_.get<double>("eig_work_inv", static_cast<i64>(std::max(want, 1)) * 6 * D);
-    ea.flags = flags_ptr();
-    ea.info = info_ptr();
-    ea.ortol = ortol;
+    const int wv = std::max(want, 1);
+    double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(D, wv)));
+    int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(D, wv)));
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "device syev D=%d want=%d", D, want);
     kbegin(kEig, 4.0 * D * D * D / 3.0);
-    launch(syev_kernel, dim3(1), dim3(1024), syev_smem_bytes(D), st_, ea);
+    STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
+    syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, st_, args...); },
+                M, ldm, D, order, wv, ortol, w_sorted, F, ldf, dbuf, ibuf, flags_ptr());
     kend();
     return true;
   }
@@ -1714,55 +1710,50 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
     if (n == 0) return;
     if (n > stg::kEigMaxN) throw std::invalid_argument("st_sym_eig_dense: order above the on-device solver limit");
     STG_CUDA(cudaSetDevice(device));
-    static bool attr = false;
-    if (!attr) {
-      STG_CUDA(cudaFuncSetAttribute(stg::syev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(stg::syev_smem_bytes(stg::kEigMaxN))));
-      attr = true;
-    }
-    // row-major copy of S' (the kernel symmetrizes (S + S')/2 itself)
+    STG_CUDA(cudaFuncSetAttribute(stg::tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(std::max(stg::tridiag_smem_bytes(stg::kEigMaxN),
+                                                            stg::tridiag_smem_bytes(stg::kEigFullN)))));
+    STG_CUDA(cudaFuncSetAttribute(stg::invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(stg::invit_smem_bytes(stg::kEigMaxN))));
+    // row-major copy of S' (the solver symmetrizes (S + S')/2 itself)
     std::vector<double> rm(static_cast<size_t>(n * n));
     for (int64_t i = 0; i < n; ++i)
       for (int64_t j = 0; j < n; ++j) rm[static_cast<size_t>(i * n + j)] = s_colmajor[j * n + i];
-    double *dm, *dw, *df, *work;
-    int* di;
+    double *dm, *dw, *df, *dbuf;
+    int *di, *ibuf;
     const int64_t wv = std::max<int64_t>(want, 1);
     STG_CUDA(cudaMalloc(&dm, sizeof(double) * n * n));
     STG_CUDA(cudaMalloc(&dw, sizeof(double) * n));
     STG_CUDA(cudaMalloc(&df, sizeof(double) * n * wv));
-    STG_CUDA(cudaMalloc(&work, sizeof(double) * 6 * n * wv));
+    STG_CUDA(cudaMalloc(&dbuf, sizeof(double) * stg::eig_scratch_doubles(static_cast<int>(n), static_cast<int>(wv))));
+    STG_CUDA(cudaMalloc(&ibuf, sizeof(int) * stg::eig_scratch_ints(static_cast<int>(n), static_cast<int>(wv))));
     STG_CUDA(cudaMalloc(&di, sizeof(int) * 2));
     STG_CUDA(cudaMemset(di, 0, sizeof(int) * 2));
     STG_CUDA(cudaMemcpy(dm, rm.data(), sizeof(double) * n * n, cudaMemcpyHostToDevice));
-    stg::EigArgs ea{};
-    ea.M = dm;
-    ea.ldm = static_cast<int>(n);
-    ea.n = static_cast<int>(n);
-    ea.order = order;
-    ea.want = static_cast<int>(want);
-    ea.w_sorted = dw;
-    ea.F = df;
-    ea.ldf = static_cast<int>(wv);
-    ea.work = work;
-    ea.flags = di;
-    ea.info = di + 1;
-    ea.ortol = 1e-3;
-    long long* prof = nullptr;
-    if (getenv("STG_EIG_PROF")) {
-      STG_CUDA(cudaMalloc(&prof, sizeof(long long) * 8));
-      ea.prof = prof;
-    }
-    stg::syev_kernel<<<1, 1024, stg::syev_smem_bytes(static_cast<int>(n))>>>(ea);
-    STG_LAUNCH();
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    stg::syev_launch(
+        [&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) {
+          kernel<<<g, bl, sm>>>(args...);
+          STG_LAUNCH();
+        },
+        dm, static_cast<int>(n), static_cast<int>(n), order, static_cast<int>(wv), 1e-3, dw, df,
+        static_cast<int>(wv), dbuf, ibuf, di);
+    cudaEventRecord(e1);
     STG_CUDA(cudaDeviceSynchronize());
-    if (prof) {
-      long long hp[8];
-      STG_CUDA(cudaMemcpy(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "syev n=%lld want=%lld cycles: sym %lld tridiag %lld bisect %lld order %lld invit %lld back %lld\n",
-              static_cast<long long>(n), static_cast<long long>(want), hp[1] - hp[0], hp[2] - hp[1], hp[3] - hp[2],
-              hp[4] - hp[3], hp[5] - hp[4], hp[6] - hp[5]);
-      cudaFree(prof);
+    if (getenv("STG_EIG_PROF")) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      fprintf(stderr, "device syev n=%lld want=%lld: %.3f ms\n", static_cast<long long>(n),
+              static_cast<long long>(want), ms);
     }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    int hflags = 0;
+    STG_CUDA(cudaMemcpy(&hflags, di, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hflags & stg::kNonFinite) throw std::invalid_argument("sym_eig_dense: non-finite entries");
     std::vector<double> f(static_cast<size_t>(n * wv));
     STG_CUDA(cudaMemcpy(values, dw, sizeof(double) * n, cudaMemcpyDeviceToHost));
     STG_CUDA(cudaMemcpy(f.data(), df, sizeof(double) * n * wv, cudaMemcpyDeviceToHost));
@@ -1771,7 +1762,8 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
     cudaFree(dm);
     cudaFree(dw);
     cudaFree(df);
-    cudaFree(work);
+    cudaFree(dbuf);
+    cudaFree(ibuf);
     cudaFree(di);
   });
 }

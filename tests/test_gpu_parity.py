@@ -168,18 +168,18 @@ def test_config1_parity_all_steps():
         check_state(gpu, orc, tag=f"cfg1 step {t}")
 
 
-def test_device_eigensolver_in_the_step():
-    # the one-CTA eigensolver (ST_FLAG_DEVICE_EIG) in place of cuSOLVER, on the RSVD path
+def test_cusolver_eigensolver_in_the_step():
+    # cuSOLVER syevd (ST_FLAG_CUSOLVER_EIG) in place of the on-device solver, on the RSVD path
     from paper_2603_19439_b200 import streams
     keys = streams.rmat_keys(12, 16, seed=9)
     s = streams.edit_stream(1 << 12, keys, 3, 10, lambda m: 20, lambda m: 0.005 * m,
                             new_nodes=lambda nn: 3 * nn // 100, new_degree=6)
     rp, col, val = s.csr0()
-    gpu, orc = pair(rp, col, val, kind="grest-rsvd", k=8, seed=2, rsvd_l=40, rsvd_p=20, device_eig=True)
+    gpu, orc = pair(rp, col, val, kind="grest-rsvd", k=8, seed=2, rsvd_l=40, rsvd_p=20, cusolver_eig=True)
     for t, upd in enumerate(s.updates):
         gpu.step(upd)
         orc.step(upd)
-        check_state(gpu, orc, tag=f"device-eig step {t}")
+        check_state(gpu, orc, tag=f"cusolver-eig step {t}")
 
 
 def test_rsvd_path_rmat_parity():

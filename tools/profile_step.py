@@ -26,7 +26,7 @@ n = len(rp) - 1
 x, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((n, args.k)))
 vals = np.linspace(100.0, 10.0, args.k)
 g = TrackerSession(rp, col, val, vals, x, kind="grest-rsvd", k=args.k, seed=0, timing=True,
-                   kernel_timing=bool(os.environ.get("STG_KLOG")))
+                   kernel_timing=bool(os.environ.get("STG_KLOG")), cusolver_eig=bool(os.environ.get("STG_CUSOLVER")))
 for t, u in enumerate(s.updates):
     t0 = time.perf_counter()
     g.step(u)
