@@ -23,6 +23,8 @@
 // O(eps ||S|| / gap); clusters get an orthonormal basis of their span.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include <cfloat>
 
 #include "common.cuh"
@@ -265,6 +267,128 @@ __global__ void __launch_bounds__(1024) tridiag_kernel(const double* M, int ldm,
 inline size_t tridiag_smem_bytes(int n) {
   const size_t words = n <= kEigFullN ? static_cast<size_t>(n) * n : static_cast<size_t>(n) * (n + 1) / 2;
   return sizeof(double) * (words + 3 * static_cast<size_t>(n) + 48);
+}
+
+// Tridiagonalization on a thread-block cluster: the 8 CTAs of one cluster own
+// the rows r = rank (mod 8) in full (n <= kEigMaxN: <= 30 rows x 232 cols per
+// CTA in shared memory). Per column: the owner of row i builds the reflector
+// and broadcasts it through distributed shared memory, every CTA computes
+// p = tau A v for its rows and all-gathers it, then updates its rows. Two
+// cluster barriers per column; v / p / partial buffers alternate by column
+// parity so a CTA never overwrites a buffer another CTA is still reading.
+constexpr int kClusterCtas = 8;
+constexpr int kTriClusterThreads = 256;
+
+__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kTriClusterThreads)
+    tridiag_cluster_kernel(const double* M, int ldm, int n, EigBufs b, int* flags) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = static_cast<int>(cluster.block_rank());
+  extern __shared__ double sm[];
+  const int nloc = (n - rank + kClusterCtas - 1) / kClusterCtas;  // rows rank, rank+8, ...
+  const int nmax = (n + kClusterCtas - 1) / kClusterCtas;          // same layout in every CTA (DSMEM offsets)
+  double* rows = sm;                                   // nmax x n
+  double* vbuf = rows + static_cast<i64>(nmax) * n;    // [2][n]
+  double* pbuf = vbuf + 2 * n;                         // [2][n]
+  double* part = pbuf + 2 * n;                         // [2][kClusterCtas]
+  double* scal = part + 2 * kClusterCtas;              // [2] tau per parity
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (i64 idx = tid; idx < static_cast<i64>(nloc) * n; idx += blockDim.x) {
+    const int lr = static_cast<int>(idx / n), c = static_cast<int>(idx % n);
+    const int r = rank + lr * kClusterCtas;
+    const double x = M[static_cast<i64>(r) * ldm + c], y = M[static_cast<i64>(c) * ldm + r];
+    if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
+    rows[static_cast<i64>(lr) * n + c] = 0.5 * (x + y);
+  }
+  cluster.sync();
+  for (int i = 0; i + 1 < n; ++i) {
+    const int par = i & 1, r0 = i + 1;
+    double* v = vbuf + par * n;
+    double* p = pbuf + par * n;
+    // 1. the owner of row i (= column i below the diagonal) builds the reflector
+    if (i % kClusterCtas == rank && warp == 0) {
+      const double* ri = rows + static_cast<i64>(i / kClusterCtas) * n;
+      double sg = 0.0;
+      for (int c = r0 + 1 + lane; c < n; c += 32) sg += ri[c] * ri[c];
+      sg = warp_sum(sg);
+      const double alpha = ri[r0];
+      double t = 0.0, sc = 0.0, beta = alpha;
+      if (sg > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sg), alpha);
+        t = (beta - alpha) / beta;
+        sc = 1.0 / (alpha - beta);
+      }
+      if (lane == 0) {
+        b.tau[i] = t;
+        b.e[i] = beta;
+        b.d[i] = ri[i];
+      }
+      for (int dst = 0; dst < kClusterCtas; ++dst) {
+        double* rv = cluster.map_shared_rank(v, dst);
+        double* rs = cluster.map_shared_rank(scal, dst);
+        for (int c = r0 + lane; c < n; c += 32) rv[c] = c == r0 ? 1.0 : ri[c] * sc;
+        if (lane == 0) rs[par] = t;
+      }
+      for (int c = r0 + lane; c < n; c += 32) b.V[static_cast<i64>(i) * n + c] = c == r0 ? 1.0 : ri[c] * sc;
+    }
+    cluster.sync();  // (1) v, tau everywhere
+    const double t = scal[par];
+    // 2. p = tau A22 v on this CTA's rows r >= r0, all-gathered
+    const int lr0 = (r0 - rank + kClusterCtas - 1) / kClusterCtas;  // first local row with r >= r0
+    double pv_local = 0.0;
+    if (t != 0.0) {
+      for (int lr = lr0 + warp; lr < nloc; lr += nw) {
+        const int r = rank + lr * kClusterCtas;
+        const double* ar = rows + static_cast<i64>(lr) * n;
+        double s = 0.0;
+        for (int c = r0 + lane; c < n; c += 32) s += ar[c] * v[c];
+        s = warp_sum(s) * t;
+        if (lane < kClusterCtas) {
+          double* rp = cluster.map_shared_rank(p, lane);
+          rp[r] = s;
+        }
+        pv_local += s * v[r];  // identical in every lane after the butterfly
+      }
+    }
+    // CTA partial of p'v (fixed order: warps, then ranks)
+    __shared__ double wpart[32];
+    if (lane == 0) wpart[warp] = pv_local;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += wpart[w];
+      for (int dst = 0; dst < kClusterCtas; ++dst) cluster.map_shared_rank(part, dst)[par * kClusterCtas + rank] = s;
+    }
+    cluster.sync();  // (2) p and partials everywhere
+    if (t == 0.0) continue;
+    double pv = 0.0;
+    for (int q = 0; q < kClusterCtas; ++q) pv += part[par * kClusterCtas + q];
+    const double b2 = t * pv;
+    // 3. update this CTA's rows: A -= v p' + p v' - b2 v v'
+    for (int lr = lr0 + warp; lr < nloc; lr += nw) {
+      const int r = rank + lr * kClusterCtas;
+      double* ar = rows + static_cast<i64>(lr) * n;
+      const double vr = v[r], pr = p[r];
+      for (int c = r0 + lane; c < n; c += 32) {
+        const double vc = v[c];
+        ar[c] -= (vr * p[c] + pr * vc) - b2 * (vr * vc);
+      }
+    }
+    __syncthreads();  // this CTA's rows are final for column i+1's owner
+  }
+  if ((n - 1) % kClusterCtas == rank && tid == 0) {
+    b.d[n - 1] = rows[static_cast<i64>((n - 1) / kClusterCtas) * n + (n - 1)];
+    b.e[n - 1] = 0.0;
+    b.tau[n - 1] = 0.0;
+  }
+  cluster.sync();
+  if (rank == 0)
+    for (int i = tid; i < n; i += blockDim.x) b.e2[i] = b.e[i] * b.e[i];
+}
+
+inline size_t tridiag_cluster_smem_bytes(int n) {
+  const int nloc = (n + kClusterCtas - 1) / kClusterCtas;
+  return sizeof(double) * (static_cast<size_t>(nloc) * n + 4 * static_cast<size_t>(n) + 2 * kClusterCtas + 2);
 }
 
 // All eigenvalues of the tridiagonal matrix by bisection on Sturm counts:
@@ -538,7 +662,8 @@ template <class Launch>
 void syev_launch(Launch&& L, const double* M, int ldm, int n, int order, int want, double ortol, double* w_sorted,
                  double* F, int ldf, double* dbuf, int* ibuf, int* flags) {
   const EigBufs b = eig_carve(dbuf, ibuf, n, want);
-  L(tridiag_kernel, dim3(1), dim3(1024), tridiag_smem_bytes(n), M, ldm, n, b, flags);
+  L(tridiag_cluster_kernel, dim3(kClusterCtas), dim3(kTriClusterThreads), tridiag_cluster_smem_bytes(n), M, ldm, n, b,
+    flags);
   L(bisect_kernel, dim3(static_cast<unsigned>(cdiv(kBisG * n, 128))), dim3(128), sizeof(double) * 2 * n, b, n);
   L(select_kernel, dim3(1), dim3(256), sizeof(int) * n, b, n, order, want, ortol, w_sorted);
   L(invit_kernel, dim3(static_cast<unsigned>(cdiv(want, kInvitThreads))), dim3(kInvitThreads), invit_smem_bytes(n), b,

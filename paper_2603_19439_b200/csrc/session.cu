@@ -776,6 +776,8 @@ class Session {
                                                               tridiag_smem_bytes(kEigFullN)))));
       STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(invit_smem_bytes(kEigMaxN))));
+      STG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(tridiag_cluster_smem_bytes(kEigMaxN))));
       attr = true;
     }
     const int wv = std::max(want, 1);
@@ -1715,6 +1717,8 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
                                                             stg::tridiag_smem_bytes(stg::kEigFullN)))));
     STG_CUDA(cudaFuncSetAttribute(stg::invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(stg::invit_smem_bytes(stg::kEigMaxN))));
+    STG_CUDA(cudaFuncSetAttribute(stg::tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(stg::tridiag_cluster_smem_bytes(stg::kEigMaxN))));
     // row-major copy of S' (the solver symmetrizes (S + S')/2 itself)
     std::vector<double> rm(static_cast<size_t>(n * n));
     for (int64_t i = 0; i < n; ++i)
