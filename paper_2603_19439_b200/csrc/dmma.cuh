@@ -68,6 +68,56 @@ constexpr int BK2 = 32;
 constexpr size_t gram_smem(int WM, int WN) { return sizeof(double) * 2 * BK2 * ((32 * WM + 4) + (32 * WN + 4)); }
 constexpr size_t kGramSmem = gram_smem(1, 4);  // the largest layout
 
+// One warp's share of a BK2-row stage: an NX x NY block of 8 x 8 output
+// fragments (TRI: only x <= y of a 4 x 4 block on the diagonal of a symmetric
+// Gram). Operand fragment (x, k-step kk) sits at pa[kk KA + x XA], (y, kk) at
+// pb[kk KB + y YB]. The block shape is warp-uniform, chosen once per tile, so
+// edge and diagonal tiles issue no DMMA whose result is discarded.
+template <int NX, int NY, bool TRI, int KA, int XA, int KB, int YB>
+__device__ __forceinline__ void warp_mma(double (&acc)[4][4][2], const double* pa, const double* pb) {
+#pragma unroll
+  for (int kk = 0; kk < BK2; kk += 4) {
+    double fa[NX], fb[NY];
+#pragma unroll
+    for (int x = 0; x < NX; ++x) fa[x] = pa[kk * KA + x * XA];
+#pragma unroll
+    for (int y = 0; y < NY; ++y) fb[y] = pb[kk * KB + y * YB];
+#pragma unroll
+    for (int x = 0; x < NX; ++x)
+#pragma unroll
+      for (int y = 0; y < NY; ++y)
+        if (!TRI || x <= y) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+  }
+}
+
+// code: 0 = no work, (NX - 1) * 4 + NY for NX, NY in 1..4, 17 = upper 4 x 4
+__device__ __forceinline__ int warp_code(int nx, int ny, bool tri) {
+  if (nx <= 0 || ny <= 0) return 0;
+  if (tri && nx == 4 && ny == 4) return 17;
+  return (nx - 1) * 4 + ny;
+}
+
+template <int KA, int XA, int KB, int YB>
+__device__ __forceinline__ void warp_mma_dispatch(int code, double (&acc)[4][4][2], const double* pa,
+                                                  const double* pb) {
+  switch (code) {
+#define STG_MMA_CASE(NX, NY) \
+  case (NX - 1) * 4 + NY: warp_mma<NX, NY, false, KA, XA, KB, YB>(acc, pa, pb); break;
+    STG_MMA_CASE(1, 1) STG_MMA_CASE(1, 2) STG_MMA_CASE(1, 3) STG_MMA_CASE(1, 4)
+    STG_MMA_CASE(2, 1) STG_MMA_CASE(2, 2) STG_MMA_CASE(2, 3) STG_MMA_CASE(2, 4)
+    STG_MMA_CASE(3, 1) STG_MMA_CASE(3, 2) STG_MMA_CASE(3, 3) STG_MMA_CASE(3, 4)
+    STG_MMA_CASE(4, 1) STG_MMA_CASE(4, 2) STG_MMA_CASE(4, 3) STG_MMA_CASE(4, 4)
+#undef STG_MMA_CASE
+    case 17: warp_mma<4, 4, true, KA, XA, KB, YB>(acc, pa, pb); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ int frags_left(i64 extent, i64 base) {
+  const i64 f = (extent - base + 7) / 8;
+  return f < 0 ? 0 : f > 4 ? 4 : static_cast<int>(f);
+}
+
 template <int TW>
 __device__ __forceinline__ void load_k_tile_w(double* s, const double* g, int ld, i64 r, i64 rend, int c0, int m,
                                               const int* mask, int mask_val) {
@@ -98,12 +148,14 @@ __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WM, wn = warp / WM;
   const int ibase = ti * TA + wm * 32, jbase = tj * TB + wn * 32;
-  bool vi[4], vj[4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    vi[x] = FULL || ibase + x * 8 < a.m1;
-    vj[x] = FULL || jbase + x * 8 < a.m2;
+  int nx = FULL ? 4 : frags_left(a.m1, ibase);
+  const int ny = FULL ? 4 : frags_left(a.m2, jbase);
+  bool tri = false;
+  if (a.sym) {  // square warp tiles: strictly below the diagonal -> mirrored by the reduction
+    if (ibase >= jbase + 32) nx = 0;
+    tri = ibase == jbase;
   }
+  const int code = warp_code(nx, ny, tri);
   double acc[4][4][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -130,28 +182,20 @@ __device__ __forceinline__ void gram_tile(const GramArgs& a, int ti, int tj, i64
     __syncthreads();
     const double* pa = sA + s * BK2 * SA + t * SA + wm * 32 + g;
     const double* pb = sB + s * BK2 * SB + t * SB + wn * 32 + g;
-#pragma unroll
-    for (int kk = 0; kk < BK2; kk += 4) {
-      double fa[4], fb[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        fa[x] = pa[kk * SA + x * 8];
-        fb[x] = pb[kk * SB + x * 8];
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-          if (FULL || (vi[x] && vj[y])) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
-    }
+    if (code == 16)
+      warp_mma<4, 4, false, SA, 8, SB, 8>(acc, pa, pb);
+    else
+      warp_mma_dispatch<SA, 8, SB, 8>(code, acc, pa, pb);
     __syncthreads();
   }
+  if (code == 0) return;
   const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
   double* out = a.partial + static_cast<i64>(blockIdx.y) * m1p * m2p;
 #pragma unroll
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
+      if (x >= nx || y >= ny) continue;
       const i64 i = ibase + x * 8 + g, j = jbase + y * 8 + 2 * t;
       *reinterpret_cast<double2*>(out + i * m2p + j) = make_double2(acc[x][y][0], acc[x][y][1]);
     }
@@ -326,7 +370,7 @@ __device__ __forceinline__ bool nn_skipped(const NNArgs& a) {
 constexpr int SAR2 = BK2 + 4;  // [64][32] A tiles: stride 36 == 4 (mod 16)
 constexpr size_t kNNSmem = sizeof(double) * 2 * (BM * SAR2 + BK2 * SST);
 
-template <bool FULL>
+template <bool FULL, bool BETA>
 __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, double* smem) {
   double* sA = smem;                  // [2][BM][SAR2]
   double* sC = smem + 2 * BM * SAR2;  // [2][BK2][SST]
@@ -335,12 +379,7 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
   const int wm = warp & 1, wn = warp >> 1;
   const int kmax = a.upper_tri_c ? min(a.m1, (tj + 1) * BN) : a.m1;
   const int nk = static_cast<int>(cdiv(kmax, BK2));
-  bool vi[4], vj[4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x) {
-    vi[x] = FULL || row0 + wm * 32 + x * 8 < a.nrows;
-    vj[x] = FULL || tj * BN + wn * 32 + x * 8 < a.m2;
-  }
+  const int code = FULL ? 16 : warp_code(frags_left(a.nrows, row0 + wm * 32), frags_left(a.m2, tj * BN + wn * 32), false);
   double acc[4][4][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -348,8 +387,8 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   // beta * B for the epilogue: issued before the K loop so its latency
   // overlaps the operand loads (the short-K projections are memory bound)
-  double bpre[4][4][2];
-  if (FULL && a.beta != 0.0) {
+  double bpre[BETA ? 4 : 1][4][2];
+  if (FULL && BETA) {
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -408,20 +447,10 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
     __syncthreads();
     const double* pa = sA + s * BM * SAR2 + (wm * 32 + g) * SAR2 + t;
     const double* pc = sC + s * BK2 * SST + t * SST + wn * 32 + g;
-#pragma unroll
-    for (int kk = 0; kk < BK2; kk += 4) {
-      double fa[4], fb[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        fa[x] = pa[x * 8 * SAR2 + kk];
-        fb[x] = pc[kk * SST + x * 8];
-      }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y)
-          if (FULL || (vi[x] && vj[y])) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
-    }
+    if (code == 16)
+      warp_mma<4, 4, false, 1, 8 * SAR2, SST, 8>(acc, pa, pc);
+    else
+      warp_mma_dispatch<1, 8 * SAR2, SST, 8>(code, acc, pa, pc);
     __syncthreads();
   }
 #pragma unroll
@@ -432,9 +461,9 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
       const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
       if (FULL) {
         double2 v = make_double2(a.alpha * acc[x][y][0], a.alpha * acc[x][y][1]);
-        if (a.beta != 0.0) {
-          v.x += a.beta * bpre[x][y][0];
-          v.y += a.beta * bpre[x][y][1];
+        if (BETA) {
+          v.x += a.beta * bpre[BETA ? x : 0][y][0];
+          v.y += a.beta * bpre[BETA ? x : 0][y][1];
         }
         *reinterpret_cast<double2*>(a.Out + r * a.ldo + col) = v;
         continue;
@@ -450,15 +479,19 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
     }
 }
 
-__global__ void __launch_bounds__(NT, 3) gemm_nn_kernel(NNArgs a) {
+template <bool BETA>  // the beta*B prefetch needs 64 more registers: 2 CTAs per SM
+__global__ void __launch_bounds__(NT, BETA ? 2 : 3) gemm_nn_kernel(NNArgs a) {
   if (nn_skipped(a)) return;
   extern __shared__ __align__(16) double dsm[];
-  const i64 row0 = static_cast<i64>(blockIdx.x) * BM;
-  const int tj = blockIdx.y;
+  // column tiles of one row block are adjacent in launch order, so the A rows
+  // they share are read from HBM once
+  const int tiles_j = static_cast<int>(cdiv(a.m2, BN));
+  const i64 row0 = static_cast<i64>(blockIdx.x / tiles_j) * BM;
+  const int tj = static_cast<int>(blockIdx.x % tiles_j);
   if (row0 + BM <= a.nrows && (tj + 1) * BN <= a.m2)
-    nn_tile<true>(a, row0, tj, dsm);
+    nn_tile<true, BETA>(a, row0, tj, dsm);
   else
-    nn_tile<false>(a, row0, tj, dsm);
+    nn_tile<false, BETA>(a, row0, tj, dsm);
 }
 
 __global__ void __launch_bounds__(NT) gemm_nn_small_kernel(NNArgs a) {

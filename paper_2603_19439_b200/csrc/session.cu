@@ -204,7 +204,9 @@ class Session {
                                   static_cast<int>(dm::gram_smem(1, 4))));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::gram_smem(4, 1))));
-    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kNNSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
     d_scal_ = arena_.get<u64>("scalars", 32);
     k = cfg.k;
@@ -388,7 +390,7 @@ class Session {
       switch (which) {
         case 0: gram(A, ld1, (flag & 1) ? A : B, (flag & 1) ? ld1 : ld2, N, m1, (flag & 1) ? m1 : m2, flag & 1, O, ld2); break;
         case 1: nn(A, ld1, N, m1, C, ld1, m2, O, ld2, 1.0, 0.0, nullptr, 0, flag & 1); break;
-        case 2: chol(C, ld1, m1, O, ld1, nullptr, 0.0, true); break;
+        case 2: chol(C, ld1, m1, O, ld1, flag ? arena_.get<double>("bk_Ri", static_cast<i64>(m1) * ld1) : nullptr, ld1, nullptr, 0.0, true); break;
         case 3: triinv(C, ld1, m1, O, ld1); break;
         case 4: {
           double* w = arena_.get<double>("bk_w", m1);
@@ -699,9 +701,8 @@ class Session {
     if (m2 <= 32)
       launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
     else
-      launch(dm::gemm_nn_kernel,
-             dim3(static_cast<unsigned>(cdiv(rows, dm::BM)), static_cast<unsigned>(cdiv(m2, dm::BN))), dim3(dm::NT),
-             dm::kNNSmem, st_, a);
+      launch(beta != 0.0 ? dm::gemm_nn_kernel<true> : dm::gemm_nn_kernel<false>,
+             dim3(static_cast<unsigned>(cdiv(rows, dm::BM) * cdiv(m2, dm::BN))), dim3(dm::NT), dm::kNNSmem, st_, a);
     kend();
   }
 
@@ -715,7 +716,9 @@ class Session {
     kend();
   }
 
-  void chol(const double* G, int ldg, int w, double* R, int ldr, const double* orig2, double tau2, bool psd) {
+  // Cholesky G = R'R; with Ri also R^-1 (triinv_kernel).
+  void chol(const double* G, int ldg, int w, double* R, int ldr, double* Ri, int ldi, const double* orig2,
+            double tau2, bool psd) {
     if (w > kCholMaxW) throw RuntimeError("chol: block wider than 238 columns");
     if (klog_) snprintf(ktag_, sizeof(ktag_), "chol w=%d", w);
     kbegin(kChol, static_cast<double>(w) * w * w / 3.0);
@@ -723,17 +726,21 @@ class Session {
     if (!attr) {
       STG_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(chol_smem_bytes(kCholMaxW))));
+      STG_CUDA(cudaFuncSetAttribute(triinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(triinv_smem_bytes(kCholMaxW))));
       attr = true;
     }
-    launch(chol_kernel, dim3(1), dim3(1024), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
+    launch(chol_kernel, dim3(1), dim3(kCholThreads), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
            flags_ptr());
     kend();
+    if (Ri) triinv(R, ldr, w, Ri, ldi);
   }
 
   void triinv(const double* R, int ldr, int w, double* Ri, int ldi) {
-    if (w > 32 * kTriMaxSlots) throw RuntimeError("triinv: block wider than 320 columns");
+    if (w > kCholMaxW) throw RuntimeError("triinv: block wider than 238 columns");
     kbegin(kTriinv, static_cast<double>(w) * w * w / 3.0);
-    launch(triinv_kernel, dim3(blocks(w, 4)), dim3(128), 0, st_, R, ldr, w, Ri, ldi);
+    launch(triinv_kernel, dim3(static_cast<unsigned>(cdiv(w, kTriWarps))), dim3(32 * kTriWarps),
+           triinv_smem_bytes(w), st_, R, ldr, w, Ri, ldi);
     kend();
   }
 
@@ -1135,34 +1142,35 @@ class Session {
     double* R = arena_.get<double>("on_R", static_cast<i64>(w) * ldw);
     double* Ri = arena_.get<double>("on_Ri", static_cast<i64>(w) * ldw);
     double* o2 = arena_.get<double>("on_o2", w);
-    // pass 1
+    // pass 1: W1 = W - A (A'W); with no `against` the Gram reads W directly
+    const double* P1 = W.p;
+    int ldp1 = W.ld;
     if (against && a > 0) {
       gram(against->p, against->ld, W.p, W.ld, G, a, w, false, C, ldw);
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, W.p, W.ld);
-    } else {
-      launch(copy2d_kernel, dim3(blocks(N * w)), dim3(256), 0, st_, static_cast<const double*>(W.p), W.ld, W1, ldw, N,
-             w);
+      P1 = W1;
+      ldp1 = ldw;
     }
-    gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
+    gram(P1, ldp1, P1, ldp1, G, w, w, true, Gm, ldw);
     launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw,
            static_cast<const double*>(C), ldw, (against ? a : 0), w, o2);
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
-    chol(Gm, ldw, w, R, ldw, o2, kSuspectTau2, false);
+    chol(Gm, ldw, w, R, ldw, Ri, ldw, o2, kSuspectTau2, false);
     read_scalars();
     if (hs_->flags & (kSuspect | kBreakdown)) return mgs2_exact(W, w, against, a, N, G, out);
-    triinv(R, ldw, w, Ri, ldw);
-    nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
+    // pass 2 input Q1 = P1 R^-1: into `out` when it is re-projected into W1,
+    // else straight into W1
+    const bool proj = against && a > 0;
+    double* Q1 = proj ? out.p : W1;
+    const int ldq1 = proj ? out.ld : ldw;
+    nn(P1, ldp1, N, w, Ri, ldw, w, Q1, ldq1, 1.0, 0.0, nullptr, 0, true);
     // pass 2
-    if (against && a > 0) {
+    if (proj) {
       gram(against->p, against->ld, out.p, out.ld, G, a, w, false, C, ldw);
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, out.p, out.ld);
-    } else {
-      launch(copy2d_kernel, dim3(blocks(N * w)), dim3(256), 0, st_, static_cast<const double*>(out.p), out.ld, W1, ldw,
-             N, w);
     }
     gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
-    chol(Gm, ldw, w, R, ldw, nullptr, 0.0, false);
-    triinv(R, ldw, w, Ri, ldw);
+    chol(Gm, ldw, w, R, ldw, Ri, ldw, nullptr, 0.0, false);
     nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
     return w;
   }
@@ -1474,7 +1482,7 @@ class Session {
       }
       double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ldr);
       gram(X_, ldx(), X_, ldx(), pt.n_old, kk, kk, true, kc, ldr);
-      chol(kc, ldr, kk, rc, ldr, nullptr, 0.0, true);
+      chol(kc, ldr, kk, rc, ldr, nullptr, 0, nullptr, 0.0, true);
       launch(copy2d_kernel, dim3(blocks(k * k)), dim3(256), 0, st_, static_cast<const double*>(rc), ldr, z.p + p * z.ld,
              z.ld, k, kk);
     } else {  // dense mode: no rows outside P, K = 0

@@ -21,100 +21,252 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Upper Cholesky G = R'R of a symmetric w x w block (row-major), one CTA,
-// the upper triangle in shared memory (rows packed: row i holds columns i..w-1).
-// Right-looking with ONE barrier per column: after the barrier every thread
-// reads the pivot U(j,j) (broadcast) and derives 1/r itself; row j of R is
-// written to global scaled, while the trailing update uses the raw row j with
-// the factor 1/d: U(i,c) -= U(j,i) U(j,c) / d. When orig2 is given, a pivot
-// d_j <= tau2 * orig2[j] raises kSuspect: the column's residual is within
-// sqrt(tau2) of its original norm, where the reference's per-column drop test
-// (ortho.hpp:34-35) must be re-evaluated exactly. With psd != 0 a
-// non-positive pivot zeroes the row (semidefinite factor) instead of failing.
+// Upper Cholesky G = R'R of a symmetric w x w block (row-major), one CTA of
+// 512 threads, the upper triangle in shared memory (rows packed: row i holds
+// columns i..w-1 at packed_row(i) + c). Blocked right-looking with panels of
+// kCholNb rows and a one-panel lookahead:
+//   A. all warps apply panel p's rank-kCholNb update to the rows of panel p+1;
+//   B. warp 0 factors panel p+1's diagonal block in registers (the latency
+//      chain: one pivot rsqrt per column) while the other warps apply panel
+//      p's update to the rest of the trailing triangle (4 x 4 register tiles);
+//   C. panel p+1's rows become R12 = R11^-T A12 (one thread per column).
+// When orig2 is given, a pivot d_j <= tau2 * orig2[j] raises kSuspect: the
+// column's residual is within sqrt(tau2) of its original norm, where the
+// reference's per-column drop test (ortho.hpp:34-35) must be re-evaluated
+// exactly. With psd != 0 a non-positive pivot zeroes the row (semidefinite
+// factor) instead of failing.
 constexpr int kCholMaxW = 238;
+constexpr int kCholNb = 16;
+constexpr int kCholThreads = 512;
 
-__global__ void __launch_bounds__(1024) chol_kernel(const double* G, int ldg, int w, double* R, int ldr,
-                                                    const double* orig2, double tau2, int psd, int* flags) {
+__device__ __forceinline__ int packed_row(int i, int w) { return i * w - (i * (i - 1)) / 2 - i; }
+
+// Diagonal block rows/cols p..p+b-1 by one warp: lane c holds column c
+// (a[t] = A(p+t, p+c), t <= c); row t of R11 is broadcast by shuffles. Slots
+// below a lane's diagonal hold don't-care values that never reach a valid
+// slot, so the full-block variant runs without predicates.
+template <bool FULL>
+__device__ __forceinline__ void chol_diag_block(double* sm, double* invd, int w, int p, int b, int lane,
+                                                const double* orig2, double tau2, int psd, int& fl) {
+  const int cl = FULL ? (lane & (kCholNb - 1)) : (lane < b ? lane : b - 1);
+  double a[kCholNb];
+#pragma unroll
+  for (int t = 0; t < kCholNb; ++t)
+    a[t] = (FULL || t < b) && t <= cl ? sm[packed_row(p + t, w) + p + cl] : 0.0;
+#pragma unroll
+  for (int t = 0; t < kCholNb; ++t) {
+    if (FULL || t < b) {
+      const double d = __shfl_sync(0xffffffffu, a[t], t);
+      const bool bad = !(d > 0.0) || !isfinite(d);
+      if (lane == 0) {
+        if (orig2 && !(d > tau2 * orig2[p + t])) fl |= kSuspect;
+        if (bad && !psd) fl |= kBreakdown;
+      }
+      const double ir = bad ? 0.0 : rsqrt(d);
+      a[t] = cl == t ? d * ir : a[t] * ir;
+      if (lane == 0) invd[t] = ir;
+#pragma unroll
+      for (int u = t + 1; u < kCholNb; ++u) {
+        const double rtu = __shfl_sync(0xffffffffu, a[t], u);  // R(t, u)
+        if (FULL || u < b) a[u] -= rtu * a[t];
+      }
+    }
+  }
+  if (lane < b) {
+#pragma unroll
+    for (int t = 0; t < kCholNb; ++t)
+      if (t <= lane) sm[packed_row(p + t, w) + p + lane] = a[t];
+  }
+}
+
+template <typename... A>
+__device__ __forceinline__ void chol_diag(int b, A... args) {
+  if (b == kCholNb) chol_diag_block<true>(args...);
+  else chol_diag_block<false>(args...);
+}
+
+// Rows p..p+b-1 (diagonal block already factored, 1/R(t,t) in invd): columns
+// c >= p + b become R12 = R11^-T A12; one thread per column.
+__device__ __forceinline__ void chol_panel(double* sm, const double* invd, int w, int p, int b, int tid, int nth) {
+  for (int c = p + b + tid; c < w; c += nth) {
+    double x[kCholNb];
+#pragma unroll
+    for (int t = 0; t < kCholNb; ++t) x[t] = t < b ? sm[packed_row(p + t, w) + c] : 0.0;
+#pragma unroll
+    for (int t = 0; t < kCholNb; ++t) {
+      if (t < b) {
+        x[t] *= invd[t];
+        const int rt = packed_row(p + t, w);
+#pragma unroll
+        for (int u = t + 1; u < kCholNb; ++u)
+          if (u < b) x[u] -= sm[rt + p + u] * x[t];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kCholNb; ++t)
+      if (t < b) sm[packed_row(p + t, w) + c] = x[t];
+  }
+}
+
+// Rank-b update by panel p (rows p..p+b-1 hold R) of the elements (i, c),
+// i in [r0, r1), c >= i, c >= q0. Work items are bands of 4 rows x 64 columns
+// owned by one warp: the 4 row factors are shared-memory broadcasts and lane l
+// owns columns c0 + l and c0 + 32 + l, so every access is conflict-free.
+__device__ __forceinline__ void chol_trailing(double* sm, int w, int p, int b, int q0, int r0, int r1, int warp,
+                                              int nwarps, int lane) {
+  if (r1 <= r0) return;
+  const int nb4 = (r1 - r0 + 3) >> 2;        // row bands
+  const int nch = (w - q0 + 63) >> 6;        // 64-column chunks
+  for (int item = warp; item < nb4 * nch; item += nwarps) {
+    const int band = item / nch, ch = item - band * nch;
+    const int i0 = r0 + 4 * band, c0 = q0 + 64 * ch;
+    if (c0 + 63 < i0) continue;  // chunk entirely left of the diagonal
+    double acc[4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) acc[x][0] = acc[x][1] = 0.0;
+    const int ca = c0 + lane, cb = c0 + 32 + lane;
+#pragma unroll 4
+    for (int t = 0; t < b; ++t) {
+      const double* rowt = sm + packed_row(p + t, w);
+      double ri[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) ri[x] = i0 + x < r1 ? rowt[i0 + x] : 0.0;
+      const double va = ca < w ? rowt[ca] : 0.0;
+      const double vb = cb < w ? rowt[cb] : 0.0;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        acc[x][0] = fma(ri[x], va, acc[x][0]);
+        acc[x][1] = fma(ri[x], vb, acc[x][1]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int i = i0 + x;
+      if (i >= r1) continue;
+      double* rowi = sm + packed_row(i, w);
+      if (ca < w && ca >= i) rowi[ca] -= acc[x][0];
+      if (cb < w && cb >= i) rowi[cb] -= acc[x][1];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(const double* G, int ldg, int w, double* R, int ldr,
+                                                            const double* orig2, double tau2, int psd, int* flags) {
   extern __shared__ double sm[];
-  int* rowoff = reinterpret_cast<int*>(sm + static_cast<i64>(w) * (w + 1) / 2);
+  double* invd = sm + static_cast<i64>(w) * (w + 1) / 2;  // [2][kCholNb]: 1 / R(j,j) per panel parity
   const int tid = threadIdx.x, nth = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
-  for (int i = tid; i < w; i += nth) rowoff[i] = i * w - (i * (i - 1)) / 2 - i;  // + c for c >= i
-  __syncthreads();
-  for (i64 idx = tid; idx < static_cast<i64>(w) * w; idx += nth) {
-    const int i = static_cast<int>(idx / w), c = static_cast<int>(idx % w);
-    if (c >= i) sm[rowoff[i] + c] = G[static_cast<i64>(i) * ldg + c];
-    else R[static_cast<i64>(i) * ldr + c] = 0.0;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int i = warp; i < w; i += nth >> 5) {  // warp per row, coalesced
+    const double* gi = G + static_cast<i64>(i) * ldg;
+    double* si = sm + packed_row(i, w);
+    double* ri = R + static_cast<i64>(i) * ldr;
+    for (int c = lane; c < w; c += 32) {
+      if (c >= i) si[c] = gi[c];
+      else ri[c] = 0.0;
+    }
   }
   __syncthreads();
-  for (int j = 0; j < w; ++j) {
-    const double* uj = sm + rowoff[j];
-    const double d = uj[j];
-    const bool bad = !(d > 0.0) || !isfinite(d);
-    if (tid == 0) {
-      if (orig2 && !(d > tau2 * orig2[j])) atomicOr(flags, kSuspect);
-      if (bad && !psd) atomicOr(flags, kBreakdown);
-    }
-    const double inv_r = bad ? 0.0 : 1.0 / sqrt(d);
-    const double inv_d = bad ? 0.0 : 1.0 / d;
-    for (int c = j + tid; c < w; c += nth) R[static_cast<i64>(j) * ldr + c] = c == j ? (bad ? 0.0 : sqrt(d)) : uj[c] * inv_r;
-    // trailing update, warp per row i > j, lanes over columns c >= i
-    for (int i = j + 1 + warp; i < w; i += nw) {
-      const double f = uj[i] * inv_d;
-      double* ui = sm + rowoff[i];
-      for (int c = i + lane; c < w; c += 32) ui[c] -= f * uj[c];
+  int fl = 0;
+  if (warp == 0) chol_diag(min(kCholNb, w), sm, invd, w, 0, min(kCholNb, w), lane, orig2, tau2, psd, fl);
+  __syncthreads();
+  chol_panel(sm, invd, w, 0, min(kCholNb, w), tid, nth);
+  __syncthreads();
+  for (int p = 0, q = 0; p < w; p += kCholNb, q ^= 1) {
+    const int b = min(kCholNb, w - p);
+    const int p1 = p + b, b1 = min(kCholNb, w - p1);  // next panel
+    // A. next panel's rows take panel p's update
+    chol_trailing(sm, w, p, b, p1, p1, p1 + b1, warp, nth >> 5, lane);
+    // rows of panel p are final
+    for (int e = tid; e < b * (w - p); e += nth) {
+      const int t = e / (w - p), c = p + (e - t * (w - p));
+      if (c >= p + t) R[static_cast<i64>(p + t) * ldr + c] = sm[packed_row(p + t, w) + c];
     }
     __syncthreads();
+    // B. warp 0: next diagonal block; the others: rest of the trailing update
+    if (warp == 0) {
+      if (b1 > 0) chol_diag(b1, sm, invd + (q ^ 1) * kCholNb, w, p1, b1, lane, orig2, tau2, psd, fl);
+    } else {
+      chol_trailing(sm, w, p, b, p1, p1 + b1, w, warp - 1, (nth >> 5) - 1, lane);
+    }
+    __syncthreads();
+    // C. next panel rows
+    if (b1 > 0) chol_panel(sm, invd + (q ^ 1) * kCholNb, w, p1, b1, tid, nth);
+    __syncthreads();
   }
+  if (fl) atomicOr(flags, fl);
 }
 
 inline size_t chol_smem_bytes(int w) {
-  return sizeof(double) * static_cast<size_t>(w) * (w + 1) / 2 + sizeof(int) * static_cast<size_t>(w);
+  return sizeof(double) * (static_cast<size_t>(w) * (w + 1) / 2 + 2 * kCholNb);
 }
 
-// Inverse of an upper-triangular R (row-major): one warp per column j of R^-1,
-// back substitution with the column held in registers (lane l owns entries
-// l + 32 t). Entries below the diagonal are written as zeros.
-constexpr int kTriMaxSlots = 10;  // w <= 320
-__global__ void __launch_bounds__(128) triinv_kernel(const double* R, int ldr, int w, double* Ri, int ldi) {
-  const int j = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (j >= w) return;
-  double x[kTriMaxSlots];
+// Inverse of an upper-triangular R (row-major, w <= 256). Each CTA stages R in
+// shared memory as packed columns (column l holds rows 0..l), then each warp
+// back-substitutes one column j of R^-1 in axpy form: once x_l is known,
+// column l of R times x_l is added to the running sums of rows i < l (lane
+// owns rows lane + 32 u), and x_{l-1} = -s_{l-1} / R(l-1,l-1) is broadcast
+// from its owner. Entries below the diagonal are written as zeros; a zero
+// pivot yields a zero row/column of the inverse.
+constexpr int kTriWarps = 8;
+constexpr int kTriMaxW = 256;
+
+// Steps l = lhi .. 32 U + 1 of one column: rows i < l <= 32 (U + 1) live in
+// slots u <= U, and x_{l-1} sits in slot U of lane (l-1) & 31.
+template <int U>
+__device__ __forceinline__ void triinv_segment(double (&s)[kTriMaxW / 32], double& xl, int lhi, int lane,
+                                               const double* rc, const double* invd, double* Ri, int ldi, int j) {
+  for (int l = lhi; l > 32 * U; --l) {
+    const double* col = rc + l * (l + 1) / 2;
 #pragma unroll
-  for (int t = 0; t < kTriMaxSlots; ++t) x[t] = 0.0;
-  const double rjj = R[static_cast<i64>(j) * ldr + j];
-  const double xj = rjj != 0.0 ? 1.0 / rjj : 0.0;
-#pragma unroll
-  for (int t = 0; t < kTriMaxSlots; ++t)
-    if (lane + 32 * t == j) x[t] = xj;
-  double rrow[kTriMaxSlots];
-  auto load_row = [&](int i) {
-#pragma unroll
-    for (int t = 0; t < kTriMaxSlots; ++t) {
-      const int l = lane + 32 * t;
-      rrow[t] = (i >= 0 && l > i && l <= j) ? R[static_cast<i64>(i) * ldr + l] : 0.0;
+    for (int u = 0; u <= U; ++u) {
+      const int i = lane + 32 * u;
+      if (i < l) s[u] = fma(col[i], xl, s[u]);
     }
-  };
-  load_row(j - 1);
-  for (int i = j - 1; i >= 0; --i) {
-    double s = 0.0;
-#pragma unroll
-    for (int t = 0; t < kTriMaxSlots; ++t) s += rrow[t] * x[t];
-    const double rii = R[static_cast<i64>(i) * ldr + i];
-    load_row(i - 1);  // prefetch the next row while reducing
-    s = warp_sum(s);
-    const double xi = rii != 0.0 ? -s / rii : 0.0;
-#pragma unroll
-    for (int t = 0; t < kTriMaxSlots; ++t)
-      if (lane + 32 * t == i) x[t] = xi;
-  }
-#pragma unroll
-  for (int t = 0; t < kTriMaxSlots; ++t) {
-    const int l = lane + 32 * t;
-    if (l < w) Ri[static_cast<i64>(l) * ldi + j] = x[t];
+    const int o = l - 1;
+    xl = -__shfl_sync(0xffffffffu, s[U], o & 31) * invd[o];
+    if (lane == (o & 31)) Ri[static_cast<i64>(o) * ldi + j] = xl;
   }
 }
+
+__global__ void __launch_bounds__(32 * kTriWarps) triinv_kernel(const double* R, int ldr, int w, double* Ri, int ldi) {
+  extern __shared__ double rc[];
+  double* invd = rc + static_cast<i64>(w) * (w + 1) / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < w; c += kTriWarps) {  // warp per column: conflict-free packed stores
+    double* dst = rc + c * (c + 1) / 2;
+    for (int i = lane; i <= c; i += 32) {
+      const double v = R[static_cast<i64>(i) * ldr + c];
+      dst[i] = v;
+      if (i == c) invd[i] = v != 0.0 ? 1.0 / v : 0.0;
+    }
+  }
+  __syncthreads();
+  const int j = blockIdx.x * kTriWarps + warp;
+  if (j >= w) return;
+  for (int i = j + 1 + lane; i < w; i += 32) Ri[static_cast<i64>(i) * ldi + j] = 0.0;
+  double s[kTriMaxW / 32];
+#pragma unroll
+  for (int u = 0; u < kTriMaxW / 32; ++u) s[u] = 0.0;
+  double xl = invd[j];
+  if (lane == (j & 31)) Ri[static_cast<i64>(j) * ldi + j] = xl;
+  int l = j;
+  while (l > 0) {
+    const int U = (l - 1) >> 5;
+    switch (U) {
+      case 0: triinv_segment<0>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 1: triinv_segment<1>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 2: triinv_segment<2>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 3: triinv_segment<3>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 4: triinv_segment<4>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 5: triinv_segment<5>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      case 6: triinv_segment<6>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+      default: triinv_segment<7>(s, xl, l, lane, rc, invd, Ri, ldi, j); break;
+    }
+    l = 32 * U;
+  }
+}
+
+inline size_t triinv_smem_bytes(int w) { return sizeof(double) * (static_cast<size_t>(w) * (w + 1) / 2 + w); }
 
 // spectral_sort (types.hpp:26-40): rank of element i = number of elements that
 // precede it under (primary key, algebraic value desc, index asc).

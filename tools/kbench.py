@@ -37,5 +37,7 @@ if "nn" in cases:
         print(f"nn   N={N} {a}x{b} tri={tri}: {t*1e3:8.1f} us  {fl/t/1e9:6.2f} TF")
 if "small" in cases:
     for w in (32, 132, 164, 200):
-        print(f"chol w={w}: {bench(2, 1, w, w)*1e3:8.1f} us   triinv: {bench(3, 1, w, w)*1e3:8.1f} us   "
+        print(f"chol w={w}: {bench(2, 1, w, w)*1e3:8.1f} us  chol+inv: {bench(2, 1, w, w, 1)*1e3:8.1f} us  triinv: {bench(3, 1, w, w)*1e3:8.1f} us   "
               f"eig(want 32): {bench(4, 1, w, 32, iters=3)*1e3:8.1f} us")
+if cases and cases[0] == "one":  # one launch for ncu: one <which> N m1 m2 flag
+    bench(int(cases[1]), int(cases[2]), int(cases[3]), int(cases[4]), int(cases[5]), iters=1)
