@@ -1,23 +1,18 @@
-// Small dense symmetric eigensolver in one CTA (order n <= kEigMaxN), kept on
-// the device for the projected Rayleigh-Ritz matrix (sym_eig_dense,
+// Small dense symmetric eigensolver (order n <= kEigMaxN) kept on the device
+// for the projected Rayleigh-Ritz matrix (sym_eig_dense,
 // proj/include/spectrack/eig.hpp:37-50) and the RSVD sketch Gram.
 //
-//   1. (S + S')/2 into shared memory: the full square when n <= kEigFullN
-//      (rows contiguous), else the packed lower triangle,
-//   2. Householder tridiagonalization (LAPACK dsytd2 recurrence) with three
-//      barriers per column: every thread derives the reflector scalars itself,
-//      p = A v runs four threads per row, and the rank-2 update is
-//      A -= v p' + p v' - tau (p'v) v v' (= v w' + w v'),
-//   3. all eigenvalues by Sturm-count bisection: one CTA-wide multisection
-//      round brackets every eigenvalue, then 4 threads per eigenvalue to
-//      full relative precision,
-//   4. spectral ordering (types.hpp:26-40), selection of the leading `want`,
-//   5. their eigenvectors by inverse iteration on the tridiagonal matrix with
+//   1. (S + S')/2 and Householder tridiagonalization (LAPACK dsytd2
+//      recurrence) in one CTA (n <= kEig1N, full square in shared memory) or
+//      a 2-CTA cluster (rows split by parity), two barriers per column,
+//   2. all eigenvalues by Sturm-count multisection, kBisG threads per
+//      eigenvalue, to the absolute accuracy of a QR-based solver,
+//   3. spectral ordering (types.hpp:26-40), selection of the leading `want`,
+//   4. their eigenvectors by inverse iteration on the tridiagonal matrix with
 //      partial pivoting and Gram-Schmidt inside eigenvalue clusters (the dstein
-//      scheme), then the Householder back-transformation with the vector in
-//      registers.
-// Only step 2 needs a single CTA; steps 3-5 are separate kernels spread over
-// the GPU (one group of threads per eigenvalue / eigenvector).
+//      scheme), then the Householder back-transformation.
+// Steps 2-4 are separate kernels spread over the GPU (one group of threads per
+// eigenvalue / eigenvector).
 // Eigenvalues are accurate to O(eps ||S||) like the reference's QR-based
 // SelfAdjointEigenSolver; eigenvectors of separated eigenvalues to
 // O(eps ||S|| / gap); clusters get an orthonormal basis of their span.
@@ -32,26 +27,9 @@
 
 namespace stg {
 
-constexpr int kEigMaxN = 232;   // packed lower triangle + vectors fit in 227 KB of shared memory
-constexpr int kEigFullN = 165;  // full square storage up to here (covers D <= 164 at config 3)
+constexpr int kEigMaxN = 232;   // 116 rows x 232 columns per CTA of a 2-CTA cluster fit in 227 KB
 constexpr int kEigMaxWant = 256;
 
-
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    s = warp_sum(s);
-    if (threadIdx.x == 0) red[32] = s;
-  }
-  __syncthreads();
-  return red[32];
-}
 
 // Number of eigenvalues of the tridiagonal (d, e2 = e^2) strictly below x.
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x, double pivmin) {
@@ -66,29 +44,6 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   }
   return c;
 }
-
-template <bool FULL>
-struct SymStore {
-  double* A;
-  int n;
-  __device__ __forceinline__ double& at(int i, int j) const {  // element (i, j) of the symmetric matrix
-    if (FULL) return A[i * n + j];
-    if (i < j) {
-      const int t = i;
-      i = j;
-      j = t;
-    }
-    return A[static_cast<i64>(j) * n - (static_cast<i64>(j) * (j - 1)) / 2 + (i - j)];
-  }
-  // reflector i, entry r > i + 1: row i (upper, contiguous) when FULL, column i when packed
-  __device__ __forceinline__ double& refl(int r, int i) const {
-    if (FULL) return A[i * n + r];
-    return A[static_cast<i64>(i) * n - (static_cast<i64>(i) * (i - 1)) / 2 + (r - i)];
-  }
-  static __host__ __device__ i64 words(int n) {
-    return FULL ? static_cast<i64>(n) * n : static_cast<i64>(n) * (n + 1) / 2;
-  }
-};
 
 // ---------------------------------------------------------------------------
 // Multi-kernel pipeline: only the tridiagonalization needs one CTA; the
@@ -109,286 +64,308 @@ struct EigBufs {
   double* tnorm;   // 1
 };
 
-template <bool FULL>
-__device__ void tridiag_body(const double* M, int ldm, int n, const EigBufs b, int* flags, double* sm) {
-  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
-  SymStore<FULL> S{sm, n};
-  double* v = sm + SymStore<FULL>::words(n);
-  double* p = v + n;
-  double* part_pv = p + n;  // n
-  double* red = part_pv + n;  // 48
-  for (i64 idx = tid; idx < static_cast<i64>(n) * n; idx += nth) {
-    const int i = static_cast<int>(idx / n), j = static_cast<int>(idx % n);
-    if (!FULL && i < j) continue;
-    const double x = M[static_cast<i64>(i) * ldm + j], y = M[static_cast<i64>(j) * ldm + i];
-    if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
-    S.at(i, j) = 0.5 * (x + y);
-  }
-  __syncthreads();
-  {
-    double part = 0.0;
-    for (int r = 2 + tid; r < n; r += nth) part += S.at(r, 0) * S.at(r, 0);
-    part = block_sum(part, red);
-    if (tid == 0) red[40] = part;
+// Householder tridiagonalization (LAPACK dsytd2 recurrence) with the rows of
+// (S + S')/2 spread over a cluster of C CTAs (C = 1: one CTA holding the full
+// square, n <= kEig1N; C = 2 up to kEigMaxN): CTA q keeps rows r = q (mod C)
+// in full width in shared memory. Column i (col = A(:, i)), its alpha and the
+// shares of its squared norm were published in every CTA by the previous step.
+// Per column, with r0 = i + 1 and v = (1, scal col[r0+1:]):
+//   S. acc_r = sum_{c > r0} A(c, r) col[c] over the CTA's rows c, using the
+//      symmetry A(c, r) = A(r, c): warp w owns 32 consecutive r and runs down
+//      the rows, so loads are conflict-free and no butterfly is needed; the
+//      sums are unscaled, so they need no reflector scalars. acc, row r0
+//      (a0 = A(r0, :), from its owner) and the unscaled pieces of (Av)'v are
+//      published; the last warp meanwhile derives beta, tau, scal.
+//      -- barrier --
+//   U. (Av)_r = a0_r + scal sum_q acc_q,r, p = tau Av, b2 = tau p'v and
+//      A(c, r) -= v_c (p_r - b2 v_r) + p_c v_r on the CTA's rows (slot count
+//      specialised, so no predicated-off lanes); the new column i+1, its alpha
+//      and squared-norm shares are published.  -- barrier --
+// Two barriers per column; every cross-CTA buffer alternates with the column
+// parity, so a write never races a read of the previous column. The
+// reference symmetrises its input (eig.hpp:47) the same way.
+constexpr int kTriThreads = 512;
+constexpr int kTriW = kTriThreads / 32;
+constexpr int kEig1N = 165;  // one CTA holds the full square up to here
+constexpr int kTriSlots = (kEigMaxN + 31) / 32;
+
+__host__ __device__ inline int tri_rows(int n, int C) { return (n + C - 1) / C; }
+
+// scratch after the rows: col[2][n], a0[n], p/v/w[3][n], acc[C * gmax][n], (Av)'v pieces
+// [2][C * kTriW][4], reflector scalars [2][4]. gmax = warps sharing one
+// 32-column block of the column sums (as many as shared memory allows, <= 4).
+inline size_t tridiag_smem_bytes(int n, int C, int gmax) {
+  return sizeof(double) * (static_cast<size_t>(tri_rows(n, C)) * n + (6 + static_cast<size_t>(C) * gmax) * n +
+                           2 * static_cast<size_t>(C) * kTriW * 4 + 8);
+}
+inline int tridiag_gmax(int n, int C) {
+  int g = 4;
+  while (g > 1 && tridiag_smem_bytes(n, C, g) > 232448) --g;
+  return g;
+}
+
+template <int C>
+__device__ __forceinline__ void tri_sync() {
+  if constexpr (C == 1) {
     __syncthreads();
+  } else {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
-  for (int i = 0; i + 1 < n; ++i) {
-    const int r0 = i + 1, m = n - r0;
-    const double sigma = red[40];
-    const double alpha = S.at(r0, i);
-    double t = 0.0, scal = 0.0, beta = alpha;
-    if (sigma > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
-      t = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
-    }
-    if (tid == 0) {
-      b.tau[i] = t;
-      b.e[i] = beta;
-      b.d[i] = S.at(i, i);
-    }
-    if (t == 0.0) {
-      double part = 0.0;
-      for (int r = i + 3 + tid; r < n; r += nth) part += S.at(r, i + 1) * S.at(r, i + 1);
-      part = block_sum(part, red);
-      if (tid == 0) red[40] = part;
-      __syncthreads();
-      continue;
-    }
-    for (int r = r0 + tid; r < n; r += nth) {
-      const double vr = r == r0 ? 1.0 : S.at(r, i) * scal;
-      v[r] = vr;
-      b.V[static_cast<i64>(i) * n + r] = vr;
-    }
-    __syncthreads();  // (1) v complete
-    // this lane's columns c = r0 + lane + 32 s: v and p are loaded once per
-    // column step and reused across the warp's rows (the loops are bound by
-    // shared-memory traffic)
-    constexpr int kS = (kEigMaxN + 31) / 32;
-    if (FULL) {
-      double vc[kS];
-#pragma unroll
-      for (int sl = 0; sl < kS; ++sl) {
-        const int c = r0 + lane + 32 * sl;
-        vc[sl] = c < n ? v[c] : 0.0;
-      }
-      for (int r = r0 + warp; r < n; r += nw) {  // p = tau A22 v, warp per row
-        const double* Ar = &S.at(r, 0);
-        double s = 0.0;
-#pragma unroll
-        for (int sl = 0; sl < kS; ++sl) {
-          const int c = r0 + lane + 32 * sl;
-          if (c < n) s += Ar[c] * vc[sl];
-        }
-        s = warp_sum(s);
-        if (lane == 0) {
-          p[r] = t * s;
-          part_pv[r - r0] = t * s * v[r];
-        }
-      }
-      __syncthreads();  // (2) p complete
-      double pv = 0.0;
-      for (int r = lane; r < m; r += 32) pv += part_pv[r];
-      pv = warp_sum(pv);
-      const double b2 = t * pv;
-      double pc[kS];
-#pragma unroll
-      for (int sl = 0; sl < kS; ++sl) {
-        const int c = r0 + lane + 32 * sl;
-        pc[sl] = c < n ? p[c] : 0.0;
-      }
-      double part = 0.0;
-      for (int r = r0 + warp; r < n; r += nw) {
-        const double vr = v[r], pr = p[r];
-        double* Ar = &S.at(r, 0);
-#pragma unroll
-        for (int sl = 0; sl < kS; ++sl) {
-          const int c = r0 + lane + 32 * sl;
-          if (c < n) {
-            const double nv = Ar[c] - ((vr * pc[sl] + pr * vc[sl]) - b2 * (vr * vc[sl]));
-            Ar[c] = nv;
-            if (c == r0 && r >= r0 + 2) part += nv * nv;
-          }
-        }
-      }
-      part = block_sum(part, red);  // (3)
-      if (tid == 0) red[40] = part;
-      __syncthreads();
-      continue;
-    }
-    {
-      const int q = tid & 3, r = r0 + (tid >> 2);
-      double s = 0.0;
-      if (r < n)
-        for (int c = r0 + q; c < n; c += 4) s += S.at(r, c) * v[c];
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (q == 0 && r < n) {
-        p[r] = t * s;
-        part_pv[r - r0] = t * s * v[r];
-      }
-    }
-    __syncthreads();  // (2) p complete
-    double pv = 0.0;
-    for (int r = lane; r < m; r += 32) pv += part_pv[r];
-    pv = warp_sum(pv);
-    const double b2 = t * pv;
-    double part = 0.0;
-    for (int c = r0 + warp; c < n; c += nw) {
-      const double vc = v[c], pc = p[c];
-      for (int r = c + lane; r < n; r += 32) {
-        const double vr = v[r];
-        const double nv = S.at(r, c) - ((vr * pc + p[r] * vc) - b2 * (vr * vc));
-        S.at(r, c) = nv;
-        if (c == r0 && r >= r0 + 2) part += nv * nv;
-      }
-    }
-    part = block_sum(part, red);  // (3)
-    if (tid == 0) red[40] = part;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    b.d[n - 1] = S.at(n - 1, n - 1);
-    b.e[n - 1] = 0.0;
-    b.tau[n - 1] = 0.0;
-  }
-  __syncthreads();
-  for (int i = tid; i < n; i += nth) b.e2[i] = b.e[i] * b.e[i];
 }
 
-__global__ void __launch_bounds__(1024) tridiag_kernel(const double* M, int ldm, int n, EigBufs b, int* flags) {
+template <int C>
+__device__ __forceinline__ double* tri_peer(double* p, int q) {
+  if constexpr (C == 1) {
+    return p;
+  } else {
+    return cooperative_groups::this_cluster().map_shared_rank(p, q);
+  }
+}
+
+#ifdef STG_TRI_PROF  // development probe (tools/microbench/tri_parts.cu): cycles per phase, thread 0
+__device__ long long g_tri_prof[8];
+#define STG_TRI_MARK(k)                                  \
+  do {                                                   \
+    if (threadIdx.x == 0) {                              \
+      const long long now_ = clock64();                  \
+      g_tri_prof[k] += now_ - prof_t_;                   \
+      prof_t_ = now_;                                    \
+    }                                                    \
+  } while (0)
+#else
+#define STG_TRI_MARK(k) \
+  do {                  \
+  } while (0)
+#endif
+
+// U for NS live 32-column slots: rows lr = lb, lb + kTriW, ... of this warp
+// U for NS live 32-column slots: A(r, c) -= v_r w_c + p_r v_c on this warp's
+// rows, w = p - b2 v; p, v, w precomputed in shared memory for the column.
+template <int NS>
+__device__ __forceinline__ void tri_update_rows(double* A, int n, int r0, int C, int rank, int lr0, int my_rows,
+                                                int warp, int lane, const double* Pv, const double* Vv,
+                                                const double* Wv) {
+  double vc[NS], wc[NS];
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    const int c = r0 + lane + 32 * sl;
+    vc[sl] = c < n ? Vv[c] : 0.0;
+    wc[sl] = c < n ? Wv[c] : 0.0;
+  }
+  for (int lb = lr0 + warp; lb < my_rows; lb += 2 * kTriW) {  // two rows per pass
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int lr = lb + u * kTriW;
+      if (lr < my_rows) {
+        const int rr = lr * C + rank;
+        const double vr = Vv[rr], pr = Pv[rr];
+        double* Ar = A + static_cast<i64>(lr) * n + r0 + lane;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          if (sl < NS - 1 || r0 + lane + 32 * sl < n) Ar[32 * sl] = fma(-vr, wc[sl], fma(-pr, vc[sl], Ar[32 * sl]));
+        }
+      }
+    }
+  }
+}
+
+template <int C>
+__device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int gmax, EigBufs b, int* flags,
+                             int rank) {
+#ifdef STG_TRI_PROF
+  long long prof_t_ = clock64();
+#endif
   extern __shared__ double sm[];
-  if (n <= kEigFullN)
-    tridiag_body<true>(M, ldm, n, b, flags, sm);
-  else
-    tridiag_body<false>(M, ldm, n, b, flags, sm);
-}
-
-inline size_t tridiag_smem_bytes(int n) {
-  const size_t words = n <= kEigFullN ? static_cast<size_t>(n) * n : static_cast<size_t>(n) * (n + 1) / 2;
-  return sizeof(double) * (words + 3 * static_cast<size_t>(n) + 48);
-}
-
-// Tridiagonalization on a thread-block cluster: the 8 CTAs of one cluster own
-// the rows r = rank (mod 8) in full (n <= kEigMaxN: <= 30 rows x 232 cols per
-// CTA in shared memory). Per column: the owner of row i builds the reflector
-// and broadcasts it through distributed shared memory, every CTA computes
-// p = tau A v for its rows and all-gathers it, then updates its rows. Two
-// cluster barriers per column; v / p / partial buffers alternate by column
-// parity so a CTA never overwrites a buffer another CTA is still reading.
-constexpr int kClusterCtas = 8;
-constexpr int kTriClusterThreads = 256;
-
-__global__ void __cluster_dims__(kClusterCtas, 1, 1) __launch_bounds__(kTriClusterThreads)
-    tridiag_cluster_kernel(const double* M, int ldm, int n, EigBufs b, int* flags) {
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = static_cast<int>(cluster.block_rank());
-  extern __shared__ double sm[];
-  const int nloc = (n - rank + kClusterCtas - 1) / kClusterCtas;  // rows rank, rank+8, ...
-  const int nmax = (n + kClusterCtas - 1) / kClusterCtas;          // same layout in every CTA (DSMEM offsets)
-  double* rows = sm;                                   // nmax x n
-  double* vbuf = rows + static_cast<i64>(nmax) * n;    // [2][n]
-  double* pbuf = vbuf + 2 * n;                         // [2][n]
-  double* part = pbuf + 2 * n;                         // [2][kClusterCtas]
-  double* scal = part + 2 * kClusterCtas;              // [2] tau per parity
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (i64 idx = tid; idx < static_cast<i64>(nloc) * n; idx += blockDim.x) {
-    const int lr = static_cast<int>(idx / n), c = static_cast<int>(idx % n);
-    const int r = rank + lr * kClusterCtas;
-    const double x = M[static_cast<i64>(r) * ldm + c], y = M[static_cast<i64>(c) * ldm + r];
-    if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
-    rows[static_cast<i64>(lr) * n + c] = 0.5 * (x + y);
+  const int nloc = tri_rows(n, C);
+  double* A = sm;                                   // nloc x n, local row lr <-> row lr C + rank
+  double* colb = A + static_cast<i64>(nloc) * n;    // [2][n] column i by parity
+  double* a0 = colb + 2 * n;                        // [n] row r0
+  double* Pv = a0 + n;                              // [n] p = tau A v
+  double* Vv = Pv + n;                              // [n] v
+  double* Wv = Vv + n;                              // [n] w = p - tau (p'v) v
+  double* acc = Wv + n;                             // [C * gmax][n] partial column sums
+  const int nacc_max = C * gmax;
+  double* pvs = acc + static_cast<i64>(nacc_max) * n;  // [2][C * kTriW][4]: (Av)'v pieces, squared-norm share
+  double* scl = pvs + 2 * C * kTriW * 4;            // [2] x {tau, scal, beta, alpha}
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int my_rows = (n - rank + C - 1) / C;
+  // load (S + S')/2 and publish column 0 (its squared norm in slot 3, its alpha)
+  double sg = 0.0;
+  for (int lr = warp; lr < my_rows; lr += kTriW) {
+    const int r = lr * C + rank;
+    double* Ar = A + static_cast<i64>(lr) * n;
+    for (int c = lane; c < n; c += 32) {
+      const double x = M[static_cast<i64>(r) * ldm + c];
+      const double y = sym_input ? x : M[static_cast<i64>(c) * ldm + r];  // producers that mirror exactly skip it
+      if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
+      const double v = 0.5 * (x + y);
+      Ar[c] = v;
+      if (c == 0) {
+        for (int q = 0; q < C; ++q) tri_peer<C>(colb, q)[r] = v;
+        if (r >= 2) sg += v * v;
+        if (r == 1)
+          for (int q = 0; q < C; ++q) tri_peer<C>(scl, q)[3] = v;
+      }
+    }
   }
-  cluster.sync();
+  sg = warp_sum(sg);
+  if (lane == 0)
+    for (int q = 0; q < C; ++q) tri_peer<C>(pvs, q)[(rank * kTriW + warp) * 4 + 3] = sg;
+  tri_sync<C>();
+  STG_TRI_MARK(0);
   for (int i = 0; i + 1 < n; ++i) {
-    const int par = i & 1, r0 = i + 1;
-    double* v = vbuf + par * n;
-    double* p = pbuf + par * n;
-    // 1. the owner of row i (= column i below the diagonal) builds the reflector
-    if (i % kClusterCtas == rank && warp == 0) {
-      const double* ri = rows + static_cast<i64>(i / kClusterCtas) * n;
-      double sg = 0.0;
-      for (int c = r0 + 1 + lane; c < n; c += 32) sg += ri[c] * ri[c];
-      sg = warp_sum(sg);
-      const double alpha = ri[r0];
-      double t = 0.0, sc = 0.0, beta = alpha;
-      if (sg > 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + sg), alpha);
+    const int par = i & 1, npar = par ^ 1, r0 = i + 1;
+    const double* col = colb + par * n;
+    double* pv = pvs + par * C * kTriW * 4;
+    double* sc = scl + par * 4;
+    const int lr0 = (r0 - rank + C - 1) / C;  // first local row with r >= r0
+    const bool owner0 = r0 % C == rank;
+    const int nblk = (n - r0 + 31) >> 5;      // <= 8
+    const int G = min(gmax, (kTriW - 1) / nblk);  // warps per 32-column block
+    const int nsw = nblk * G;                 // summing warps (< kTriW: the last one is free)
+    // S: unscaled column sums (warps < nsw), reflector scalars (last warp)
+    if (warp < nsw) {
+      const int blk = warp % nblk, g = warp / nblk;
+      const int r = r0 + 32 * blk + lane;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (r < n) {
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int lr = lr0 + (owner0 ? 1 : 0) + g;  // rows c > r0, every G-th
+        for (; lr + 3 * G < my_rows; lr += 4 * G) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            a4[u] = fma(A[static_cast<i64>(lr + u * G) * n + r], col[(lr + u * G) * C + rank], a4[u]);
+        }
+        for (; lr < my_rows; lr += G) a4[0] = fma(A[static_cast<i64>(lr) * n + r], col[lr * C + rank], a4[0]);
+        const double ac = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        STG_TRI_MARK(6);
+        for (int q = 0; q < C; ++q) tri_peer<C>(acc + static_cast<i64>(rank * G + g) * n, q)[r] = ac;
+        if (r == r0) {
+          s3 = ac;
+        } else {
+          s2 = ac * col[r];
+        }
+        if (owner0 && g == 0) {
+          const double x = A[static_cast<i64>(lr0) * n + r];  // row r0
+          for (int q = 0; q < C; ++q) tri_peer<C>(a0, q)[r] = x;
+          if (r != r0) s1 = x * col[r];
+        }
+      }
+      STG_TRI_MARK(7);
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      s3 = warp_sum(s3);
+      if (lane < C) {
+        double* d = tri_peer<C>(pv, lane) + (rank * kTriW + warp) * 4;
+        d[0] = s1;
+        d[1] = s2;
+        d[2] = s3;
+      }
+    } else if (warp == kTriW - 1) {
+      const double sigma = warp_sum(lane < C * kTriW ? pv[lane * 4 + 3] : 0.0);
+      const double alpha = sc[3];
+      double t = 0.0, scal = 0.0, beta = alpha;
+      if (sigma > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
         t = (beta - alpha) / beta;
-        sc = 1.0 / (alpha - beta);
+        scal = 1.0 / (alpha - beta);
       }
       if (lane == 0) {
-        b.tau[i] = t;
-        b.e[i] = beta;
-        b.d[i] = ri[i];
-      }
-      for (int dst = 0; dst < kClusterCtas; ++dst) {
-        double* rv = cluster.map_shared_rank(v, dst);
-        double* rs = cluster.map_shared_rank(scal, dst);
-        for (int c = r0 + lane; c < n; c += 32) rv[c] = c == r0 ? 1.0 : ri[c] * sc;
-        if (lane == 0) rs[par] = t;
-      }
-      for (int c = r0 + lane; c < n; c += 32) b.V[static_cast<i64>(i) * n + c] = c == r0 ? 1.0 : ri[c] * sc;
-    }
-    cluster.sync();  // (1) v, tau everywhere
-    const double t = scal[par];
-    // 2. p = tau A22 v on this CTA's rows r >= r0, all-gathered
-    const int lr0 = (r0 - rank + kClusterCtas - 1) / kClusterCtas;  // first local row with r >= r0
-    double pv_local = 0.0;
-    if (t != 0.0) {
-      for (int lr = lr0 + warp; lr < nloc; lr += nw) {
-        const int r = rank + lr * kClusterCtas;
-        const double* ar = rows + static_cast<i64>(lr) * n;
-        double s = 0.0;
-        for (int c = r0 + lane; c < n; c += 32) s += ar[c] * v[c];
-        s = warp_sum(s) * t;
-        if (lane < kClusterCtas) {
-          double* rp = cluster.map_shared_rank(p, lane);
-          rp[r] = s;
+        sc[0] = t;
+        sc[1] = scal;
+        sc[2] = beta;
+        if (rank == 0) {
+          b.tau[i] = t;
+          b.e[i] = beta;
+          b.e2[i] = beta * beta;
         }
-        pv_local += s * v[r];  // identical in every lane after the butterfly
+      }
+      if (rank == 0)
+        for (int c = r0 + lane; c < n; c += 32) b.V[static_cast<i64>(i) * n + c] = c == r0 ? 1.0 : col[c] * scal;
+      if (i % C == rank && lane == 0) b.d[i] = A[static_cast<i64>(i / C) * n + i];
+    }
+    STG_TRI_MARK(1);
+    tri_sync<C>();
+    STG_TRI_MARK(2);
+    // U
+    const double t = sc[0], scal = sc[1];
+    if (t != 0.0) {
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (lane < C * kTriW && (lane % kTriW) < nsw) {
+        s1 = pv[lane * 4 + 0];
+        s2 = pv[lane * 4 + 1];
+        s3 = pv[lane * 4 + 2];
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      s3 = warp_sum(s3);
+      const double avv = a0[r0] + scal * (s3 + s1) + scal * scal * s2;  // (Av)'v
+      const double b2 = t * t * avv;
+      const int nacc = C * G;
+      for (int r = r0 + tid; r < n; r += kTriThreads) {
+        double sa = 0.0;
+        for (int q = 0; q < nacc; ++q) sa += acc[q * n + r];
+        const double pr = t * fma(scal, sa, a0[r]);
+        const double vr = r == r0 ? 1.0 : scal * col[r];
+        Pv[r] = pr;
+        Vv[r] = vr;
+        Wv[r] = pr - b2 * vr;
+      }
+      __syncthreads();
+      switch (nblk) {
+        case 1: tri_update_rows<1>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 2: tri_update_rows<2>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 3: tri_update_rows<3>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 4: tri_update_rows<4>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 5: tri_update_rows<5>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 6: tri_update_rows<6>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        case 7: tri_update_rows<7>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+        default: tri_update_rows<8>(A, n, r0, C, rank, lr0, my_rows, warp, lane, Pv, Vv, Wv); break;
+      }
+      __syncwarp();
+    }
+    STG_TRI_MARK(3);
+    // publish column i + 1 from the rows this warp owns (lane u: its u-th row)
+    double* Pn = colb + npar * n;
+    double sg2 = 0.0;
+    for (int lb = lr0 + warp; lb < my_rows; lb += 32 * kTriW) {
+      const int lr = lb + lane * kTriW;
+      if (lr < my_rows) {
+        const int rr = lr * C + rank;
+        if (rr >= r0 + 1) {
+          const double x = A[static_cast<i64>(lr) * n + r0];
+          for (int q = 0; q < C; ++q) tri_peer<C>(Pn, q)[rr] = x;
+          if (rr >= r0 + 2) sg2 = fma(x, x, sg2);
+          if (rr == r0 + 1)
+            for (int q = 0; q < C; ++q) tri_peer<C>(scl + npar * 4, q)[3] = x;
+        }
       }
     }
-    // CTA partial of p'v (fixed order: warps, then ranks)
-    __shared__ double wpart[32];
-    if (lane == 0) wpart[warp] = pv_local;
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += wpart[w];
-      for (int dst = 0; dst < kClusterCtas; ++dst) cluster.map_shared_rank(part, dst)[par * kClusterCtas + rank] = s;
-    }
-    cluster.sync();  // (2) p and partials everywhere
-    if (t == 0.0) continue;
-    double pv = 0.0;
-    for (int q = 0; q < kClusterCtas; ++q) pv += part[par * kClusterCtas + q];
-    const double b2 = t * pv;
-    // 3. update this CTA's rows: A -= v p' + p v' - b2 v v'
-    for (int lr = lr0 + warp; lr < nloc; lr += nw) {
-      const int r = rank + lr * kClusterCtas;
-      double* ar = rows + static_cast<i64>(lr) * n;
-      const double vr = v[r], pr = p[r];
-      for (int c = r0 + lane; c < n; c += 32) {
-        const double vc = v[c];
-        ar[c] -= (vr * p[c] + pr * vc) - b2 * (vr * vc);
-      }
-    }
-    __syncthreads();  // this CTA's rows are final for column i+1's owner
+    sg2 = warp_sum(sg2);
+    if (lane == 0)
+      for (int q = 0; q < C; ++q) tri_peer<C>(pvs + npar * C * kTriW * 4, q)[(rank * kTriW + warp) * 4 + 3] = sg2;
+    STG_TRI_MARK(4);
+    tri_sync<C>();
+    STG_TRI_MARK(5);
   }
-  if ((n - 1) % kClusterCtas == rank && tid == 0) {
-    b.d[n - 1] = rows[static_cast<i64>((n - 1) / kClusterCtas) * n + (n - 1)];
+  if ((n - 1) % C == rank && tid == 0) {
+    b.d[n - 1] = A[static_cast<i64>((n - 1) / C) * n + (n - 1)];
     b.e[n - 1] = 0.0;
+    b.e2[n - 1] = 0.0;
     b.tau[n - 1] = 0.0;
   }
-  cluster.sync();
-  if (rank == 0)
-    for (int i = tid; i < n; i += blockDim.x) b.e2[i] = b.e[i] * b.e[i];
 }
 
-inline size_t tridiag_cluster_smem_bytes(int n) {
-  const int nloc = (n + kClusterCtas - 1) / kClusterCtas;
-  return sizeof(double) * (static_cast<size_t>(nloc) * n + 4 * static_cast<size_t>(n) + 2 * kClusterCtas + 2);
+__global__ void __launch_bounds__(kTriThreads) tridiag1_kernel(const double* M, int ldm, int n, int sym_input,
+                                                               int gmax, EigBufs b, int* flags) {
+  tridiag_body<1>(M, ldm, n, sym_input, gmax, b, flags, 0);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads)
+    tridiag2_kernel(const double* M, int ldm, int n, int sym_input, int gmax, EigBufs b, int* flags) {
+  tridiag_body<2>(M, ldm, n, sym_input, gmax, b, flags,
+                  static_cast<int>(cooperative_groups::this_cluster().block_rank()));
 }
 
 // All eigenvalues of the tridiagonal matrix by bisection on Sturm counts:
@@ -658,12 +635,27 @@ inline EigBufs eig_carve(double* dbuf, int* ibuf, int n, int want) {
   return b;
 }
 
+inline void eig_set_attributes() {
+  STG_CUDA(cudaFuncSetAttribute(tridiag1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                232448));
+  STG_CUDA(cudaFuncSetAttribute(tridiag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                232448));
+  STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(invit_smem_bytes(kEigMaxN))));
+}
+
 template <class Launch>
-void syev_launch(Launch&& L, const double* M, int ldm, int n, int order, int want, double ortol, double* w_sorted,
+void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int order, int want, double ortol,
+                 double* w_sorted,
                  double* F, int ldf, double* dbuf, int* ibuf, int* flags) {
   const EigBufs b = eig_carve(dbuf, ibuf, n, want);
-  L(tridiag_cluster_kernel, dim3(kClusterCtas), dim3(kTriClusterThreads), tridiag_cluster_smem_bytes(n), M, ldm, n, b,
-    flags);
+  if (n <= kEig1N) {
+    const int g = tridiag_gmax(n, 1);
+    L(tridiag1_kernel, dim3(1), dim3(kTriThreads), tridiag_smem_bytes(n, 1, g), M, ldm, n, sym_input, g, b, flags);
+  } else {
+    const int g = tridiag_gmax(n, 2);
+    L(tridiag2_kernel, dim3(2), dim3(kTriThreads), tridiag_smem_bytes(n, 2, g), M, ldm, n, sym_input, g, b, flags);
+  }
   L(bisect_kernel, dim3(static_cast<unsigned>(cdiv(kBisG * n, 128))), dim3(128), sizeof(double) * 2 * n, b, n);
   L(select_kernel, dim3(1), dim3(256), sizeof(int) * n, b, n, order, want, ortol, w_sorted);
   L(invit_kernel, dim3(static_cast<unsigned>(cdiv(want, kInvitThreads))), dim3(kInvitThreads), invit_smem_bytes(n), b,

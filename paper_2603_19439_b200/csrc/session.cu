@@ -778,13 +778,7 @@ class Session {
     if (D > kEigMaxN || want > kEigMaxWant) return false;
     static bool attr = false;
     if (!attr) {
-      STG_CUDA(cudaFuncSetAttribute(tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(std::max(tridiag_smem_bytes(kEigMaxN),
-                                                              tridiag_smem_bytes(kEigFullN)))));
-      STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(invit_smem_bytes(kEigMaxN))));
-      STG_CUDA(cudaFuncSetAttribute(tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(tridiag_cluster_smem_bytes(kEigMaxN))));
+      eig_set_attributes();
       attr = true;
     }
     const int wv = std::max(want, 1);
@@ -794,7 +788,8 @@ class Session {
     kbegin(kEig, 4.0 * D * D * D / 3.0);
     STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
     syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, st_, args...); },
-                M, ldm, D, order, wv, ortol, w_sorted, F, ldf, dbuf, ibuf, flags_ptr());
+                M, ldm, D, /*sym_input: exactly mirrored Grams / RR matrix*/ 1, order, wv, ortol, w_sorted, F, ldf,
+                dbuf, ibuf, flags_ptr());
     kend();
     return true;
   }
@@ -1720,13 +1715,7 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
     if (n == 0) return;
     if (n > stg::kEigMaxN) throw std::invalid_argument("st_sym_eig_dense: order above the on-device solver limit");
     STG_CUDA(cudaSetDevice(device));
-    STG_CUDA(cudaFuncSetAttribute(stg::tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(std::max(stg::tridiag_smem_bytes(stg::kEigMaxN),
-                                                            stg::tridiag_smem_bytes(stg::kEigFullN)))));
-    STG_CUDA(cudaFuncSetAttribute(stg::invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(stg::invit_smem_bytes(stg::kEigMaxN))));
-    STG_CUDA(cudaFuncSetAttribute(stg::tridiag_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(stg::tridiag_cluster_smem_bytes(stg::kEigMaxN))));
+    stg::eig_set_attributes();
     // row-major copy of S' (the solver symmetrizes (S + S')/2 itself)
     std::vector<double> rm(static_cast<size_t>(n * n));
     for (int64_t i = 0; i < n; ++i)
@@ -1751,7 +1740,7 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
           kernel<<<g, bl, sm>>>(args...);
           STG_LAUNCH();
         },
-        dm, static_cast<int>(n), static_cast<int>(n), order, static_cast<int>(wv), 1e-3, dw, df,
+        dm, static_cast<int>(n), static_cast<int>(n), /*sym_input*/ 0, order, static_cast<int>(wv), 1e-3, dw, df,
         static_cast<int>(wv), dbuf, ibuf, di);
     cudaEventRecord(e1);
     STG_CUDA(cudaDeviceSynchronize());

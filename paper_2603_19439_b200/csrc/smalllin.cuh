@@ -322,15 +322,18 @@ __global__ void orthocheck_kernel(const double* Gm, int ldg, int D, double tol, 
   if (!(fabs(v) <= tol)) atomicOr(flags, kNotOrthonormal);
 }
 
-// M(D x D) = zx diag(lam) zx' + T   (Eq. 14, trackers.cpp:300-301)
+// M(D x D) = zx diag(lam) zx' + T   (Eq. 14, trackers.cpp:300-301), evaluated
+// on (min(i,j), max(i,j)) so M is exactly symmetric (T, a mirrored Gram, is),
+// and the eigensolver's (M + M')/2 (eig.hpp:47) is M itself.
 __global__ void rr_matrix_kernel(const double* zx, int ldzx, const double* lam, int k, const double* T, int ldt,
                                  int D, double* M, int ldm) {
   const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<i64>(D) * D) return;
   const int i = static_cast<int>(idx / D), j = static_cast<int>(idx % D);
+  const int lo = min(i, j), hi = max(i, j);
   double s = 0.0;
-  for (int l = 0; l < k; ++l) s += zx[static_cast<i64>(i) * ldzx + l] * lam[l] * zx[static_cast<i64>(j) * ldzx + l];
-  M[static_cast<i64>(i) * ldm + j] = s + T[static_cast<i64>(i) * ldt + j];
+  for (int l = 0; l < k; ++l) s += zx[static_cast<i64>(lo) * ldzx + l] * lam[l] * zx[static_cast<i64>(hi) * ldzx + l];
+  M[static_cast<i64>(i) * ldm + j] = s + T[static_cast<i64>(lo) * ldt + hi];
 }
 
 // orig2[c] = G1[c][c] + sum_l C[l][c]^2: squared norm of the column before the
