@@ -18,13 +18,18 @@ ap.add_argument("--scale", type=int, default=20)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--k", type=int, default=32)
+ap.add_argument("--real-x0", action="store_true", help="leading eigenpairs (as bench.py) instead of a random basis")
 args = ap.parse_args()
 
 s = streams.config3(scale=args.scale, steps=args.warmup + args.steps)
 rp, col, val = s.csr0()
 n = len(rp) - 1
-x, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((n, args.k)))
-vals = np.linspace(100.0, 10.0, args.k)
+if args.real_x0:
+    from paper_2603_19439_b200 import init_eig  # noqa: E402
+    vals, x = init_eig.leading_eigenpairs(rp, col, val, args.k, "abs_desc", device="cuda:0")
+else:
+    x, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((n, args.k)))
+    vals = np.linspace(100.0, 10.0, args.k)
 g = TrackerSession(rp, col, val, vals, x, kind="grest-rsvd", k=args.k, seed=0, timing=True,
                    kernel_timing=bool(os.environ.get("STG_KLOG")), cusolver_eig=bool(os.environ.get("STG_CUSOLVER")))
 for t, u in enumerate(s.updates):
