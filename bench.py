@@ -260,12 +260,20 @@ def run_ours(args):
     own = {k_: v for k_, v in classes.items() if k_ != "eigensolver"}
     dom = max(own, key=lambda k_: own[k_]["ms_per_step"]) if own else None
     roof = None
+    traffic = {}
+    try:  # DRAM bytes of one representative launch per class, from the committed ncu --set full capture
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")) as fh:
+            traffic = json.load(fh)
+    except (OSError, ValueError):
+        traffic = {}
     if dom is not None:
         st = kstats[dom]
         ach = st["work"] / (st["ms"] / 1e3)
         if dom in ("dmma_gram", "dmma_gemm", "masked_gram_x"):
+            tr = traffic.get(dom)
             roof = dict(kernel=dom, bound="tensor", achieved=ach / 1e12, peak=FP64_PEAK_MEASURED, unit="TFLOP/s",
-                        frac=ach / 1e12 / FP64_PEAK_MEASURED, traffic=None,
+                        frac=ach / 1e12 / FP64_PEAK_MEASURED, traffic=tr["bytes_per_launch"] if tr else None,
+                        traffic_launch=tr, 
                         peak_source="measured cuBLAS DGEMM 8192^3 on this pool (FP64 not in MEASURED_PEAKS.json)",
                         algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="flop")
         else:
