@@ -73,10 +73,10 @@ constexpr size_t kGramSmem = gram_smem(1, 4);  // the largest layout
 // Gram). Operand fragment (x, k-step kk) sits at pa[kk KA + x XA], (y, kk) at
 // pb[kk KB + y YB]. The block shape is warp-uniform, chosen once per tile, so
 // edge and diagonal tiles issue no DMMA whose result is discarded.
-template <int NX, int NY, bool TRI, int KA, int XA, int KB, int YB>
+template <int NX, int NY, bool TRI, int KA, int XA, int KB, int YB, int KR = BK2>
 __device__ __forceinline__ void warp_mma(double (&acc)[4][4][2], const double* pa, const double* pb) {
 #pragma unroll
-  for (int kk = 0; kk < BK2; kk += 4) {
+  for (int kk = 0; kk < KR; kk += 4) {
     double fa[NX], fb[NY];
 #pragma unroll
     for (int x = 0; x < NX; ++x) fa[x] = pa[kk * KA + x * XA];
@@ -97,18 +97,18 @@ __device__ __forceinline__ int warp_code(int nx, int ny, bool tri) {
   return (nx - 1) * 4 + ny;
 }
 
-template <int KA, int XA, int KB, int YB>
+template <int KA, int XA, int KB, int YB, int KR = BK2>
 __device__ __forceinline__ void warp_mma_dispatch(int code, double (&acc)[4][4][2], const double* pa,
                                                   const double* pb) {
   switch (code) {
 #define STG_MMA_CASE(NX, NY) \
-  case (NX - 1) * 4 + NY: warp_mma<NX, NY, false, KA, XA, KB, YB>(acc, pa, pb); break;
+  case (NX - 1) * 4 + NY: warp_mma<NX, NY, false, KA, XA, KB, YB, KR>(acc, pa, pb); break;
     STG_MMA_CASE(1, 1) STG_MMA_CASE(1, 2) STG_MMA_CASE(1, 3) STG_MMA_CASE(1, 4)
     STG_MMA_CASE(2, 1) STG_MMA_CASE(2, 2) STG_MMA_CASE(2, 3) STG_MMA_CASE(2, 4)
     STG_MMA_CASE(3, 1) STG_MMA_CASE(3, 2) STG_MMA_CASE(3, 3) STG_MMA_CASE(3, 4)
     STG_MMA_CASE(4, 1) STG_MMA_CASE(4, 2) STG_MMA_CASE(4, 3) STG_MMA_CASE(4, 4)
 #undef STG_MMA_CASE
-    case 17: warp_mma<4, 4, true, KA, XA, KB, YB>(acc, pa, pb); break;
+    case 17: warp_mma<4, 4, true, KA, XA, KB, YB, KR>(acc, pa, pb); break;
     default: break;
   }
 }
@@ -223,6 +223,112 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2) gram_tn_kernel(GramArgs 
     gram_tile<true, WM, WN>(a, ti, tj, r0, r1, dsm);
   else
     gram_tile<false, WM, WN>(a, ti, tj, r0, r1, dsm);
+}
+
+// ---- TMA pipeline variant (default when the operands are 16-byte aligned
+// and no row mask applies). Each 16-row stage of the A and B column slabs is
+// one 2-D TMA box per operand ({32 WM + 4} x 16 and {32 WN + 4} x 16: the box
+// is 4 columns wider than the tile, so it lands with the conflict-free padded
+// row pitch; columns/rows outside the matrix arrive as zeros). kStages stages
+// form a ring with full (transaction-counted) and empty mbarriers: the four
+// warps never meet at a CTA barrier and no thread computes load addresses.
+constexpr int kBK = 16, kStages = 4;
+
+template <int WM, int WN>
+constexpr size_t gram_tma_smem() {
+  return 128 + sizeof(double) * kStages * kBK * ((32 * WM + 4) + (32 * WN + 4));
+}
+
+template <int WM, int WN>
+__global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
+    gram_tma_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
+  unsigned long long* empty = full + kStages;
+  double* stage0 = reinterpret_cast<double*>(smraw + 128);
+  constexpr int TA = 32 * WM, TB = 32 * WN, SA = TA + 4, SB = TB + 4, STG = kBK * (SA + SB);
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  int ti, tj;
+  if (a.sym) {
+    int t = blockIdx.x;
+    ti = 0;
+    while (t >= a.tiles_i - ti) {
+      t -= a.tiles_i - ti;
+      ++ti;
+    }
+    tj = ti + t;
+  } else {
+    ti = blockIdx.x / a.tiles_j;
+    tj = blockIdx.x % a.tiles_j;
+  }
+  const i64 r0 = static_cast<i64>(blockIdx.y) * a.rows_per_split;
+  const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % WM, wn = warp / WM;
+  const int ibase = ti * TA + wm * 32, jbase = tj * TB + wn * 32;
+  int nx = frags_left(a.m1, ibase);
+  const int ny = frags_left(a.m2, jbase);
+  bool tri = false;
+  if (a.sym) {
+    if (ibase >= jbase + 32) nx = 0;
+    tri = ibase == jbase;
+  }
+  const int code = warp_code(nx, ny, tri);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const i64 nch = r1 > r0 ? cdiv(r1 - r0, kBK) : 0;
+  const int ca = ti * TA, cb = tj * TB;
+  auto produce = [&](i64 q) {  // one thread
+    const int st = static_cast<int>(q % kStages);
+    double* sa = stage0 + st * STG;
+    const int row0 = static_cast<int>(r0 + q * kBK);
+    mbar_arrive_expect_tx(&full[st], kStageBytes);
+    tma_load_2d(sa, &tmA, ca, row0, &full[st]);
+    tma_load_2d(sa + kBK * SA, &tmB, cb, row0, &full[st]);
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  if (threadIdx.x == 0)
+    for (i64 q = 0; q < min(nch, static_cast<i64>(kStages - 1)); ++q) produce(q);
+  for (i64 q = 0; q < nch; ++q) {
+    if (threadIdx.x == 0 && q + kStages - 1 < nch) {
+      const i64 qq = q + kStages - 1;  // refills the stage chunk q - 1 used
+      if (qq >= kStages) mbar_wait(&empty[qq % kStages], static_cast<unsigned>((qq / kStages - 1) & 1));
+      produce(qq);
+    }
+    const int st = static_cast<int>(q % kStages);
+    mbar_wait(&full[st], static_cast<unsigned>((q / kStages) & 1));
+    const double* sa = stage0 + st * STG;
+    const double* pa = sa + t * SA + wm * 32 + g;
+    const double* pb = sa + kBK * SA + t * SB + wn * 32 + g;
+    if (code == 16)
+      warp_mma<4, 4, false, SA, 8, SB, 8, kBK>(acc, pa, pb);
+    else
+      warp_mma_dispatch<SA, 8, SB, 8, kBK>(code, acc, pa, pb);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  if (code == 0) return;
+  const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
+  double* out = a.partial + static_cast<i64>(blockIdx.y) * m1p * m2p;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      if (x >= nx || y >= ny) continue;
+      const i64 i = ibase + x * 8 + g, j = jbase + y * 8 + 2 * t;
+      *reinterpret_cast<double2*>(out + i * m2p + j) = make_double2(acc[x][y][0], acc[x][y][1]);
+    }
 }
 
 // Deterministic split reduction, one warp per output element: lane l sums

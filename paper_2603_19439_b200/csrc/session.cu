@@ -204,6 +204,12 @@ class Session {
                                   static_cast<int>(dm::gram_smem(1, 4))));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::gram_smem(4, 1))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tma_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<2, 2>())));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tma_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<1, 4>())));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_tma_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<4, 1>())));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -659,8 +665,20 @@ class Session {
     if (klog_) snprintf(ktag_, sizeof(ktag_), "gram %lldx%dx%d%s", rows, m1, m2, sym ? " sym" : "");
     kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
     const dim3 grid(ntiles, static_cast<unsigned>(splits));
+    const bool bulk = !mask && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                      lda % 2 == 0 && ldb % 2 == 0;
     if (narrow)
       launch(dm::gram_tn_small_kernel, grid, dim3(dm::NT), 0, st_, a);
+    else if (bulk) {
+      const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, dm::kBK);
+      const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, dm::kBK);
+      if (layout == 1)
+        launch(dm::gram_tma_kernel<1, 4>, grid, dim3(dm::NT), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb);
+      else if (layout == 2)
+        launch(dm::gram_tma_kernel<4, 1>, grid, dim3(dm::NT), dm::gram_tma_smem<4, 1>(), st_, a, ma, mb);
+      else
+        launch(dm::gram_tma_kernel<2, 2>, grid, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb);
+    }
     else if (layout == 1)
       launch(dm::gram_tn_kernel<1, 4>, grid, dim3(dm::NT), dm::gram_smem(1, 4), st_, a);
     else if (layout == 2)
