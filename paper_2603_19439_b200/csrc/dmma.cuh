@@ -585,6 +585,119 @@ __device__ __forceinline__ void nn_tile(const NNArgs& a, i64 row0, int tj, doubl
     }
 }
 
+// TMA pipeline variant of nn_tile: per 32-wide K chunk one 2-D box of A
+// ({36, 64}: 64 rows, the padded K pitch) and one of C ({68, 32}); two stages
+// with full/empty mbarriers; out-of-range rows/columns arrive as zeros.
+constexpr int kNNStages = 2;
+constexpr size_t kNNTmaSmem = 128 + sizeof(double) * kNNStages * (BM * SAR2 + BK2 * SST);
+
+template <bool FULL, bool BETA>
+__device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmC, i64 row0,
+                                            int tj, unsigned char* smraw) {
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
+  unsigned long long* empty = full + kNNStages;
+  double* stage0 = reinterpret_cast<double*>(smraw + 128);
+  constexpr int STG = BM * SAR2 + BK2 * SST;
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int kmax = a.upper_tri_c ? min(a.m1, (tj + 1) * BN) : a.m1;
+  const int nk = static_cast<int>(cdiv(kmax, BK2));
+  const int code = FULL ? 16 : warp_code(frags_left(a.nrows, row0 + wm * 32), frags_left(a.m2, tj * BN + wn * 32), false);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kNNStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto produce = [&](int q) {
+    const int st = q % kNNStages;
+    double* sa = stage0 + st * STG;
+    mbar_arrive_expect_tx(&full[st], kStageBytes);
+    tma_load_2d(sa, tmA, q * BK2, static_cast<int>(row0), &full[st]);
+    tma_load_2d(sa + BM * SAR2, tmC, tj * BN, q * BK2, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(nk, kNNStages - 1); ++q) produce(q);
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  double bpre[BETA ? 4 : 1][4][2];
+  if (FULL && BETA) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const i64 r = row0 + wm * 32 + x * 8 + g;
+        const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
+        const double2 v = *reinterpret_cast<const double2*>(a.Bm + r * a.ldb + col);
+        bpre[x][y][0] = v.x;
+        bpre[x][y][1] = v.y;
+      }
+  }
+  for (int q = 0; q < nk; ++q) {
+    if (threadIdx.x == 0 && q + kNNStages - 1 < nk) {
+      const int qq = q + kNNStages - 1;
+      if (qq >= kNNStages) mbar_wait(&empty[qq % kNNStages], static_cast<unsigned>((qq / kNNStages - 1) & 1));
+      produce(qq);
+    }
+    const int st = q % kNNStages;
+    mbar_wait(&full[st], static_cast<unsigned>((q / kNNStages) & 1));
+    const double* sa = stage0 + st * STG;
+    const double* pa = sa + (wm * 32 + g) * SAR2 + t;
+    const double* pc = sa + BM * SAR2 + t * SST + wn * 32 + g;
+    if (code == 16)
+      warp_mma<4, 4, false, 1, 8 * SAR2, SST, 8>(acc, pa, pc);
+    else
+      warp_mma_dispatch<1, 8 * SAR2, SST, 8>(code, acc, pa, pc);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const i64 r = row0 + wm * 32 + x * 8 + g;
+      const int col = tj * BN + wn * 32 + y * 8 + 2 * t;
+      if (FULL) {
+        double2 v = make_double2(a.alpha * acc[x][y][0], a.alpha * acc[x][y][1]);
+        if (BETA) {
+          v.x += a.beta * bpre[BETA ? x : 0][y][0];
+          v.y += a.beta * bpre[BETA ? x : 0][y][1];
+        }
+        *reinterpret_cast<double2*>(a.Out + r * a.ldo + col) = v;
+        continue;
+      }
+      if (r >= a.nrows) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (col + h >= a.m2) continue;
+        double v = a.alpha * acc[x][y][h];
+        if (a.beta != 0.0) v += a.beta * a.Bm[r * a.ldb + col + h];
+        a.Out[r * a.ldo + col + h] = v;
+      }
+    }
+}
+
+template <bool BETA>
+__global__ void __launch_bounds__(NT, BETA ? 2 : 3)
+    gemm_nn_tma_kernel(NNArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC) {
+  if (nn_skipped(a)) return;
+  extern __shared__ __align__(128) unsigned char nsm[];
+  const int tiles_j = static_cast<int>(cdiv(a.m2, BN));
+  const i64 row0 = static_cast<i64>(blockIdx.x / tiles_j) * BM;
+  const int tj = static_cast<int>(blockIdx.x % tiles_j);
+  if (row0 + BM <= a.nrows && (tj + 1) * BN <= a.m2)
+    nn_tma_tile<true, BETA>(a, &tmA, &tmC, row0, tj, nsm);
+  else
+    nn_tma_tile<false, BETA>(a, &tmA, &tmC, row0, tj, nsm);
+}
+
 template <bool BETA>  // the beta*B prefetch needs 64 more registers: 2 CTAs per SM
 __global__ void __launch_bounds__(NT, BETA ? 2 : 3) gemm_nn_kernel(NNArgs a) {
   if (nn_skipped(a)) return;

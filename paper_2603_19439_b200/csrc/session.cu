@@ -214,6 +214,10 @@ class Session {
                                   static_cast<int>(dm::kNNSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kNNTmaSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kNNTmaSmem)));
     d_scal_ = arena_.get<u64>("scalars", 32);
     k = cfg.k;
     n = n0;
@@ -719,8 +723,20 @@ class Session {
     if (m2 <= 32)
       launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
     else
-      launch(beta != 0.0 ? dm::gemm_nn_kernel<true> : dm::gemm_nn_kernel<false>,
-             dim3(static_cast<unsigned>(cdiv(rows, dm::BM) * cdiv(m2, dm::BN))), dim3(dm::NT), dm::kNNSmem, st_, a);
+    {
+      const dim3 grid(static_cast<unsigned>(cdiv(rows, dm::BM) * cdiv(m2, dm::BN)));
+      const bool tma = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 && lda % 2 == 0 &&
+                       ldc % 2 == 0;
+      if (tma) {
+        const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
+        const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
+        launch(beta != 0.0 ? dm::gemm_nn_tma_kernel<true> : dm::gemm_nn_tma_kernel<false>, grid, dim3(dm::NT),
+               dm::kNNTmaSmem, st_, a, ma, mc);
+      } else {
+        launch(beta != 0.0 ? dm::gemm_nn_kernel<true> : dm::gemm_nn_kernel<false>, grid, dim3(dm::NT), dm::kNNSmem,
+               st_, a);
+      }
+    }
     kend();
   }
 
