@@ -1186,7 +1186,8 @@ class Session {
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
     chol(Gm, ldw, w, R, ldw, Ri, ldw, o2, kSuspectTau2, false);
     read_scalars();
-    if (hs_->flags & (kSuspect | kBreakdown)) return mgs2_exact(W, w, against, a, N, G, out);
+    last_ortho_exact_ = (hs_->flags & (kSuspect | kBreakdown)) != 0;
+    if (last_ortho_exact_) return mgs2_exact(W, w, against, a, N, G, out);
     // pass 2 input Q1 = P1 R^-1: into `out` when it is re-projected into W1,
     // else straight into W1
     const bool proj = against && a > 0;
@@ -1204,6 +1205,7 @@ class Session {
     return w;
   }
 
+  bool last_ortho_exact_ = false;  // the last orthonormalize took the column-by-column replica
   static constexpr double kSuspectTau2 = 1e-10;  // residual / original norm below 1e-5
   static constexpr double kRrOrtol = 1e-9;       // eigenvector cluster threshold for the RR solve
 
@@ -1372,11 +1374,20 @@ class Session {
     double* M = arena_.get<double>("Msk", N * ldy);
     const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy});
     if (qm == 0) return 0;
-    // bt_m = d2' (M - X (X'M)): rows of the appended nodes times the projected M
-    double* cm = arena_.get<double>("cm", static_cast<i64>(kk) * ldy);
-    gram(z.p, z.ld, M, ldy, G, kk, qm, false, cm, ldy);
-    double* Mp = arena_.get<double>("Mp", p * ldy);
-    nn(z.p, z.ld, p, kk, cm, ldy, qm, Mp, ldy, -1.0, 1.0, M, ldy);
+    // bt_m = d2' (M - X (X'M)) (trackers.cpp:262-266). On the CholQR2 path
+    // M = (P Y) R^-1 spans a block already projected against X-bar, so
+    // X-bar'M is rounding-level (eps kappa(Y), kappa(Y) < 1e5 there: a
+    // worse-conditioned Y trips the suspect-pivot test); the projection then
+    // changes bt_m by that relative amount only and is skipped. After the
+    // column-by-column replica (near rank loss) it is applied as written.
+    const double* Msrc = M;
+    if (last_ortho_exact_) {
+      double* cm = arena_.get<double>("cm", static_cast<i64>(kk) * ldy);
+      gram(z.p, z.ld, M, ldy, G, kk, qm, false, cm, ldy);
+      double* Mp = arena_.get<double>("Mp", p * ldy);
+      nn(z.p, z.ld, p, kk, cm, ldy, qm, Mp, ldy, -1.0, 1.0, M, ldy);
+      Msrc = Mp;
+    }
     double* btm = arena_.get<double>("btm", pt.S * ldy);
     SpmmArgs sb{};
     sb.rows = pt.S;
@@ -1384,7 +1395,7 @@ class Session {
     sb.rowptr = pt.lrp;
     sb.col = pt.lcol;
     sb.val = pt.val;
-    sb.X = Mp;
+    sb.X = Msrc;
     sb.ldx = ldy;
     sb.m = qm;
     sb.Y = btm;
