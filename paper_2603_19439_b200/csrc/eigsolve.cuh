@@ -38,7 +38,7 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   if (fabs(q) < pivmin) q = -pivmin;
   c += q < 0.0;
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e2[i - 1] / q;
+    q = d[i] - x - e2[i - 1] * __drcp_rn(q);
     if (fabs(q) < pivmin) q = -pivmin;
     c += q < 0.0;
   }
@@ -268,8 +268,8 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
       double t = 0.0, scal = 0.0, beta = alpha;
       if (sigma > 0.0) {
         beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
-        t = (beta - alpha) / beta;
-        scal = 1.0 / (alpha - beta);
+        t = (beta - alpha) * __drcp_rn(beta);  // reciprocals: the column's latency chain
+        scal = __drcp_rn(alpha - beta);
       }
       if (lane == 0) {
         sc[0] = t;
@@ -369,10 +369,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads)
 }
 
 // All eigenvalues of the tridiagonal matrix by bisection on Sturm counts:
-// 8 threads per eigenvalue multisect (9-way split per step) until the bracket
+// a warp per eigenvalue multisects (33-way split per step) until the bracket
 // is below max(2 eps |lambda|, eps ||T||), the absolute accuracy of QR-based
 // solvers; the returned value is the bracket's lower end (count <= j).
-constexpr int kBisG = 8;
+constexpr int kBisG = 32;  // one warp per eigenvalue: a 33-way split per Sturm round
 __global__ void __launch_bounds__(128) bisect_kernel(EigBufs b, int n) {
   extern __shared__ double sh[];
   double* d = sh;
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) 
       const double sub_e = e[i];
       const double nd = d[i + 1] - lambda, nu = i + 2 < n ? e[i + 1] : 0.0;
       if (fabs(cur_d) >= fabs(sub_e)) {
-        const double mlt = cur_d != 0.0 ? sub_e / cur_d : 0.0;
+        const double mlt = cur_d != 0.0 ? sub_e * __drcp_rn(cur_d) : 0.0;
         dl[i] = mlt;
         dd[i] = cur_d;
         du[i] = cur_u;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) 
         cur_d = nd - mlt * cur_u;
         cur_u = nu;
       } else {
-        const double mlt = cur_d / sub_e;
+        const double mlt = cur_d * __drcp_rn(sub_e);
         ipm[i >> 5] |= 1u << (i & 31);
         dl[i] = mlt;
         dd[i] = sub_e;
@@ -513,8 +513,10 @@ __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) 
     du[n - 1] = 0.0;
     du2[n - 1] = 0.0;
     const double eps_piv = DBL_EPSILON * tnorm;
-    for (int i = 0; i < n; ++i)
+    for (int i = 0; i < n; ++i) {  // store 1 / pivot: the three solves multiply
       if (fabs(dd[i]) < eps_piv) dd[i] = dd[i] < 0.0 ? -eps_piv : eps_piv;
+      dd[i] = __drcp_rn(dd[i]);
+    }
     for (int i = 0; i < n; ++i) x[i] = 1.0 + 0.5 * __sinf(1.0f + 0.7f * i + 1.3f * q);
     for (int it = 0; it < 3; ++it) {
       double carry = x[0];
@@ -531,7 +533,7 @@ __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) 
       x[n - 1] = carry;
       double x1 = 0.0, x2 = 0.0;
       for (int i = n - 1; i >= 0; --i) {
-        const double xi = (x[i] - du[i] * x1 - du2[i] * x2) / dd[i];
+        const double xi = (x[i] - du[i] * x1 - du2[i] * x2) * dd[i];
         x[i] = xi;
         x2 = x1;
         x1 = xi;
@@ -556,10 +558,14 @@ inline size_t invit_smem_bytes(int n) { return sizeof(double) * (2 + 5 * kInvitT
 
 // Back-transformation Q y with the reflectors (last to first), warp per vector
 // in registers; the CTA's 4 warps share reflector rows staged through shared
-// memory 16 at a time. Column c of F = the c-th leading eigenvector.
+// memory kBtRows at a time. Rows of V are contiguous in global memory, so a
+// block of reflectors is one contiguous range: it is copied with cp.async
+// (all requests in flight at once) into a double buffer while the previous
+// block is applied; entries at or left of the unit diagonal are masked on use.
+// Column c of F = the c-th leading eigenvector.
 constexpr int kBtRows = 16;
 __global__ void __launch_bounds__(128) backtransform_kernel(EigBufs b, int n, int want, double* F, int ldf) {
-  extern __shared__ double vs[];  // kBtRows x n
+  extern __shared__ double vs[];  // [2][kBtRows x n]
   const int c = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const bool active = c < want;
@@ -577,31 +583,46 @@ __global__ void __launch_bounds__(128) backtransform_kernel(EigBufs b, int n, in
       xr[s] = r < n ? yg[r] : 0.0;
     }
   }
+  auto stage = [&](int top, int buf) {  // rows max(0, top - kBtRows + 1) .. top
+    const int lo = max(0, top - kBtRows + 1);
+    const double* src = b.V + static_cast<i64>(lo) * n;
+    double* dst = vs + buf * kBtRows * n;
+    const int cnt = (top - lo + 1) * n;
+    for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) cp_async8(dst + idx, src + idx);
+    cp_async_commit();
+  };
+  int buf = 0;
+  if (n >= 2) stage(n - 2, 0);
   for (int top = n - 2; top >= 0; top -= kBtRows) {
     const int lo = max(0, top - kBtRows + 1);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (top - lo + 1) * n; idx += blockDim.x) {
-      const int ii = lo + idx / n, r = idx % n;
-      vs[(ii - lo) * n + r] = r == ii + 1 ? 1.0 : (r > ii + 1 ? b.V[static_cast<i64>(ii) * n + r] : 0.0);
+    if (lo > 0) {
+      stage(lo - 1, buf ^ 1);  // next block in flight while this one is applied
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (!active) continue;
-    for (int i = top; i >= lo; --i) {
-      const double ti = b.tau[i];
-      if (ti == 0.0) continue;
-      const double* vrow = vs + (i - lo) * n;
-      double vr[kSlots];
-      double s = 0.0;
+    if (active) {
+      const double* blk = vs + buf * kBtRows * n;
+      for (int i = top; i >= lo; --i) {
+        const double ti = b.tau[i];
+        if (ti == 0.0) continue;
+        const double* vrow = blk + (i - lo) * n;
+        double vr[kSlots];
+        double s = 0.0;
 #pragma unroll
-      for (int sl = 0; sl < kSlots; ++sl) {
-        const int r = lane + 32 * sl;
-        vr[sl] = r < n ? vrow[r] : 0.0;
-        s += vr[sl] * xr[sl];
+        for (int sl = 0; sl < kSlots; ++sl) {
+          const int r = lane + 32 * sl;
+          vr[sl] = r > i + 1 && r < n ? vrow[r] : (r == i + 1 ? 1.0 : 0.0);
+          s += vr[sl] * xr[sl];
+        }
+        s = warp_sum(s) * ti;
+#pragma unroll
+        for (int sl = 0; sl < kSlots; ++sl) xr[sl] -= s * vr[sl];
       }
-      s = warp_sum(s) * ti;
-#pragma unroll
-      for (int sl = 0; sl < kSlots; ++sl) xr[sl] -= s * vr[sl];
     }
+    __syncthreads();  // the buffer is restaged two blocks later
+    buf ^= 1;
   }
   if (!active) return;
 #pragma unroll
@@ -640,6 +661,8 @@ inline void eig_set_attributes() {
                                 232448));
   STG_CUDA(cudaFuncSetAttribute(tridiag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 232448));
+  STG_CUDA(cudaFuncSetAttribute(backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(sizeof(double) * 2 * kBtRows * kEigMaxN)));
   STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(invit_smem_bytes(kEigMaxN))));
 }
@@ -660,8 +683,8 @@ void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int
   L(select_kernel, dim3(1), dim3(256), sizeof(int) * n, b, n, order, want, ortol, w_sorted);
   L(invit_kernel, dim3(static_cast<unsigned>(cdiv(want, kInvitThreads))), dim3(kInvitThreads), invit_smem_bytes(n), b,
     n);
-  L(backtransform_kernel, dim3(static_cast<unsigned>(cdiv(want, 4))), dim3(128), sizeof(double) * kBtRows * n, b, n,
-    want, F, ldf);
+  L(backtransform_kernel, dim3(static_cast<unsigned>(cdiv(want, 4))), dim3(128), sizeof(double) * 2 * kBtRows * n, b,
+    n, want, F, ldf);
 }
 
 }  // namespace stg

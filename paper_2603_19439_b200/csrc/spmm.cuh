@@ -53,7 +53,28 @@ __global__ void __launch_bounds__(256) spmm_kernel(SpmmArgs a) {
       c_l = a.col[base + lane];
       v_l = a.val[base + lane];
     }
-    for (int q = 0; q < cnt; ++q) {
+    // four nonzeros per pass: their row loads are issued together (memory
+    // parallelism for long rows), the sums still run in column order
+    int q = 0;
+    for (; q + 4 <= cnt; q += 4) {
+      double xv[4][T], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = __shfl_sync(0xffffffffu, c_l, q + u);
+        vv[u] = __shfl_sync(0xffffffffu, v_l, q + u);
+        const double* xr = a.X + static_cast<i64>(c) * a.ldx;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          const int cc = lane + 32 * t;
+          xv[u][t] = cc < a.m ? __ldg(xr + cc) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int t = 0; t < T; ++t) acc[t] = __dadd_rn(acc[t], __dmul_rn(vv[u], xv[u][t]));
+    }
+    for (; q < cnt; ++q) {
       const int c = __shfl_sync(0xffffffffu, c_l, q);
       const double v = __shfl_sync(0xffffffffu, v_l, q);
       const double* xr = a.X + static_cast<i64>(c) * a.ldx;
