@@ -192,20 +192,42 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
   const int my_rows = (n - rank + C - 1) / C;
   // load (S + S')/2 and publish column 0 (its squared norm in slot 3, its alpha)
   double sg = 0.0;
-  for (int lr = warp; lr < my_rows; lr += kTriW) {
-    const int r = lr * C + rank;
-    double* Ar = A + static_cast<i64>(lr) * n;
-    for (int c = lane; c < n; c += 32) {
-      const double x = M[static_cast<i64>(r) * ldm + c];
-      const double y = sym_input ? x : M[static_cast<i64>(c) * ldm + r];  // producers that mirror exactly skip it
-      if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
-      const double v = 0.5 * (x + y);
-      Ar[c] = v;
-      if (c == 0) {
-        for (int q = 0; q < C; ++q) tri_peer<C>(colb, q)[r] = v;
-        if (r >= 2) sg += v * v;
-        if (r == 1)
-          for (int q = 0; q < C; ++q) tri_peer<C>(scl, q)[3] = v;
+  if (sym_input) {  // exactly mirrored producers: (S + S')/2 = S, rows copied with every request in flight
+    for (int lr = warp; lr < my_rows; lr += kTriW) {
+      const int r = lr * C + rank;
+      for (int c = lane; c < n; c += 32) cp_async8(A + static_cast<i64>(lr) * n + c, M + static_cast<i64>(r) * ldm + c);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    int bad = 0;
+    for (int lr = warp; lr < my_rows; lr += kTriW)
+      for (int c = lane; c < n; c += 32) bad |= !isfinite(A[static_cast<i64>(lr) * n + c]);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, kNonFinite);
+    for (int lr = tid; lr < my_rows; lr += kTriThreads) {
+      const int r = lr * C + rank;
+      const double v = A[static_cast<i64>(lr) * n];
+      for (int q = 0; q < C; ++q) tri_peer<C>(colb, q)[r] = v;
+      if (r >= 2) sg += v * v;
+      if (r == 1)
+        for (int q = 0; q < C; ++q) tri_peer<C>(scl, q)[3] = v;
+    }
+  } else {
+    for (int lr = warp; lr < my_rows; lr += kTriW) {
+      const int r = lr * C + rank;
+      double* Ar = A + static_cast<i64>(lr) * n;
+      for (int c = lane; c < n; c += 32) {
+        const double x = M[static_cast<i64>(r) * ldm + c];
+        const double y = M[static_cast<i64>(c) * ldm + r];
+        if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
+        const double v = 0.5 * (x + y);
+        Ar[c] = v;
+        if (c == 0) {
+          for (int q = 0; q < C; ++q) tri_peer<C>(colb, q)[r] = v;
+          if (r >= 2) sg += v * v;
+          if (r == 1)
+            for (int q = 0; q < C; ++q) tri_peer<C>(scl, q)[3] = v;
+        }
       }
     }
   }

@@ -750,7 +750,7 @@ class Session {
     kend();
   }
 
-  // Cholesky G = R'R; with Ri also R^-1 (triinv_kernel).
+  // Cholesky G = R'R; with Ri also R^-1 (triinv_kernel on R', written by chol).
   void chol(const double* G, int ldg, int w, double* R, int ldr, double* Ri, int ldi, const double* orig2,
             double tau2, bool psd) {
     if (w > kCholMaxW) throw RuntimeError("chol: block wider than 238 columns");
@@ -764,17 +764,20 @@ class Session {
                                     static_cast<int>(triinv_smem_bytes(kCholMaxW))));
       attr = true;
     }
-    launch(chol_kernel, dim3(1), dim3(kCholThreads), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, orig2, tau2, psd ? 1 : 0,
-           flags_ptr());
+    const int ldt = ld_for(w);
+    double* Rt = Ri ? arena_.get<double>("chol_Rt", static_cast<i64>(w) * ldt) : nullptr;
+    launch(chol_kernel, dim3(1), dim3(kCholThreads), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, Rt, ldt, orig2, tau2,
+           psd ? 1 : 0, flags_ptr());
     kend();
-    if (Ri) triinv(R, ldr, w, Ri, ldi);
+    if (Ri) triinv(Rt, ldt, w, Ri, ldi);
   }
 
-  void triinv(const double* R, int ldr, int w, double* Ri, int ldi) {
+  // R^-1 from R' (row-major, lower triangle)
+  void triinv(const double* Rt, int ldrt, int w, double* Ri, int ldi) {
     if (w > kCholMaxW) throw RuntimeError("triinv: block wider than 238 columns");
     kbegin(kTriinv, static_cast<double>(w) * w * w / 3.0);
     launch(triinv_kernel, dim3(static_cast<unsigned>(cdiv(w, kTriWarps))), dim3(32 * kTriWarps),
-           triinv_smem_bytes(w), st_, R, ldr, w, Ri, ldi);
+           triinv_smem_bytes(w), st_, Rt, ldrt, w, Ri, ldi);
     kend();
   }
 

@@ -151,20 +151,25 @@ __device__ __forceinline__ void chol_trailing(double* sm, int w, int p, int b, i
 }
 
 __global__ void __launch_bounds__(kCholThreads) chol_kernel(const double* G, int ldg, int w, double* R, int ldr,
-                                                            const double* orig2, double tau2, int psd, int* flags) {
+                                                            double* Rt, int ldrt, const double* orig2, double tau2,
+                                                            int psd, int* flags) {
   extern __shared__ double sm[];
   double* invd = sm + static_cast<i64>(w) * (w + 1) / 2;  // [2][kCholNb]: 1 / R(j,j) per panel parity
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5;
-  for (int i = warp; i < w; i += nth >> 5) {  // warp per row, coalesced
+  for (int i = warp; i < w; i += nth >> 5) {  // warp per row, all copies in flight at once
     const double* gi = G + static_cast<i64>(i) * ldg;
     double* si = sm + packed_row(i, w);
     double* ri = R + static_cast<i64>(i) * ldr;
     for (int c = lane; c < w; c += 32) {
-      if (c >= i) si[c] = gi[c];
+      if (c >= i) cp_async8(si + c, gi + c);
       else ri[c] = 0.0;
     }
+    if (Rt)
+      for (int c = lane; c < i; c += 32) Rt[static_cast<i64>(i) * ldrt + c] = 0.0;  // R' is lower triangular
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   int fl = 0;
   if (warp == 0) chol_diag(min(kCholNb, w), sm, invd, w, 0, min(kCholNb, w), lane, orig2, tau2, psd, fl);
@@ -179,7 +184,11 @@ __global__ void __launch_bounds__(kCholThreads) chol_kernel(const double* G, int
     // rows of panel p are final
     for (int e = tid; e < b * (w - p); e += nth) {
       const int t = e / (w - p), c = p + (e - t * (w - p));
-      if (c >= p + t) R[static_cast<i64>(p + t) * ldr + c] = sm[packed_row(p + t, w) + c];
+      if (c >= p + t) {
+        const double v = sm[packed_row(p + t, w) + c];
+        R[static_cast<i64>(p + t) * ldr + c] = v;
+        if (Rt) Rt[static_cast<i64>(c) * ldrt + p + t] = v;
+      }
     }
     __syncthreads();
     // B. warp 0: next diagonal block; the others: rest of the trailing update
@@ -200,8 +209,9 @@ inline size_t chol_smem_bytes(int w) {
   return sizeof(double) * (static_cast<size_t>(w) * (w + 1) / 2 + 2 * kCholNb);
 }
 
-// Inverse of an upper-triangular R (row-major, w <= 256). Each CTA stages R in
-// shared memory as packed columns (column l holds rows 0..l), then each warp
+// Inverse of an upper-triangular R given as R' (row-major lower triangle, as
+// chol_kernel writes it; w <= 256). Each CTA stages R in shared memory as
+// packed columns (column l holds rows 0..l), then each warp
 // back-substitutes one column j of R^-1 in axpy form: once x_l is known,
 // column l of R times x_l is added to the running sums of rows i < l (lane
 // owns rows lane + 32 u), and x_{l-1} = -s_{l-1} / R(l-1,l-1) is broadcast
@@ -228,17 +238,23 @@ __device__ __forceinline__ void triinv_segment(double (&s)[kTriMaxW / 32], doubl
   }
 }
 
-__global__ void __launch_bounds__(32 * kTriWarps) triinv_kernel(const double* R, int ldr, int w, double* Ri, int ldi) {
+__global__ void __launch_bounds__(32 * kTriWarps) triinv_kernel(const double* Rt, int ldrt, int w, double* Ri,
+                                                                 int ldi) {
   extern __shared__ double rc[];
   double* invd = rc + static_cast<i64>(w) * (w + 1) / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int c = warp; c < w; c += kTriWarps) {  // warp per column: conflict-free packed stores
+  // column c of R = row c of R' (rows 0..c), contiguous: copies all in flight
+  for (int c = warp; c < w; c += kTriWarps) {
     double* dst = rc + c * (c + 1) / 2;
-    for (int i = lane; i <= c; i += 32) {
-      const double v = R[static_cast<i64>(i) * ldr + c];
-      dst[i] = v;
-      if (i == c) invd[i] = v != 0.0 ? 1.0 / v : 0.0;
-    }
+    const double* src = Rt + static_cast<i64>(c) * ldrt;
+    for (int i = lane; i <= c; i += 32) cp_async8(dst + i, src + i);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (int i = tid; i < w; i += blockDim.x) {
+    const double v = rc[i * (i + 1) / 2 + i];
+    invd[i] = v != 0.0 ? 1.0 / v : 0.0;
   }
   __syncthreads();
   const int j = blockIdx.x * kTriWarps + warp;
