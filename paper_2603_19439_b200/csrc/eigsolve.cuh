@@ -27,7 +27,7 @@
 
 namespace stg {
 
-constexpr int kEigMaxN = 232;   // 116 rows x 232 columns per CTA of a 2-CTA cluster fit in 227 KB
+constexpr int kEigMaxN = 228;   // 114 rows x 228 columns per CTA of a 2-CTA cluster + scratch fit in 227 KB (D <= 228 at configs 4-5)
 constexpr int kEigMaxWant = 256;
 
 
@@ -91,11 +91,11 @@ constexpr int kTriSlots = (kEigMaxN + 31) / 32;
 
 __host__ __device__ inline int tri_rows(int n, int C) { return (n + C - 1) / C; }
 
-// scratch after the rows: col[2][n], a0[n], p/v/w[3][n], acc[C * gmax][n], (Av)'v pieces
+// scratch after the rows: col[2][n], a0[2][n], p/v/w[3][n], acc[2][C * gmax][n], (Av)'v pieces
 // [2][C * kTriW][4], reflector scalars [2][4]. gmax = warps sharing one
 // 32-column block of the column sums (as many as shared memory allows, <= 4).
 inline size_t tridiag_smem_bytes(int n, int C, int gmax) {
-  return sizeof(double) * (static_cast<size_t>(tri_rows(n, C)) * n + (6 + static_cast<size_t>(C) * gmax) * n +
+  return sizeof(double) * (static_cast<size_t>(tri_rows(n, C)) * n + (7 + 2 * static_cast<size_t>(C) * gmax) * n +
                            2 * static_cast<size_t>(C) * kTriW * 4 + 8);
 }
 inline int tridiag_gmax(int n, int C) {
@@ -180,13 +180,13 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
   const int nloc = tri_rows(n, C);
   double* A = sm;                                   // nloc x n, local row lr <-> row lr C + rank
   double* colb = A + static_cast<i64>(nloc) * n;    // [2][n] column i by parity
-  double* a0 = colb + 2 * n;                        // [n] row r0
-  double* Pv = a0 + n;                              // [n] p = tau A v
+  double* a0b = colb + 2 * n;                       // [2][n] row r0 by parity
+  double* Pv = a0b + 2 * n;                         // [n] p = tau A v
   double* Vv = Pv + n;                              // [n] v
   double* Wv = Vv + n;                              // [n] w = p - tau (p'v) v
-  double* acc = Wv + n;                             // [C * gmax][n] partial column sums
+  double* accb = Wv + n;                            // [2][C * gmax][n] partial column sums by parity
   const int nacc_max = C * gmax;
-  double* pvs = acc + static_cast<i64>(nacc_max) * n;  // [2][C * kTriW][4]: (Av)'v pieces, squared-norm share
+  double* pvs = accb + 2 * static_cast<i64>(nacc_max) * n;  // [2][C * kTriW][4]: (Av)'v pieces, squared-norm share
   double* scl = pvs + 2 * C * kTriW * 4;            // [2] x {tau, scal, beta, alpha}
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int my_rows = (n - rank + C - 1) / C;
@@ -239,6 +239,8 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
   for (int i = 0; i + 1 < n; ++i) {
     const int par = i & 1, npar = par ^ 1, r0 = i + 1;
     const double* col = colb + par * n;
+    double* a0 = a0b + par * n;
+    double* acc = accb + static_cast<i64>(par) * nacc_max * n;
     double* pv = pvs + par * C * kTriW * 4;
     double* sc = scl + par * 4;
     const int lr0 = (r0 - rank + C - 1) / C;  // first local row with r >= r0
@@ -284,7 +286,7 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
         d[1] = s2;
         d[2] = s3;
       }
-    } else if (warp == kTriW - 1) {
+    } else if (C == 1 && warp == kTriW - 1) {
       const double sigma = warp_sum(lane < C * kTriW ? pv[lane * 4 + 3] : 0.0);
       const double alpha = sc[3];
       double t = 0.0, scal = 0.0, beta = alpha;
@@ -311,7 +313,31 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
     tri_sync<C>();
     STG_TRI_MARK(2);
     // U
-    const double t = sc[0], scal = sc[1];
+    double t, scal;
+    if constexpr (C == 1) {
+      t = sc[0];
+      scal = sc[1];
+    } else {  // the cluster meets once per column: every warp derives the reflector here
+      const double sigma = warp_sum(lane < C * kTriW ? pv[lane * 4 + 3] : 0.0);
+      const double alpha = sc[3];
+      double beta = alpha;
+      t = 0.0;
+      scal = 0.0;
+      if (sigma > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
+        t = (beta - alpha) * __drcp_rn(beta);
+        scal = __drcp_rn(alpha - beta);
+      }
+      if (rank == 0) {
+        if (tid == 0) {
+          b.tau[i] = t;
+          b.e[i] = beta;
+          b.e2[i] = beta * beta;
+        }
+        for (int c = r0 + tid; c < n; c += kTriThreads) b.V[static_cast<i64>(i) * n + c] = c == r0 ? 1.0 : col[c] * scal;
+      }
+      if (i % C == rank && tid == 0) b.d[i] = A[static_cast<i64>(i / C) * n + i];
+    }
     if (t != 0.0) {
       double s1 = 0.0, s2 = 0.0, s3 = 0.0;
       if (lane < C * kTriW && (lane % kTriW) < nsw) {
@@ -368,9 +394,14 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
     if (lane == 0)
       for (int q = 0; q < C; ++q) tri_peer<C>(pvs + npar * C * kTriW * 4, q)[(rank * kTriW + warp) * 4 + 3] = sg2;
     STG_TRI_MARK(4);
-    tri_sync<C>();
+    if constexpr (C == 1) {
+      __syncthreads();
+    } else {  // S of the next column reads only this CTA's rows; a local barrier suffices
+      __syncthreads();
+    }
     STG_TRI_MARK(5);
   }
+  if constexpr (C > 1) tri_sync<C>();  // no CTA leaves while a peer may still write into it
   if ((n - 1) % C == rank && tid == 0) {
     b.d[n - 1] = A[static_cast<i64>((n - 1) / C) * n + (n - 1)];
     b.e[n - 1] = 0.0;
