@@ -218,11 +218,75 @@ __device__ __forceinline__ void merge_p_segment(i64 pos, i64 seg_end, int s, int
   }
 }
 
+// Rows of P with at most 31 Delta entries (nearly all): the row's Delta
+// entries live one per lane (lb = insertion position in the old row from
+// merge_classify, found/pruned flags, new value, running size change), so an
+// old entry j's output slot is o + j + shift(#entries with lb + found <= j)
+// with no dependent global loads in the loop; only the entries that land in
+// the current 32-entry window are walked.
+__device__ __forceinline__ void merge_p_segment_small(i64 pos, i64 seg_end, int s, int o, int ds, int dn, int lane,
+                                                      const int* __restrict__ acol, const double* __restrict__ aval,
+                                                      const int* __restrict__ lb, const int* __restrict__ flag,
+                                                      const double* __restrict__ newv,
+                                                      const int* __restrict__ prefix, int* __restrict__ ncol,
+                                                      double* __restrict__ nval) {
+  const int p0 = prefix[ds];
+  int key = 0x7fffffff, lbv = -1, fl = 0, pre = 0;
+  double nv = 0.0;
+  if (lane < dn) {
+    fl = flag[ds + lane];
+    lbv = lb[ds + lane];
+    key = lbv + (fl & 1);
+    nv = newv[ds + lane];
+  }
+  if (lane <= dn) pre = prefix[ds + lane] - p0;
+  // four 32-entry windows per pass, all loads issued before any use (in-order
+  // issue would otherwise leave one load in flight per warp)
+  for (i64 base = pos; base < seg_end; base += 128) {
+    int cv[4];
+    double vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const i64 q = base + 32 * u + lane;
+      cv[u] = q < seg_end ? acol[q] : 0;
+      vv[u] = q < seg_end ? aval[q] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const i64 wb = base + 32 * u;
+      if (wb >= seg_end) break;
+      const i64 q = wb + lane;
+      const bool valid = q < seg_end;
+      const int j0 = static_cast<int>(wb - s), j = j0 + lane;
+      int cnt = __popc(__ballot_sync(0xffffffffu, lane < dn && key < j0));
+      unsigned inr = __ballot_sync(0xffffffffu, lane < dn && ((key >= j0 && key <= j0 + 31) ||
+                                                                ((fl & 1) && lbv >= j0 && lbv <= j0 + 31)));
+      int hit = -1;
+      while (inr) {
+        const int k = __ffs(inr) - 1;
+        inr &= inr - 1;
+        const int kk = __shfl_sync(0xffffffffu, key, k);
+        const int lk = __shfl_sync(0xffffffffu, lbv, k);
+        const int fk = __shfl_sync(0xffffffffu, fl, k);
+        if (kk >= j0 && kk <= j) ++cnt;
+        if ((fk & 1) && lk == j) hit = k;
+      }
+      const int shift = __shfl_sync(0xffffffffu, pre, cnt);
+      const double hv = __shfl_sync(0xffffffffu, nv, hit < 0 ? 0 : hit);
+      const int hf = __shfl_sync(0xffffffffu, fl, hit < 0 ? 0 : hit);
+      if (!valid || (hit >= 0 && (hf & 2))) continue;  // pruned: cancelled to exactly zero
+      const int out = o + j + shift;
+      ncol[out] = cv[u];
+      nval[out] = hit >= 0 ? hv : vv[u];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) merge_chunks_kernel(const int* __restrict__ arp, const int* __restrict__ acol,
                                                            const double* __restrict__ aval, i64 n_old,
                                                            const int* __restrict__ mark, int stamp,
                                                            const int* __restrict__ drp, const int* __restrict__ dcol,
-                                                           const int* __restrict__ flag,
+                                                           const int* __restrict__ lb, const int* __restrict__ flag,
                                                            const double* __restrict__ newv,
                                                            const int* __restrict__ prefix,
                                                            const int* __restrict__ nrp, int* __restrict__ ncol,
@@ -248,23 +312,35 @@ __global__ void __launch_bounds__(256) merge_chunks_kernel(const int* __restrict
     const int o = in ? nrp[rr] : 0;
     const bool pm = in && mark[rr] == stamp;
     const i64 gend = min(static_cast<i64>(__shfl_sync(0xffffffffu, re, 31)), e1);
-    // untouched rows: entry-parallel shifted copy
-    for (i64 base = pos; base < gend; base += 32) {
-      const i64 q = base + lane;
-      int idx = 0;  // last lane whose row starts at or before q
+    // untouched rows: entry-parallel shifted copy, four windows per pass with
+    // every load issued first
+    for (i64 base = pos; base < gend; base += 128) {
+      int cv[4];
+      double vv[4];
 #pragma unroll
-      for (int st = 16; st > 0; st >>= 1) {
-        const int cand = idx + st;
-        const int rsc = __shfl_sync(0xffffffffu, rs, cand);
-        if (rsc <= q) idx = cand;
+      for (int u = 0; u < 4; ++u) {
+        const i64 q = base + 32 * u + lane;
+        cv[u] = q < gend ? acol[q] : 0;
+        vv[u] = q < gend ? aval[q] : 0.0;
       }
-      const int rs_i = __shfl_sync(0xffffffffu, rs, idx);
-      const int o_i = __shfl_sync(0xffffffffu, o, idx);
-      const bool p_i = __shfl_sync(0xffffffffu, pm ? 1 : 0, idx);
-      if (q < gend && !p_i) {
-        const i64 dst = o_i + (q - rs_i);
-        ncol[dst] = acol[q];
-        nval[dst] = aval[q];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const i64 q = base + 32 * u + lane;
+        int idx = 0;  // last lane whose row starts at or before q
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+          const int cand = idx + st;
+          const int rsc = __shfl_sync(0xffffffffu, rs, cand);
+          if (rsc <= q) idx = cand;
+        }
+        const int rs_i = __shfl_sync(0xffffffffu, rs, idx);
+        const int o_i = __shfl_sync(0xffffffffu, o, idx);
+        const bool p_i = __shfl_sync(0xffffffffu, pm ? 1 : 0, idx);
+        if (q < gend && !p_i) {
+          const i64 dst = o_i + (q - rs_i);
+          ncol[dst] = cv[u];
+          nval[dst] = vv[u];
+        }
       }
     }
     // rows of P overlapping [pos, gend)
@@ -277,8 +353,12 @@ __global__ void __launch_bounds__(256) merge_chunks_kernel(const int* __restrict
       const int o_l = __shfl_sync(0xffffffffu, o, l);
       const i64 row = r + l;
       const int ds = drp[row], dn = drp[row + 1] - ds;
-      merge_p_segment(max(pos, static_cast<i64>(s_l)), min(static_cast<i64>(e_l), gend), s_l, o_l, ds, dn, lane,
-                      acol, aval, dcol, flag, newv, prefix, ncol, nval);
+      if (dn < 32)
+        merge_p_segment_small(max(pos, static_cast<i64>(s_l)), min(static_cast<i64>(e_l), gend), s_l, o_l, ds, dn,
+                              lane, acol, aval, lb, flag, newv, prefix, ncol, nval);
+      else
+        merge_p_segment(max(pos, static_cast<i64>(s_l)), min(static_cast<i64>(e_l), gend), s_l, o_l, ds, dn, lane,
+                        acol, aval, dcol, flag, newv, prefix, ncol, nval);
     }
     // next group starts at the row holding gend
     if (gend >= e1) break;

@@ -1023,7 +1023,8 @@ class Session {
       launch(merge_chunks_kernel, dim3(blocks(cdiv(a.nnz, kMergeChunk), 8)), dim3(256), 0, st_,
              static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
              static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
-             static_cast<const int*>(dcol), static_cast<const int*>(mflag), static_cast<const double*>(newv),
+             static_cast<const int*>(dcol), static_cast<const int*>(lb), static_cast<const int*>(mflag),
+             static_cast<const double*>(newv),
              static_cast<const int*>(prefix), static_cast<const int*>(an.rp), an.col, an.val);
     if (n2 > 0)
       launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, st_, n2, static_cast<const int*>(drow),
