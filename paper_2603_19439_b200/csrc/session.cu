@@ -127,6 +127,7 @@ struct Scalars {  // pinned host mirror of device scalars read at sync points
   int flags;
   int info;
   double alpha;
+  double sk_lam[kEigMaxN];  // sketch eigenvalues, copied asynchronously (pageable memory would block the host)
 };
 
 static const char* edit_message(int code) {
@@ -194,6 +195,13 @@ class Session {
     STG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
     STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
+    {  // high priority: the eigensolve's CTAs take SMs ahead of the wide kernels it overlaps
+      int lo = 0, hi = 0;
+      STG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      STG_CUDA(cudaStreamCreateWithPriority(&st_eig_, cudaStreamNonBlocking, hi));
+    }
+    STG_CUDA(cudaEventCreateWithFlags(&ev_gb_, cudaEventDisableTiming));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_eig_, cudaEventDisableTiming));
     for (auto& e : tev_) STG_CUDA(cudaEventCreate(&e));
     if (cusolverDnCreate(&solver_) != CUSOLVER_STATUS_SUCCESS) throw CudaError("cusolverDnCreate failed");
     cusolverDnSetStream(solver_, st_);
@@ -259,6 +267,10 @@ class Session {
     for (auto& e : tev_) cudaEventDestroy(e);
     cudaEventDestroy(ev_rng_);
     cudaStreamDestroy(st_rng_);
+    cudaStreamSynchronize(st_eig_);
+    cudaEventDestroy(ev_gb_);
+    cudaEventDestroy(ev_eig_);
+    cudaStreamDestroy(st_eig_);
     cudaStreamDestroy(st_);
   }
 
@@ -472,6 +484,8 @@ class Session {
   Pinned pin_;
   cudaStream_t st_ = nullptr, st_rng_ = nullptr;
   cudaEvent_t ev_rng_ = nullptr;
+  cudaStream_t st_eig_ = nullptr;  // the sketch's eigensolve (few SMs) runs beside the basis work
+  cudaEvent_t ev_gb_ = nullptr, ev_eig_ = nullptr;
   cudaEvent_t tev_[8];
   int tev_n_ = 0;
   cusolverDnHandle_t solver_ = nullptr;
@@ -539,8 +553,12 @@ class Session {
       kstats[p.cls].ms += ms;
       kstats[p.cls].work += p.work;
       kstats[p.cls].launches += 1;
-      if (klog_) fprintf(stderr, "klog cls=%d %-40s %9.1f us  work=%.3g  rate=%.3g/s\n", p.cls, p.tag, 1e3 * ms,
-                         p.work, ms > 0 ? p.work / (ms * 1e-3) : 0.0);
+      if (klog_) {
+        float t0 = 0;  // start offset from the step's first timed launch (timeline across streams)
+        cudaEventElapsedTime(&t0, pend_.front().a, p.a);
+        fprintf(stderr, "klog cls=%d %-40s %9.1f us  @%8.1f us  work=%.3g  rate=%.3g/s\n", p.cls, p.tag, 1e3 * ms,
+                1e3 * t0, p.work, ms > 0 ? p.work / (ms * 1e-3) : 0.0);
+      }
     }
     pend_.clear();
     open_.clear();
@@ -559,6 +577,7 @@ class Session {
   int ldx() const { return static_cast<int>(k % 2 ? k + 1 : k); }
   int* flags_ptr() { return reinterpret_cast<int*>(d_scal_ + 3); }
   int* info_ptr() { return reinterpret_cast<int*>(d_scal_ + 4); }
+  int* side_flags_ptr() { return reinterpret_cast<int*>(d_scal_ + 5); }
 
   template <typename K, typename... Args>
   void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
@@ -808,7 +827,7 @@ class Session {
   // On-device eigensolver (one CTA) for order <= kEigMaxN: all eigenvalues in
   // spectral order (w_sorted) and the leading `want` eigenvectors (F, row-major).
   bool eig_fast(const double* M, int ldm, int D, int order, int want, double* w_sorted, double* F, int ldf,
-                double ortol = 1e-3) {
+                double ortol = 1e-3, cudaStream_t s = nullptr, int* flagsp = nullptr) {
     // cuSOLVER syevd on request (ST_FLAG_CUSOLVER_EIG) or above the one-CTA
     // tridiagonalization's shared-memory limit
     if (cfg.flags & ST_FLAG_CUSOLVER_EIG) return false;
@@ -822,12 +841,13 @@ class Session {
     double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(D, wv)));
     int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(D, wv)));
     if (klog_) snprintf(ktag_, sizeof(ktag_), "device syev D=%d want=%d", D, want);
-    kbegin(kEig, 4.0 * D * D * D / 3.0);
-    STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
-    syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, st_, args...); },
+    cudaStream_t es = s ? s : st_;
+    kbegin(kEig, 4.0 * D * D * D / 3.0, es);
+    if (!s) STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
+    syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, es, args...); },
                 M, ldm, D, /*sym_input: exactly mirrored Grams / RR matrix*/ 1, order, wv, ortol, w_sorted, F, ldf,
-                dbuf, ibuf, flags_ptr());
-    kend();
+                dbuf, ibuf, flagsp ? flagsp : flags_ptr());
+    kend(es);
     return true;
   }
 
@@ -1342,7 +1362,20 @@ class Session {
           w += static_cast<int>(S);
         }
       } else {
-        w += rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc});
+        // The candidates are orthonormalized in two blocks, column order kept
+        // (ortho.hpp:26-37 walks them in order): (I - XX') Delta X first, while
+        // the sketch's eigensolve runs beside it, then the RSVD columns against
+        // [X-bar, that block].
+        int q1 = 0;
+        const int wt = rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc}, [&] {
+          q1 = orthonormalize(Blk{cand, ldc}, kk, &z, kk, N, G, Blk{Z + kk, ldz});
+        });
+        int q2 = 0;
+        if (wt > 0) {
+          const Blk against{Z, ldz};
+          q2 = orthonormalize(Blk{cand + kk, ldc}, wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz});
+        }
+        return Basis{z, kk + q1 + q2};
       }
     }
     // ---- extra = orthonormalize(candidates, X-bar) written next to X-bar
@@ -1351,7 +1384,10 @@ class Session {
   }
 
   // rsvd_basis (rsvd.hpp:34-66) with the closures of trackers.cpp:256-267.
-  int rsvd_trailing(const Pert& pt, Blk z, int q, const double* omega, int ldo, Blk out) {
+  // `during_eig` enqueues independent work on the main stream while the
+  // sketch's eigensolve (one or two SMs) runs on st_eig_.
+  template <class F>
+  int rsvd_trailing(const Pert& pt, Blk z, int q, const double* omega, int ldo, Blk out, F&& during_eig) {
     const i64 p = pt.p, N = p + 2 * k, G = p + k;
     const int kk = static_cast<int>(k);
     const int ldy = ld_for(q);
@@ -1377,7 +1413,10 @@ class Session {
     // M = orthonormalize(Y)
     double* M = arena_.get<double>("Msk", N * ldy);
     const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy});
-    if (qm == 0) return 0;
+    if (qm == 0) {
+      during_eig();
+      return 0;
+    }
     // bt_m = d2' (M - X (X'M)) (trackers.cpp:262-266). On the CholQR2 path
     // M = (P Y) R^-1 spans a block already projected against X-bar, so
     // X-bar'M is rounding-level (eps kappa(Y), kappa(Y) < 1e5 there: a
@@ -1415,11 +1454,19 @@ class Session {
     std::vector<double> lam(static_cast<size_t>(qm));
     // only span(U_keep) matters here (R is re-orthonormalized with the basis),
     // so clusters are re-orthogonalized only when nearly degenerate
-    if (eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10)) {
-      STG_CUDA(cudaMemcpyAsync(lam.data(), lamd, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
-      read_scalars();
+    STG_CUDA(cudaEventRecord(ev_gb_, st_));
+    STG_CUDA(cudaStreamWaitEvent(st_eig_, ev_gb_, 0));
+    if (eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10, st_eig_, side_flags_ptr())) {
+      STG_CUDA(cudaMemcpyAsync(hs_->sk_lam, lamd, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_eig_));
+      STG_CUDA(cudaEventRecord(ev_eig_, st_eig_));
+      during_eig();
+      STG_CUDA(cudaStreamWaitEvent(st_, ev_eig_, 0));
+      STG_CUDA(cudaStreamSynchronize(st_eig_));
+      std::copy(hs_->sk_lam, hs_->sk_lam + qm, lam.begin());
+      hs_->info = 0;
       std::reverse(lam.begin(), lam.end());  // ascending like the cuSOLVER path
     } else {
+      during_eig();
       double *w = nullptr, *V = nullptr;
       eig(gb, ldy, qm, &w, &V, "sk");
       STG_CUDA(cudaMemcpyAsync(lam.data(), w, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
