@@ -771,7 +771,7 @@ class Session {
 
   // Cholesky G = R'R; with Ri also R^-1 (triinv_kernel on R', written by chol).
   void chol(const double* G, int ldg, int w, double* R, int ldr, double* Ri, int ldi, const double* orig2,
-            double tau2, bool psd) {
+            double tau2, bool psd, const int* gate = nullptr) {
     if (w > kCholMaxW) throw RuntimeError("chol: block wider than 238 columns");
     if (klog_) snprintf(ktag_, sizeof(ktag_), "chol w=%d", w);
     kbegin(kChol, static_cast<double>(w) * w * w / 3.0);
@@ -786,17 +786,26 @@ class Session {
     const int ldt = ld_for(w);
     double* Rt = Ri ? arena_.get<double>("chol_Rt", static_cast<i64>(w) * ldt) : nullptr;
     launch(chol_kernel, dim3(1), dim3(kCholThreads), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, Rt, ldt, orig2, tau2,
-           psd ? 1 : 0, flags_ptr());
+           psd ? 1 : 0, flags_ptr(), static_cast<const int*>(gate));
     kend();
-    if (Ri) triinv(Rt, ldt, w, Ri, ldi);
+    if (Ri) triinv(Rt, ldt, w, Ri, ldi, gate);
+  }
+
+  // R^-1 of a Gram that is the identity to rounding (second CholQR pass): the
+  // first-order factor when max|G - I| <= kNearIdTol, else the Cholesky path
+  // (decided on the device: the gated kernels exit at once when not needed).
+  void chol_inverse_near_identity(const double* G, int ldg, int w, double* R, int ldr, double* Ri, int ldi) {
+    int* gate = reinterpret_cast<int*>(d_scal_ + 6);
+    launch(near_identity_inverse_kernel, dim3(1), dim3(1024), 0, st_, G, ldg, w, Ri, ldi, gate);
+    chol(G, ldg, w, R, ldr, Ri, ldi, nullptr, 0.0, false, gate);
   }
 
   // R^-1 from R' (row-major, lower triangle)
-  void triinv(const double* Rt, int ldrt, int w, double* Ri, int ldi) {
+  void triinv(const double* Rt, int ldrt, int w, double* Ri, int ldi, const int* gate = nullptr) {
     if (w > kCholMaxW) throw RuntimeError("triinv: block wider than 238 columns");
     kbegin(kTriinv, static_cast<double>(w) * w * w / 3.0);
     launch(triinv_kernel, dim3(static_cast<unsigned>(cdiv(w, kTriWarps))), dim3(32 * kTriWarps),
-           triinv_smem_bytes(w), st_, Rt, ldrt, w, Ri, ldi);
+           triinv_smem_bytes(w), st_, Rt, ldrt, w, Ri, ldi, gate);
     kend();
   }
 
@@ -1224,7 +1233,7 @@ class Session {
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, out.p, out.ld);
     }
     gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
-    chol(Gm, ldw, w, R, ldw, Ri, ldw, nullptr, 0.0, false);
+    chol_inverse_near_identity(Gm, ldw, w, R, ldw, Ri, ldw);
     nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
     return w;
   }
@@ -1241,7 +1250,7 @@ class Session {
     double* Ri = arena_.get<double>("os_Ri", static_cast<i64>(kk) * ldf);
     double* F2 = arena_.get<double>("os_F", static_cast<i64>(D) * ldf);
     gram(F, ldf, F, ldf, D, kk, kk, true, G, ldf);
-    chol(G, ldf, kk, R, ldf, Ri, ldf, nullptr, 0.0, /*psd*/ true);
+    chol_inverse_near_identity(G, ldf, kk, R, ldf, Ri, ldf);
     nn(F, ldf, D, kk, Ri, ldf, kk, F2, ldf, 1.0, 0.0, nullptr, 0, /*tri*/ true);
     return F2;
   }

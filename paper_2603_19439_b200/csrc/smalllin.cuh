@@ -152,7 +152,8 @@ __device__ __forceinline__ void chol_trailing(double* sm, int w, int p, int b, i
 
 __global__ void __launch_bounds__(kCholThreads) chol_kernel(const double* G, int ldg, int w, double* R, int ldr,
                                                             double* Rt, int ldrt, const double* orig2, double tau2,
-                                                            int psd, int* flags) {
+                                                            int psd, int* flags, const int* gate) {
+  if (gate && *gate == 0) return;  // near_identity_inverse_kernel already produced R^-1
   extern __shared__ double sm[];
   double* invd = sm + static_cast<i64>(w) * (w + 1) / 2;  // [2][kCholNb]: 1 / R(j,j) per panel parity
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -239,7 +240,8 @@ __device__ __forceinline__ void triinv_segment(double (&s)[kTriMaxW / 32], doubl
 }
 
 __global__ void __launch_bounds__(32 * kTriWarps) triinv_kernel(const double* Rt, int ldrt, int w, double* Ri,
-                                                                 int ldi) {
+                                                                 int ldi, const int* gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ double rc[];
   double* invd = rc + static_cast<i64>(w) * (w + 1) / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -283,6 +285,35 @@ __global__ void __launch_bounds__(32 * kTriWarps) triinv_kernel(const double* Rt
 }
 
 inline size_t triinv_smem_bytes(int w) { return sizeof(double) * (static_cast<size_t>(w) * (w + 1) / 2 + w); }
+
+// Second CholQR pass: G = Q1'Q1 = I + E with E at rounding level. Then
+// R = I + split(E) + O(|E|^2) (split: strict upper part plus half the
+// diagonal) and R^-1 = I - split(E) + O(|E|^2), and Q1 R^-1 is orthonormal to
+// O(|E|^2 + eps): with max|E| <= kNearIdTol that is the same factor as the
+// Cholesky one to rounding, without the w sequential pivots. One CTA writes
+// that R^-1 and sets *gate = 1 (exact Cholesky still needed) when max|E| is
+// larger; chol_kernel / triinv_kernel run only then.
+constexpr double kNearIdTol = 1e-9;
+__global__ void __launch_bounds__(1024) near_identity_inverse_kernel(const double* G, int ldg, int w, double* Ri,
+                                                                     int ldi, int* gate) {
+  __shared__ int big;
+  if (threadIdx.x == 0) big = 0;
+  __syncthreads();
+  int local = 0;
+  for (int i = threadIdx.x >> 5; i < w; i += blockDim.x >> 5) {
+    const double* gi = G + static_cast<i64>(i) * ldg;
+    double* ri = Ri + static_cast<i64>(i) * ldi;
+    for (int c = threadIdx.x & 31; c < w; c += 32) {
+      const double g = gi[c];
+      const double e = c == i ? g - 1.0 : g;
+      if (!(fabs(e) <= kNearIdTol)) local = 1;
+      ri[c] = c < i ? 0.0 : (c == i ? 1.0 - 0.5 * e : -e);
+    }
+  }
+  if (local) big = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) *gate = big;
+}
 
 // spectral_sort (types.hpp:26-40): rank of element i = number of elements that
 // precede it under (primary key, algebraic value desc, index asc).
