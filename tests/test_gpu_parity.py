@@ -194,3 +194,31 @@ def test_rsvd_path_rmat_parity():
         gpu.step(upd)
         orc.step(upd)
         check_state(gpu, orc, tag=f"rmat14 step {t}")
+
+
+@pytest.mark.gpu
+def test_config3_shape_parity_rmat17():
+    """Config 3's shapes at a scale the oracle finishes in seconds: R-MAT s17,
+    k = 32, L = P = 100 (q = 200 sketch, D = 164 Ritz basis), 1% new nodes with
+    10 preferential-attachment edges and 0.5% deletions per step, both paths
+    starting from the same leading eigenpairs (block Krylov, as bench.py).
+    Exercises the two-block candidate orthonormalization, the first-order
+    second CholQR pass, the skipped re-projection of the sketch basis, the
+    2-CTA tridiagonalization (q = 200) and the block re-orthonormalization of
+    the Ritz vectors at realistic sizes."""
+    from paper_2603_19439_b200 import TrackerSession, init_eig, streams
+
+    s = streams.config3(scale=17, steps=3)
+    rp, col, val = s.csr0()
+    k = 32
+    vals, vecs = init_eig.leading_eigenpairs(rp, col, val, k, "abs_desc", device="cuda:0")
+    n = len(rp) - 1
+    a = po.Csr(n, np.asarray(rp, np.int32), np.asarray(col, np.int32), np.asarray(val, np.float64))
+    orc = po.Session(a, kind="grest-rsvd", k=k, seed=5, values=vals, vectors=vecs)
+    gpu = TrackerSession(a.rowptr, a.col, a.val, vals, vecs, kind="grest-rsvd", k=k, seed=5)
+    for t, upd in enumerate(s.updates):
+        assert upd.n_new > 200  # the sketch is q = 200 wide
+        gpu.step(upd)
+        orc.step(upd)
+        ve, sa = check_state(gpu, orc, tag=f"cfg3-s17 step {t}")
+        print(f"cfg3-s17 step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
