@@ -713,6 +713,102 @@ __global__ void __launch_bounds__(NT, BETA ? 2 : 3) gemm_nn_kernel(NNArgs a) {
     nn_tile<false, BETA>(a, row0, tj, dsm);
 }
 
+// Narrow streaming NN (m1 <= 32, m2 <= 32: projections against the k-wide
+// block, the final rotation X <- X A_new of all n rows). Persistent CTAs walk
+// 128-row tiles; each tile of A arrives as one TMA box {36, 128} through a
+// 4-deep mbarrier ring, C (<= 32 x 32) sits in shared memory once. Safe in
+// place (Out == A): a tile is fully staged before its rows are written.
+constexpr int kStreamRows = 128, kStreamStages = 4, kStreamPitch = 36;
+constexpr size_t kStreamSmem =
+    128 + sizeof(double) * (static_cast<size_t>(kStreamStages) * kStreamRows * kStreamPitch + 32 * SS);
+
+__global__ void __launch_bounds__(NT, 2)
+    gemm_nn_stream_kernel(NNArgs a, const __grid_constant__ CUtensorMap tmA, int ntiles) {
+  if (nn_skipped(a)) return;
+  extern __shared__ __align__(128) unsigned char ssm[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ssm);
+  unsigned long long* empty = full + kStreamStages;
+  double* stage0 = reinterpret_cast<double*>(ssm + 128);
+  double* sC = stage0 + kStreamStages * kStreamRows * kStreamPitch;  // [32][SS]
+  constexpr int STG = kStreamRows * kStreamPitch;
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+    const int r = idx >> 5, c = idx & 31;
+    sC[r * SS + c] = (r < a.m1 && c < a.m2) ? a.C[static_cast<i64>(r) * a.ldc + c] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStreamStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int G = gridDim.x, b = blockIdx.x;
+  const int my = b < ntiles ? (ntiles - 1 - b) / G + 1 : 0;  // tiles b, b + G, ...
+  auto produce = [&](int q) {
+    const int st = q % kStreamStages;
+    if (q >= kStreamStages) mbar_wait(&empty[st], static_cast<unsigned>((q / kStreamStages - 1) & 1));
+    mbar_arrive_expect_tx(&full[st], kStageBytes);
+    tma_load_2d(stage0 + st * STG, &tmA, 0, (b + q * G) * kStreamRows, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(my, kStreamStages - 1); ++q) produce(q);
+  const int nxw = frags_left(a.m2, 0);  // live 8-column fragments
+  for (int q = 0; q < my; ++q) {
+    if (threadIdx.x == 0 && q + kStreamStages - 1 < my) produce(q + kStreamStages - 1);
+    const int st = q % kStreamStages;
+    mbar_wait(&full[st], static_cast<unsigned>((q / kStreamStages) & 1));
+    const double* sa = stage0 + st * STG;
+    double acc[4][4][2];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    const double* pa = sa + (warp * 32 + g) * kStreamPitch + t;
+    const double* pc = sC + t * SS + g;
+#pragma unroll
+    for (int kk = 0; kk < 32; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = pa[x * 8 * kStreamPitch + kk];
+        fb[x] = pc[kk * SS + x * 8];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (y < nxw) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // A is in registers' products now; the slot may refill
+    const i64 row0 = static_cast<i64>(b + q * G) * kStreamRows + warp * 32;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const i64 r = row0 + x * 8 + g;
+      if (r >= a.nrows) continue;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int col = y * 8 + 2 * t;
+        if (col >= a.m2) continue;
+        double v0 = a.alpha * acc[x][y][0], v1 = a.alpha * acc[x][y][1];
+        if (a.beta != 0.0) {
+          v0 += a.beta * a.Bm[r * a.ldb + col];
+          if (col + 1 < a.m2) v1 += a.beta * a.Bm[r * a.ldb + col + 1];
+        }
+        if (col + 1 < a.m2) {
+          *reinterpret_cast<double2*>(a.Out + r * a.ldo + col) = make_double2(v0, v1);
+        } else {
+          a.Out[r * a.ldo + col] = v0;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT) gemm_nn_small_kernel(NNArgs a) {
   if (nn_skipped(a)) return;
   __shared__ __align__(16) double sA[2][NBM][NSAR];

@@ -222,6 +222,8 @@ class Session {
                                   static_cast<int>(dm::kNNSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::kStreamSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNTmaSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -740,7 +742,19 @@ class Session {
     if (klog_) snprintf(ktag_, sizeof(ktag_), "nn %lldx%dx%d%s", rows, m1, m2, tri ? " tri" : "");
     kbegin(kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
     if (m2 <= 32)
-      launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
+    {
+      const bool stream = m1 <= 32 && beta == 0.0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && lda % 2 == 0 &&
+                          (reinterpret_cast<uintptr_t>(Out) & 15) == 0 && ldo % 2 == 0;
+      if (stream) {
+        const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::kStreamPitch, dm::kStreamRows);
+        const int ntiles = static_cast<int>(cdiv(rows, dm::kStreamRows));
+        const int G = std::min(ntiles, 148 * 2);
+        launch(dm::gemm_nn_stream_kernel, dim3(static_cast<unsigned>(G)), dim3(dm::NT), dm::kStreamSmem, st_, a, ma,
+               ntiles);
+      } else {
+        launch(dm::gemm_nn_small_kernel, dim3(static_cast<unsigned>(cdiv(rows, dm::NBM))), dim3(dm::NT), 0, st_, a);
+      }
+    }
     else
     {
       const dim3 grid(static_cast<unsigned>(cdiv(rows, dm::BM) * cdiv(m2, dm::BN)));
