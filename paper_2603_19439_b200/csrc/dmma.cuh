@@ -809,6 +809,96 @@ __global__ void __launch_bounds__(NT, 2)
   }
 }
 
+// Narrow streaming Gram (m1, m2 <= 32): persistent CTAs walk 64-row tiles
+// of A (and B unless A == B) through a 4-deep TMA ring; the four warps take
+// 16 rows of each tile, so each warp keeps one 32 x 32 accumulator for the
+// whole CTA; the warps' sums are combined in fixed order into one partial per
+// CTA, reduced by gram_reduce_kernel (one split per CTA).
+constexpr int kGsRows = 64;  // rows per tile (16 per warp)
+constexpr size_t gram_stream_smem(bool same) {
+  return 128 + sizeof(double) * ((same ? 1 : 2) * static_cast<size_t>(kStreamStages) * kGsRows * kStreamPitch);
+}
+
+__global__ void __launch_bounds__(NT, 3)
+    gram_stream_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       int same, int ntiles) {
+  extern __shared__ __align__(128) unsigned char gsm[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(gsm);
+  unsigned long long* empty = full + kStreamStages;
+  double* stage0 = reinterpret_cast<double*>(gsm + 128);
+  constexpr int STG = kGsRows * kStreamPitch;  // per operand
+  const int ops = same ? 1 : 2;
+  const unsigned stage_bytes = static_cast<unsigned>(sizeof(double) * STG * ops);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStreamStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int G = gridDim.x, b = blockIdx.x;
+  const int my = b < ntiles ? (ntiles - 1 - b) / G + 1 : 0;
+  auto produce = [&](int q) {
+    const int st = q % kStreamStages;
+    if (q >= kStreamStages) mbar_wait(&empty[st], static_cast<unsigned>((q / kStreamStages - 1) & 1));
+    double* sa = stage0 + st * ops * STG;
+    mbar_arrive_expect_tx(&full[st], stage_bytes);
+    const int row0 = (b + q * G) * kGsRows;
+    tma_load_2d(sa, &tmA, 0, row0, &full[st]);
+    if (!same) tma_load_2d(sa + STG, &tmB, 0, row0, &full[st]);
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < min(my, kStreamStages - 1); ++q) produce(q);
+  const int nx = frags_left(a.m1, 0), ny = frags_left(a.m2, 0);
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  for (int q = 0; q < my; ++q) {
+    if (threadIdx.x == 0 && q + kStreamStages - 1 < my) produce(q + kStreamStages - 1);
+    const int st = q % kStreamStages;
+    mbar_wait(&full[st], static_cast<unsigned>((q / kStreamStages) & 1));
+    const double* sa = stage0 + st * ops * STG + warp * 16 * kStreamPitch;  // this warp's 16 rows
+    const double* sb = same ? sa : sa + STG;
+    const double* pa = sa + t * kStreamPitch + g;
+    const double* pb = sb + t * kStreamPitch + g;
+#pragma unroll
+    for (int kk = 0; kk < 16; kk += 4) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        fa[x] = pa[kk * kStreamPitch + x * 8];
+        fb[x] = pb[kk * kStreamPitch + x * 8];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          if (x < nx && y < ny && (!a.sym || x <= y)) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  // combine the four warps (fixed order) through the (drained) stage buffers
+  __syncthreads();
+  double* red = stage0;  // 4 x 32 x 32 (fits: >= 4 stages x 64 x 36 doubles)
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = x * 8 + g, j = y * 8 + 2 * t;
+      red[warp * 1024 + i * 32 + j] = acc[x][y][0];
+      red[warp * 1024 + i * 32 + j + 1] = acc[x][y][1];
+    }
+  __syncthreads();
+  double* out = a.partial + static_cast<i64>(b) * 1024;
+  for (int e = threadIdx.x; e < 1024; e += NT) out[e] = ((red[e] + red[1024 + e]) + red[2048 + e]) + red[3072 + e];
+}
+
 __global__ void __launch_bounds__(NT) gemm_nn_small_kernel(NNArgs a) {
   if (nn_skipped(a)) return;
   __shared__ __align__(16) double sA[2][NBM][NSAR];

@@ -222,6 +222,8 @@ class Session {
                                   static_cast<int>(dm::kNNSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_stream_smem(false))));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kStreamSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -692,6 +694,20 @@ class Session {
     const dim3 grid(ntiles, static_cast<unsigned>(splits));
     const bool bulk = !mask && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
                       lda % 2 == 0 && ldb % 2 == 0;
+    if (narrow && bulk) {
+      const bool same = A == B && lda == ldb;
+      const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::kStreamPitch, dm::kGsRows);
+      const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, dm::kStreamPitch, dm::kGsRows);
+      const int ntl = static_cast<int>(cdiv(std::max<i64>(rows, 1), dm::kGsRows));
+      const int G = std::min(ntl, 148 * (same ? 3 : 1));
+      a.partial = arena_.get<double>("gram_partial", static_cast<i64>(G) * 1024);
+      launch(dm::gram_stream_kernel, dim3(static_cast<unsigned>(G)), dim3(dm::NT), dm::gram_stream_smem(same), st_,
+             a, ma, mb, same ? 1 : 0, ntl);
+      launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2, 8)), dim3(256), 0, st_,
+             static_cast<const double*>(a.partial), G, m1, m2, 32, 32, a.sym, out, ldo, alpha);
+      kend();
+      return;
+    }
     if (narrow)
       launch(dm::gram_tn_small_kernel, grid, dim3(dm::NT), 0, st_, a);
     else if (bulk) {
