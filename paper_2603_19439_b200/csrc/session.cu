@@ -680,7 +680,7 @@ class Session {
     a.mask_val = mask_val;
     if (narrow) a.tiles_i = a.tiles_j = 1;
     const int ntiles = narrow ? 1 : (sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j);
-    const i64 target = 148 * (layout == 0 ? 6 : 4);
+    const i64 target = 148 * (layout == 0 ? 24 : 4);  // square tiles: ~8 short waves keep the tail of unequal tile pairs small
     const i64 rows_min = narrow ? 256 : 128;
     i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
     splits = std::min<i64>(splits, 65535);
