@@ -1225,7 +1225,11 @@ class Session {
   // ortho.hpp:13-39 on the stacked coordinates: BCGS2 + CholQR2 when every
   // column is clearly independent, the exact column-by-column MGS2 replica when
   // a pivot is suspect. W (N x w) is consumed; Q is written to `out`.
-  int orthonormalize(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out) {
+  // With `Cpre` the block was already projected once outside (W = W0 - A Cpre,
+  // Cpre = A'W0, a x w with leading dimension ldcpre): pass 1 starts at its
+  // Gram, and the exact replica, if needed, rebuilds W0.
+  int orthonormalize(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out, const double* Cpre = nullptr,
+                     int ldcpre = 0) {
     if (w == 0) return 0;
     const int ldw = ld_for(w);
     double* W1 = arena_.get<double>("on_W1", N * ldw);
@@ -1237,20 +1241,32 @@ class Session {
     // pass 1: W1 = W - A (A'W); with no `against` the Gram reads W directly
     const double* P1 = W.p;
     int ldp1 = W.ld;
-    if (against && a > 0) {
+    const double* Cuse = C;
+    int ldc1 = ldw;
+    if (against && a > 0 && Cpre) {
+      Cuse = Cpre;
+      ldc1 = ldcpre;
+    } else if (against && a > 0) {
       gram(against->p, against->ld, W.p, W.ld, G, a, w, false, C, ldw);
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, W.p, W.ld);
       P1 = W1;
       ldp1 = ldw;
     }
     gram(P1, ldp1, P1, ldp1, G, w, w, true, Gm, ldw);
-    launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw,
-           static_cast<const double*>(C), ldw, (against ? a : 0), w, o2);
+    launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw, Cuse, ldc1,
+           (against ? a : 0), w, o2);
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
     chol(Gm, ldw, w, R, ldw, Ri, ldw, o2, kSuspectTau2, false);
     read_scalars();
     last_ortho_exact_ = (hs_->flags & (kSuspect | kBreakdown)) != 0;
-    if (last_ortho_exact_) return mgs2_exact(W, w, against, a, N, G, out);
+    if (last_ortho_exact_) {
+      if (against && a > 0 && Cpre) {  // the replica starts from the unprojected block
+        double* W0 = arena_.get<double>("on_W0", N * ldw);
+        nn(against->p, against->ld, N, a, Cpre, ldcpre, w, W0, ldw, 1.0, 1.0, W.p, W.ld);
+        return mgs2_exact(Blk{W0, ldw}, w, against, a, N, G, out);
+      }
+      return mgs2_exact(W, w, against, a, N, G, out);
+    }
     // pass 2 input Q1 = P1 R^-1: into `out` when it is re-projected into W1,
     // else straight into W1
     const bool proj = against && a > 0;
@@ -1269,6 +1285,13 @@ class Session {
   }
 
   bool last_ortho_exact_ = false;  // the last orthonormalize took the column-by-column replica
+  // sketch basis projected against [X-bar, first candidate block] while the
+  // sketch's eigensolve runs (rsvd_trailing / build_basis)
+  const double* pre_pm_ = nullptr;
+  const double* pre_c1_ = nullptr;
+  int pre_a_ = 0;
+  double* pre_cr_ = nullptr;
+  int pre_ldcr_ = 0;
   static constexpr double kSuspectTau2 = 1e-10;  // residual / original norm below 1e-5
   static constexpr double kRrOrtol = 1e-9;       // eigenvector cluster threshold for the RR solve
 
@@ -1406,14 +1429,30 @@ class Session {
         // the sketch's eigensolve runs beside it, then the RSVD columns against
         // [X-bar, that block].
         int q1 = 0;
-        const int wt = rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc}, [&] {
+        pre_pm_ = pre_c1_ = nullptr;
+        pre_cr_ = nullptr;
+        const int wt = rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc},
+                                     [&](const double* Msk, int ldm, int qm) {
           q1 = orthonormalize(Blk{cand, ldc}, kk, &z, kk, N, G, Blk{Z + kk, ldz});
+          if (Msk && qm > 0) {  // project the sketch basis against [X-bar, Q1] before U is known
+            const int a = kk + q1;
+            double* c1 = arena_.get<double>("pm_C1", static_cast<i64>(a) * ldm);
+            double* pm = arena_.get<double>("pm_PM", N * ldm);
+            gram(Z, ldz, Msk, ldm, G, a, qm, false, c1, ldm);
+            nn(Z, ldz, N, a, c1, ldm, qm, pm, ldm, -1.0, 1.0, Msk, ldm);
+            pre_pm_ = pm;
+            pre_c1_ = c1;
+            pre_a_ = a;
+          }
         });
         int q2 = 0;
         if (wt > 0) {
           const Blk against{Z, ldz};
-          q2 = orthonormalize(Blk{cand + kk, ldc}, wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz});
+          q2 = orthonormalize(Blk{cand + kk, ldc}, wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz}, pre_cr_,
+                              pre_ldcr_);
         }
+        pre_pm_ = pre_c1_ = nullptr;
+        pre_cr_ = nullptr;
         return Basis{z, kk + q1 + q2};
       }
     }
@@ -1453,7 +1492,7 @@ class Session {
     double* M = arena_.get<double>("Msk", N * ldy);
     const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy});
     if (qm == 0) {
-      during_eig();
+      during_eig(static_cast<const double*>(nullptr), ldy, 0);
       return 0;
     }
     // bt_m = d2' (M - X (X'M)) (trackers.cpp:262-266). On the CholQR2 path
@@ -1498,14 +1537,14 @@ class Session {
     if (eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10, st_eig_, side_flags_ptr())) {
       STG_CUDA(cudaMemcpyAsync(hs_->sk_lam, lamd, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_eig_));
       STG_CUDA(cudaEventRecord(ev_eig_, st_eig_));
-      during_eig();
+      during_eig(static_cast<const double*>(M), ldy, qm);
       STG_CUDA(cudaStreamWaitEvent(st_, ev_eig_, 0));
       STG_CUDA(cudaStreamSynchronize(st_eig_));
       std::copy(hs_->sk_lam, hs_->sk_lam + qm, lam.begin());
       hs_->info = 0;
       std::reverse(lam.begin(), lam.end());  // ascending like the cuSOLVER path
     } else {
-      during_eig();
+      during_eig(static_cast<const double*>(M), ldy, qm);
       double *w = nullptr, *V = nullptr;
       eig(gb, ldy, qm, &w, &V, "sk");
       STG_CUDA(cudaMemcpyAsync(lam.data(), w, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_));
@@ -1522,8 +1561,18 @@ class Session {
     while (rank < qm && sv[rank] > cutoff && sv[rank] > 0.0) ++rank;
     const int keep = static_cast<int>(std::min<i64>(cfg.rsvd_l, rank));
     if (keep == 0) return 0;
-    // R = M U_keep
-    nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+    // R = M U_keep; when the caller projected M against its basis meanwhile
+    // (pre_pm_ = M - B C1), R's first projection is PM U_keep with
+    // coefficients C1 U_keep
+    if (pre_pm_) {
+      nn(pre_pm_, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+      const int ldcp = ld_for(keep);
+      pre_cr_ = arena_.get<double>("pm_CR", static_cast<i64>(pre_a_) * ldcp);
+      pre_ldcr_ = ldcp;
+      nn(pre_c1_, ldy, pre_a_, qm, U, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
+    } else {
+      nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+    }
     return keep;
   }
 
