@@ -286,6 +286,7 @@ class Session {
   // ---------------------------------------------------------------- public ops
   void step(const st_update& u, bool device_ptrs = false) {
     launches = 0;
+    rr_pre_.valid = false;
     kdiscard();  // a failed or probe call may have left unflushed entries
     timing_begin();
     const u64 basis_seed = mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken);
@@ -1444,6 +1445,8 @@ class Session {
             pre_c1_ = c1;
             pre_a_ = a;
           }
+          // the Rayleigh-Ritz products of [X-bar, Q1] do not depend on the sketch
+          rr_prefix(pt, z, kk + q1, kk + q1 + static_cast<int>(std::min<i64>(cfg.rsvd_l, q)));
         });
         int q2 = 0;
         if (wt > 0) {
@@ -1686,42 +1689,84 @@ class Session {
   // ---------------------------------------------------------------- Rayleigh-Ritz
   // rayleigh_ritz_step (trackers.cpp:282-308). write_state: rotate X in place;
   // otherwise expand the new vectors (dense mode only) into host `wout`.
+  // The RR products of the first `a` basis columns (X-bar and the first
+  // candidate block), computed while the sketch's eigensolve runs:
+  // G11 = Z1'Z1, Delta Z1, T11 = Z1'(Delta Z1) into the rr_* buffers.
+  struct RrPrefix {
+    bool valid = false;
+    int a = 0, ldd = 0;
+  } rr_pre_;
+
+  void rr_prefix(const Pert& pt, Blk z, int a, int dmax) {
+    const i64 p = pt.p, G = p + k;
+    const int ldd = ld_for(dmax);
+    double* gz = arena_.get<double>("rr_gz", static_cast<i64>(dmax) * ldd);
+    double* dz = arena_.get<double>("rr_dz", p * ldd);
+    double* tm = arena_.get<double>("rr_t", static_cast<i64>(dmax) * ldd);
+    gram(z.p, z.ld, z.p, z.ld, G, a, a, true, gz, ldd);
+    rr_spmm(pt, z.p, z.ld, a, dz, ldd);
+    gram(z.p, z.ld, dz, ldd, p, a, a, true, tm, ldd);
+    rr_pre_ = RrPrefix{true, a, ldd};
+  }
+
+  void rr_spmm(const Pert& pt, const double* X, int ldx, int m, double* Y, int ldy) {
+    SpmmArgs sa{};
+    sa.rows = pt.p;
+    sa.rowptr = pt.lrp;
+    sa.col = pt.lcol;
+    sa.val = pt.val;
+    sa.X = X;
+    sa.ldx = ldx;
+    sa.m = m;
+    sa.Y = Y;
+    sa.ldy = ldy;
+    do_spmm(sa, pt.nnz, pt.p);
+  }
+
   void rayleigh_ritz(const Pert& pt, const Basis& b, std::vector<double>& newvals, bool write_state, double* wout,
                      i64 wrows, Blk xbar_override = Blk{}) {
     const i64 p = pt.p, N = p + 2 * k, G = p + k;
     const int D = b.D, kk = static_cast<int>(k);
     const Blk xb = xbar_override.p ? xbar_override : b.z;
-    const int ldd = ld_for(D);
-    // Gram check (trackers.cpp:293-295)
+    const bool pre = rr_pre_.valid && !xbar_override.p && rr_pre_.a <= D;
+    const int a = pre ? rr_pre_.a : 0;
+    const int ldd = pre ? rr_pre_.ldd : ld_for(D);
+    rr_pre_.valid = false;
+    // Gram check (trackers.cpp:293-295); the products are symmetric, so only
+    // their upper triangles are formed / read from here on
     double* gz = arena_.get<double>("rr_gz", static_cast<i64>(D) * ldd);
-    gram(b.z.p, b.z.ld, b.z.p, b.z.ld, G, D, D, true, gz, ldd);
+    double* dz = arena_.get<double>("rr_dz", p * ldd);
+    double* tm = arena_.get<double>("rr_t", static_cast<i64>(D) * ldd);
+    if (pre) {  // columns a.. : [Z1'Z2; Z2'Z2], Delta Z2, [Z1'(Delta Z2); Z2'(Delta Z2)]
+      if (D > a) {
+        gram(b.z.p, b.z.ld, b.z.p + a, b.z.ld, G, D, D - a, false, gz + a, ldd);
+        rr_spmm(pt, b.z.p + a, b.z.ld, D - a, dz + a, ldd);
+        gram(b.z.p, b.z.ld, dz + a, ldd, p, D, D - a, false, tm + a, ldd);
+      }
+    } else {
+      gram(b.z.p, b.z.ld, b.z.p, b.z.ld, G, D, D, true, gz, ldd);
+      rr_spmm(pt, b.z.p, b.z.ld, D, dz, ldd);
+      // Z'(Delta Z) is symmetric (Delta is): tile pairs ti <= tj, mirrored;
+      // the reference symmetrizes the projected matrix anyway (eig.hpp:47)
+      gram(b.z.p, b.z.ld, dz, ldd, p, D, D, true, tm, ldd);
+    }
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
     launch(orthocheck_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_,
            static_cast<const double*>(gz), ldd, D, 1e-6, flags_ptr());
-    // zx = Z' X-bar (D x k)
+    // zx = Z' X-bar (D x k): the first k columns of Z'Z when X-bar = Z[:, :k]
     const int ldk = ld_for(kk);
-    double* zx = arena_.get<double>("rr_zx", static_cast<i64>(D) * ldk);
-    gram(b.z.p, b.z.ld, xb.p, xb.ld, G, D, kk, false, zx, ldk);
-    // dz = Delta Z (rows of P), T = Z_P' dz
-    double* dz = arena_.get<double>("rr_dz", p * ldd);
-    SpmmArgs sa{};
-    sa.rows = p;
-    sa.rowptr = pt.lrp;
-    sa.col = pt.lcol;
-    sa.val = pt.val;
-    sa.X = b.z.p;
-    sa.ldx = b.z.ld;
-    sa.m = D;
-    sa.Y = dz;
-    sa.ldy = ldd;
-    do_spmm(sa, pt.nnz, p);
-    double* tm = arena_.get<double>("rr_t", static_cast<i64>(D) * ldd);
-    // Z'(Delta Z) is symmetric (Delta is): compute tile pairs ti <= tj and mirror;
-    // the reference symmetrizes the projected matrix anyway (eig.hpp:47)
-    gram(b.z.p, b.z.ld, dz, ldd, p, D, D, true, tm, ldd);
+    const double* zx = gz;
+    int ldzx = ldd, zx_sym = 1;
+    if (xbar_override.p) {
+      double* zxo = arena_.get<double>("rr_zx", static_cast<i64>(D) * ldk);
+      gram(b.z.p, b.z.ld, xb.p, xb.ld, G, D, kk, false, zxo, ldk);
+      zx = zxo;
+      ldzx = ldk;
+      zx_sym = 0;
+    }
     double* mm = arena_.get<double>("rr_m", static_cast<i64>(D) * ldd);
-    launch(rr_matrix_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_, static_cast<const double*>(zx),
-           ldk, static_cast<const double*>(d_values_), kk, static_cast<const double*>(tm), ldd, D, mm, ldd);
+    launch(rr_matrix_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_, zx, ldzx,
+           static_cast<const double*>(d_values_), kk, static_cast<const double*>(tm), ldd, D, mm, ldd, zx_sym);
     timing_mark(2);
     double* F = arena_.get<double>("rr_F", static_cast<i64>(D) * ldk);
     double* nv = arena_.get<double>("rr_vals", std::max(D, kk));

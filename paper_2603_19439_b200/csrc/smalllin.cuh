@@ -360,11 +360,12 @@ __global__ void symmetrize_kernel(const double* M, int ldm, int D, double* out, 
   out[static_cast<i64>(j) * D + i] = 0.5 * (a + b);
 }
 
-// max |G - I| > tol -> kNotOrthonormal
+// max |G - I| > tol -> kNotOrthonormal (G symmetric: its upper triangle is read)
 __global__ void orthocheck_kernel(const double* Gm, int ldg, int D, double tol, int* flags) {
   const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<i64>(D) * D) return;
   const int i = static_cast<int>(idx / D), j = static_cast<int>(idx % D);
+  if (i > j) return;
   const double v = Gm[static_cast<i64>(i) * ldg + j] - (i == j ? 1.0 : 0.0);
   if (!(fabs(v) <= tol)) atomicOr(flags, kNotOrthonormal);
 }
@@ -372,14 +373,20 @@ __global__ void orthocheck_kernel(const double* Gm, int ldg, int D, double tol, 
 // M(D x D) = zx diag(lam) zx' + T   (Eq. 14, trackers.cpp:300-301), evaluated
 // on (min(i,j), max(i,j)) so M is exactly symmetric (T, a mirrored Gram, is),
 // and the eigensolver's (M + M')/2 (eig.hpp:47) is M itself.
+// With zx_sym, zx is the symmetric D x D Gram Z'Z (X-bar = its first k
+// columns) and only its upper triangle is read: zx(i, l) = G(min, max).
 __global__ void rr_matrix_kernel(const double* zx, int ldzx, const double* lam, int k, const double* T, int ldt,
-                                 int D, double* M, int ldm) {
+                                 int D, double* M, int ldm, int zx_sym) {
   const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<i64>(D) * D) return;
   const int i = static_cast<int>(idx / D), j = static_cast<int>(idx % D);
   const int lo = min(i, j), hi = max(i, j);
+  auto zxa = [&](int r, int l) {
+    if (!zx_sym) return zx[static_cast<i64>(r) * ldzx + l];
+    return zx[static_cast<i64>(min(r, l)) * ldzx + max(r, l)];
+  };
   double s = 0.0;
-  for (int l = 0; l < k; ++l) s += zx[static_cast<i64>(lo) * ldzx + l] * lam[l] * zx[static_cast<i64>(hi) * ldzx + l];
+  for (int l = 0; l < k; ++l) s += zxa(lo, l) * lam[l] * zxa(hi, l);
   M[static_cast<i64>(i) * ldm + j] = s + T[static_cast<i64>(lo) * ldt + hi];
 }
 
