@@ -485,27 +485,47 @@ __global__ void __launch_bounds__(128) bisect_kernel(EigBufs b, int n) {
 // (consecutive selected values closer than ortol ||T||_1, dstein's ORTOL).
 __global__ void __launch_bounds__(1024) select_kernel(EigBufs b, int n, int order, int want, double ortol,
                                                       double* w_sorted) {
-  extern __shared__ int shi[];
-  int* chosen = shi;
-  const double* lam = b.lam;
+  extern __shared__ double shl[];  // lam[n], then int chosen[n], sel[n], start[n]
+  double* lam = shl;
+  int* chosen = reinterpret_cast<int*>(lam + n);
+  int* sel = chosen + n;
+  int* start = sel + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lam[i] = b.lam[i];
+  __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     int rank = 0;
     const double vi = lam[i];
     for (int jj = 0; jj < n; ++jj)
       if (jj != i && spectral_before(lam[jj], jj, vi, i, order)) ++rank;
     b.perm[rank] = i;
+    w_sorted[rank] = vi;
     chosen[i] = rank < want ? 1 : 0;
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < n; c += blockDim.x) w_sorted[c] = lam[b.perm[c]];
+  // selected indices in ascending order (prefix counts; n is small)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (!chosen[i]) continue;
+    int pos = 0;
+    for (int jj = 0; jj < i; ++jj) pos += chosen[jj];
+    sel[pos] = i;
+  }
+  __syncthreads();
+  const int m = min(want, n);
+  const double tol = ortol * *b.tnorm;
+  for (int q = threadIdx.x; q < m; q += blockDim.x) {
+    b.sel[q] = sel[q];
+    start[q] = (q == 0 || lam[sel[q]] - lam[sel[q - 1]] > tol) ? 1 : 0;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < m; q += blockDim.x) {
+    if (!start[q]) continue;
+    int c = 0;
+    for (int jj = 0; jj < q; ++jj) c += start[jj];
+    b.cstart[c] = q;
+  }
   if (threadIdx.x == 0) {
-    const double tn = *b.tnorm;
-    int m = 0;
-    for (int i = 0; i < n; ++i)
-      if (chosen[i]) b.sel[m++] = i;
     int ncl = 0;
-    for (int q = 0; q < m; ++q)
-      if (q == 0 || lam[b.sel[q]] - lam[b.sel[q - 1]] > ortol * tn) b.cstart[ncl++] = q;
+    for (int q = 0; q < m; ++q) ncl += start[q];
     b.cstart[ncl] = m;
     *b.ncl = ncl;
   }
@@ -733,7 +753,7 @@ void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int
     L(tridiag2_kernel, dim3(2), dim3(kTriThreads), tridiag_smem_bytes(n, 2, g), M, ldm, n, sym_input, g, b, flags);
   }
   L(bisect_kernel, dim3(static_cast<unsigned>(cdiv(kBisG * n, 128))), dim3(128), sizeof(double) * 2 * n, b, n);
-  L(select_kernel, dim3(1), dim3(256), sizeof(int) * n, b, n, order, want, ortol, w_sorted);
+  L(select_kernel, dim3(1), dim3(256), (sizeof(double) + 3 * sizeof(int)) * n, b, n, order, want, ortol, w_sorted);
   L(invit_kernel, dim3(static_cast<unsigned>(cdiv(want, kInvitThreads))), dim3(kInvitThreads), invit_smem_bytes(n), b,
     n);
   L(backtransform_kernel, dim3(static_cast<unsigned>(cdiv(want, 4))), dim3(128), sizeof(double) * 2 * kBtRows * n, b,
