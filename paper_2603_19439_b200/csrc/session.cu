@@ -1092,21 +1092,28 @@ class Session {
              static_cast<const int*>(mflag), static_cast<const double*>(newv), static_cast<const int*>(prefix),
              static_cast<const int*>(drp), static_cast<const int*>(an.rp), an.col, an.val);
     kend();
-    // ---- sync 1: validation outcome and sizes
+    // ---- validation outcome and sizes: read back here for the Laplacian
+    // operators (their assembly needs nnz); the adjacency path folds this read
+    // into the P-size sync below (nothing is committed before either)
     STG_CUDA(cudaMemcpyAsync(&hs_->err_edit, err_edit, sizeof(u64) * 3, cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaMemcpyAsync(&hs_->nnz_new, an.rp + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
-    STG_CUDA(cudaStreamSynchronize(st_));
-    if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
-    if (hs_->err_apply != kSentinel) {
-      if (hs_->err_apply & 1ULL) throw InvalidArgument("apply_update: update drives an edge weight negative");
-      throw InvalidArgument("apply_update: invalid deletion (no such edge)");
+    auto check_validation = [&]() {
+      if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
+      if (hs_->err_apply != kSentinel) {
+        if (hs_->err_apply & 1ULL) throw InvalidArgument("apply_update: update drives an edge weight negative");
+        throw InvalidArgument("apply_update: invalid deletion (no such edge)");
+      }
+      an.nnz = hs_->nnz_new;
+      A_[slot] = an;
+      anext_ = slot;
+      pt.nnz = static_cast<i64>(hs_->nvalid);
+      if (ktiming())  // read old CSR + write new CSR (SURVEY 8(d) ingestion bytes, edits excluded)
+        pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (n_old + 1) + 12.0 * an.nnz + 4.0 * (n_total + 1);
+    };
+    if (is_laplacian()) {
+      STG_CUDA(cudaStreamSynchronize(st_));
+      check_validation();
     }
-    an.nnz = hs_->nnz_new;
-    pt.nnz = static_cast<i64>(hs_->nvalid);
-    if (ktiming())  // read old CSR + write new CSR (SURVEY 8(d) ingestion bytes, edits excluded)
-      pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (n_old + 1) + 12.0 * an.nnz + 4.0 * (n_total + 1);
-    anext_ = slot;
-    A_[slot] = an;
     // ---- the tracked operator's perturbation
     const int* grp = drp;
     const int* gcol = dcol;
@@ -1173,6 +1180,7 @@ class Session {
            static_cast<const int*>(pos), n_total, P, posmap_);
     STG_CUDA(cudaMemcpyAsync(&hs_->p, pos + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaStreamSynchronize(st_));
+    if (!is_laplacian()) check_validation();
     pt.p = hs_->p;
     pt.p_old = pt.p - S;
     pt.P = P;
@@ -1232,6 +1240,16 @@ class Session {
   int orthonormalize(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out, const double* Cpre = nullptr,
                      int ldcpre = 0) {
     if (w == 0) return 0;
+    if (w > kCholMaxW) {  // wider than the one-CTA Cholesky: the exact column-by-column replica
+      last_ortho_exact_ = true;
+      if (against && a > 0 && Cpre) {
+        const int ldw0 = ld_for(w);
+        double* W0 = arena_.get<double>("on_W0", N * ldw0);
+        nn(against->p, against->ld, N, a, Cpre, ldcpre, w, W0, ldw0, 1.0, 1.0, W.p, W.ld);
+        return mgs2_exact(Blk{W0, ldw0}, w, against, a, N, G, out);
+      }
+      return mgs2_exact(W, w, against, a, N, G, out);
+    }
     const int ldw = ld_for(w);
     double* W1 = arena_.get<double>("on_W1", N * ldw);
     double* C = arena_.get<double>("on_C", static_cast<i64>(std::max(a, 1)) * ldw);
