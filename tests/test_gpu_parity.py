@@ -222,3 +222,21 @@ def test_config3_shape_parity_rmat17():
         orc.step(upd)
         ve, sa = check_state(gpu, orc, tag=f"cfg3-s17 step {t}")
         print(f"cfg3-s17 step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
+
+
+@pytest.mark.gpu
+def test_wide_sketch_takes_exact_paths():
+    """A sketch wider than the one-CTA Cholesky (q = L + P = 260 > 238) and the
+    on-device eigensolver (> 228): the column-by-column orthonormalization
+    replica and the cuSOLVER eigensolve run instead, with the same parity."""
+    from paper_2603_19439_b200 import streams
+    keys = streams.rmat_keys(12, 8, seed=9)
+    s = streams.edit_stream(1 << 12, keys, 2, 4, lambda m: 0, lambda m: 0.005 * m,
+                            new_nodes=lambda nn: 300, new_degree=4)
+    rp, col, val = s.csr0()
+    gpu, orc = pair(rp, col, val, kind="grest-rsvd", k=6, rsvd_l=140, rsvd_p=120, seed=2)
+    for t, upd in enumerate(s.updates):
+        assert upd.n_new > 260
+        gpu.step(upd)
+        orc.step(upd)
+        check_state(gpu, orc, tag=f"wide sketch step {t}")
