@@ -531,10 +531,14 @@ __global__ void __launch_bounds__(1024) select_kernel(EigBufs b, int n, int orde
   }
 }
 
-// Inverse iteration (dlagtf/dlagts with partial pivoting, 3 sweeps) for each
+// Inverse iteration (dlagtf/dlagts with partial pivoting, kInvitSweeps) for each
 // selected eigenvalue; one thread owns one cluster and re-orthogonalizes its
 // members in order. Working vectors live in shared memory (8 threads / CTA).
 constexpr int kInvitThreads = 8;
+// Sweeps of inverse iteration: with the eigenvalue accurate to eps ||T|| one
+// solve from a generic start already amplifies the wanted direction by
+// ~1 / (eps ||T||); the second refines it (dstein stops after two more).
+constexpr int kInvitSweeps = 2;
 __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) {
   extern __shared__ double sh[];
   const int cl = blockIdx.x * blockDim.x + threadIdx.x;
@@ -591,7 +595,7 @@ __global__ void __launch_bounds__(kInvitThreads) invit_kernel(EigBufs b, int n) 
       dd[i] = __drcp_rn(dd[i]);
     }
     for (int i = 0; i < n; ++i) x[i] = 1.0 + 0.5 * __sinf(1.0f + 0.7f * i + 1.3f * q);
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < kInvitSweeps; ++it) {
       double carry = x[0];
       for (int i = 0; i + 1 < n; ++i) {
         const double nx = x[i + 1];
