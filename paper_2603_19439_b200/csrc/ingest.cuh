@@ -34,6 +34,7 @@ struct EditsDev {
   const double* nw;
   i64 n_add, n_rem, n_newe;
   i64 n_old, S;
+  int kb;  // key field width: 2^kb > n_old + S, keys are (row << kb | col)
 };
 
 __device__ __forceinline__ void edit_at(const EditsDev& d, i64 g, int& list, i64& i, i64& j, double& w) {
@@ -69,7 +70,7 @@ __global__ void edit_check_kernel(EditsDev d, u64* pkey, i64* pval, int* code, i
   code[g] = c;
   post[g] = p;
   const i64 lo = i < j ? i : j, hi = i < j ? j : i;
-  pkey[g] = c == kErrNone ? ((static_cast<u64>(lo) << 32) | static_cast<u64>(hi)) : kSentinel;
+  pkey[g] = c == kErrNone ? ((static_cast<u64>(lo) << d.kb) | static_cast<u64>(hi)) : kSentinel;
   pval[g] = g;
 }
 
@@ -83,7 +84,7 @@ __global__ void dup_mark_kernel(const u64* skey, const i64* sval, i64 E, int* du
 }
 
 // Final per-edit status (first failing check) -> first error in edit order;
-// valid edits emit their two directed entries (row << 32 | col, weight).
+// valid edits emit their two directed entries (row << kb | col, weight).
 __global__ void edit_emit_kernel(EditsDev d, const int* code, const int* dup, const int* post, u64* err,
                                  u64* ekey, double* eval, unsigned long long* nvalid) {
   const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -102,19 +103,20 @@ __global__ void edit_emit_kernel(EditsDev d, const int* code, const int* dup, co
   i64 i, j;
   double w;
   edit_at(d, g, list, i, j, w);
-  ekey[2 * g] = (static_cast<u64>(i) << 32) | static_cast<u64>(j);
-  ekey[2 * g + 1] = (static_cast<u64>(j) << 32) | static_cast<u64>(i);
+  ekey[2 * g] = (static_cast<u64>(i) << d.kb) | static_cast<u64>(j);
+  ekey[2 * g + 1] = (static_cast<u64>(j) << d.kb) | static_cast<u64>(i);
   eval[2 * g] = eval[2 * g + 1] = w;
   atomicAdd(nvalid, 2ULL);
 }
 
 // Sorted entries -> row/col arrays, per-row counts, and row marks.
-__global__ void delta_rows_kernel(const u64* skey, i64 n2, int* drow, int* dcol, int* rowcnt, int* mark, int stamp) {
+__global__ void delta_rows_kernel(const u64* skey, i64 n2, int* drow, int* dcol, int* rowcnt, int* mark, int stamp,
+                                  int kb) {
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n2) return;
   const u64 k = skey[e];
   if (k == kSentinel) return;
-  const int r = static_cast<int>(k >> 32), c = static_cast<int>(k & 0xffffffffULL);
+  const int r = static_cast<int>(k >> kb), c = static_cast<int>(k & ((1ULL << kb) - 1));
   drow[e] = r;
   dcol[e] = c;
   atomicAdd(rowcnt + r, 1);
@@ -130,7 +132,7 @@ __global__ void mark_range_kernel(int* mark, i64 lo, i64 hi, int stamp) {
 // Pass 1 (per Delta entry): locate in A's row, classify, count, check.
 __global__ void merge_classify_kernel(const u64* skey, const double* sval, i64 n2, const int* arp, const int* acol,
                                       const double* aval, i64 n_old, int* lb, int* flag, double* newv, int* contrib,
-                                      int* rowcnt, u64* err) {
+                                      int* rowcnt, u64* err, int kb) {
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n2) return;
   const u64 k = skey[e];
@@ -138,7 +140,7 @@ __global__ void merge_classify_kernel(const u64* skey, const double* sval, i64 n
     contrib[e] = 0;
     return;
   }
-  const int r = static_cast<int>(k >> 32), c = static_cast<int>(k & 0xffffffffULL);
+  const int r = static_cast<int>(k >> kb), c = static_cast<int>(k & ((1ULL << kb) - 1));
   const double dv = sval[e];
   int s = 0, len = 0;
   if (r < n_old) {

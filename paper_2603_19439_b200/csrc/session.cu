@@ -1011,6 +1011,11 @@ class Session {
     ed.n_newe = u.n_new_edges;
     ed.n_old = n_old;
     ed.S = S;
+    // narrowest key packing that keeps every index below the all-ones sentinel:
+    // the radix sorts then run over 2*kb bits instead of 64
+    ed.kb = 1;
+    while ((1LL << ed.kb) <= n_total) ++ed.kb;
+    const int key_bits = 2 * ed.kb;
     u64* err_edit = d_scal_;
     u64* err_apply = d_scal_ + 1;
     unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(d_scal_ + 2);
@@ -1030,17 +1035,17 @@ class Session {
     if (E > 0) {
       launch(edit_check_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, pkey, pval, code, post);
       size_t tmp = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, 64, st_);
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits, st_);
       void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
-      cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, 64, st_);
+      cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits, st_);
       launch(dup_mark_kernel, dim3(blocks(E)), dim3(256), 0, st_, static_cast<const u64*>(pkey_s),
              static_cast<const i64*>(pval_s), E, dup);
       launch(edit_emit_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, static_cast<const int*>(code),
              static_cast<const int*>(dup), static_cast<const int*>(post), err_edit, ekey, eval, nvalid);
       tmp = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, 64, st_);
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits, st_);
       t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
-      cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, 64, st_);
+      cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits, st_);
     }
     // ---- Delta (global CSR over n_total rows)
     const std::string sfx = keep_delta ? "" : "_probe";
@@ -1051,7 +1056,7 @@ class Session {
     STG_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (n_total + 1), st_));
     if (n2 > 0)
       launch(delta_rows_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s), n2, drow, dcol,
-             dcnt, mark_delta_, stamp_);
+             dcnt, mark_delta_, stamp_, ed.kb);
     scan_int(dcnt, drp, n_total + 1);
     // ---- apply_update merge (A_next in the spare slot)
     const DevCsr& a = A();
@@ -1074,7 +1079,7 @@ class Session {
     if (n2 > 0)
       launch(merge_classify_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s),
              static_cast<const double*>(eval_s), n2, static_cast<const int*>(a.rp), static_cast<const int*>(a.col),
-             static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply);
+             static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply, ed.kb);
     scan_int(ncnt, an.rp, n_total + 1);
     scan_int(contrib, prefix, n2 + 1);
     kbegin(kMerge, 0.0);

@@ -19,6 +19,7 @@ ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--k", type=int, default=32)
 ap.add_argument("--real-x0", action="store_true", help="leading eigenpairs (as bench.py) instead of a random basis")
+ap.add_argument("--device-edits", action="store_true", help="edit lists resident in HBM (st_step_device, as bench.py)")
 args = ap.parse_args()
 
 s = streams.config3(scale=args.scale, steps=args.warmup + args.steps)
@@ -32,8 +33,14 @@ else:
     vals = np.linspace(100.0, 10.0, args.k)
 g = TrackerSession(rp, col, val, vals, x, kind="grest-rsvd", k=args.k, seed=0, timing=True,
                    kernel_timing=bool(os.environ.get("STG_KLOG")), cusolver_eig=bool(os.environ.get("STG_CUSOLVER")))
+if args.device_edits:
+    from paper_2603_19439_b200 import DeviceUpdate  # noqa: E402
+    dev = [DeviceUpdate(u, device="cuda:0") for u in s.updates]
 for t, u in enumerate(s.updates):
     t0 = time.perf_counter()
-    g.step(u)
+    if args.device_edits:
+        g.step_device(dev[t])
+    else:
+        g.step(u)
     print(f"step {t}: {1e3 * (time.perf_counter() - t0):.2f} ms wall, phases {np.round(g.timings(), 3).tolist()}, "
           f"launches {g.launches()}", flush=True)
