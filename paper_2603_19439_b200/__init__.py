@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspectrack_b200.so")
+LIB_PATH = os.environ.get("STG_LIB") or os.path.join(_HERE, "libspectrack_b200.so")  # STG_LIB: development A/B only
 
 I64 = C.c_int64
 DP = C.POINTER(C.c_double)

@@ -109,6 +109,109 @@ __global__ void edit_emit_kernel(EditsDev d, const int* code, const int* dup, co
   atomicAdd(nvalid, 2ULL);
 }
 
+// ---- sort-free Delta assembly (the normal path) ---------------------------
+// The same checks, keys and outcome as edit_check -> sort -> dup_mark ->
+// edit_emit -> sort -> delta_rows, without the two radix sorts: each edit
+// that passes the per-edit checks claims a slot in the buckets of its two
+// rows (atomic counters), the counters are scanned into row starts, and every
+// bucket entry finds its place in the row by counting the entries before it
+// in (column, edit index) order. Equal columns within a row are exactly the
+// duplicate pairs: the later edit is flagged (dup) and its entry becomes a
+// sentinel. A row longer than kRankMaxRow makes the counting quadratic; it
+// is reported through err_edit = 0 (no real error encodes as 0) and the host
+// re-runs the ingestion on the sorting path.
+constexpr int kRankMaxRow = 4096;
+
+__global__ void edit_bucket_kernel(EditsDev d, int* code, int* post, int* rowcnt, int2* slot, int* mark, int stamp) {
+  const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 E = d.n_add + d.n_rem + d.n_newe;
+  if (g >= E) return;
+  int list;
+  i64 i, j;
+  double w;
+  edit_at(d, g, list, i, j, w);
+  const i64 n_total = d.n_old + d.S;
+  int c = kErrNone, p = 0;
+  if (list == 0 && w == 0.0) c = kErrZeroWeight;
+  else if (list < 2 && (i < 0 || j < 0 || i >= d.n_old || j >= d.n_old)) c = kErrEditRange;
+  else if (list == 2 && (i < 0 || j < 0 || i >= n_total || j >= n_total)) c = kErrNewRange;
+  else if (list == 2 && w <= 0.0) c = kErrNewWeight;
+  else if (i == j) c = kErrSelfLoop;
+  if (list == 2 && c == kErrNone && (i > j ? i : j) < d.n_old) p = 1;
+  code[g] = c;
+  post[g] = p;
+  if (c == kErrNone) {
+    slot[g] = make_int2(atomicAdd(rowcnt + i, 1), atomicAdd(rowcnt + j, 1));
+    mark[i] = stamp;
+    mark[j] = stamp;
+  }
+}
+
+__global__ void edit_scatter_kernel(EditsDev d, const int* code, const int2* slot, const int* rstart, int* brow,
+                                    int* bcol, int* bedit) {
+  const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 E = d.n_add + d.n_rem + d.n_newe;
+  if (g >= E || code[g] != kErrNone) return;
+  int list;
+  i64 i, j;
+  double w;
+  edit_at(d, g, list, i, j, w);
+  const int2 s = slot[g];
+  const int qi = rstart[i] + s.x, qj = rstart[j] + s.y;
+  brow[qi] = static_cast<int>(i);
+  bcol[qi] = static_cast<int>(j);
+  bedit[qi] = static_cast<int>(g);
+  brow[qj] = static_cast<int>(j);
+  bcol[qj] = static_cast<int>(i);
+  bedit[qj] = static_cast<int>(g);
+}
+
+// Bucket entry -> its slot in the row's column order; ekey tail past the
+// entry count must hold sentinels (memset by the caller).
+__global__ void delta_rank_kernel(EditsDev d, i64 n2, const int* rstart, const int* brow, const int* bcol,
+                                  const int* bedit, u64* skey, double* sval, int* drow, int* dcol, int* dup,
+                                  u64* err) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 n_total = d.n_old + d.S;
+  if (e >= n2 || e >= rstart[n_total]) return;
+  const int r = brow[e], c = bcol[e], g = bedit[e];
+  const int s = rstart[r], t = rstart[r + 1];
+  if (t - s > kRankMaxRow) {
+    atomicMin(err, 0ULL);
+    return;
+  }
+  int rank = 0;
+  bool later = false;
+  for (int q = s; q < t; ++q) {
+    const int c2 = bcol[q];
+    const bool before = c2 < c || (c2 == c && bedit[q] < g);
+    rank += before ? 1 : 0;
+    later |= c2 == c && bedit[q] < g;
+  }
+  int list;
+  i64 i, j;
+  double w;
+  edit_at(d, g, list, i, j, w);
+  const int pos = s + rank;
+  drow[pos] = r;
+  dcol[pos] = c;
+  sval[pos] = later ? 0.0 : w;
+  skey[pos] = later ? kSentinel : ((static_cast<u64>(r) << d.kb) | static_cast<u64>(c));
+  if (later) dup[g] = 1;
+}
+
+// Final per-edit status for the sort-free path (as edit_emit, entries already placed).
+__global__ void edit_status_kernel(i64 E, const int* code, const int* dup, const int* post, u64* err,
+                                   unsigned long long* nvalid) {
+  const i64 g = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (g >= E) return;
+  int c = code[g];
+  if (c == kErrNone && dup[g]) c = kErrDuplicate;
+  if (c == kErrNone && post[g]) c = kErrNewOldOnly;
+  if (c != kErrNone) atomicMin(err, (static_cast<u64>(g) << 8) | static_cast<u64>(c));
+  else atomicAdd(nvalid, 2ULL);
+}
+
 // Sorted entries -> row/col arrays, per-row counts, and row marks.
 __global__ void delta_rows_kernel(const u64* skey, i64 n2, int* drow, int* dcol, int* rowcnt, int* mark, int stamp,
                                   int kb) {
@@ -136,8 +239,11 @@ __global__ void merge_classify_kernel(const u64* skey, const double* sval, i64 n
   const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= n2) return;
   const u64 k = skey[e];
-  if (k == kSentinel) {
+  if (k == kSentinel) {  // inert in the merge: never counted, never a hit
     contrib[e] = 0;
+    lb[e] = 0x3fffffff;
+    flag[e] = 0;
+    newv[e] = 0.0;
     return;
   }
   const int r = static_cast<int>(k >> kb), c = static_cast<int>(k & ((1ULL << kb) - 1));

@@ -192,14 +192,18 @@ class Session {
           const double* evec, i64 ld)
       : cfg(c) {
     STG_CUDA(cudaSetDevice(cfg.device));
-    STG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-    STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
-    STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
-    {  // high priority: the eigensolve's CTAs take SMs ahead of the wide kernels it overlaps
+    {  // priorities: the eigensolve's CTAs take SMs ahead of the wide kernels it
+       // overlaps; the CSR merge copy fills whatever the step leaves idle
       int lo = 0, hi = 0;
       STG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      STG_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, (lo + hi) / 2));
       STG_CUDA(cudaStreamCreateWithPriority(&st_eig_, cudaStreamNonBlocking, hi));
+      STG_CUDA(cudaStreamCreateWithPriority(&st_mg_, cudaStreamNonBlocking, lo));
     }
+    STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_mg_fork_, cudaEventDisableTiming));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_mg_, cudaEventDisableTiming));
     STG_CUDA(cudaEventCreateWithFlags(&ev_gb_, cudaEventDisableTiming));
     STG_CUDA(cudaEventCreateWithFlags(&ev_eig_, cudaEventDisableTiming));
     for (auto& e : tev_) STG_CUDA(cudaEventCreate(&e));
@@ -275,6 +279,10 @@ class Session {
     cudaEventDestroy(ev_gb_);
     cudaEventDestroy(ev_eig_);
     cudaStreamDestroy(st_eig_);
+    cudaStreamSynchronize(st_mg_);
+    cudaEventDestroy(ev_mg_fork_);
+    cudaEventDestroy(ev_mg_);
+    cudaStreamDestroy(st_mg_);
     cudaStreamDestroy(st_);
   }
 
@@ -491,6 +499,11 @@ class Session {
   cudaEvent_t ev_rng_ = nullptr;
   cudaStream_t st_eig_ = nullptr;  // the sketch's eigensolve (few SMs) runs beside the basis work
   cudaEvent_t ev_gb_ = nullptr, ev_eig_ = nullptr;
+  // the adjacency merge's entry copy (A_next's col/val; nothing in the step
+  // reads them) runs beside the basis work; joined before the graph commits
+  // and before the next ingest touches the spare slot or the Delta marks
+  cudaStream_t st_mg_ = nullptr;
+  cudaEvent_t ev_mg_fork_ = nullptr, ev_mg_ = nullptr;
   cudaEvent_t tev_[8];
   int tev_n_ = 0;
   cusolverDnHandle_t solver_ = nullptr;
@@ -952,12 +965,13 @@ class Session {
 
   // ---------------------------------------------------------------- ingestion
   // Validation, Delta, A_next (and T_next, Delta_T), P. Nothing committed.
-  Pert ingest(const st_update& u, bool keep_delta, bool device_ptrs = false) {
+  Pert ingest(const st_update& u, bool keep_delta, bool device_ptrs = false, bool sort_path = false) {
     if (u.n_new < 0) throw InvalidArgument("assemble_update: negative node count");
     if (u.n_added < 0 || u.n_removed < 0 || u.n_new_edges < 0) throw InvalidArgument("st_step: negative list length");
     const i64 n_old = n, S = u.n_new, n_total = n_old + S;
     if (n_total >= (1LL << 31)) throw InvalidArgument("st_step: node count exceeds int32 CSR indexing");
     const i64 E = u.n_added + u.n_removed + u.n_new_edges;
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_mg_, 0));  // a merge left running by a failed step
     ensure_node_capacity(n_total);
     ++stamp_;
     if (stamp_ == 0x7fffffff) stamp_ = 1;
@@ -1020,44 +1034,68 @@ class Session {
     u64* err_apply = d_scal_ + 1;
     unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(d_scal_ + 2);
     const i64 n2 = 2 * E;
-    // ---- validation + Delta entries
-    u64* pkey = arena_.get<u64>("pkey", E);
-    i64* pval = arena_.get<i64>("pval", E);
-    u64* pkey_s = arena_.get<u64>("pkey_s", E);
-    i64* pval_s = arena_.get<i64>("pval_s", E);
+    // ---- validation + Delta entries -> Delta (global CSR over n_total rows)
     int* code = arena_.get<int>("code", E);
     int* post = arena_.get<int>("post", E);
     int* dup = arena_.get<int>("dup", E);
-    u64* ekey = arena_.get<u64>("ekey", n2);
-    double* eval = arena_.get<double>("eval", n2);
     u64* ekey_s = arena_.get<u64>(keep_delta ? "ekey_s" : "ekey_s_probe", n2);
     double* eval_s = arena_.get<double>(keep_delta ? "eval_s" : "eval_s_probe", n2);
-    if (E > 0) {
-      launch(edit_check_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, pkey, pval, code, post);
-      size_t tmp = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits, st_);
-      void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
-      cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits, st_);
-      launch(dup_mark_kernel, dim3(blocks(E)), dim3(256), 0, st_, static_cast<const u64*>(pkey_s),
-             static_cast<const i64*>(pval_s), E, dup);
-      launch(edit_emit_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, static_cast<const int*>(code),
-             static_cast<const int*>(dup), static_cast<const int*>(post), err_edit, ekey, eval, nvalid);
-      tmp = 0;
-      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits, st_);
-      t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
-      cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits, st_);
-    }
-    // ---- Delta (global CSR over n_total rows)
     const std::string sfx = keep_delta ? "" : "_probe";
     int* drow = arena_.get<int>("drow" + sfx, n2);
     int* dcol = arena_.get<int>("dcol" + sfx, n2);
     int* dcnt = arena_.get<int>("dcnt", n_total + 1);
     int* drp = arena_.get<int>("drp" + sfx, n_total + 1);
     STG_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (n_total + 1), st_));
-    if (n2 > 0)
-      launch(delta_rows_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s), n2, drow, dcol,
-             dcnt, mark_delta_, stamp_, ed.kb);
-    scan_int(dcnt, drp, n_total + 1);
+    if (!sort_path) {
+      // buckets by row, then each entry's rank in its row (edit_bucket_kernel)
+      int2* slot = arena_.get<int2>("e_slot", E);
+      int* brow = arena_.get<int>("b_row", n2);
+      int* bcol = arena_.get<int>("b_col", n2);
+      int* bedit = arena_.get<int>("b_edit", n2);
+      if (E > 0)
+        launch(edit_bucket_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, code, post, dcnt, slot, mark_delta_,
+               stamp_);
+      scan_int(dcnt, drp, n_total + 1);
+      if (E > 0) {
+        launch(edit_scatter_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, static_cast<const int*>(code),
+               static_cast<const int2*>(slot), static_cast<const int*>(drp), brow, bcol, bedit);
+        STG_CUDA(cudaMemsetAsync(dup, 0, sizeof(int) * E, st_));
+        STG_CUDA(cudaMemsetAsync(ekey_s, 0xff, sizeof(u64) * n2, st_));
+        launch(delta_rank_kernel, dim3(blocks(n2)), dim3(256), 0, st_, ed, n2, static_cast<const int*>(drp),
+               static_cast<const int*>(brow), static_cast<const int*>(bcol), static_cast<const int*>(bedit), ekey_s,
+               eval_s, drow, dcol, dup, err_edit);
+        launch(edit_status_kernel, dim3(blocks(E)), dim3(256), 0, st_, E, static_cast<const int*>(code),
+               static_cast<const int*>(dup), static_cast<const int*>(post), err_edit, nvalid);
+      }
+    } else {
+      // two radix sorts: pair keys for the duplicate test, then the entries
+      u64* pkey = arena_.get<u64>("pkey", E);
+      i64* pval = arena_.get<i64>("pval", E);
+      u64* pkey_s = arena_.get<u64>("pkey_s", E);
+      i64* pval_s = arena_.get<i64>("pval_s", E);
+      u64* ekey = arena_.get<u64>("ekey", n2);
+      double* eval = arena_.get<double>("eval", n2);
+      if (E > 0) {
+        launch(edit_check_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, pkey, pval, code, post);
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits,
+                                        st_);
+        void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+        cub::DeviceRadixSort::SortPairs(t, tmp, pkey, pkey_s, pval, pval_s, static_cast<int>(E), 0, key_bits, st_);
+        launch(dup_mark_kernel, dim3(blocks(E)), dim3(256), 0, st_, static_cast<const u64*>(pkey_s),
+               static_cast<const i64*>(pval_s), E, dup);
+        launch(edit_emit_kernel, dim3(blocks(E)), dim3(256), 0, st_, ed, static_cast<const int*>(code),
+               static_cast<const int*>(dup), static_cast<const int*>(post), err_edit, ekey, eval, nvalid);
+        tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits,
+                                        st_);
+        t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+        cub::DeviceRadixSort::SortPairs(t, tmp, ekey, ekey_s, eval, eval_s, static_cast<int>(n2), 0, key_bits, st_);
+        launch(delta_rows_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s), n2, drow,
+               dcol, dcnt, mark_delta_, stamp_, ed.kb);
+      }
+      scan_int(dcnt, drp, n_total + 1);
+    }
     // ---- apply_update merge (A_next in the spare slot)
     const DevCsr& a = A();
     int* lb = arena_.get<int>("m_lb", n2);
@@ -1082,21 +1120,31 @@ class Session {
              static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply, ed.kb);
     scan_int(ncnt, an.rp, n_total + 1);
     scan_int(contrib, prefix, n2 + 1);
-    kbegin(kMerge, 0.0);
+    // row pointers, counts and the apply checks above stay on st_ (the
+    // validation read below needs them); the entry copy may run aside
+    const bool merge_aside = keep_delta && !is_laplacian();
+    cudaStream_t ms = st_;
+    if (merge_aside) {
+      STG_CUDA(cudaEventRecord(ev_mg_fork_, st_));
+      STG_CUDA(cudaStreamWaitEvent(st_mg_, ev_mg_fork_, 0));
+      ms = st_mg_;
+    }
+    kbegin(kMerge, 0.0, ms);
     const size_t merge_pend = pend_.size() - (ktiming() ? 1 : 0);
     if (a.nnz > 0)
-      launch(merge_chunks_kernel, dim3(blocks(cdiv(a.nnz, kMergeChunk), 8)), dim3(256), 0, st_,
+      launch(merge_chunks_kernel, dim3(blocks(cdiv(a.nnz, kMergeChunk), 8)), dim3(256), 0, ms,
              static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
              static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
              static_cast<const int*>(dcol), static_cast<const int*>(lb), static_cast<const int*>(mflag),
              static_cast<const double*>(newv),
              static_cast<const int*>(prefix), static_cast<const int*>(an.rp), an.col, an.val);
     if (n2 > 0)
-      launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, st_, n2, static_cast<const int*>(drow),
+      launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, ms, n2, static_cast<const int*>(drow),
              static_cast<const int*>(dcol), static_cast<const u64*>(ekey_s), static_cast<const int*>(lb),
              static_cast<const int*>(mflag), static_cast<const double*>(newv), static_cast<const int*>(prefix),
              static_cast<const int*>(drp), static_cast<const int*>(an.rp), an.col, an.val);
-    kend();
+    kend(ms);
+    if (merge_aside) STG_CUDA(cudaEventRecord(ev_mg_, st_mg_));
     // ---- validation outcome and sizes: read back here for the Laplacian
     // operators (their assembly needs nnz); the adjacency path folds this read
     // into the P-size sync below (nothing is committed before either)
@@ -1115,8 +1163,11 @@ class Session {
       if (ktiming())  // read old CSR + write new CSR (SURVEY 8(d) ingestion bytes, edits excluded)
         pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (n_old + 1) + 12.0 * an.nnz + 4.0 * (n_total + 1);
     };
+    // a Delta row too long for the counting path: redo on the sorting path
+    auto redo = [&]() { return !sort_path && hs_->err_edit == 0; };
     if (is_laplacian()) {
       STG_CUDA(cudaStreamSynchronize(st_));
+      if (redo()) return ingest(u, keep_delta, device_ptrs, true);
       check_validation();
     }
     // ---- the tracked operator's perturbation
@@ -1185,7 +1236,10 @@ class Session {
            static_cast<const int*>(pos), n_total, P, posmap_);
     STG_CUDA(cudaMemcpyAsync(&hs_->p, pos + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaStreamSynchronize(st_));
-    if (!is_laplacian()) check_validation();
+    if (!is_laplacian()) {
+      if (redo()) return ingest(u, keep_delta, device_ptrs, true);
+      check_validation();
+    }
     pt.p = hs_->p;
     pt.p_old = pt.p - S;
     pt.P = P;
@@ -1216,6 +1270,7 @@ class Session {
   }
 
   void commit_graph(const Pert& pt) {
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_mg_, 0));
     if (anext_ >= 0) {
       acur_ = anext_;
       anext_ = -1;

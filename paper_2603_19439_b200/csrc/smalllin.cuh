@@ -80,9 +80,9 @@ __device__ __forceinline__ void chol_diag_block(double* sm, double* invd, int w,
 }
 
 template <typename... A>
-__device__ __forceinline__ void chol_diag(int b, A... args) {
-  if (b == kCholNb) chol_diag_block<true>(args...);
-  else chol_diag_block<false>(args...);
+__device__ __forceinline__ void chol_diag(int b, A&&... args) {  // forwarded: fl is an out-parameter
+  if (b == kCholNb) chol_diag_block<true>(static_cast<A&&>(args)...);
+  else chol_diag_block<false>(static_cast<A&&>(args)...);
 }
 
 // Rows p..p+b-1 (diagonal block already factored, 1/R(t,t) in invd): columns

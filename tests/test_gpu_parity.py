@@ -240,3 +240,79 @@ def test_wide_sketch_takes_exact_paths():
         gpu.step(upd)
         orc.step(upd)
         check_state(gpu, orc, tag=f"wide sketch step {t}")
+
+
+def _ring(n, chords=0, seed=0):
+    rng = np.random.default_rng(seed)
+    e = {(i, (i + 1) % n) if i < (i + 1) % n else ((i + 1) % n, i) for i in range(n)}
+    while chords > 0:
+        i, j = sorted(rng.integers(0, n, 2).tolist())
+        if i != j and (i, j) not in e:
+            e.add((i, j))
+            chords -= 1
+    return po.from_edges(n, sorted(e))
+
+
+def test_hub_row_takes_the_sorting_path():
+    """A Delta row longer than the counting path's limit (4096 entries):
+    the ingestion re-runs on the radix-sort path; results stay bit-exact and
+    the next (ordinary) step is back on the sort-free path."""
+    a = _ring(5000, chords=300, seed=4)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest2", k=4)
+    rp, col, _ = gpu.csr(0)
+    nb0 = set(col[rp[0]:rp[1]].tolist())
+    hub = [(0, j, 1.0) for j in range(2, 4700) if j not in nb0]
+    assert len(hub) > 4096
+    upd = U(hub, [], 2, [(5000, 0, 1.0), (5001, 3, 2.0), (5000, 5001, 1.0)])
+    gpu.step(upd)
+    orc.step(upd)
+    check_state(gpu, orc, tag="hub step")
+    upd = U([(10, 20, 1.0)], [(0, 5)], 1, [(5002, 0, 1.0)])
+    gpu.step(upd)
+    orc.step(upd)
+    check_state(gpu, orc, tag="after hub")
+
+
+@pytest.mark.parametrize("hub", [False, True])
+def test_duplicate_orientations_and_lists(hub):
+    """Duplicates are unordered pairs across all three lists, on both Delta
+    assembly paths: the later edit is the one reported."""
+    from paper_2603_19439_b200 import TrackerError
+    a = _ring(5000, chords=50, seed=5)
+    nb1 = set(a.col[a.rowptr[1]:a.rowptr[2]].tolist())
+    extra = [(1, j, 1.0) for j in range(3, 4300) if j not in nb1] if hub else []
+    cases = [dict(added=extra + [(7, 40, 1.0), (40, 7, 2.0)]),
+             dict(added=extra + [(7, 40, 1.0)], removed=[(0, 1)], n_new=1, new_edges=[(40, 5000, 1.0), (7, 40, 1.0)]),
+             dict(added=extra, removed=[(0, 1), (1, 0)])]
+    for c in cases:
+        gpu, orc = pair(a.rowptr, a.col, a.val, kind="grest2", k=3)
+        u = U(**c)
+        with pytest.raises(po.OracleError) as eo:
+            orc.step(u)
+        with pytest.raises(TrackerError) as eg:
+            gpu.step(u)
+        assert str(eg.value) == str(eo.value) and eg.value.kind == eo.value.kind
+        assert gpu.info()["steps_taken"] == 0
+
+
+@pytest.mark.parametrize("kind", ["grest2", "grest3", "grest-rsvd"])
+@pytest.mark.parametrize("fan,n_new", [(1, 0), (8, 0), (8, 2), (98, 2)])
+def test_rank_deficient_candidates_are_dropped(kind, fan, n_new):
+    """Edits at one node make Delta X-bar rank <= 2: the reference drops the
+    dependent candidates (ortho.hpp:34-35); the basis width and the step
+    must follow it (the Cholesky's suspect/breakdown flags route the block to
+    the column-by-column replica)."""
+    n = 500
+    a = _ring(n, chords=30, seed=4)
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind=kind, k=4)
+    nb0 = set(a.col[a.rowptr[0]:a.rowptr[1]].tolist())
+    hub = [(0, j, 1.0) for j in range(2, 2 + fan) if j not in nb0]
+    upd = U(hub, [], n_new, [(n, 0, 1.0), (n + 1, 3, 2.0), (n, n + 1, 1.0)] if n_new else [])
+    zg = gpu.probe_basis(upd, kind, 0)
+    zo = orc.probe_basis(upd, kind, 0)
+    assert zg.shape == zo.shape
+    assert np.abs(zg.T @ zg - np.eye(zg.shape[1])).max() < 1e-12
+    assert sin_angle(zg, zo) < SIN_TOL
+    gpu.step(upd)
+    orc.step(upd)
+    check_state(gpu, orc, tag=f"{kind} fan {fan}")
