@@ -1,0 +1,79 @@
+"""Edge cases of the step against the CPU oracle (parity bar as elsewhere):
+isolated new nodes, removal-only batches, rank-1 sketches, hub rows on the
+Laplacian operators, k above the candidate count."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from harness import check_state, pair
+
+pytestmark = pytest.mark.gpu
+
+
+def U(*a, **k):
+    from paper_2603_19439_b200 import Update
+    return Update.make(*a, **k)
+
+
+def ring(n, chords=0, seed=0):
+    rng = np.random.default_rng(seed)
+    e = {tuple(sorted((i, (i + 1) % n))) for i in range(n)}
+    while chords > 0:
+        i, j = sorted(rng.integers(0, n, 2).tolist())
+        if i != j and (i, j) not in e:
+            e.add((i, j))
+            chords -= 1
+    return po.from_edges(n, sorted(e))
+
+
+def run(a, steps, kind="grest-rsvd", k=4, operator="adjacency", L=100, P=100):
+    gpu, orc = pair(a.rowptr, a.col, a.val, kind=kind, k=k, operator=operator, rsvd_l=L, rsvd_p=P, seed=7)
+    for t, upd in enumerate(steps):
+        orc.step(upd)
+        gpu.step(upd)
+        check_state(gpu, orc, laplacian=operator != "adjacency", tag=f"{kind}/{operator} step {t}")
+
+
+KINDS = ["iasc", "grest2", "grest3", "grest-rsvd"]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_isolated_new_nodes(kind):
+    """New nodes with no edges: zero Delta columns, dropped candidates."""
+    a = ring(300, 40, 1)
+    run(a, [U([], [], 3, []), U([(0, 150, 1.0)], [], 2, [(303, 5, 1.0), (304, 301, 1.0)])], kind=kind)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_removal_only(kind):
+    a = ring(300, 60, 2)
+    rp, col = a.rowptr, a.col
+    rem = [(i, int(col[rp[i]])) for i in range(0, 300, 7) if col[rp[i]] > i][:12]
+    run(a, [U([], rem, 0, [])], kind=kind)
+
+
+@pytest.mark.parametrize("L,P", [(4, 3), (8, 8)])
+def test_rank_one_sketch(L, P):
+    """Every new node attaches to node 0 only: Delta_2 has rank 1, the RSVD
+    sketch Y = Delta_2 Omega is rank 1 and its orthonormalization drops all
+    but one column."""
+    a = ring(400, 50, 3)
+    n = 400
+    S = 40
+    run(a, [U([], [], S, [(n + s, 0, 1.0) for s in range(S)])], kind="grest-rsvd", L=L, P=P)
+
+
+@pytest.mark.parametrize("operator", ["laplacian", "normalized-laplacian"])
+@pytest.mark.parametrize("kind", ["grest2", "grest-rsvd"])
+def test_hub_edits_on_laplacians(operator, kind):
+    a = ring(400, 50, 4)
+    nb0 = set(a.col[a.rowptr[0]:a.rowptr[1]].tolist())
+    hub = [(0, j, 1.0) for j in range(2, 60) if j not in nb0]
+    run(a, [U(hub, [], 2, [(400, 0, 1.0), (401, 7, 1.0)]), U([(3, 90, 2.0)], [(0, 2)], 0, [])],
+        kind=kind, operator=operator)
+
+
+def test_k_above_candidate_rank():
+    """k = 12 with a single edit: Delta X-bar has rank 2, ten candidates drop."""
+    a = ring(300, 80, 5)
+    run(a, [U([(10, 200, 1.0)], [], 0, [])], kind="grest2", k=12)
