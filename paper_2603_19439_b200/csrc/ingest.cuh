@@ -476,6 +476,175 @@ __global__ void __launch_bounds__(256) merge_chunks_kernel(const int* __restrict
   }
 }
 
+// Pass 2a, run form: between two rows of P every row keeps its length, so a
+// maximal run of untouched rows moves as one block by a constant shift
+// (new start - old start). Work is split along the merge path of (rows,
+// entries): warp w takes diagonal units [w kRunDiag, (w + 1) kRunDiag) of the
+// walk that visits each row's entries then its end, so a warp covers at most
+// kRunDiag rows plus entries (hub rows and long runs of tiny rows alike). Its
+// first row comes from chunk_rows_kernel (no search); it loads the metadata
+// of 32 rows at a time, copies each untouched run with a plain strided loop
+// (32-bit indices, four 32-entry windows in flight) and walks the rows of P
+// over their Delta entries (merge_p_walk).
+constexpr int kRunDiag = 1024;
+
+__device__ __forceinline__ void merge_copy_run(int a0, int a1, int shift, int lane, const int* __restrict__ acol,
+                                               const double* __restrict__ aval, int* __restrict__ ncol,
+                                               double* __restrict__ nval) {
+  for (int q = a0 + lane; q < a1; q += 128) {
+    int cv[4];
+    double vv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int qq = q + 32 * u;
+      cv[u] = qq < a1 ? acol[qq] : 0;
+      vv[u] = qq < a1 ? aval[qq] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int qq = q + 32 * u;
+      if (qq < a1) {
+        ncol[qq + shift] = cv[u];
+        nval[qq + shift] = vv[u];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void merge_p_walk(int jpos, int jend, int s, int o, int ds, int dn, int lane,
+                                             const int* __restrict__ acol, const double* __restrict__ aval,
+                                             const int* __restrict__ lb, const int* __restrict__ flag,
+                                             const double* __restrict__ newv, const int* __restrict__ prefix,
+                                             int* __restrict__ ncol, double* __restrict__ nval) {
+  const int p0 = prefix[ds];
+  int t0 = 0, hi = dn;  // first event at or after jpos
+  while (t0 < hi) {
+    const int mid = (t0 + hi) >> 1;
+    if (lb[ds + mid] < jpos) t0 = mid + 1; else hi = mid;
+  }
+  int S = prefix[ds + t0] - p0;  // size change of the events before t0
+  int cur = jpos;
+  for (int tb = t0; tb < dn; tb += 32) {
+    int lbv = 0x7fffffff, fl = 0, pn = 0;
+    double nv = 0.0;
+    if (tb + lane < dn) {
+      lbv = lb[ds + tb + lane];
+      fl = flag[ds + tb + lane];
+      nv = newv[ds + tb + lane];
+      pn = prefix[ds + tb + lane + 1] - p0;
+    }
+    const int cnt = min(32, dn - tb);
+    for (int k = 0; k < cnt; ++k) {
+      const int target = __shfl_sync(0xffffffffu, lbv, k);
+      const int f = __shfl_sync(0xffffffffu, fl, k);
+      const double v = __shfl_sync(0xffffffffu, nv, k);
+      const int snext = __shfl_sync(0xffffffffu, pn, k);
+      const int stop = min(target, jend);
+      if (stop > cur) merge_copy_run(s + cur, s + stop, o - s + S, lane, acol, aval, ncol, nval);
+      if (target >= jend) return;
+      if (f & 1) {  // the event's own old entry: updated in place, or pruned
+        if (!(f & 2) && lane == 0 && target >= jpos) {
+          ncol[o + target + S] = acol[s + target];
+          nval[o + target + S] = v;
+        }
+        cur = max(cur, target + 1);
+      } else {
+        cur = max(cur, target);
+      }
+      S = snext;
+    }
+  }
+  if (jend > cur) merge_copy_run(s + cur, s + jend, o - s + S, lane, acol, aval, ncol, nval);
+}
+
+__global__ void chunk_rows_kernel(const int* arp, int n_old, int* map) {
+  const int r = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n_old) return;
+  const i64 d0 = static_cast<i64>(r) + arp[r], d1 = static_cast<i64>(r) + arp[r + 1];  // entries, then the row end
+  for (i64 k = (d0 + kRunDiag - 1) / kRunDiag; k * kRunDiag <= d1; ++k) map[k] = r;
+}
+
+__device__ __forceinline__ int run_entry_start(const int* arp, const int* map, int w) {
+  const int r = map[w];
+  return static_cast<int>(min(static_cast<i64>(w) * kRunDiag - r, static_cast<i64>(arp[r + 1])));
+}
+
+__global__ void __launch_bounds__(256) merge_runs_kernel(const int* __restrict__ arp, const int* __restrict__ acol,
+                                                         const double* __restrict__ aval, int n_old, int nnz,
+                                                         const int* __restrict__ map, const int* __restrict__ mark,
+                                                         int stamp, const int* __restrict__ drp,
+                                                         const int* __restrict__ dcol, const int* __restrict__ lb,
+                                                         const int* __restrict__ flag,
+                                                         const double* __restrict__ newv,
+                                                         const int* __restrict__ prefix, const int* __restrict__ nrp,
+                                                         int* __restrict__ ncol, double* __restrict__ nval, int mode) {
+  const int w = static_cast<int>((static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int nw = static_cast<int>((static_cast<i64>(n_old) + nnz + kRunDiag - 1) / kRunDiag);
+  if (w >= nw) return;
+  const int e0 = run_entry_start(arp, map, w);
+  const int e1 = w + 1 < nw ? run_entry_start(arp, map, w + 1) : nnz;
+  if (e0 >= e1) return;
+  int r = map[w], pos = e0;
+  while (pos < e1) {
+    const int rr = r + lane;
+    const bool in = rr < n_old;
+    const int rs = in ? arp[rr] : nnz;
+    const int re = in ? arp[rr + 1] : nnz;
+    const int o = in ? nrp[rr] : 0;
+    const bool pm = in && mark[rr] == stamp;
+    const int gend = min(__shfl_sync(0xffffffffu, re, 31), e1);
+    const bool live = in && re > pos && rs < gend;
+    // untouched runs: maximal groups of consecutive live lanes without P
+    unsigned todo = __ballot_sync(0xffffffffu, live && !pm && (mode & 1));
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      const unsigned tail = ~(todo >> l);
+      const int len = tail ? __ffs(tail) - 1 : 32 - l;
+      todo &= len >= 32 ? 0u : ~(((1u << len) - 1u) << l);
+      const int rs_l = __shfl_sync(0xffffffffu, rs, l);
+      const int shift = __shfl_sync(0xffffffffu, o, l) - rs_l;
+      const int sb = max(pos, rs_l);
+      const int se = min(gend, __shfl_sync(0xffffffffu, re, l + len - 1));
+      for (int q = sb + lane; q < se; q += 128) {
+        int cv[4];
+        double vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = q + 32 * u;
+          cv[u] = qq < se ? acol[qq] : 0;
+          vv[u] = qq < se ? aval[qq] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = q + 32 * u;
+          if (qq < se) {
+            ncol[qq + shift] = cv[u];
+            nval[qq + shift] = vv[u];
+          }
+        }
+      }
+    }
+    // rows of P overlapping [pos, gend)
+    unsigned ptodo = __ballot_sync(0xffffffffu, live && pm && (mode & 2));
+    while (ptodo) {
+      const int l = __ffs(ptodo) - 1;
+      ptodo &= ptodo - 1;
+      const int s_l = __shfl_sync(0xffffffffu, rs, l);
+      const int e_l = __shfl_sync(0xffffffffu, re, l);
+      const int o_l = __shfl_sync(0xffffffffu, o, l);
+      const int row = r + l;
+      const int ds = drp[row], dn = drp[row + 1] - ds;
+      merge_p_walk(max(pos, s_l) - s_l, min(e_l, gend) - s_l, s_l, o_l, ds, dn, lane, acol, aval, lb, flag, newv,
+                   prefix, ncol, nval);
+    }
+    if (gend >= e1) break;
+    const unsigned before = __ballot_sync(0xffffffffu, rs <= gend);
+    r += 31 - __clz(before);
+    pos = gend;
+  }
+}
+
 // Pass 2b: Delta entries with no stored counterpart in A.
 __global__ void merge_insert_kernel(i64 n2, const int* drow, const int* dcol, const u64* skey, const int* lb,
                                     const int* flag, const double* newv, const int* prefix, const int* drp,

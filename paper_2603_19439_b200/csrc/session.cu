@@ -694,7 +694,8 @@ class Session {
     a.mask_val = mask_val;
     if (narrow) a.tiles_i = a.tiles_j = 1;
     const int ntiles = narrow ? 1 : (sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j);
-    const i64 target = 148 * (layout == 0 ? 24 : 4);  // square tiles: ~8 short waves keep the tail of unequal tile pairs small
+    static const int env_waves = getenv("STG_GRAM_WAVES") ? atoi(getenv("STG_GRAM_WAVES")) : 0;  // development scans
+    const i64 target = 148 * (env_waves > 0 ? env_waves : layout == 0 ? 24 : 4);  // square tiles: ~8 short waves keep the tail of unequal tile pairs small
     const i64 rows_min = narrow ? 256 : 128;
     i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
     splits = std::min<i64>(splits, 65535);
@@ -805,11 +806,72 @@ class Session {
 
   // CSR x dense with compulsory-traffic accounting: 12 B per nonzero, the row
   // pointers, and one read of each referenced dense row plus the output rows.
+  // Segment plans (spmm.cuh) of the CSR row ranges multiplied in this step,
+  // keyed by (rowptr, row_off, rows); rebuilt after every ingestion.
+  struct PlanEntry {
+    const int* rowptr;
+    i64 row_off, rows, nnz;
+    int epoch;
+    SpmmPlan pl;
+    i64 vmax, split_max, smax;
+    std::string tag;
+  };
+  std::vector<PlanEntry> plans_;
+  int plan_epoch_ = 0;
+  const int merge_mode_ = getenv("STG_MERGE_MODE") ? atoi(getenv("STG_MERGE_MODE")) : 3;  // development A/B
+
+  PlanEntry& spmm_plan(const SpmmArgs& a, i64 nnz) {
+    for (auto& e : plans_)
+      if (e.epoch == plan_epoch_ && e.rowptr == a.rowptr && e.row_off == a.row_off && e.rows == a.rows) return e;
+    PlanEntry* e = nullptr;
+    for (auto& q : plans_)
+      if (q.epoch != plan_epoch_) { e = &q; break; }
+    if (!e) {
+      plans_.emplace_back();
+      e = &plans_.back();
+      e->tag = "sp" + std::to_string(plans_.size() - 1) + "_";
+    }
+    e->rowptr = a.rowptr;
+    e->row_off = a.row_off;
+    e->rows = a.rows;
+    e->nnz = nnz;
+    e->epoch = plan_epoch_;
+    e->vmax = a.rows + cdiv(nnz, kSegNnz);
+    e->split_max = std::min<i64>(a.rows, nnz / (kSegNnz + 1));
+    e->smax = 2 * cdiv(nnz, kSegNnz) + 1;
+    int* cnt = arena_.get<int>(e->tag + "cnt", a.rows + 1);
+    int* cnt2 = arena_.get<int>(e->tag + "cnt2", a.rows + 1);
+    int* vstart = arena_.get<int>(e->tag + "vstart", a.rows + 1);
+    int* sstart = arena_.get<int>(e->tag + "sstart", a.rows + 1);
+    int* vrow = arena_.get<int>(e->tag + "vrow", e->vmax);
+    int* split_rows = arena_.get<int>(e->tag + "split", std::max<i64>(e->split_max, 1));
+    int* nsplit = arena_.get<int>(e->tag + "nsplit", 1);
+    launch(seg_count_kernel, dim3(blocks(a.rows + 1)), dim3(256), 0, st_, a.rowptr, a.row_off, a.rows, cnt, cnt2);
+    scan_int(cnt, vstart, a.rows + 1);
+    scan_int(cnt2, sstart, a.rows + 1);
+    STG_CUDA(cudaMemsetAsync(nsplit, 0, sizeof(int), st_));
+    launch(seg_fill_kernel, dim3(blocks(a.rows)), dim3(256), 0, st_, static_cast<const int*>(vstart), a.rows, vrow,
+           split_rows, nsplit);
+    e->pl = SpmmPlan{vrow, vstart, sstart, split_rows, nsplit, nullptr, 0};
+    return *e;
+  }
+
   void do_spmm(const SpmmArgs& a, i64 nnz, i64 distinct_cols, int cls = kSpmm) {
+    if (a.rows <= 0 || a.m <= 0) return;
+    PlanEntry& pe = spmm_plan(a, nnz);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "spmm %lld rows m=%d", a.rows, a.m);
     kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
-    spmm(a, st_);
-    launches += cdiv(a.m, 256);
+    SpmmPlan pl = pe.pl;
+    pl.lds = static_cast<int>(round_up(std::min(a.m, 256), 2));
+    pl.scratch = arena_.get<double>("spmm_scratch", pe.smax * pl.lds);
+    for (int c0 = 0; c0 < a.m; c0 += 256) {  // dense blocks wider than 256 columns: 256-column slabs
+      SpmmArgs b = a;
+      b.X = a.X + c0;
+      b.Y = a.Y + c0;
+      b.m = std::min(a.m - c0, 256);
+      spmm_launch(b, pl, pe.vmax, pe.split_max, st_);
+      launches += pe.split_max > 0 ? 2 : 1;
+    }
     kend();
   }
 
@@ -975,6 +1037,7 @@ class Session {
     ensure_node_capacity(n_total);
     ++stamp_;
     if (stamp_ == 0x7fffffff) stamp_ = 1;
+    ++plan_epoch_;  // the Delta CSRs are rebuilt below
     Pert pt;
     pt.n_old = n_old;
     pt.S = S;
@@ -1131,13 +1194,19 @@ class Session {
     }
     kbegin(kMerge, 0.0, ms);
     const size_t merge_pend = pend_.size() - (ktiming() ? 1 : 0);
-    if (a.nnz > 0)
-      launch(merge_chunks_kernel, dim3(blocks(cdiv(a.nnz, kMergeChunk), 8)), dim3(256), 0, ms,
-             static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val), n_old,
+    if (a.nnz > 0) {
+      const i64 nwarp = cdiv(n_old + a.nnz, kRunDiag);
+      int* cmap = arena_.get<int>("m_chunkmap", nwarp);
+      launch(chunk_rows_kernel, dim3(blocks(n_old)), dim3(256), 0, ms, static_cast<const int*>(a.rp),
+             static_cast<int>(n_old), cmap);
+      launch(merge_runs_kernel, dim3(blocks(nwarp, 8)), dim3(256), 0, ms,
+             static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val),
+             static_cast<int>(n_old), static_cast<int>(a.nnz), static_cast<const int*>(cmap),
              static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
              static_cast<const int*>(dcol), static_cast<const int*>(lb), static_cast<const int*>(mflag),
-             static_cast<const double*>(newv),
-             static_cast<const int*>(prefix), static_cast<const int*>(an.rp), an.col, an.val);
+             static_cast<const double*>(newv), static_cast<const int*>(prefix), static_cast<const int*>(an.rp),
+             an.col, an.val, merge_mode_);
+    }
     if (n2 > 0)
       launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, ms, n2, static_cast<const int*>(drow),
              static_cast<const int*>(dcol), static_cast<const u64*>(ekey_s), static_cast<const int*>(lb),

@@ -41,3 +41,15 @@ if "small" in cases:
               f"eig(want 32): {bench(4, 1, w, 32, iters=3)*1e3:8.1f} us")
 if cases and cases[0] == "one":  # one launch for ncu: one <which> N m1 m2 flag
     bench(int(cases[1]), int(cases[2]), int(cases[3]), int(cases[4]), int(cases[5]), iters=1)
+if cases and cases[0] == "stepshapes":  # the cfg3 step's Gram/GEMM shapes at p ~ 109K rows
+    N = 109268
+    for (a, b, sym) in [(200, 200, 1), (164, 100, 0), (64, 200, 0), (100, 100, 1), (64, 100, 0), (32, 200, 0),
+                        (64, 64, 1)]:
+        t = bench(0, N, a, b, sym)
+        fl = N * a * (a + 1) if sym else 2 * N * a * b
+        print(f"gram N={N} {a}x{b} sym={sym}: {t*1e3:8.1f} us  {fl/t/1e9:6.2f} TF")
+    for (a, b, tri) in [(200, 200, 1), (200, 100, 0), (64, 200, 0), (100, 100, 1), (64, 100, 0), (32, 200, 0),
+                        (164, 32, 0)]:
+        t = bench(1, N, a, b, tri)
+        fl = N * a * (a + 1) if tri else 2 * N * a * b
+        print(f"nn   N={N} {a}x{b} tri={tri}: {t*1e3:8.1f} us  {fl/t/1e9:6.2f} TF")
