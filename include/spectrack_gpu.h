@@ -133,6 +133,52 @@ st_status st_probe_basis(st_session* s, const st_update* upd, int32_t basis_kind
 st_status st_probe_rr(st_session* s, const st_update* upd, const double* z, int64_t rows, int64_t cols, int64_t ldz,
                       double* values, double* vectors, int64_t ldv);
 
+/* ---- Row-sharded sessions (one session per GPU of a box).
+ *
+ * The collectives a sharded session issues, supplied by the caller (NCCL in
+ * production, e.g. ncclAllReduce / ncclAllGather on the given stream; any
+ * transport in tests). Buffers are device pointers; `stream` is the session's
+ * cudaStream_t and the operation must be ordered on it (enqueued on it, or
+ * completed before returning). Results must be bitwise identical on every
+ * rank. A callback returns 0 on success. */
+typedef struct {
+  int32_t rank;
+  int32_t size;
+  void* ctx;
+  /* in-place elementwise sum over ranks of `count` doubles */
+  int32_t (*allreduce_sum_f64)(void* ctx, double* buf, int64_t count, void* stream);
+  /* recv[r * bytes .. (r + 1) * bytes) = send of rank r, for every rank r */
+  int32_t (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes, void* stream);
+} st_comm;
+
+/* Sharded counterpart of st_create. Every rank passes the same cfg and
+ * n_global and its own contiguous block [row_lo, row_hi) of the initial nodes
+ * (the blocks must tile [0, n_global) in rank order): the CSR rows of that
+ * block (rowptr row_hi - row_lo + 1 entries, global column ids) and the same
+ * rows of the initial eigenvectors (column-major, leading dimension ld), plus
+ * the k eigenvalues. Appended nodes keep their global ids n_old + j and are
+ * dealt to the ranks round-robin in chunks of `chunk` ids. Every rank then
+ * calls st_step / st_step_device with the SAME update batch, in the same
+ * order; st_get_embedding returns the owned rows (st_shard_rows gives their
+ * global ids, ascending), st_get_csr(0) the owned rows of A (global columns),
+ * st_get_csr(2) the full perturbation. Adjacency operator, k <= 64; the probe
+ * calls are not available on sharded sessions. */
+st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n_global, int64_t row_lo,
+                            int64_t row_hi, int64_t chunk, const int32_t* rowptr, const int32_t* colidx,
+                            const double* values_csr, const double* eig_values, const double* eig_vectors,
+                            int64_t ld, st_session** out);
+
+/* Owned rows of a (sharded) session: *n_local, and their global ids when
+ * global_ids is not NULL. An unsharded session owns every row. */
+st_status st_shard_rows(const st_session* s, int64_t* n_local, int64_t* global_ids);
+
+/* Host-only ownership map (no device work): the global ids, ascending, that
+ * rank `rank` owns when the graph has n_total nodes, for initial bounds
+ * bounds[0..size] and the given chunk. Returns the row count; writes at most
+ * cap ids. */
+int64_t st_shard_layout(int32_t size, const int64_t* bounds, int64_t chunk, int32_t rank, int64_t n_total,
+                        int64_t* global_ids, int64_t cap);
+
 /* Message of the last failed call on this session (or of st_create when s is NULL). */
 const char* st_last_error(const st_session* s);
 

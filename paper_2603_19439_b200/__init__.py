@@ -90,8 +90,15 @@ def lib():
         L.st_sym_eig_dense.restype = C.c_int
         L.st_gaussian_matrix.argtypes = [C.c_int32, C.c_uint64, I64, I64, DP]
         L.st_gaussian_matrix.restype = C.c_int
+        from . import shard as _shard
+
+        L.st_create_sharded.argtypes = [C.POINTER(StConfig), C.POINTER(_shard.StComm), I64, I64, I64, I64, I32P,
+                                        I32P, DP, DP, DP, I64, C.POINTER(C.c_void_p)]
+        L.st_shard_rows.argtypes = [C.c_void_p, I64P, I64P]
+        L.st_shard_layout.argtypes = [C.c_int32, I64P, I64, C.c_int32, I64, I64P, I64]
+        L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
-                  "st_probe_basis", "st_probe_rr"):
+                  "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib

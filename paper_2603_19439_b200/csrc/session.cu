@@ -31,6 +31,7 @@
 #include "eigsolve.cuh"
 #include "ingest.cuh"
 #include "rng.cuh"
+#include "shard.cuh"
 #include "smalllin.cuh"
 #include "spmm.cuh"
 #include "stepk.cuh"
@@ -158,6 +159,18 @@ struct Pert {
   const int* posmap = nullptr;
   const int* mark = nullptr;  // rows of P: mark[r] == stamp
   int stamp = 0;
+  // Row-sharded sessions (shard.cuh) keep the rows of P they own: p, p_old
+  // and S_loc count owned rows; G = rows entering a Gram (the k coordinate
+  // rows R_c a are counted by rank 0 only); X rows by local index.
+  i64 G = 0;                 // p + k (unsharded)
+  i64 S_loc = 0;             // appended rows in P here (= S unsharded)
+  i64 x_old = 0, x_total = 0;  // rows of the X storage before / after the step
+  i64 pmax = 0;              // halo rows per rank (sharded)
+  const int* Ploc = nullptr;   // X storage row of each row of P (= P unsharded)
+  const int* Pglob = nullptr;  // global id of each row of P (= P unsharded)
+  const double* gval = nullptr;  // values of the global Delta CSR (grp/gcol)
+  const int* scol = nullptr;  // sketch SpMM columns: only cols >= scol_lo, X row = col - scol_lo
+  int scol_lo = 0;
   bool empty() const { return S == 0 && nnz == 0; }
 };
 
@@ -188,8 +201,13 @@ class Session {
   static constexpr int kClasses = 12;
   KStat kstats[kClasses];
 
+  struct ShardInit {
+    st_comm comm;
+    i64 n_global, lo, hi, chunk;
+  };
+
   Session(const st_config& c, i64 n0, const int* rp, const int* col, const double* val, const double* ev,
-          const double* evec, i64 ld)
+          const double* evec, i64 ld, const ShardInit* shard = nullptr)
       : cfg(c) {
     STG_CUDA(cudaSetDevice(cfg.device));
     {  // priorities: the eigensolve's CTAs take SMs ahead of the wide kernels it
@@ -237,6 +255,10 @@ class Session {
     d_scal_ = arena_.get<u64>("scalars", 32);
     k = cfg.k;
     n = n0;
+    if (shard) {  // n0 = rows of this rank's block; n = the global node count
+      init_shard(*shard);
+      n = shard->n_global;
+    }
     if (k < 1 || k > n) throw InvalidArgument("tracker_init: k must satisfy 1 <= k <= n");
     if (cfg.kind < ST_IASC || cfg.kind > ST_GREST_RSVD)
       throw InvalidArgument("st_create: tracker kind outside the G-REST path");
@@ -252,7 +274,8 @@ class Session {
     STG_CUDA(cudaMemcpyAsync(A_[0].col, col, sizeof(int) * std::max<i64>(nnz, 1), cudaMemcpyHostToDevice, st_));
     STG_CUDA(cudaMemcpyAsync(A_[0].val, val, sizeof(double) * std::max<i64>(nnz, 1), cudaMemcpyHostToDevice, st_));
     acur_ = 0;
-    ensure_node_capacity(n0);
+    ensure_node_capacity(n, n0);
+    nloc_ = n0;
     // eigenpairs: column-major host -> row-major device
     values.assign(ev, ev + k);
     std::vector<double> xr(static_cast<size_t>(n0 * k));
@@ -290,6 +313,71 @@ class Session {
   const DevCsr& A() const { return A_[acur_]; }
   const DevCsr& T() const { return T_[tcur_]; }
   i64 nnz_delta() const { return last_delta_nnz_; }
+
+  // ---------------------------------------------------------------- sharding
+  bool sh_ = false;
+  st_comm comm_{};
+  ShardMap map_;             // device bounds (kernels)
+  std::vector<i64> bounds_;  // host copy
+  i64 nloc_ = 0;             // rows stored here (= n unsharded)
+  int* mark_dl_ = nullptr;   // Delta-row marks by local row (sharded merge)
+
+  void init_shard(const ShardInit& si) {
+    if (si.comm.size < 1 || si.comm.rank < 0 || si.comm.rank >= si.comm.size || !si.comm.allreduce_sum_f64 ||
+        !si.comm.allgather)
+      throw InvalidArgument("st_create_sharded: invalid communicator");
+    if (si.chunk < 1) throw InvalidArgument("st_create_sharded: chunk must be positive");
+    if (si.lo < 0 || si.hi < si.lo || si.hi > si.n_global)
+      throw InvalidArgument("st_create_sharded: row block outside [0, n_global)");
+    if (cfg.op != ST_ADJACENCY) throw InvalidArgument("st_create_sharded: sharded sessions track the adjacency operator");
+    if (cfg.k > 64) throw InvalidArgument("st_create_sharded: sharded sessions support k <= 64");
+    sh_ = true;
+    comm_ = si.comm;
+    const int R = comm_.size;
+    std::vector<u64> lohi = allgather_u64({static_cast<u64>(si.lo), static_cast<u64>(si.hi)});
+    bounds_.assign(static_cast<size_t>(R) + 1, 0);
+    for (int r = 0; r < R; ++r) {
+      const i64 lo = static_cast<i64>(lohi[2 * r]), hi = static_cast<i64>(lohi[2 * r + 1]);
+      if (lo != bounds_[r]) throw InvalidArgument("st_create_sharded: row blocks must tile [0, n_global) in rank order");
+      bounds_[r + 1] = hi;
+    }
+    if (bounds_[R] != si.n_global) throw InvalidArgument("st_create_sharded: row blocks must tile [0, n_global) in rank order");
+    i64* db = arena_.get<i64>("shard_bounds", R + 1);
+    STG_CUDA(cudaMemcpy(db, bounds_.data(), sizeof(i64) * (R + 1), cudaMemcpyHostToDevice));
+    map_.n0 = si.n_global;
+    map_.chunk = si.chunk;
+    map_.size = R;
+    map_.rank = comm_.rank;
+    map_.bounds = db;
+    map_.own0 = si.hi - si.lo;
+    map_.lo = si.lo;
+  }
+
+  ShardMap host_map() const {
+    ShardMap m = map_;
+    m.bounds = bounds_.data();
+    return m;
+  }
+  i64 rows_at(int r, i64 n_total) const { return sm_rows(map_, r, n_total, bounds_.data()); }
+
+  void allreduce(double* buf, i64 count) {
+    if (count <= 0) return;
+    if (comm_.allreduce_sum_f64(comm_.ctx, buf, count, st_) != 0) throw RuntimeError("st_comm: allreduce failed");
+  }
+  void allgather(const void* send, void* recv, i64 bytes) {
+    if (comm_.allgather(comm_.ctx, send, recv, bytes, st_) != 0) throw RuntimeError("st_comm: allgather failed");
+  }
+  // small host values of every rank (rank-major), through device staging
+  std::vector<u64> allgather_u64(const std::vector<u64>& mine) {
+    const i64 m = static_cast<i64>(mine.size());
+    u64* d = arena_.get<u64>("ag_u64", m * (comm_.size + 1));
+    STG_CUDA(cudaMemcpyAsync(d, mine.data(), sizeof(u64) * m, cudaMemcpyHostToDevice, st_));
+    allgather(d, d + m, sizeof(u64) * m);
+    std::vector<u64> all(static_cast<size_t>(m * comm_.size));
+    STG_CUDA(cudaMemcpyAsync(all.data(), d + m, sizeof(u64) * m * comm_.size, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    return all;
+  }
 
   // ---------------------------------------------------------------- public ops
   void step(const st_update& u, bool device_ptrs = false) {
@@ -460,11 +548,23 @@ class Session {
       for (i64 i = 0; i < rows; ++i) out[c * rows + i] = xr[static_cast<size_t>(i * k + c)];
   }
 
+  // values and the stored rows of X (all rows, or the owned rows of a shard)
   void get_embedding(double* vals, double* vecs, i64 ld) {
     std::memcpy(vals, values.data(), sizeof(double) * k);
-    std::vector<double> x(static_cast<size_t>(n * k));
-    copy_x_colmajor(x.data(), n);
-    for (i64 c = 0; c < k; ++c) std::memcpy(vecs + c * ld, x.data() + c * n, sizeof(double) * n);
+    const i64 rows = nloc_;
+    std::vector<double> x(static_cast<size_t>(rows * k));
+    copy_x_colmajor(x.data(), rows);
+    for (i64 c = 0; c < k; ++c) std::memcpy(vecs + c * ld, x.data() + c * rows, sizeof(double) * rows);
+  }
+
+  i64 local_rows() const { return nloc_; }
+  void local_ids(i64* ids) const {
+    if (!sh_) {
+      for (i64 i = 0; i < nloc_; ++i) ids[i] = i;
+      return;
+    }
+    const ShardMap m = host_map();
+    for (i64 l = 0; l < nloc_; ++l) ids[l] = sm_global(m, l);
   }
 
   void get_csr(int which, int* rp, int* col, double* val) {
@@ -650,17 +750,28 @@ class Session {
     return m;
   }
 
-  void ensure_node_capacity(i64 need) {
-    if (need <= nodecap_ && X_) return;
-    const i64 cap = std::max<i64>(need + need / 4, 1024);
-    double* nx = nullptr;
-    STG_CUDA(cudaMalloc(&nx, sizeof(double) * cap * ldx()));
-    if (X_) {
-      STG_CUDA(cudaMemcpyAsync(nx, X_, sizeof(double) * nodecap_ * ldx(), cudaMemcpyDeviceToDevice, st_));
-      STG_CUDA(cudaStreamSynchronize(st_));
-      STG_CUDA(cudaFree(X_));
+  // need: global node count (marks, posmap); need_x: rows of the X storage
+  // (the owned rows of a sharded session).
+  void ensure_node_capacity(i64 need, i64 need_x = -1) {
+    if (need_x < 0) need_x = need;
+    if (need_x > xcap_ || !X_) {
+      const i64 cap = std::max<i64>(need_x + need_x / 4, 1024);
+      double* nx = nullptr;
+      STG_CUDA(cudaMalloc(&nx, sizeof(double) * cap * ldx()));
+      if (X_) {
+        STG_CUDA(cudaMemcpyAsync(nx, X_, sizeof(double) * xcap_ * ldx(), cudaMemcpyDeviceToDevice, st_));
+        STG_CUDA(cudaStreamSynchronize(st_));
+        STG_CUDA(cudaFree(X_));
+      }
+      X_ = nx;
+      if (sh_) {
+        mark_dl_ = arena_.get<int>("mark_dl_" + std::to_string(cap), cap);
+        STG_CUDA(cudaMemsetAsync(mark_dl_, 0xff, sizeof(int) * cap, st_));
+      }
+      xcap_ = cap;
     }
-    X_ = nx;
+    if (need <= nodecap_) return;
+    const i64 cap = std::max<i64>(need + need / 4, 1024);
     // fresh mark arrays start at -1 (stamps are per step and always >= 1)
     mark_delta_ = arena_.get<int>("mark_delta_" + std::to_string(cap), cap);
     mark_p_ = arena_.get<int>("mark_p_" + std::to_string(cap), cap);
@@ -745,6 +856,43 @@ class Session {
            static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
            static_cast<int>(m2p), a.sym, out, ldo, alpha);
     kend();
+  }
+
+  // Gram over rows partitioned across the ranks of a sharded session: local
+  // split-K partial, allreduce, copy out (symmetric results re-mirrored).
+  void pgram(const double* A, int lda, const double* B, int ldb, i64 rows, int m1, int m2, bool sym, double* out,
+             int ldo) {
+    if (!sh_) {
+      gram(A, lda, B, ldb, rows, m1, m2, sym, out, ldo);
+      return;
+    }
+    if (m1 <= 0 || m2 <= 0) return;
+    const i64 mm = static_cast<i64>(m1) * m2;
+    double* tmp = arena_.get<double>("pg_tmp", mm);
+    if (rows > 0) gram(A, lda, B, ldb, rows, m1, m2, sym, tmp, m2);
+    else STG_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * mm, st_));
+    allreduce(tmp, mm);
+    launch(gram_out_kernel, dim3(blocks(mm)), dim3(256), 0, st_, static_cast<const double*>(tmp), m1, m2, sym ? 1 : 0,
+           out, ldo);
+  }
+
+  // Dense SpMM operand over the rows of P: the stacked block itself, or in a
+  // sharded session the halo of every rank's owned rows (rank-major, pmax
+  // rows per rank; the compressed columns are positions in it).
+  const double* halo(const Pert& pt, const double* X, int ldx, int m, int* ld_out) {
+    if (!sh_) {
+      *ld_out = ldx;
+      return X;
+    }
+    const int ldh = ld_for(m);
+    const i64 rows = std::max<i64>(pt.pmax, 1);
+    double* send = arena_.get<double>("halo_send", rows * ldh);
+    double* recv = arena_.get<double>("halo_recv", rows * ldh * comm_.size);
+    if (pt.p > 0)
+      launch(copy2d_kernel, dim3(blocks(pt.p * m)), dim3(256), 0, st_, X, ldx, send, ldh, pt.p, m);
+    allgather(send, recv, static_cast<i64>(sizeof(double)) * rows * ldh);
+    *ld_out = ldh;
+    return recv;
   }
 
   void nn(const double* A, int lda, i64 rows, int m1, const double* C, int ldc, int m2, double* Out, int ldo,
@@ -1025,6 +1173,67 @@ class Session {
     cub::DeviceScan::ExclusiveSum(t, tmp, in, out, static_cast<int>(count), st_);
   }
 
+  // A_next = pad(A) + Delta (graph.cpp:102-115) into slot `slot`: per-entry
+  // classification and checks, row pointers, then the entry copy (on the
+  // merge side stream when `merge_aside`). Rows are those of `a` (n_old) plus
+  // appended rows up to n_total; keys are (row << kb | col), sorted.
+  DevCsr merge_launch(const DevCsr& a, i64 n_old, i64 n_total, const u64* ekey_s, const double* eval_s, i64 n2,
+                      const int* drow, const int* dcol, const int* drp, const int* mark, int kb, int slot,
+                      bool merge_aside, u64* err_apply, size_t* merge_pend) {
+    int* lb = arena_.get<int>("m_lb", n2);
+    int* mflag = arena_.get<int>("m_flag", n2);
+    double* newv = arena_.get<double>("m_newv", n2);
+    int* contrib = arena_.get<int>("m_contrib", n2 + 1);
+    int* prefix = arena_.get<int>("m_prefix", n2 + 1);
+    int* ncnt = arena_.get<int>("m_ncnt", n_total + 1);
+    const std::string aname = "A" + std::to_string(slot);
+    DevCsr an;
+    an.n = n_total;
+    an.rp = arena_.get<int>(aname + ".rp", n_total + 1);
+    an.col = arena_.get<int>(aname + ".col", a.nnz + n2);
+    an.val = arena_.get<double>(aname + ".val", a.nnz + n2);
+    launch(row_len_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(a.rp), n_old, n_total,
+           ncnt);
+    STG_CUDA(cudaMemsetAsync(contrib, 0, sizeof(int) * (n2 + 1), st_));
+    if (n2 > 0)
+      launch(merge_classify_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s),
+             static_cast<const double*>(eval_s), n2, static_cast<const int*>(a.rp), static_cast<const int*>(a.col),
+             static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply, kb);
+    scan_int(ncnt, an.rp, n_total + 1);
+    scan_int(contrib, prefix, n2 + 1);
+    // row pointers, counts and the apply checks above stay on st_ (the
+    // validation read below needs them); the entry copy may run aside
+    cudaStream_t ms = st_;
+    if (merge_aside) {
+      STG_CUDA(cudaEventRecord(ev_mg_fork_, st_));
+      STG_CUDA(cudaStreamWaitEvent(st_mg_, ev_mg_fork_, 0));
+      ms = st_mg_;
+    }
+    kbegin(kMerge, 0.0, ms);
+    *merge_pend = pend_.size() - (ktiming() ? 1 : 0);
+    if (a.nnz > 0) {
+      const i64 nwarp = cdiv(n_old + a.nnz, kRunDiag);
+      int* cmap = arena_.get<int>("m_chunkmap", nwarp);
+      launch(chunk_rows_kernel, dim3(blocks(n_old)), dim3(256), 0, ms, static_cast<const int*>(a.rp),
+             static_cast<int>(n_old), cmap);
+      launch(merge_runs_kernel, dim3(blocks(nwarp, 8)), dim3(256), 0, ms,
+             static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val),
+             static_cast<int>(n_old), static_cast<int>(a.nnz), static_cast<const int*>(cmap),
+             static_cast<const int*>(mark), stamp_, static_cast<const int*>(drp),
+             static_cast<const int*>(dcol), static_cast<const int*>(lb), static_cast<const int*>(mflag),
+             static_cast<const double*>(newv), static_cast<const int*>(prefix), static_cast<const int*>(an.rp),
+             an.col, an.val, merge_mode_);
+    }
+    if (n2 > 0)
+      launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, ms, n2, static_cast<const int*>(drow),
+             static_cast<const int*>(dcol), static_cast<const u64*>(ekey_s), static_cast<const int*>(lb),
+             static_cast<const int*>(mflag), static_cast<const double*>(newv), static_cast<const int*>(prefix),
+             static_cast<const int*>(drp), static_cast<const int*>(an.rp), an.col, an.val);
+    kend(ms);
+    if (merge_aside) STG_CUDA(cudaEventRecord(ev_mg_, st_mg_));
+    return an;
+  }
+
   // ---------------------------------------------------------------- ingestion
   // Validation, Delta, A_next (and T_next, Delta_T), P. Nothing committed.
   Pert ingest(const st_update& u, bool keep_delta, bool device_ptrs = false, bool sort_path = false) {
@@ -1034,7 +1243,8 @@ class Session {
     if (n_total >= (1LL << 31)) throw InvalidArgument("st_step: node count exceeds int32 CSR indexing");
     const i64 E = u.n_added + u.n_removed + u.n_new_edges;
     STG_CUDA(cudaStreamWaitEvent(st_, ev_mg_, 0));  // a merge left running by a failed step
-    ensure_node_capacity(n_total);
+    if (sh_ && !keep_delta) throw InvalidArgument("st_probe: not available on sharded sessions");
+    ensure_node_capacity(n_total, sh_ ? rows_at(comm_.rank, n_total) : n_total);
     ++stamp_;
     if (stamp_ == 0x7fffffff) stamp_ = 1;
     ++plan_epoch_;  // the Delta CSRs are rebuilt below
@@ -1159,61 +1369,13 @@ class Session {
       }
       scan_int(dcnt, drp, n_total + 1);
     }
+    if (sh_) return ingest_shard_tail(pt, u, device_ptrs, sort_path, ed, ekey_s, eval_s, dcol, drp, n2);
     // ---- apply_update merge (A_next in the spare slot)
     const DevCsr& a = A();
-    int* lb = arena_.get<int>("m_lb", n2);
-    int* mflag = arena_.get<int>("m_flag", n2);
-    double* newv = arena_.get<double>("m_newv", n2);
-    int* contrib = arena_.get<int>("m_contrib", n2 + 1);
-    int* prefix = arena_.get<int>("m_prefix", n2 + 1);
-    int* ncnt = arena_.get<int>("m_ncnt", n_total + 1);
     const int slot = keep_delta ? 1 - acur_ : 2;  // probes never touch the live buffers
-    const std::string aname = "A" + std::to_string(slot);
-    DevCsr an;
-    an.n = n_total;
-    an.rp = arena_.get<int>(aname + ".rp", n_total + 1);
-    an.col = arena_.get<int>(aname + ".col", a.nnz + n2);
-    an.val = arena_.get<double>(aname + ".val", a.nnz + n2);
-    launch(row_len_kernel, dim3(blocks(n_total + 1)), dim3(256), 0, st_, static_cast<const int*>(a.rp), n_old, n_total,
-           ncnt);
-    STG_CUDA(cudaMemsetAsync(contrib, 0, sizeof(int) * (n2 + 1), st_));
-    if (n2 > 0)
-      launch(merge_classify_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s),
-             static_cast<const double*>(eval_s), n2, static_cast<const int*>(a.rp), static_cast<const int*>(a.col),
-             static_cast<const double*>(a.val), n_old, lb, mflag, newv, contrib, ncnt, err_apply, ed.kb);
-    scan_int(ncnt, an.rp, n_total + 1);
-    scan_int(contrib, prefix, n2 + 1);
-    // row pointers, counts and the apply checks above stay on st_ (the
-    // validation read below needs them); the entry copy may run aside
-    const bool merge_aside = keep_delta && !is_laplacian();
-    cudaStream_t ms = st_;
-    if (merge_aside) {
-      STG_CUDA(cudaEventRecord(ev_mg_fork_, st_));
-      STG_CUDA(cudaStreamWaitEvent(st_mg_, ev_mg_fork_, 0));
-      ms = st_mg_;
-    }
-    kbegin(kMerge, 0.0, ms);
-    const size_t merge_pend = pend_.size() - (ktiming() ? 1 : 0);
-    if (a.nnz > 0) {
-      const i64 nwarp = cdiv(n_old + a.nnz, kRunDiag);
-      int* cmap = arena_.get<int>("m_chunkmap", nwarp);
-      launch(chunk_rows_kernel, dim3(blocks(n_old)), dim3(256), 0, ms, static_cast<const int*>(a.rp),
-             static_cast<int>(n_old), cmap);
-      launch(merge_runs_kernel, dim3(blocks(nwarp, 8)), dim3(256), 0, ms,
-             static_cast<const int*>(a.rp), static_cast<const int*>(a.col), static_cast<const double*>(a.val),
-             static_cast<int>(n_old), static_cast<int>(a.nnz), static_cast<const int*>(cmap),
-             static_cast<const int*>(mark_delta_), stamp_, static_cast<const int*>(drp),
-             static_cast<const int*>(dcol), static_cast<const int*>(lb), static_cast<const int*>(mflag),
-             static_cast<const double*>(newv), static_cast<const int*>(prefix), static_cast<const int*>(an.rp),
-             an.col, an.val, merge_mode_);
-    }
-    if (n2 > 0)
-      launch(merge_insert_kernel, dim3(blocks(n2)), dim3(256), 0, ms, n2, static_cast<const int*>(drow),
-             static_cast<const int*>(dcol), static_cast<const u64*>(ekey_s), static_cast<const int*>(lb),
-             static_cast<const int*>(mflag), static_cast<const double*>(newv), static_cast<const int*>(prefix),
-             static_cast<const int*>(drp), static_cast<const int*>(an.rp), an.col, an.val);
-    kend(ms);
-    if (merge_aside) STG_CUDA(cudaEventRecord(ev_mg_, st_mg_));
+    size_t merge_pend = 0;
+    DevCsr an = merge_launch(a, n_old, n_total, ekey_s, eval_s, n2, drow, dcol, drp, mark_delta_, ed.kb, slot,
+                             keep_delta && !is_laplacian(), err_apply, &merge_pend);
     // ---- validation outcome and sizes: read back here for the Laplacian
     // operators (their assembly needs nnz); the adjacency path folds this read
     // into the P-size sync below (nothing is committed before either)
@@ -1326,7 +1488,144 @@ class Session {
                static_cast<const int*>(posmap_), lcol);
       pt.lrp = lrp;
       pt.lcol = lcol;
+      unsharded_fields(pt);
     }
+    return pt;
+  }
+
+  // Sharded ingestion after the replicated validation and Delta assembly:
+  // the owned rows of Delta (local row ids) are merged into the owned rows of
+  // A, the owned rows of P are found, P is exchanged (halo positions), and the
+  // owned rows of Delta are compressed. Errors are decided identically on
+  // every rank (edit errors are replicated; apply errors are gathered and the
+  // one at the smallest global (row, col) is reported, as on one GPU).
+  Pert ingest_shard_tail(Pert pt, const st_update& u, bool device_ptrs, bool sort_path, const EditsDev& ed,
+                         const u64* ekey_s, const double* eval_s, const int* dcol, const int* drp, i64 n2) {
+    const i64 n_old = pt.n_old, n_total = pt.n_total;
+    const int R = comm_.size, rank = comm_.rank, kb = ed.kb;
+    const i64 xo = nloc_, xt = rows_at(rank, n_total);
+    u64* err_edit = d_scal_;
+    u64* err_apply = d_scal_ + 1;
+    // ---- owned rows of Delta, renumbered to local rows
+    int* ef = arena_.get<int>("sh_eflag", n2 + 1);
+    int* ep = arena_.get<int>("sh_epos", n2 + 1);
+    u64* lkey = arena_.get<u64>("sh_lkey", n2);
+    double* lval = arena_.get<double>("sh_lval", n2);
+    int* lrow = arena_.get<int>("sh_lrow", n2);
+    int* lcolg = arena_.get<int>("sh_lcolg", n2);
+    int* lcnt = arena_.get<int>("sh_lcnt", xt + 1);
+    int* ldrp = arena_.get<int>("sh_ldrp", xt + 1);
+    STG_CUDA(cudaMemsetAsync(lcnt, 0, sizeof(int) * (xt + 1), st_));
+    STG_CUDA(cudaMemsetAsync(lkey, 0xff, sizeof(u64) * std::max<i64>(n2, 1), st_));
+    launch(own_entry_flag_kernel, dim3(blocks(n2 + 1)), dim3(256), 0, st_, ekey_s, n2, kb, map_, ef);
+    scan_int(ef, ep, n2 + 1);
+    if (n2 > 0)
+      launch(own_entry_scatter_kernel, dim3(blocks(n2)), dim3(256), 0, st_, ekey_s, eval_s, n2, kb, map_,
+             static_cast<const int*>(ef), static_cast<const int*>(ep), lkey, lval, lrow, lcolg, lcnt, mark_dl_,
+             stamp_);
+    scan_int(lcnt, ldrp, xt + 1);
+    const DevCsr& a = A();
+    const int slot = 1 - acur_;
+    size_t merge_pend = 0;
+    DevCsr an = merge_launch(a, xo, xt, lkey, lval, n2, lrow, lcolg, ldrp, mark_dl_, kb, slot, true, err_apply,
+                             &merge_pend);
+    // ---- P marks (global): Delta rows + appended nodes
+    if (n_total > 0)
+      STG_CUDA(cudaMemcpyAsync(mark_p_, mark_delta_, sizeof(int) * n_total, cudaMemcpyDeviceToDevice, st_));
+    if (pt.S > 0)
+      launch(mark_range_kernel, dim3(blocks(pt.S)), dim3(256), 0, st_, mark_p_, n_old, n_total, stamp_);
+    int* pf = arena_.get<int>("sh_pflag", xt + 1);
+    int* pp = arena_.get<int>("sh_ppos", xt + 1);
+    launch(own_p_flag_kernel, dim3(blocks(xt + 1)), dim3(256), 0, st_, static_cast<const int*>(mark_p_), stamp_,
+           map_, xt, 0, pf);
+    scan_int(pf, pp, xt + 1);
+    // ---- validation outcome (one sync)
+    STG_CUDA(cudaMemcpyAsync(&hs_->err_edit, err_edit, sizeof(u64) * 3, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&hs_->nnz_new, an.rp + xt, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&hs_->p, pp + xt, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    if (!sort_path && hs_->err_edit == 0) return ingest(u, true, device_ptrs, true);  // replicated decision
+    if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
+    u64 mine = hs_->err_apply;
+    if (mine != kSentinel) {  // local row -> global row in the error key
+      const u64 g = static_cast<u64>(sm_global(host_map(), static_cast<i64>(mine >> 32)));
+      mine = (g << 32) | (mine & 0xffffffffULL);
+    }
+    const std::vector<u64> info = allgather_u64({mine, static_cast<u64>(hs_->p)});
+    u64 first = kSentinel;
+    i64 p_all = 0;
+    std::vector<i64> cnt(static_cast<size_t>(R));
+    for (int r = 0; r < R; ++r) {
+      first = std::min(first, info[2 * r]);
+      cnt[r] = static_cast<i64>(info[2 * r + 1]);
+      p_all += cnt[r];
+    }
+    if (first != kSentinel) {
+      if (first & 1ULL) throw InvalidArgument("apply_update: update drives an edge weight negative");
+      throw InvalidArgument("apply_update: invalid deletion (no such edge)");
+    }
+    an.nnz = hs_->nnz_new;
+    A_[slot] = an;
+    anext_ = slot;
+    pt.nnz = static_cast<i64>(hs_->nvalid);
+    if (ktiming())
+      pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (xo + 1) + 12.0 * an.nnz + 4.0 * (xt + 1);
+    pt.grp = drp;
+    pt.gcol = dcol;
+    pt.gval = eval_s;
+    pt.x_old = xo;
+    pt.x_total = xt;
+    pt.S_loc = xt - xo;
+    if (pt.empty()) return pt;
+    // ---- owned rows of P (all owned rows in dense mode, a global decision)
+    pt.dense = (cfg.flags & ST_FLAG_FORCE_DENSE) || 2 * p_all > n_total;
+    if (pt.dense) {
+      launch(own_p_flag_kernel, dim3(blocks(xt + 1)), dim3(256), 0, st_, static_cast<const int*>(mark_p_), stamp_,
+             map_, xt, 1, pf);
+      scan_int(pf, pp, xt + 1);
+      for (int r = 0; r < R; ++r) cnt[r] = rows_at(r, n_total);
+    }
+    const i64 p = cnt[rank];
+    i64 pmax = 1;
+    for (int r = 0; r < R; ++r) pmax = std::max(pmax, cnt[r]);
+    int* ploc = arena_.get<int>("sh_Ploc", xt + 1);
+    int* pglob = arena_.get<int>("sh_Pglob", xt + 1);
+    int* psend = arena_.get<int>("sh_psend", pmax);
+    int* pall = arena_.get<int>("sh_pall", pmax * R);
+    launch(own_p_scatter_kernel, dim3(blocks(xt)), dim3(256), 0, st_, static_cast<const int*>(pf),
+           static_cast<const int*>(pp), map_, xt, ploc, pglob);
+    STG_CUDA(cudaMemsetAsync(psend, 0xff, sizeof(int) * pmax, st_));
+    if (p > 0) STG_CUDA(cudaMemcpyAsync(psend, pglob, sizeof(int) * p, cudaMemcpyDeviceToDevice, st_));
+    STG_CUDA(cudaMemsetAsync(pall, 0xff, sizeof(int) * pmax * R, st_));
+    allgather(psend, pall, static_cast<i64>(sizeof(int)) * pmax);
+    launch(halo_posmap_kernel, dim3(blocks(pmax * R)), dim3(256), 0, st_, static_cast<const int*>(pall), pmax * R,
+           posmap_);
+    // ---- compressed CSR of the owned rows (columns = halo positions)
+    int* rl = arena_.get<int>("sh_rowlen", p + 1);
+    int* lrp = arena_.get<int>("lrp", p + 1);
+    int* lcol = arena_.get<int>("lcol", pt.nnz);
+    int* scol = arena_.get<int>("sh_scol", pt.nnz);
+    double* val = arena_.get<double>("sh_val", pt.nnz);
+    launch(own_rowlen_kernel, dim3(blocks(p + 1)), dim3(256), 0, st_, drp, static_cast<const int*>(pglob), p, rl);
+    scan_int(rl, lrp, p + 1);
+    if (p > 0)
+      launch(own_compress_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, drp, dcol, eval_s,
+             static_cast<const int*>(pglob), p, static_cast<const int*>(lrp), static_cast<const int*>(posmap_), lcol,
+             scol, val);
+    pt.p = p;
+    pt.p_old = p - pt.S_loc;
+    pt.pmax = pmax;
+    pt.G = p + (rank == 0 ? k : 0);
+    pt.P = pglob;
+    pt.Ploc = ploc;
+    pt.Pglob = pglob;
+    pt.posmap = posmap_;
+    pt.mark = mark_p_;
+    pt.lrp = lrp;
+    pt.lcol = lcol;
+    pt.val = val;
+    pt.scol = scol;
+    pt.scol_lo = static_cast<int>(n_old);
     return pt;
   }
 
@@ -1336,6 +1635,20 @@ class Session {
     pt.p_old = pt.n_old;
     pt.lrp = pt.grp;
     pt.lcol = pt.gcol;
+    unsharded_fields(pt);
+  }
+
+  // one GPU holds every row: P doubles as the X row list and the global ids
+  void unsharded_fields(Pert& pt) {
+    pt.G = pt.p + k;
+    pt.S_loc = pt.S;
+    pt.x_old = pt.n_old;
+    pt.x_total = pt.n_total;
+    pt.Ploc = pt.P;
+    pt.Pglob = pt.P;
+    pt.gval = pt.val;
+    pt.scol = pt.lcol;
+    pt.scol_lo = static_cast<int>(pt.p_old);
   }
 
   void commit_graph(const Pert& pt) {
@@ -1352,10 +1665,11 @@ class Session {
     }
     last_delta_.rp = const_cast<int*>(pt.grp);
     last_delta_.col = const_cast<int*>(pt.gcol);
-    last_delta_.val = const_cast<double*>(pt.val);
+    last_delta_.val = const_cast<double*>(pt.gval);
     last_delta_nnz_ = pt.nnz;
     last_delta_n_ = pt.n_total;
     n = pt.n_total;
+    nloc_ = pt.x_total;
     // rows appended to X are zero until the rotation writes them (padded_vectors)
   }
 
@@ -1395,12 +1709,12 @@ class Session {
       Cuse = Cpre;
       ldc1 = ldcpre;
     } else if (against && a > 0) {
-      gram(against->p, against->ld, W.p, W.ld, G, a, w, false, C, ldw);
+      pgram(against->p, against->ld, W.p, W.ld, G, a, w, false, C, ldw);
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, W.p, W.ld);
       P1 = W1;
       ldp1 = ldw;
     }
-    gram(P1, ldp1, P1, ldp1, G, w, w, true, Gm, ldw);
+    pgram(P1, ldp1, P1, ldp1, G, w, w, true, Gm, ldw);
     launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw, Cuse, ldc1,
            (against ? a : 0), w, o2);
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
@@ -1423,10 +1737,10 @@ class Session {
     nn(P1, ldp1, N, w, Ri, ldw, w, Q1, ldq1, 1.0, 0.0, nullptr, 0, true);
     // pass 2
     if (proj) {
-      gram(against->p, against->ld, out.p, out.ld, G, a, w, false, C, ldw);
+      pgram(against->p, against->ld, out.p, out.ld, G, a, w, false, C, ldw);
       nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, out.p, out.ld);
     }
-    gram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
+    pgram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
     chol_inverse_near_identity(Gm, ldw, w, R, ldw, Ri, ldw);
     nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
     return w;
@@ -1458,7 +1772,7 @@ class Session {
 
   double host_norm_g(const double* v, int ldv, i64 G) {
     double* g1 = arena_.get<double>("mgs_g1", 8);
-    gram(v, ldv, v, ldv, G, 1, 1, true, g1, 1);
+    pgram(v, ldv, v, ldv, G, 1, 1, true, g1, 1);
     double h = 0;
     STG_CUDA(cudaMemcpyAsync(&h, g1, sizeof(double), cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaStreamSynchronize(st_));
@@ -1477,11 +1791,11 @@ class Session {
       if (orig == 0.0) continue;
       for (int pass = 0; pass < 2; ++pass) {
         if (against && a > 0) {
-          gram(against->p, against->ld, v, ldv, G, a, 1, false, t, ldv);
+          pgram(against->p, against->ld, v, ldv, G, a, 1, false, t, ldv);
           nn(against->p, against->ld, N, a, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
         }
         if (r > 0) {
-          gram(out.p, out.ld, v, ldv, G, r, 1, false, t, ldv);
+          pgram(out.p, out.ld, v, ldv, G, r, 1, false, t, ldv);
           nn(out.p, out.ld, N, r, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
         }
       }
@@ -1502,7 +1816,7 @@ class Session {
   // build_projection_basis (trackers.cpp:226-280) in stacked coordinates.
   // Z columns [0, k) hold X-bar; returns Z with D columns.
   Basis build_basis(const Pert& pt, int basis_kind, u64 seed) {
-    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const i64 p = pt.p, N = p + 2 * k, G = pt.G;
     const i64 S = pt.S;
     const int kk = static_cast<int>(k);
     // widths
@@ -1534,7 +1848,10 @@ class Session {
     if (basis_kind == 0) {
       // iasc: [[X, 0], [0, I_S]] (trackers.cpp:233-238)
       STG_CUDA(cudaMemset2DAsync(Z + kk, sizeof(double) * ldz, 0, sizeof(double) * S, N, st_));
-      if (S > 0)
+      if (sh_ && pt.S_loc > 0)
+        launch(unit_cols_own_kernel, dim3(blocks(pt.S_loc)), dim3(256), 0, st_, Z + kk, ldz, pt.Pglob, pt.p_old,
+               pt.S_loc, pt.n_old);
+      else if (!sh_ && S > 0)
         launch(unit_cols_kernel, dim3(blocks(S)), dim3(256), 0, st_, Z + kk, ldz, pt.p_old, S);
       return Basis{z, static_cast<int>(kk + S)};
     }
@@ -1550,24 +1867,27 @@ class Session {
     sa.rowptr = pt.lrp;
     sa.col = pt.lcol;
     sa.val = pt.val;
-    sa.X = Z;
-    sa.ldx = ldz;
+    sa.X = halo(pt, Z, ldz, kk, &sa.ldx);
     sa.m = kk;
     sa.Y = cand;
     sa.ldy = ldc;
     do_spmm(sa, pt.nnz, p);
-    gram(Z, ldz, cand, ldc, G, kk, kk, false, ck, ldc);
+    pgram(Z, ldz, cand, ldc, G, kk, kk, false, ck, ldc);
     nn(Z, ldz, N, kk, ck, ldc, kk, cand, ldc, -1.0, 1.0, cand, ldc);
     int w = kk;
     if (basis_kind >= 2) {
       if (!rsvd) {
         // d2 dense: column j = Delta[:, n_old + j]; by symmetry row p_old + j of the local CSR
         if (S > 0) {
-          launch(d2_dense_kernel, dim3(blocks(S, 8)), dim3(256), 0, st_, pt.lrp, pt.lcol, pt.val, pt.p_old, S,
-                 cand + kk, ldc);
+          if (sh_)
+            launch(d2_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, pt.lrp, pt.scol, pt.val, p, pt.n_old,
+                   cand + kk, ldc);
+          else
+            launch(d2_dense_kernel, dim3(blocks(S, 8)), dim3(256), 0, st_, pt.lrp, pt.lcol, pt.val, pt.p_old, S,
+                   cand + kk, ldc);
           const int lck = ld_for(S);
           double* c2 = arena_.get<double>("c2", static_cast<i64>(kk) * lck);
-          gram(Z, ldz, cand + kk, ldc, G, kk, static_cast<int>(S), false, c2, lck);
+          pgram(Z, ldz, cand + kk, ldc, G, kk, static_cast<int>(S), false, c2, lck);
           nn(Z, ldz, N, kk, c2, lck, static_cast<int>(S), cand + kk, ldc, -1.0, 1.0, cand + kk, ldc);
           w += static_cast<int>(S);
         }
@@ -1586,7 +1906,7 @@ class Session {
             const int a = kk + q1;
             double* c1 = arena_.get<double>("pm_C1", static_cast<i64>(a) * ldm);
             double* pm = arena_.get<double>("pm_PM", N * ldm);
-            gram(Z, ldz, Msk, ldm, G, a, qm, false, c1, ldm);
+            pgram(Z, ldz, Msk, ldm, G, a, qm, false, c1, ldm);
             nn(Z, ldz, N, a, c1, ldm, qm, pm, ldm, -1.0, 1.0, Msk, ldm);
             pre_pm_ = pm;
             pre_c1_ = c1;
@@ -1616,7 +1936,7 @@ class Session {
   // sketch's eigensolve (one or two SMs) runs on st_eig_.
   template <class F>
   int rsvd_trailing(const Pert& pt, Blk z, int q, const double* omega, int ldo, Blk out, F&& during_eig) {
-    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const i64 p = pt.p, N = p + 2 * k, G = pt.G;
     const int kk = static_cast<int>(k);
     const int ldy = ld_for(q);
     double* Y = arena_.get<double>("Y", N * ldy);
@@ -1626,17 +1946,17 @@ class Session {
     SpmmArgs sa{};
     sa.rows = p;
     sa.rowptr = pt.lrp;
-    sa.col = pt.lcol;
+    sa.col = pt.scol;
     sa.val = pt.val;
-    sa.col_lo = static_cast<int>(pt.p_old);
-    sa.X = omega - pt.p_old * ldo;
+    sa.col_lo = pt.scol_lo;
+    sa.X = omega - static_cast<i64>(pt.scol_lo) * ldo;
     sa.ldx = ldo;
     sa.m = q;
     sa.Y = Y;
     sa.ldy = ldy;
     do_spmm(sa, pt.nnz, pt.S, kSpmmSketch);
     double* cy = arena_.get<double>("cy", static_cast<i64>(kk) * ldy);
-    gram(z.p, z.ld, Y, ldy, G, kk, q, false, cy, ldy);
+    pgram(z.p, z.ld, Y, ldy, G, kk, q, false, cy, ldy);
     nn(z.p, z.ld, N, kk, cy, ldy, q, Y, ldy, -1.0, 1.0, Y, ldy);
     // M = orthonormalize(Y)
     double* M = arena_.get<double>("Msk", N * ldy);
@@ -1654,27 +1974,26 @@ class Session {
     const double* Msrc = M;
     if (last_ortho_exact_) {
       double* cm = arena_.get<double>("cm", static_cast<i64>(kk) * ldy);
-      gram(z.p, z.ld, M, ldy, G, kk, qm, false, cm, ldy);
+      pgram(z.p, z.ld, M, ldy, G, kk, qm, false, cm, ldy);
       double* Mp = arena_.get<double>("Mp", p * ldy);
       nn(z.p, z.ld, p, kk, cm, ldy, qm, Mp, ldy, -1.0, 1.0, M, ldy);
       Msrc = Mp;
     }
-    double* btm = arena_.get<double>("btm", pt.S * ldy);
+    double* btm = arena_.get<double>("btm", std::max<i64>(pt.S_loc, 1) * ldy);
     SpmmArgs sb{};
-    sb.rows = pt.S;
+    sb.rows = pt.S_loc;
     sb.row_off = pt.p_old;
     sb.rowptr = pt.lrp;
     sb.col = pt.lcol;
     sb.val = pt.val;
-    sb.X = Msrc;
-    sb.ldx = ldy;
+    sb.X = halo(pt, Msrc, ldy, qm, &sb.ldx);
     sb.m = qm;
     sb.Y = btm;
     sb.ldy = ldy;
     do_spmm(sb, pt.nnz, p, kSpmmSketch);
     // thin U of (M'B) = eigenvectors of bt_m' bt_m, singular values descending
     double* gb = arena_.get<double>("gb", static_cast<i64>(qm) * ldy);
-    gram(btm, ldy, btm, ldy, pt.S, qm, qm, true, gb, ldy);
+    pgram(btm, ldy, btm, ldy, pt.S_loc, qm, qm, true, gb, ldy);
     const int wantu = static_cast<int>(std::min<i64>(cfg.rsvd_l, qm));
     const int ldu = ld_for(wantu);
     double* U = arena_.get<double>("Ukeep", static_cast<i64>(qm) * ldu);
@@ -1817,14 +2136,14 @@ class Session {
     const int ldr = ld_for(kk);
     double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ldr);
     launch(gather_xbar_kernel, dim3(blocks((p + 2 * k) * k)), dim3(256), 0, st_, static_cast<const double*>(X_), ldx(),
-           pt.P, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(nullptr), ldr, z.p, z.ld);
+           pt.Ploc, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(nullptr), ldr, z.p, z.ld);
     if (!pt.dense) {
       if (pt.p_old > 0) {
-        launch(zero_rows_kernel, dim3(blocks(pt.p_old, 8)), dim3(256), 0, st_, X_, ldx(), pt.P, pt.p_old, kk);
-        xrestore_ = XRestore{true, pt.P, pt.p_old, z.p, z.ld};
+        launch(zero_rows_kernel, dim3(blocks(pt.p_old, 8)), dim3(256), 0, st_, X_, ldx(), pt.Ploc, pt.p_old, kk);
+        xrestore_ = XRestore{true, pt.Ploc, pt.p_old, z.p, z.ld};
       }
       double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ldr);
-      gram(X_, ldx(), X_, ldx(), pt.n_old, kk, kk, true, kc, ldr);
+      pgram(X_, ldx(), X_, ldx(), pt.x_old, kk, kk, true, kc, ldr);
       chol(kc, ldr, kk, rc, ldr, nullptr, 0, nullptr, 0.0, true);
       launch(copy2d_kernel, dim3(blocks(k * k)), dim3(256), 0, st_, static_cast<const double*>(rc), ldr, z.p + p * z.ld,
              z.ld, k, kk);
@@ -1850,9 +2169,9 @@ class Session {
     double* gz = arena_.get<double>("rr_gz", static_cast<i64>(dmax) * ldd);
     double* dz = arena_.get<double>("rr_dz", p * ldd);
     double* tm = arena_.get<double>("rr_t", static_cast<i64>(dmax) * ldd);
-    gram(z.p, z.ld, z.p, z.ld, G, a, a, true, gz, ldd);
+    pgram(z.p, z.ld, z.p, z.ld, G, a, a, true, gz, ldd);
     rr_spmm(pt, z.p, z.ld, a, dz, ldd);
-    gram(z.p, z.ld, dz, ldd, p, a, a, true, tm, ldd);
+    pgram(z.p, z.ld, dz, ldd, p, a, a, true, tm, ldd);
     rr_pre_ = RrPrefix{true, a, ldd};
   }
 
@@ -1862,8 +2181,7 @@ class Session {
     sa.rowptr = pt.lrp;
     sa.col = pt.lcol;
     sa.val = pt.val;
-    sa.X = X;
-    sa.ldx = ldx;
+    sa.X = halo(pt, X, ldx, m, &sa.ldx);
     sa.m = m;
     sa.Y = Y;
     sa.ldy = ldy;
@@ -1872,7 +2190,7 @@ class Session {
 
   void rayleigh_ritz(const Pert& pt, const Basis& b, std::vector<double>& newvals, bool write_state, double* wout,
                      i64 wrows, Blk xbar_override = Blk{}) {
-    const i64 p = pt.p, N = p + 2 * k, G = p + k;
+    const i64 p = pt.p, N = p + 2 * k, G = pt.G;
     const int D = b.D, kk = static_cast<int>(k);
     const Blk xb = xbar_override.p ? xbar_override : b.z;
     const bool pre = rr_pre_.valid && !xbar_override.p && rr_pre_.a <= D;
@@ -1886,16 +2204,16 @@ class Session {
     double* tm = arena_.get<double>("rr_t", static_cast<i64>(D) * ldd);
     if (pre) {  // columns a.. : [Z1'Z2; Z2'Z2], Delta Z2, [Z1'(Delta Z2); Z2'(Delta Z2)]
       if (D > a) {
-        gram(b.z.p, b.z.ld, b.z.p + a, b.z.ld, G, D, D - a, false, gz + a, ldd);
+        pgram(b.z.p, b.z.ld, b.z.p + a, b.z.ld, G, D, D - a, false, gz + a, ldd);
         rr_spmm(pt, b.z.p + a, b.z.ld, D - a, dz + a, ldd);
-        gram(b.z.p, b.z.ld, dz + a, ldd, p, D, D - a, false, tm + a, ldd);
+        pgram(b.z.p, b.z.ld, dz + a, ldd, p, D, D - a, false, tm + a, ldd);
       }
     } else {
-      gram(b.z.p, b.z.ld, b.z.p, b.z.ld, G, D, D, true, gz, ldd);
+      pgram(b.z.p, b.z.ld, b.z.p, b.z.ld, G, D, D, true, gz, ldd);
       rr_spmm(pt, b.z.p, b.z.ld, D, dz, ldd);
       // Z'(Delta Z) is symmetric (Delta is): tile pairs ti <= tj, mirrored;
       // the reference symmetrizes the projected matrix anyway (eig.hpp:47)
-      gram(b.z.p, b.z.ld, dz, ldd, p, D, D, true, tm, ldd);
+      pgram(b.z.p, b.z.ld, dz, ldd, p, D, D, true, tm, ldd);
     }
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
     launch(orthocheck_kernel, dim3(blocks(static_cast<i64>(D) * D)), dim3(256), 0, st_,
@@ -1946,9 +2264,9 @@ class Session {
       // then the rows of P take W's rows. Both are skipped if the step failed.
       kbegin(kRotate, 16.0 * k * pt.n_total + 8.0 * pt.n_total);
       if (!pt.dense && k <= 64)
-        nn(X_, ldx(), pt.n_old, kk, W + (p + k) * ldk, ldk, kk, X_, ldx(), 1.0, 0.0, nullptr, 0, false, true);
+        nn(X_, ldx(), pt.x_old, kk, W + (p + k) * ldk, ldk, kk, X_, ldx(), 1.0, 0.0, nullptr, 0, false, true);
       if (pt.dense || k <= 64)
-        launch(scatter_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, X_, ldx(), pt.P, pt.dense ? 1 : 0, p,
+        launch(scatter_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, X_, ldx(), pt.Ploc, pt.dense ? 1 : 0, p,
                static_cast<const double*>(W), ldk, kk, static_cast<const int*>(flags_ptr()),
                static_cast<const int*>(info_ptr()));
       else
@@ -2042,6 +2360,48 @@ st_status st_create(const st_config* cfg, int64_t n, const int32_t* rowptr, cons
 
 void st_destroy(st_session* s) { delete s; }
 
+st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n_global, int64_t row_lo,
+                            int64_t row_hi, int64_t chunk, const int32_t* rowptr, const int32_t* colidx,
+                            const double* values_csr, const double* eig_values, const double* eig_vectors,
+                            int64_t ld, st_session** out) {
+  return guarded(nullptr, [&] {
+    if (!cfg || !comm || !out || !rowptr || !eig_values || (!eig_vectors && row_hi > row_lo))
+      throw std::invalid_argument("st_create_sharded: null argument");
+    if (n_global < 1) throw std::invalid_argument("st_create: empty graph");
+    if (ld < row_hi - row_lo) throw std::invalid_argument("st_create: leading dimension below n");
+    stg::Session::ShardInit si{*comm, n_global, row_lo, row_hi, chunk};
+    auto s = std::make_unique<st_session>();
+    s->impl = std::make_unique<stg::Session>(*cfg, row_hi - row_lo, rowptr, colidx, values_csr, eig_values,
+                                             eig_vectors, ld, &si);
+    *out = s.release();
+  });
+}
+
+st_status st_shard_rows(const st_session* s, int64_t* n_local, int64_t* global_ids) {
+  auto* ms = const_cast<st_session*>(s);
+  return guarded(ms, [&] {
+    if (n_local) *n_local = ms->impl->local_rows();
+    if (global_ids) ms->impl->local_ids(reinterpret_cast<stg::i64*>(global_ids));
+  });
+}
+
+int64_t st_shard_layout(int32_t size, const int64_t* bounds, int64_t chunk, int32_t rank, int64_t n_total,
+                        int64_t* global_ids, int64_t cap) {
+  if (size < 1 || rank < 0 || rank >= size || chunk < 1 || !bounds) return -1;
+  stg::ShardMap m;
+  m.n0 = bounds[size];
+  m.chunk = chunk;
+  m.size = size;
+  m.rank = rank;
+  const stg::i64* b = reinterpret_cast<const stg::i64*>(bounds);
+  m.bounds = b;
+  m.own0 = bounds[rank + 1] - bounds[rank];
+  m.lo = bounds[rank];
+  const int64_t rows = stg::sm_rows(m, rank, n_total, b);
+  for (int64_t l = 0; l < rows && l < cap; ++l) global_ids[l] = stg::sm_global(m, l);
+  return rows;
+}
+
 st_status st_step(st_session* s, const st_update* upd) {
   return guarded(s, [&] {
     if (!upd) throw std::invalid_argument("st_step: null update");
@@ -2065,7 +2425,7 @@ st_status st_info(const st_session* s, int64_t* n, int64_t* k, uint64_t* steps_t
 st_status st_get_embedding(const st_session* s, double* values, double* vectors, int64_t ld) {
   auto* ms = const_cast<st_session*>(s);
   return guarded(ms, [&] {
-    if (ld < ms->impl->n) throw std::invalid_argument("st_get_embedding: leading dimension below n");
+    if (ld < ms->impl->local_rows()) throw std::invalid_argument("st_get_embedding: leading dimension below n");
     ms->impl->get_embedding(values, vectors, ld);
   });
 }

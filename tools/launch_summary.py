@@ -11,7 +11,7 @@ h = rows[hi]
 k, v = h.index("Kernel Name"), h.index("Metric Value")
 ks = [(r[k], float(r[v])) for r in rows[hi + 1:] if len(r) > v]
 ours = [(n, t) for n, t in ks if "stg::" in n or "dm::" in n]
-starts = [i for i, (n, _) in enumerate(ours) if "edit_check_kernel" in n]
+starts = [i for i, (n, _) in enumerate(ours) if "edit_check_kernel" in n or "edit_bucket_kernel" in n]
 nsteps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 sel = starts[-nsteps:]
 steps = [ours[a:b] for a, b in zip(sel, sel[1:] + [len(ours)])]
