@@ -321,6 +321,7 @@ class Session {
   std::vector<i64> bounds_;  // host copy
   i64 nloc_ = 0;             // rows stored here (= n unsharded)
   int* mark_dl_ = nullptr;   // Delta-row marks by local row (sharded merge)
+  const bool shard_debug_ = getenv("STG_SHARD_DEBUG") != nullptr;
 
   void init_shard(const ShardInit& si) {
     if (si.comm.size < 1 || si.comm.rank < 0 || si.comm.rank >= si.comm.size || !si.comm.allreduce_sum_f64 ||
@@ -872,6 +873,15 @@ class Session {
     if (rows > 0) gram(A, lda, B, ldb, rows, m1, m2, sym, tmp, m2);
     else STG_CUDA(cudaMemsetAsync(tmp, 0, sizeof(double) * mm, st_));
     allreduce(tmp, mm);
+    if (shard_debug_) {  // development: checksums of the reduced Grams, in call order
+      std::vector<double> h(static_cast<size_t>(mm));
+      STG_CUDA(cudaMemcpyAsync(h.data(), tmp, sizeof(double) * mm, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      double sum = 0, sa = 0;
+      for (double v : h) { sum += v; sa += std::fabs(v); }
+      fprintf(stderr, "[r%d] pgram %d x %d rows %lld sum %.15e abs %.15e\n", comm_.rank, m1, m2,
+              static_cast<long long>(rows), sum, sa);
+    }
     launch(gram_out_kernel, dim3(blocks(mm)), dim3(256), 0, st_, static_cast<const double*>(tmp), m1, m2, sym ? 1 : 0,
            out, ldo);
   }
@@ -2164,7 +2174,7 @@ class Session {
   } rr_pre_;
 
   void rr_prefix(const Pert& pt, Blk z, int a, int dmax) {
-    const i64 p = pt.p, G = p + k;
+    const i64 p = pt.p, G = pt.G;
     const int ldd = ld_for(dmax);
     double* gz = arena_.get<double>("rr_gz", static_cast<i64>(dmax) * ldd);
     double* dz = arena_.get<double>("rr_dz", p * ldd);
