@@ -176,7 +176,29 @@ def cpu_baseline(stream, x0_vals, x0_vecs, wl, threads: int):
     return dt, o.last_tracker_seconds
 
 
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
 def run_ours(args):
+    # native libraries (NCCL's banner, ...) may write to fd 1: keep it on
+    # stderr until the one JSON line is printed
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        _run_ours(args, saved_stdout)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved_stdout, 1)
+        os.close(saved_stdout)
+
+
+def _run_ours(args, saved_stdout):
     import torch
 
     from paper_2603_19439_b200 import KERNEL_CLASSES, DeviceUpdate, TrackerSession, init_eig
@@ -185,15 +207,37 @@ def run_ours(args):
     torch.cuda.set_device(local)
     W, K = args.warmup, args.steps
     t_setup = time.time()
-    stream, wl = make_workload(args.config, W + K, seed_offset=rank if world > 1 else 0, scale=args.scale)
+    replicas = world > 1 and args.replicas
+    stream, wl = make_workload(args.config, W + K, seed_offset=rank if replicas else 0, scale=args.scale)
     rp, col, val = stream.csr0()
     orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
     vals0, vecs0 = init_eig.leading_eigenpairs(orp, ocol, oval, wl["k"], wl["order"], device=f"cuda:{local}")
     setup_s = time.time() - t_setup
     kw = dict(kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0, device=local)
 
+    sharded = args.sharded or (world > 1 and not args.replicas)
+    comm = None
+    if sharded:
+        import torch.distributed as dist
+
+        from paper_2603_19439_b200.shard import ShardedTrackerSession, TorchComm, local_block, shard_bounds
+
+        if not dist.is_initialized():  # --sharded on one GPU: a one-rank NCCL group
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
+        comm = TorchComm("nccl")
+        bounds = shard_bounds(rp, world)
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        blk = local_block(rp, col, val, vecs0, lo, hi)
+        kw_sh = {k_: v for k_, v in kw.items() if k_ != "operator"}
+
+    def new_session(kernel_timing=False):
+        if sharded:
+            return ShardedTrackerSession(comm, len(rp) - 1, lo, hi, blk[0], blk[1], blk[2], vals0, blk[3],
+                                         chunk=1024, kernel_timing=kernel_timing, **kw_sh)
+        return TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, **kw)
+
     # ---- value: edit lists resident in HBM
-    sess = TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=True, **kw)
+    sess = new_session(kernel_timing=True)
     dev_updates = [DeviceUpdate(u, device=f"cuda:{local}") for u in stream.updates]
     for t in range(W):
         sess.step_device(dev_updates[t])
@@ -220,7 +264,7 @@ def run_ours(args):
     del dev_updates
 
     # ---- e2e: host edit lists through the C ABI, Ritz values read back
-    sess = TrackerSession(rp, col, val, vals0, vecs0, **kw)
+    sess = new_session()
     for t in range(W):
         sess.step(stream.updates[t])
     torch.cuda.synchronize()
@@ -237,8 +281,9 @@ def run_ours(args):
     ms_e2e = dist_max(f0.elapsed_time(f1), world)
     sess.close()
 
-    value = world * K / (ms / 1e3)
-    e2e = world * K / (ms_e2e / 1e3)
+    streams_run = 1 if sharded else world  # one row-sharded stream, or one stream per replica
+    value = streams_run * K / (ms / 1e3)
+    e2e = streams_run * K / (ms_e2e / 1e3)
     hbm_peak, hbm_src = measured_peaks()
 
     # ---- roofline of the dominant kernel class (by device time)
@@ -282,12 +327,14 @@ def run_ours(args):
                         algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="byte")
     out = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded R-MAT + preferential-attachment stream; BASELINE config 3 shapes)",
         "config": {"workload": wl["workload"], "n0": int(len(rp) - 1), "nnz0": int(rp[-1]), "k": wl["k"],
                    "kind": wl["kind"], "rsvd_l": 100, "rsvd_p": 100, "n_final": info["n"],
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (row sharding: round 2)",
-                   "l2": "inputs larger than L2 (CSR ~0.38 GB + X ~0.27 GB per replica)",
+                   "parallelism": (f"row-sharded over {world} GPU(s) (NCCL allreduce of Grams, allgather halo)"
+                                   if sharded else "single GPU" if world == 1 else f"{world} independent replicas"),
+                   "l2": "inputs larger than L2 (CSR ~0.38 GB + X ~0.27 GB per stream)",
                    "setup_s": round(setup_s, 1)},
         "roofline": roof,
         "kernel_classes": classes,
@@ -304,9 +351,12 @@ def run_ours(args):
                                          f"tracker_step via the oracle restatement, OpenMP {threads} threads; "
                                          f"tracker_step alone {dt_tracker:.2f} s",
                                "seconds_per_step": dt}
+    if comm is not None:
+        out["comm"] = {"calls_per_step": {k_: v / (2 * (W + K)) for k_, v in comm.calls.items()}}
     if rank == 0:
-        print(json.dumps(out))
-    if world > 1:
+        sys.stdout.flush()
+        os.write(saved_stdout, (json.dumps(out) + "\n").encode())
+    if world > 1 or sharded:
         import torch.distributed as dist
 
         dist.destroy_process_group()
@@ -366,6 +416,8 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3"])
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (development)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="row-sharded sessions even on one GPU (NCCL group of 1)")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of row sharding")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -15,6 +15,7 @@ the contiguous row blocks the ranks start from.
 from __future__ import annotations
 
 import ctypes as C
+import time
 
 import numpy as np
 
@@ -54,12 +55,13 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
-        self.calls = {"allreduce": 0, "allgather": 0, "bytes": 0}
+        self.calls = {"allreduce": 0, "allgather": 0, "bytes": 0, "host_s": 0.0}
         self._ar = ALLREDUCE_FN(self._allreduce)
         self._ag = ALLGATHER_FN(self._allgather)
         self.struct = StComm(self.rank, self.size, None, self._ar, self._ag)
 
     def _allreduce(self, ctx, buf, count, stream):
+        t0 = time.perf_counter()
         try:
             import torch
             import torch.distributed as dist
@@ -80,12 +82,14 @@ class TorchComm:
                 with torch.cuda.stream(ext):
                     t.copy_(h)
                 ext.synchronize()
+            self.calls["host_s"] += time.perf_counter() - t0
             return 0
         except Exception as e:  # a failed collective must not unwind through C
             print(f"[rank {self.rank}] st_comm allreduce failed: {e!r}", flush=True)
             return 1
 
     def _allgather(self, ctx, send, recv, nbytes, stream):
+        t0 = time.perf_counter()
         try:
             import torch
             import torch.distributed as dist
@@ -109,6 +113,7 @@ class TorchComm:
                 with torch.cuda.stream(ext):
                     r.copy_(h)
                 ext.synchronize()
+            self.calls["host_s"] += time.perf_counter() - t0
             return 0
         except Exception as e:
             print(f"[rank {self.rank}] st_comm allgather failed: {e!r}", flush=True)
