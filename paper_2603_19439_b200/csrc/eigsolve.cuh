@@ -749,7 +749,8 @@ void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int
                  double* w_sorted,
                  double* F, int ldf, double* dbuf, int* ibuf, int* flags) {
   const EigBufs b = eig_carve(dbuf, ibuf, n, want);
-  if (n <= kEig1N) {
+  static const int one_cta_max = getenv("STG_EIG1N") ? atoi(getenv("STG_EIG1N")) : kEig1N;  // development A/B
+  if (n <= one_cta_max) {
     const int g = tridiag_gmax(n, 1);
     L(tridiag1_kernel, dim3(1), dim3(kTriThreads), tridiag_smem_bytes(n, 1, g), M, ldm, n, sym_input, g, b, flags);
   } else {

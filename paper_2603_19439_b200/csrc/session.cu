@@ -994,7 +994,7 @@ class Session {
     e->rows = a.rows;
     e->nnz = nnz;
     e->epoch = plan_epoch_;
-    e->vmax = a.rows + cdiv(nnz, kSegNnz);
+    e->vmax = 2 * cdiv(nnz, kSegNnz) + 1;  // segments of the rows longer than kSegNnz
     e->split_max = std::min<i64>(a.rows, nnz / (kSegNnz + 1));
     e->smax = 2 * cdiv(nnz, kSegNnz) + 1;
     int* cnt = arena_.get<int>(e->tag + "cnt", a.rows + 1);
@@ -1028,7 +1028,7 @@ class Session {
       b.Y = a.Y + c0;
       b.m = std::min(a.m - c0, 256);
       spmm_launch(b, pl, pe.vmax, pe.split_max, st_);
-      launches += pe.split_max > 0 ? 2 : 1;
+      launches += pe.split_max > 0 ? 3 : 1;
     }
     kend();
   }

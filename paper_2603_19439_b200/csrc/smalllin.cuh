@@ -109,44 +109,44 @@ __device__ __forceinline__ void chol_panel(double* sm, const double* invd, int w
 }
 
 // Rank-b update by panel p (rows p..p+b-1 hold R) of the elements (i, c),
-// i in [r0, r1), c >= i, c >= q0. Work items are bands of 4 rows x 64 columns
-// owned by one warp: the 4 row factors are shared-memory broadcasts and lane l
-// owns columns c0 + l and c0 + 32 + l, so every access is conflict-free.
+// i in [r0, r1), c >= i, c >= q0, on the FP64 tensor pipe: a work item is an
+// 8-row x 16-column block owned by one warp, A(i, c) -= sum_t R(t, i) R(t, c)
+// as mma.sync m8n8k4 (SASS DMMA) over the b <= 16 panel rows, fragments
+// loaded straight from the packed triangle (lane: panel row 4kk + lane % 4,
+// matrix row/column lane / 4). The sum is formed first and then subtracted,
+// as the scalar form did.
 __device__ __forceinline__ void chol_trailing(double* sm, int w, int p, int b, int q0, int r0, int r1, int warp,
                                               int nwarps, int lane) {
   if (r1 <= r0) return;
-  const int nb4 = (r1 - r0 + 3) >> 2;        // row bands
-  const int nch = (w - q0 + 63) >> 6;        // 64-column chunks
-  for (int item = warp; item < nb4 * nch; item += nwarps) {
+  const int nb8 = (r1 - r0 + 7) >> 3;        // 8-row bands
+  const int nch = (w - q0 + 15) >> 4;        // 16-column chunks
+  const int tq = lane & 3, g = lane >> 2;
+  int rb[4];                                 // packed row of panel row 4 kk + tq (-1: beyond the panel)
+#pragma unroll
+  for (int kk = 0; kk < 4; ++kk) rb[kk] = 4 * kk + tq < b ? packed_row(p + 4 * kk + tq, w) : -1;
+  for (int item = warp; item < nb8 * nch; item += nwarps) {
     const int band = item / nch, ch = item - band * nch;
-    const int i0 = r0 + 4 * band, c0 = q0 + 64 * ch;
-    if (c0 + 63 < i0) continue;  // chunk entirely left of the diagonal
-    double acc[4][2];
+    const int i0 = r0 + 8 * band, c0 = q0 + 16 * ch;
+    if (c0 + 15 < i0) continue;  // chunk entirely left of the diagonal
+    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+    const int ia = i0 + g, ca = c0 + g, cb = c0 + 8 + g;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) acc[x][0] = acc[x][1] = 0.0;
-    const int ca = c0 + lane, cb = c0 + 32 + lane;
-#pragma unroll 4
-    for (int t = 0; t < b; ++t) {
-      const double* rowt = sm + packed_row(p + t, w);
-      double ri[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) ri[x] = i0 + x < r1 ? rowt[i0 + x] : 0.0;
-      const double va = ca < w ? rowt[ca] : 0.0;
-      const double vb = cb < w ? rowt[cb] : 0.0;
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        acc[x][0] = fma(ri[x], va, acc[x][0]);
-        acc[x][1] = fma(ri[x], vb, acc[x][1]);
-      }
+    for (int kk = 0; kk < 4; ++kk) {
+      const bool t_ok = rb[kk] >= 0;
+      const double fa = t_ok && ia < w ? sm[rb[kk] + ia] : 0.0;
+      const double fb0 = t_ok && ca < w ? sm[rb[kk] + ca] : 0.0;
+      const double fb1 = t_ok && cb < w ? sm[rb[kk] + cb] : 0.0;
+      dmma(a0, a1, fa, fb0);
+      dmma(b0, b1, fa, fb1);
     }
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int i = i0 + x;
-      if (i >= r1) continue;
-      double* rowi = sm + packed_row(i, w);
-      if (ca < w && ca >= i) rowi[ca] -= acc[x][0];
-      if (cb < w && cb >= i) rowi[cb] -= acc[x][1];
-    }
+    const int i = i0 + g;
+    if (i >= r1) continue;
+    double* rowi = sm + packed_row(i, w);
+    const int cx = c0 + 2 * tq, cy = c0 + 8 + 2 * tq;
+    if (cx < w && cx >= i) rowi[cx] -= a0;
+    if (cx + 1 < w && cx + 1 >= i) rowi[cx + 1] -= a1;
+    if (cy < w && cy >= i) rowi[cy] -= b0;
+    if (cy + 1 < w && cy + 1 >= i) rowi[cy + 1] -= b1;
   }
 }
 

@@ -105,6 +105,158 @@ __global__ void __launch_bounds__(256) spmm_kernel(SpmmArgs a, SpmmPlan pl) {
   }
 }
 
+// Rows of at most kSegNnz nonzeros, kGroupRows consecutive rows per warp:
+// the group's row pointers come in one load and its (col, val) pairs in one
+// 32-wide window, so the per-row dependent chain is only the gather of X rows
+// (issued four nonzeros at a time). Each row is summed exactly as above
+// (column order, separate multiply and add: bit-identical). With VEC a warp
+// covers a 64-column slab, lane l owning columns 2l, 2l+1 (128-bit loads and
+// stores; X, Y 16-byte aligned, even leading dimensions and m); otherwise a
+// 32-column slab, one column per lane. blockIdx.y = column slab. Longer rows
+// are skipped here (spmm_kernel over the long-row plan writes them).
+constexpr int kGroupRows = 8;
+
+template <bool VEC>
+__device__ __forceinline__ void spmm_load_x(const double* xr, int lane, bool on, double& x0, double& x1) {
+  if (VEC) {
+    const double2 t = on ? __ldg(reinterpret_cast<const double2*>(xr) + lane) : make_double2(0.0, 0.0);
+    x0 = t.x;
+    x1 = t.y;
+  } else {
+    x0 = on ? __ldg(xr + lane) : 0.0;
+    x1 = 0.0;
+  }
+}
+
+template <bool VEC>
+__device__ __forceinline__ void spmm_store_row(double* yr, int lane, bool on, double a0, double a1) {
+  if (!on) return;
+  if (VEC) reinterpret_cast<double2*>(yr)[lane] = make_double2(a0, a1);
+  else yr[lane] = a0;
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(256, 4) spmm_group_kernel(SpmmArgs a) {
+  constexpr int W = VEC ? 64 : 32;
+  constexpr int B = VEC ? 4 : 8;  // X rows gathered per batch
+  const i64 g = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  const i64 r0 = g * kGroupRows;
+  if (r0 >= a.rows) return;
+  const int nr = static_cast<int>(min(static_cast<i64>(kGroupRows), a.rows - r0));
+  const int c0 = static_cast<int>(blockIdx.y) * W;
+  const int m = min(W, a.m - c0);
+  const int* rp = a.rowptr + a.row_off + r0;
+  const int rp_l = lane <= nr ? rp[lane] : 0;
+  const int gend = __shfl_sync(0xffffffffu, rp_l, nr);
+  int base = __shfl_sync(0xffffffffu, rp_l, 0);
+  int c_l = 0;
+  double v_l = 0.0;
+  if (base + lane < gend) {
+    c_l = a.col[base + lane];
+    v_l = a.val[base + lane];
+  }
+  const double* X = a.X + c0;
+  double* Y = a.Y + c0;
+  const bool on = VEC ? 2 * lane < m : lane < m;
+  if (gend - base <= 32) {
+    // The group's entries fit one window and no row is long: the active
+    // entries (col >= col_lo) of all rows are gathered B at a time across row
+    // boundaries; each row still sums its own entries in column order.
+    int row_l = 0;  // row (within the group) of entry `lane`
+#pragma unroll
+    for (int i = 1; i < kGroupRows; ++i) {
+      const int ri = __shfl_sync(0xffffffffu, rp_l, i);
+      row_l += (i < nr && base + lane >= ri) ? 1 : 0;
+    }
+    unsigned act = __ballot_sync(0xffffffffu, base + lane < gend && c_l >= a.col_lo);
+    // rows without an active entry are zero rows
+    bool has = false;
+    const int rp_next = __shfl_down_sync(0xffffffffu, rp_l, 1);
+    if (lane < nr) {
+      const int s = rp_l - base, e = rp_next - base;
+      const unsigned hi = e >= 32 ? 0xffffffffu : ((1u << e) - 1u);
+      const unsigned lo = s >= 32 ? 0xffffffffu : ((1u << s) - 1u);
+      has = (act & hi & ~lo) != 0;
+    }
+    unsigned empty = __ballot_sync(0xffffffffu, lane < nr && !has);
+    while (empty) {
+      const int r = __ffs(empty) - 1;
+      empty &= empty - 1;
+      spmm_store_row<VEC>(Y + (r0 + r) * static_cast<i64>(a.ldy), lane, on, 0.0, 0.0);
+    }
+    int cur = -1;
+    double acc0 = 0.0, acc1 = 0.0;
+    while (act) {
+      double x0[B], x1[B], vv[B];
+      int rw[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int j = act ? __ffs(act) - 1 : -1;
+        act &= act ? act - 1 : 0u;
+        rw[u] = j >= 0 ? __shfl_sync(0xffffffffu, row_l, j) : -1;
+        const int c = __shfl_sync(0xffffffffu, c_l, j < 0 ? 0 : j);
+        vv[u] = __shfl_sync(0xffffffffu, v_l, j < 0 ? 0 : j);
+        spmm_load_x<VEC>(X + static_cast<i64>(c) * a.ldx, lane, on && j >= 0, x0[u], x1[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (rw[u] < 0) break;
+        if (rw[u] != cur) {
+          if (cur >= 0) spmm_store_row<VEC>(Y + (r0 + cur) * static_cast<i64>(a.ldy), lane, on, acc0, acc1);
+          cur = rw[u];
+          acc0 = acc1 = 0.0;
+        }
+        acc0 = __dadd_rn(acc0, __dmul_rn(vv[u], x0[u]));
+        if (VEC) acc1 = __dadd_rn(acc1, __dmul_rn(vv[u], x1[u]));
+      }
+    }
+    if (cur >= 0) spmm_store_row<VEC>(Y + (r0 + cur) * static_cast<i64>(a.ldy), lane, on, acc0, acc1);
+    return;
+  }
+  // general case: row by row, the window moving with the rows
+  for (int i = 0; i < nr; ++i) {
+    const int s = __shfl_sync(0xffffffffu, rp_l, i), e = __shfl_sync(0xffffffffu, rp_l, i + 1);
+    if (e - s > kSegNnz) continue;
+    if (e > base + 32) {  // the window moves to this row (warp-uniform)
+      base = s;
+      c_l = 0;
+      v_l = 0.0;
+      if (base + lane < gend) {
+        c_l = a.col[base + lane];
+        v_l = a.val[base + lane];
+      }
+    }
+    int q = s - base;
+    const int qe = e - base;
+    if (a.col_lo > 0) q += __popc(__ballot_sync(0xffffffffu, lane >= q && lane < qe && c_l < a.col_lo));
+    double acc0 = 0.0, acc1 = 0.0;
+    for (; q + 4 <= qe; q += 4) {
+      double x0[4], x1[4], vv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = __shfl_sync(0xffffffffu, c_l, q + u);
+        vv[u] = __shfl_sync(0xffffffffu, v_l, q + u);
+        spmm_load_x<VEC>(X + static_cast<i64>(c) * a.ldx, lane, on, x0[u], x1[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc0 = __dadd_rn(acc0, __dmul_rn(vv[u], x0[u]));
+        if (VEC) acc1 = __dadd_rn(acc1, __dmul_rn(vv[u], x1[u]));
+      }
+    }
+    for (; q < qe; ++q) {
+      const int c = __shfl_sync(0xffffffffu, c_l, q);
+      const double vq = __shfl_sync(0xffffffffu, v_l, q);
+      double t0, t1;
+      spmm_load_x<VEC>(X + static_cast<i64>(c) * a.ldx, lane, on, t0, t1);
+      acc0 = __dadd_rn(acc0, __dmul_rn(vq, t0));
+      if (VEC) acc1 = __dadd_rn(acc1, __dmul_rn(vq, t1));
+    }
+    spmm_store_row<VEC>(Y + (r0 + i) * static_cast<i64>(a.ldy), lane, on, acc0, acc1);
+  }
+}
+
 // Rows of several segments: partial sums added in segment order.
 __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl) {
   const int i = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -115,7 +267,15 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl
   const double* p0 = pl.scratch + static_cast<i64>(pl.sstart[r]) * pl.lds;
   for (int cc = lane; cc < a.m; cc += 32) {
     double y = 0.0;
-    for (int s = 0; s < nseg; ++s) y = __dadd_rn(y, p0[static_cast<i64>(s) * pl.lds + cc]);
+    int s = 0;
+    for (; s + 8 <= nseg; s += 8) {  // eight loads in flight, sums still in segment order
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = p0[static_cast<i64>(s + u) * pl.lds + cc];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) y = __dadd_rn(y, t[u]);
+    }
+    for (; s < nseg; ++s) y = __dadd_rn(y, p0[static_cast<i64>(s) * pl.lds + cc]);
     a.Y[static_cast<i64>(r) * a.ldy + cc] = y;
   }
 }
@@ -129,7 +289,7 @@ __global__ void seg_count_kernel(const int* rowptr, i64 row_off, i64 rows, int* 
     return;
   }
   const int len = rowptr[r + row_off + 1] - rowptr[r + row_off];
-  const int c = len > kSegNnz ? (len + kSegNnz - 1) / kSegNnz : 1;
+  const int c = len > kSegNnz ? (len + kSegNnz - 1) / kSegNnz : 0;  // short rows: spmm_group_kernel
   cnt[r] = c;
   cnt2[r] = c > 1 ? c : 0;
 }
@@ -143,6 +303,16 @@ __global__ void seg_fill_kernel(const int* vstart, i64 rows, int* vrow, int* spl
 }
 
 inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 split_max, cudaStream_t st) {
+  {  // rows of at most kSegNnz nonzeros
+    const bool vec = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 &&
+                     ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
+    const int w = vec ? 64 : 32;
+    const dim3 g(static_cast<unsigned>(cdiv(cdiv(a.rows, kGroupRows), 8)), static_cast<unsigned>(cdiv(a.m, w)));
+    if (vec) spmm_group_kernel<true><<<g, 256, 0, st>>>(a);
+    else spmm_group_kernel<false><<<g, 256, 0, st>>>(a);
+    STG_LAUNCH();
+  }
+  if (split_max <= 0) return;  // no row longer than kSegNnz can exist
   const unsigned grid = static_cast<unsigned>(cdiv(vmax, 8));
   const int T = static_cast<int>(cdiv(a.m < 1 ? 1 : a.m, 32));
   switch (T) {
