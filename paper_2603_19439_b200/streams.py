@@ -215,3 +215,42 @@ def config3(seed=3, scale=20, steps=10, edge_factor=16):
     n = 1 << scale
     return edit_stream(n, keys, steps, seed + 1, lambda m: 0, lambda m: 0.005 * m,
                        new_nodes=lambda nn: nn // 100, new_degree=10, name=f"cfg3-rmat-s{scale}")
+
+
+def config4(seed=4, n=1 << 22, blocks=64, steps=10, avg_deg=32.0, intra=0.8, new_degree=16):
+    """SBM n=2^22, 64 equal blocks, average degree 32 with 80% of edges intra-block.
+    Per step: 1% edge inserts, 0.5% edge deletes, 0.5% * n new nodes with 16
+    edges each (80% into one random block, the rest anywhere), and 0.1% * n node
+    "removals". The reference has no node removal; as SURVEY.md
+    8(d) proposes, a removal deletes every incident edge and keeps the index as
+    an isolated node, which the reference's update model expresses exactly."""
+    bs = n // blocks
+    p_in = avg_deg * intra / (bs - 1)
+    p_out = avg_deg * (1 - intra) / (n - bs)
+    keys0 = sbm_keys(n, blocks, p_in, p_out, seed)
+    rng = np.random.default_rng(seed + 1)
+    es = _EdgeSet(n, keys0)
+    s = Stream(n, es.keys.copy(), name=f"cfg4-sbm{n}")
+    for _ in range(steps):
+        m = len(es.keys)
+        cur = es.n
+        # node removals: all incident edges
+        gone = np.unique(rng.integers(0, cur, size=max(1, cur // 1000)))
+        u, v = _unkey(es.keys)
+        inc = es.keys[np.isin(u, gone) | np.isin(v, gone)]
+        rnd = es.sample_existing(rng, int(0.005 * m))
+        removed = np.unique(np.concatenate([inc, rnd]))
+        added = es.sample_absent(rng, int(0.01 * m), forbid=removed)
+        au, av = _unkey(added)
+        added = added[~(np.isin(au, gone) | np.isin(av, gone))]
+        # new nodes: 16 distinct edges each, 80% into one random block
+        S = cur // 200
+        blk = rng.integers(0, blocks, size=S)
+        inb = rng.random((S, new_degree)) < intra
+        tgt = np.where(inb, blk[:, None] * bs + rng.integers(0, bs, size=(S, new_degree)),
+                       rng.integers(0, cur, size=(S, new_degree)))
+        newcomers = cur + np.repeat(np.arange(S), new_degree)
+        new_keys = np.unique(_keys(tgt.reshape(-1), newcomers))
+        s.updates.append(_update(added, removed, S, new_keys))
+        es.apply(added, removed, S, new_keys)
+    return s

@@ -36,7 +36,15 @@ def _cases():
         rp, col, val = s.csr0()
         return rp, col, val, dict(kind="grest-rsvd", k=8, seed=11), ("fixed", s.updates)
 
+    def cfg3_s15(steps=2):
+        from paper_2603_19439_b200 import streams
+
+        s = streams.config3(scale=15, steps=steps)
+        rp, col, val = s.csr0()
+        return rp, col, val, dict(kind="grest-rsvd", k=32, seed=5), ("fixed", s.updates), "init_eig"
+
     return {
+        "cfg3_s15": cfg3_s15,
         "rsvd_small": lambda: random_stream("grest-rsvd", 4, 3, False),
         "rsvd_bypass": lambda: random_stream("grest-rsvd", 100, 100, False),
         "grest2": lambda: random_stream("grest2", 100, 100, False),
@@ -62,12 +70,22 @@ def run(rank, world, port, case, chunk, q):
         from paper_2603_19439_b200.shard import ShardedTrackerSession, TorchComm, local_block, shard_bounds
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        rp, col, val, cfg, stream = _cases()[case]()
+        rp, col, val, cfg, stream, *init = _cases()[case]()
         n = len(rp) - 1
         a = po.Csr(n, np.asarray(rp, np.int32), np.asarray(col, np.int32), np.asarray(val, np.float64))
         ocfg = {k: v for k, v in cfg.items() if k != "force_dense"}
-        orc = po.Session(a, **ocfg)
-        vals, vecs = orc.embedding()
+        if init:  # leading eigenpairs from rank 0 (block Krylov on the GPU), shared by all ranks
+            from paper_2603_19439_b200 import init_eig
+
+            box = [None]
+            if rank == 0:
+                box[0] = init_eig.leading_eigenpairs(rp, col, val, cfg["k"], "abs_desc", device="cuda:0")
+            dist.broadcast_object_list(box, src=0)
+            vals, vecs = box[0]
+            orc = po.Session(a, values=vals, vectors=vecs, **ocfg)
+        else:
+            orc = po.Session(a, **ocfg)
+            vals, vecs = orc.embedding()
         bounds = shard_bounds(a.rowptr, world)
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         lrp, lcol, lval, lx = local_block(a.rowptr, a.col, a.val, vecs, lo, hi)

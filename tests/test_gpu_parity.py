@@ -316,3 +316,31 @@ def test_rank_deficient_candidates_are_dropped(kind, fan, n_new):
     gpu.step(upd)
     orc.step(upd)
     check_state(gpu, orc, tag=f"{kind} fan {fan}")
+
+
+@pytest.mark.gpu
+def test_config4_shape_parity_sbm():
+    """Config 4's shapes at a scale the oracle finishes in seconds: SBM with 64
+    equal blocks, average degree 32 (80% intra-block), k = 64, L = P = 100;
+    per step 1% inserts, 0.5% deletes, 0.5% new nodes with 16 edges each and
+    0.1% node removals (every incident edge deleted, the index kept isolated,
+    SURVEY.md 8(d)). D reaches 2k + L = 228: the 2-CTA tridiagonalization, a
+    164-wide candidate block and the sketch's q = 163..165 columns."""
+    from paper_2603_19439_b200 import TrackerSession, init_eig, streams
+
+    s = streams.config4(n=1 << 15, steps=3)
+    rp, col, val = s.csr0()
+    k = 64
+    vals, vecs = init_eig.leading_eigenpairs(rp, col, val, k, "abs_desc", device="cuda:0")
+    n = len(rp) - 1
+    a = po.Csr(n, np.asarray(rp, np.int32), np.asarray(col, np.int32), np.asarray(val, np.float64))
+    orc = po.Session(a, kind="grest-rsvd", k=k, seed=9, values=vals, vectors=vecs)
+    gpu = TrackerSession(a.rowptr, a.col, a.val, vals, vecs, kind="grest-rsvd", k=k, seed=9)
+    for t, upd in enumerate(s.updates):
+        assert upd.n_new > 100  # the randomized range finder runs
+        gpu.step(upd)
+        orc.step(upd)
+        ve, sa = check_state(gpu, orc, tag=f"cfg4-sbm32k step {t}")
+        print(f"cfg4-sbm32k step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
+        rp_t = gpu.csr(0)[0]
+        assert np.all(np.diff(rp_t)[:n] >= 0)

@@ -56,3 +56,10 @@ def test_sharded_one_rank():
 @pytest.mark.gpu
 def test_sharded_rmat_two_ranks():
     _run(2, "rmat13", chunk=16)
+
+
+@pytest.mark.gpu
+def test_sharded_config3_shape_two_ranks():
+    """Config 3's shapes (R-MAT s15, k = 32, L = P = 100: q = 200 sketch, D = 164)
+    row-sharded over two ranks."""
+    _run(2, "cfg3_s15", chunk=64)
