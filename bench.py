@@ -58,6 +58,12 @@ def make_workload(name: str, steps: int, seed_offset: int = 0, scale: int | None
         s = streams.config1(seed=1 + seed_offset, steps=steps)
         return s, dict(k=8, kind="grest-rsvd", order="abs_desc", operator="adjacency",
                        workload="cfg1 SBM n=10,000 4 blocks p_in=0.01 p_out=0.001, k=8; 500 inserts + 100 deletes")
+    if name == "cfg4":
+        s = streams.config4(seed=4 + seed_offset, steps=steps, n=1 << (scale or 22))
+        return s, dict(k=64, kind="grest-rsvd", order="abs_desc", operator="adjacency",
+                       workload=f"cfg4 SBM n=2^{scale or 22} 64 blocks avg deg 32 (80% intra), k=64 grest-rsvd "
+                                f"L=P=100; per step 1% inserts + 0.5% deletes + 0.5% new nodes x 16 edges + 0.1% "
+                                f"node removals")
     if name == "cfg2":
         s = streams.config2(seed=2 + seed_offset, steps=steps)
         return s, dict(k=16, kind="grest-rsvd", order="alg_desc", operator="normalized-laplacian",
@@ -236,14 +242,13 @@ def _run_ours(args, saved_stdout):
                                          chunk=1024, kernel_timing=kernel_timing, **kw_sh)
         return TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, **kw)
 
-    # ---- value: edit lists resident in HBM
-    sess = new_session(kernel_timing=True)
+    # ---- value: edit lists resident in HBM (no per-launch timing events)
     dev_updates = [DeviceUpdate(u, device=f"cuda:{local}") for u in stream.updates]
+    sess = new_session()
     for t in range(W):
         sess.step_device(dev_updates[t])
     torch.cuda.synchronize()
     barrier(world)
-    sess.reset_kernel_stats()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -254,12 +259,24 @@ def _run_ours(args, saved_stdout):
     for t in range(W, W + K):
         sess.step_device(dev_updates[t])
         launches += sess.launches()
+    torch.cuda.synchronize()  # the session's side streams included
     e1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = dist_max(e0.elapsed_time(e1), world)
-    kstats = sess.kernel_stats()
     info = sess.info()
+    sess.close()
+
+    # ---- per-kernel-class device time: the same steps again, CUDA events
+    # around every launch (ST_FLAG_KERNEL_TIMING), outside the timed region
+    sess = new_session(kernel_timing=True)
+    for t in range(W):
+        sess.step_device(dev_updates[t])
+    sess.reset_kernel_stats()
+    for t in range(W, W + K):
+        sess.step_device(dev_updates[t])
+    torch.cuda.synchronize()
+    kstats = sess.kernel_stats()
     sess.close()
     del dev_updates
 
@@ -276,6 +293,7 @@ def _run_ours(args, saved_stdout):
         sess.step(stream.updates[t])
         _ = sess.values()
         h2d += stream.updates[t].h2d_bytes()
+    torch.cuda.synchronize()
     f1.record()
     torch.cuda.synchronize()
     ms_e2e = dist_max(f0.elapsed_time(f1), world)
@@ -413,7 +431,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (development)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="row-sharded sessions even on one GPU (NCCL group of 1)")

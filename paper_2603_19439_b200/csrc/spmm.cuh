@@ -135,11 +135,20 @@ __device__ __forceinline__ void spmm_store_row(double* yr, int lane, bool on, do
   else yr[lane] = a0;
 }
 
+constexpr int kGroupWarps = 4;   // warps per CTA of spmm_group_kernel
+constexpr int kStageRows = 16;   // X rows staged per warp and batch
+
 template <bool VEC>
-__global__ void __launch_bounds__(256, 4) spmm_group_kernel(SpmmArgs a) {
+constexpr size_t spmm_group_smem() {
+  return sizeof(double) * kGroupWarps * kStageRows * (VEC ? 64 : 32);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(32 * kGroupWarps) spmm_group_kernel(SpmmArgs a) {
   constexpr int W = VEC ? 64 : 32;
-  constexpr int B = VEC ? 4 : 8;  // X rows gathered per batch
-  const i64 g = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  extern __shared__ __align__(16) double spmm_sx[];
+  const int wib = threadIdx.x >> 5;
+  const i64 g = static_cast<i64>(blockIdx.x) * kGroupWarps + wib;
   const int lane = threadIdx.x & 31;
   const i64 r0 = g * kGroupRows;
   if (r0 >= a.rows) return;
@@ -160,9 +169,11 @@ __global__ void __launch_bounds__(256, 4) spmm_group_kernel(SpmmArgs a) {
   double* Y = a.Y + c0;
   const bool on = VEC ? 2 * lane < m : lane < m;
   if (gend - base <= 32) {
-    // The group's entries fit one window and no row is long: the active
-    // entries (col >= col_lo) of all rows are gathered B at a time across row
-    // boundaries; each row still sums its own entries in column order.
+    // The group's entries fit one window and no row is long. The X rows of
+    // its active entries (col >= col_lo) are staged into shared memory with
+    // cp.async, up to kStageRows per batch, all in flight at once; the rows
+    // then sum their own entries in column order (bit-identical to above).
+    double* sx = spmm_sx + wib * kStageRows * W;
     int row_l = 0;  // row (within the group) of entry `lane`
 #pragma unroll
     for (int i = 1; i < kGroupRows; ++i) {
@@ -170,8 +181,7 @@ __global__ void __launch_bounds__(256, 4) spmm_group_kernel(SpmmArgs a) {
       row_l += (i < nr && base + lane >= ri) ? 1 : 0;
     }
     unsigned act = __ballot_sync(0xffffffffu, base + lane < gend && c_l >= a.col_lo);
-    // rows without an active entry are zero rows
-    bool has = false;
+    bool has = false;  // rows without an active entry are zero rows
     const int rp_next = __shfl_down_sync(0xffffffffu, rp_l, 1);
     if (lane < nr) {
       const int s = rp_l - base, e = rp_next - base;
@@ -188,28 +198,44 @@ __global__ void __launch_bounds__(256, 4) spmm_group_kernel(SpmmArgs a) {
     int cur = -1;
     double acc0 = 0.0, acc1 = 0.0;
     while (act) {
-      double x0[B], x1[B], vv[B];
-      int rw[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int j = act ? __ffs(act) - 1 : -1;
-        act &= act ? act - 1 : 0u;
-        rw[u] = j >= 0 ? __shfl_sync(0xffffffffu, row_l, j) : -1;
-        const int c = __shfl_sync(0xffffffffu, c_l, j < 0 ? 0 : j);
-        vv[u] = __shfl_sync(0xffffffffu, v_l, j < 0 ? 0 : j);
-        spmm_load_x<VEC>(X + static_cast<i64>(c) * a.ldx, lane, on && j >= 0, x0[u], x1[u]);
+      unsigned rest = act;
+      int ns = 0;
+      for (; ns < kStageRows && rest; ++ns) {
+        const int j = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const int c = __shfl_sync(0xffffffffu, c_l, j);
+        const double* xr = X + static_cast<i64>(c) * a.ldx;
+        if (on) {
+          if (VEC) cp_async16(sx + ns * W + 2 * lane, xr + 2 * lane);
+          else cp_async8(sx + ns * W + lane, xr + lane);
+        }
       }
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        if (rw[u] < 0) break;
-        if (rw[u] != cur) {
+      cp_async_commit();
+      unsigned batch = act & ~rest;
+      act = rest;
+      cp_async_wait<0>();
+      __syncwarp();
+      for (int s2 = 0; s2 < ns; ++s2) {
+        const int j = __ffs(batch) - 1;
+        batch &= batch - 1;
+        const int rw = __shfl_sync(0xffffffffu, row_l, j);
+        const double vq = __shfl_sync(0xffffffffu, v_l, j);
+        if (rw != cur) {
           if (cur >= 0) spmm_store_row<VEC>(Y + (r0 + cur) * static_cast<i64>(a.ldy), lane, on, acc0, acc1);
-          cur = rw[u];
+          cur = rw;
           acc0 = acc1 = 0.0;
         }
-        acc0 = __dadd_rn(acc0, __dmul_rn(vv[u], x0[u]));
-        if (VEC) acc1 = __dadd_rn(acc1, __dmul_rn(vv[u], x1[u]));
+        if (on) {
+          if (VEC) {
+            const double2 t = *reinterpret_cast<const double2*>(sx + s2 * W + 2 * lane);
+            acc0 = __dadd_rn(acc0, __dmul_rn(vq, t.x));
+            acc1 = __dadd_rn(acc1, __dmul_rn(vq, t.y));
+          } else {
+            acc0 = __dadd_rn(acc0, __dmul_rn(vq, sx[s2 * W + lane]));
+          }
+        }
       }
+      __syncwarp();  // the next batch overwrites the staging rows
     }
     if (cur >= 0) spmm_store_row<VEC>(Y + (r0 + cur) * static_cast<i64>(a.ldy), lane, on, acc0, acc1);
     return;
@@ -307,9 +333,9 @@ inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 spl
     const bool vec = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 &&
                      ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
     const int w = vec ? 64 : 32;
-    const dim3 g(static_cast<unsigned>(cdiv(cdiv(a.rows, kGroupRows), 8)), static_cast<unsigned>(cdiv(a.m, w)));
-    if (vec) spmm_group_kernel<true><<<g, 256, 0, st>>>(a);
-    else spmm_group_kernel<false><<<g, 256, 0, st>>>(a);
+    const dim3 g(static_cast<unsigned>(cdiv(cdiv(a.rows, kGroupRows), kGroupWarps)), static_cast<unsigned>(cdiv(a.m, w)));
+    if (vec) spmm_group_kernel<true><<<g, 32 * kGroupWarps, spmm_group_smem<true>(), st>>>(a);
+    else spmm_group_kernel<false><<<g, 32 * kGroupWarps, spmm_group_smem<false>(), st>>>(a);
     STG_LAUNCH();
   }
   if (split_max <= 0) return;  // no row longer than kSegNnz can exist
