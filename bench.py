@@ -64,6 +64,15 @@ def make_workload(name: str, steps: int, seed_offset: int = 0, scale: int | None
                        workload=f"cfg4 SBM n=2^{scale or 22} 64 blocks avg deg 32 (80% intra), k=64 grest-rsvd "
                                 f"L=P=100; per step 1% inserts + 0.5% deletes + 0.5% new nodes x 16 edges + 0.1% "
                                 f"node removals")
+    if name == "cfg5":
+        import torch
+
+        sc = scale or 25
+        s = streams.config5(seed=5 + seed_offset, scale=sc, steps=steps, device=f"cuda:{torch.cuda.current_device()}")
+        return s, dict(k=32, kind="grest-rsvd", order="abs_desc", operator="adjacency",
+                       workload=f"cfg5 R-MAT scale {sc} ef16 (0.57,0.19,0.19,0.05) symmetrized+dedup, k=32 "
+                                f"grest-rsvd L=P=100; per step 0.1% edge inserts + 0.1% new nodes x 16 PA edges "
+                                f"(graph generated on the GPU with torch's generator)")
     if name == "cfg2":
         s = streams.config2(seed=2 + seed_offset, steps=steps)
         return s, dict(k=16, kind="grest-rsvd", order="alg_desc", operator="normalized-laplacian",
@@ -215,9 +224,20 @@ def _run_ours(args, saved_stdout):
     t_setup = time.time()
     replicas = world > 1 and args.replicas
     stream, wl = make_workload(args.config, W + K, seed_offset=rank if replicas else 0, scale=args.scale)
-    rp, col, val = stream.csr0()
-    orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
-    vals0, vecs0 = init_eig.leading_eigenpairs(orp, ocol, oval, wl["k"], wl["order"], device=f"cuda:{local}")
+    if hasattr(stream, "csr0_torch"):  # config 5: the start graph is already on the device
+        trp, tcol, tval = stream.csr0_torch()
+        n_ = trp.numel() - 1
+        A_t = torch.sparse_csr_tensor(trp, tcol, tval, size=(n_, n_))
+        v_t, x_t = init_eig.leading_eigenpairs_torch(A_t, wl["k"], wl["order"], depth=1, restarts=5)
+        vals0, vecs0 = v_t.cpu().numpy(), x_t.cpu().numpy()
+        del A_t, v_t, x_t, trp, tcol, tval
+        rp, col, val = stream.csr0()
+        stream.release()
+        torch.cuda.empty_cache()
+    else:
+        rp, col, val = stream.csr0()
+        orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
+        vals0, vecs0 = init_eig.leading_eigenpairs(orp, ocol, oval, wl["k"], wl["order"], device=f"cuda:{local}")
     setup_s = time.time() - t_setup
     kw = dict(kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0, device=local)
 
@@ -347,12 +367,13 @@ def _run_ours(args, saved_stdout):
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded R-MAT + preferential-attachment stream; BASELINE config 3 shapes)",
+        "data": f"synthetic (seeded stream, BASELINE {args.config} shapes)",
         "config": {"workload": wl["workload"], "n0": int(len(rp) - 1), "nnz0": int(rp[-1]), "k": wl["k"],
                    "kind": wl["kind"], "rsvd_l": 100, "rsvd_p": 100, "n_final": info["n"],
                    "parallelism": (f"row-sharded over {world} GPU(s) (NCCL allreduce of Grams, allgather halo)"
                                    if sharded else "single GPU" if world == 1 else f"{world} independent replicas"),
-                   "l2": "inputs larger than L2 (CSR ~0.38 GB + X ~0.27 GB per stream)",
+                   "l2": f"inputs larger than L2 (CSR {12 * int(rp[-1]) / 1e9:.2f} GB + X "
+                         f"{8 * wl['k'] * (len(rp) - 1) / 1e9:.2f} GB per stream)",
                    "setup_s": round(setup_s, 1)},
         "roofline": roof,
         "kernel_classes": classes,
@@ -361,7 +382,11 @@ def _run_ours(args, saved_stdout):
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and args.config == "cfg5" and not args.no_cpu_baseline:
+        out["cpu_baseline"] = {"value": None, "unit": "steps/s", "cores": os.cpu_count() or 1, "kind": "port",
+                               "sample": "not run: one oracle step at R-MAT s25 is hours of CPU work and ~150 GB "
+                                         "of host RAM (SURVEY.md 8(d)); see the cfg3 line for the CPU baseline"}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         dt, dt_tracker = cpu_baseline(stream, vals0, vecs0, wl, threads)
         out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "steps/s", "cores": threads, "kind": "port",
@@ -431,7 +456,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (development)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="row-sharded sessions even on one GPU (NCCL group of 1)")

@@ -18,6 +18,18 @@ def leading_eigenpairs(rowptr, col, val, k: int, order: str = "abs_desc", depth:
     A = torch.sparse_csr_tensor(torch.as_tensor(np.asarray(rowptr, np.int64)),
                                 torch.as_tensor(np.asarray(col, np.int64)),
                                 torch.as_tensor(np.asarray(val, np.float64)), size=(n, n)).to(device)
+    vals, X = leading_eigenpairs_torch(A, k, order, depth, restarts, seed)
+    return vals.cpu().numpy(), X.cpu().numpy()
+
+
+def leading_eigenpairs_torch(A, k: int, order: str = "abs_desc", depth: int = 6, restarts: int = 3, seed: int = 0):
+    """The same on a torch sparse CSR operator already on the device (int32
+    indices are fine); returns device tensors. Memory ~ (depth + 3) n x (k+16)
+    doubles, so R-MAT s25 runs it with depth 1."""
+    import torch
+
+    n = A.shape[0]
+    device = A.device
     g = torch.Generator(device=device).manual_seed(seed)
     b = min(n, k + 16)
     Q, _ = torch.linalg.qr(torch.randn(n, b, dtype=torch.float64, device=device, generator=g))
@@ -40,5 +52,6 @@ def leading_eigenpairs(rowptr, col, val, k: int, order: str = "abs_desc", depth:
         Q = V @ F[:, :b]
     X = V @ F[:, :k]
     X, _ = torch.linalg.qr(X)  # exact orthonormality for the tracker
+    del V, F, Q
     vals = torch.diag(X.T @ torch.sparse.mm(A, X))
-    return vals.cpu().numpy(), X.cpu().numpy()
+    return vals, X

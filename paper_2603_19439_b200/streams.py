@@ -254,3 +254,152 @@ def config4(seed=4, n=1 << 22, blocks=64, steps=10, avg_deg=32.0, intra=0.8, new
         s.updates.append(_update(added, removed, S, new_keys))
         es.apply(added, removed, S, new_keys)
     return s
+
+
+# ------------------------------------------------- config 5 (device-side generator)
+class TorchStream:
+    """A stream whose start graph is built and kept as torch tensors (GPU for
+    R-MAT scale 25: ~1.07B stored entries, out of reach of the numpy path).
+    `csr0()` returns host arrays like `Stream.csr0`; `csr0_torch()` the device
+    ones (int32 rowptr / int32 col / fp64 val)."""
+
+    def __init__(self, n0, rowptr, col, updates, name):
+        self.n0 = n0
+        self._rp, self._col = rowptr, col
+        self.updates = updates
+        self.name = name
+
+    @property
+    def nnz0(self) -> int:
+        return int(self._col.numel())
+
+    def csr0_torch(self):
+        import torch
+
+        return self._rp, self._col, torch.ones(self._col.numel(), dtype=torch.float64, device=self._col.device)
+
+    def csr0(self):
+        return (self._rp.cpu().numpy(), self._col.cpu().numpy(), np.ones(self._col.numel(), np.float64))
+
+    def release(self):
+        self._rp = self._col = None
+
+
+def rmat_keys_torch(scale: int, edge_factor: int, abcd=(0.57, 0.19, 0.19, 0.05), seed: int = 0, device="cuda"):
+    """`rmat_keys` on a torch device (torch's Philox stream instead of numpy's
+    PCG64, so the graph differs from rmat_keys at the same seed; same model:
+    one draw in [0, 100) per level per edge, symmetrized, self-loops dropped,
+    deduplicated, sorted undirected keys lo << 32 | hi)."""
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    m = edge_factor << scale
+    pa, pb, pc = (int(round(100 * x)) for x in abcd[:3])
+    t1, t2, t3 = pa, pa + pb, pa + pb + pc
+    u = torch.zeros(m, dtype=torch.int64, device=device)
+    v = torch.zeros(m, dtype=torch.int64, device=device)
+    for lvl in range(scale):
+        r = torch.randint(0, 100, (m,), generator=g, device=device, dtype=torch.int16)
+        sh = scale - 1 - lvl
+        down = r >= t2
+        right = (r >= t1) ^ down ^ (r >= t3)
+        del r
+        u |= down.to(torch.int64) << sh
+        v |= right.to(torch.int64) << sh
+        del down, right
+    keep = u != v
+    lo = torch.minimum(u, v)[keep]
+    hi = torch.maximum(u, v)[keep]
+    del u, v, keep
+    k = (lo << 32) | hi
+    del lo, hi
+    return torch.unique(k)  # sorted
+
+
+def csr_from_keys_torch(n: int, keys):
+    """`csr_from_keys` (unit weights) on a torch device: int32 rowptr / col."""
+    import torch
+
+    lo, hi = keys >> 32, keys & 0xFFFFFFFF
+    both = torch.cat([(lo << 32) | hi, (hi << 32) | lo])
+    del lo, hi
+    both, _ = torch.sort(both)
+    rows = both >> 32
+    col = (both & 0xFFFFFFFF).to(torch.int32)
+    del both
+    rowptr = torch.zeros(n + 1, dtype=torch.int64, device=keys.device)
+    rowptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
+    del rows
+    return rowptr.to(torch.int32), col
+
+
+def config5(seed=5, scale=25, steps=5, edge_factor=16, new_degree=16, device="cuda"):
+    """R-MAT scale 25, ef 16, (0.57,0.19,0.19,0.05), symmetrized and
+    deduplicated; per step 0.1% of the edges inserted uniformly over
+    non-edges and 0.1% new nodes with `new_degree` distinct preferential-
+    attachment edges each (targets drawn proportional to pre-step degree from
+    the endpoint pool, as edit_stream). Built on `device` with torch; the
+    update batches are host edit lists like every other stream."""
+    import torch
+
+    n = 1 << scale
+    keys0 = rmat_keys_torch(scale, edge_factor, seed=seed, device=device)
+    rowptr, col = csr_from_keys_torch(n, keys0)
+    g = torch.Generator(device=device).manual_seed(seed + 1)
+    nnz0 = col.numel()
+    extra = torch.zeros(0, dtype=torch.int64, device=device)  # endpoints of edges added by earlier steps
+    prior = torch.zeros(0, dtype=torch.int64, device=device)  # keys added by earlier steps (sorted)
+    m_edges, cur = keys0.numel(), n
+    updates = []
+
+    def has(k):
+        pos = torch.searchsorted(keys0, k).clamp_max(keys0.numel() - 1)
+        hit = keys0[pos] == k
+        if prior.numel():
+            p2 = torch.searchsorted(prior, k).clamp_max(prior.numel() - 1)
+            hit |= prior[p2] == k
+        return hit
+
+    def by_degree(size):
+        idx = torch.randint(0, nnz0 + extra.numel(), (size,), generator=g, device=device)
+        out = col[idx.clamp_max(nnz0 - 1)].to(torch.int64)
+        if extra.numel():
+            ex = idx >= nnz0
+            out[ex] = extra[idx[ex] - nnz0]
+        return out
+
+    for _ in range(steps):
+        n_ins = m_edges // 1000
+        added = torch.zeros(0, dtype=torch.int64, device=device)
+        while added.numel() < n_ins:
+            want = 2 * (n_ins - added.numel()) + 16
+            a = torch.randint(0, cur, (want,), generator=g, device=device)
+            b = torch.randint(0, cur, (want,), generator=g, device=device)
+            ok = a != b
+            k = (torch.minimum(a, b)[ok] << 32) | torch.maximum(a, b)[ok]
+            k = torch.unique(k)
+            k = k[~has(k)]
+            added = torch.unique(torch.cat([added, k]))
+        added = added[torch.randperm(added.numel(), generator=g, device=device)[:n_ins]]
+        S = cur // 1000
+        tgt = by_degree(S * new_degree).reshape(S, new_degree)
+        for _r in range(64):  # redraw repeated targets of one newcomer
+            srt, _ = torch.sort(tgt, dim=1)
+            dup = torch.zeros_like(srt, dtype=torch.bool)
+            dup[:, 1:] = srt[:, 1:] == srt[:, :-1]
+            if not bool(dup.any()):
+                break
+            tgt = srt
+            tgt[dup] = by_degree(int(dup.sum()))
+        newcomers = cur + torch.arange(S, device=device).repeat_interleave(new_degree)
+        tg = tgt.reshape(-1)
+        new_keys = torch.unique((torch.minimum(tg, newcomers) << 32) | torch.maximum(tg, newcomers))
+        hk = lambda t: t.cpu().numpy()  # noqa: E731
+        updates.append(_update(hk(added), np.zeros(0, np.int64), S, hk(new_keys)))
+        ends = torch.cat([added >> 32, added & 0xFFFFFFFF, new_keys >> 32, new_keys & 0xFFFFFFFF])
+        extra = torch.cat([extra, ends])
+        prior, _ = torch.sort(torch.cat([prior, added, new_keys]))
+        m_edges += added.numel() + new_keys.numel()
+        cur += S
+    del keys0, prior, extra
+    return TorchStream(n, rowptr, col, updates, name=f"cfg5-rmat-s{scale}")

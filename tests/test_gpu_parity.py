@@ -344,3 +344,28 @@ def test_config4_shape_parity_sbm():
         print(f"cfg4-sbm32k step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
         rp_t = gpu.csr(0)[0]
         assert np.all(np.diff(rp_t)[:n] >= 0)
+
+
+@pytest.mark.gpu
+def test_config5_shape_parity_rmat17():
+    """Config 5's stream rules at a scale the oracle finishes in seconds
+    (R-MAT s17 from the device generator bench.py uses at s25): per step 0.1%
+    of the edges inserted over non-edges and 0.1% new nodes (131 > L, so the
+    randomized range finder runs) with 16 preferential-attachment edges each,
+    no deletions, k = 32, both paths from the same leading eigenpairs."""
+    from paper_2603_19439_b200 import TrackerSession, init_eig, streams
+
+    s = streams.config5(scale=17, steps=3, device="cuda:0")
+    rp, col, val = s.csr0()
+    k = 32
+    vals, vecs = init_eig.leading_eigenpairs(rp, col, val, k, "abs_desc", device="cuda:0")
+    n = len(rp) - 1
+    a = po.Csr(n, np.asarray(rp, np.int32), np.asarray(col, np.int32), np.asarray(val, np.float64))
+    orc = po.Session(a, kind="grest-rsvd", k=k, seed=7, values=vals, vectors=vecs)
+    gpu = TrackerSession(a.rowptr, a.col, a.val, vals, vecs, kind="grest-rsvd", k=k, seed=7)
+    for t, upd in enumerate(s.updates):
+        assert upd.n_new > 100 and len(upd.removed[0]) == 0
+        gpu.step(upd)
+        orc.step(upd)
+        ve, sa = check_state(gpu, orc, tag=f"cfg5-s17 step {t}")
+        print(f"cfg5-s17 step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
