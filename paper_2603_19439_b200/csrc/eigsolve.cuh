@@ -426,7 +426,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads)
 // is below max(2 eps |lambda|, eps ||T||), the absolute accuracy of QR-based
 // solvers; the returned value is the bracket's lower end (count <= j).
 constexpr int kBisG = 32;  // one warp per eigenvalue: a 33-way split per Sturm round
-__global__ void __launch_bounds__(128) bisect_kernel(EigBufs b, int n) {
+// The Sturm chains are FP64 latency-bound and lose most of their issue slots
+// to co-resident DMMA CTAs when the sketch's solve overlaps the basis work on
+// the side stream (706 vs ~130 us measured at D = 200). Each CTA therefore
+// reserves more shared memory than an SM keeps free beside any Gram/NN CTA
+// (>= 70 KB each), so it only lands on an SM of its own.
+constexpr int kBisThreads = 256;
+constexpr size_t kBisSmem = 164 * 1024;
+static_assert(kBisSmem >= sizeof(double) * 2 * kEigMaxN, "d and e2 fit");
+__global__ void __launch_bounds__(kBisThreads) bisect_kernel(EigBufs b, int n) {
   extern __shared__ double sh[];
   double* d = sh;
   double* e2 = sh + n;
@@ -742,6 +750,8 @@ inline void eig_set_attributes() {
                                 static_cast<int>(sizeof(double) * 2 * kBtRows * kEigMaxN)));
   STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(invit_smem_bytes(kEigMaxN))));
+  STG_CUDA(cudaFuncSetAttribute(bisect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kBisSmem)));
 }
 
 template <class Launch>
@@ -757,7 +767,9 @@ void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int
     const int g = tridiag_gmax(n, 2);
     L(tridiag2_kernel, dim3(2), dim3(kTriThreads), tridiag_smem_bytes(n, 2, g), M, ldm, n, sym_input, g, b, flags);
   }
-  L(bisect_kernel, dim3(static_cast<unsigned>(cdiv(kBisG * n, 128))), dim3(128), sizeof(double) * 2 * n, b, n);
+  static const bool bis_shared = !getenv("STG_BIS_NOISOLATE");  // development A/B
+  L(bisect_kernel, dim3(static_cast<unsigned>(cdiv(kBisG * n, kBisThreads))), dim3(kBisThreads),
+    bis_shared ? kBisSmem : sizeof(double) * 2 * n, b, n);
   L(select_kernel, dim3(1), dim3(256), (sizeof(double) + 3 * sizeof(int)) * n, b, n, order, want, ortol, w_sorted);
   L(invit_kernel, dim3(static_cast<unsigned>(cdiv(want, kInvitThreads))), dim3(kInvitThreads), invit_smem_bytes(n), b,
     n);

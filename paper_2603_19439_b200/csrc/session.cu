@@ -1117,7 +1117,16 @@ class Session {
     cudaStream_t es = s ? s : st_;
     kbegin(kEig, 4.0 * D * D * D / 3.0, es);
     if (!s) STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
-    syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, es, args...); },
+    int part = 0;
+    syev_launch(
+        [&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) {
+          if (klog_) {  // timeline of the solver's kernels (double-counted in kstats: STG_KLOG only)
+            snprintf(ktag_, sizeof(ktag_), "  eig D=%d part %d grid %u", D, part++, g.x);
+            kbegin(kEig, 0.0, es);
+          }
+          launch(kernel, g, bl, sm, es, args...);
+          if (klog_) kend(es);
+        },
                 M, ldm, D, /*sym_input: exactly mirrored Grams / RR matrix*/ 1, order, wv, ortol, w_sorted, F, ldf,
                 dbuf, ibuf, flagsp ? flagsp : flags_ptr());
     kend(es);
@@ -1265,6 +1274,8 @@ class Session {
     pt.stamp = stamp_;
     STG_CUDA(cudaMemsetAsync(d_scal_, 0xff, sizeof(u64) * 2, st_));  // err_edit, err_apply = MAX
     STG_CUDA(cudaMemsetAsync(d_scal_ + 2, 0, sizeof(u64) * 3, st_));  // nvalid, flags, info
+    if (klog_) snprintf(ktag_, sizeof(ktag_), "ingest: upload, validation, Delta");
+    kbegin(kIngestOther, 0.0);
     EditsDev ed;
     if (device_ptrs) {
       ed.ai = reinterpret_cast<const i64*>(u.added_i);
@@ -1379,6 +1390,7 @@ class Session {
       }
       scan_int(dcnt, drp, n_total + 1);
     }
+    kend();
     if (sh_) return ingest_shard_tail(pt, u, device_ptrs, sort_path, ed, ekey_s, eval_s, dcol, drp, n2);
     // ---- apply_update merge (A_next in the spare slot)
     const DevCsr& a = A();
@@ -1386,6 +1398,9 @@ class Session {
     size_t merge_pend = 0;
     DevCsr an = merge_launch(a, n_old, n_total, ekey_s, eval_s, n2, drow, dcol, drp, mark_delta_, ed.kb, slot,
                              keep_delta && !is_laplacian(), err_apply, &merge_pend);
+    const bool kt_p = !is_laplacian();  // (the Laplacian path syncs inside)
+    if (kt_p && klog_) snprintf(ktag_, sizeof(ktag_), "ingest: P, sizes");
+    if (kt_p) kbegin(kIngestOther, 0.0);
     // ---- validation outcome and sizes: read back here for the Laplacian
     // operators (their assembly needs nnz); the adjacency path folds this read
     // into the P-size sync below (nothing is committed before either)
@@ -1476,6 +1491,7 @@ class Session {
     launch(scatter_p_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const int*>(flag),
            static_cast<const int*>(pos), n_total, P, posmap_);
     STG_CUDA(cudaMemcpyAsync(&hs_->p, pos + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    if (kt_p) kend();
     STG_CUDA(cudaStreamSynchronize(st_));
     if (!is_laplacian()) {
       if (redo()) return ingest(u, keep_delta, device_ptrs, true);
