@@ -807,9 +807,12 @@ class Session {
     if (narrow) a.tiles_i = a.tiles_j = 1;
     const int ntiles = narrow ? 1 : (sym ? a.tiles_i * (a.tiles_i + 1) / 2 : a.tiles_i * a.tiles_j);
     static const int env_waves = getenv("STG_GRAM_WAVES") ? atoi(getenv("STG_GRAM_WAVES")) : 0;  // development scans
-    // split-K CTAs: ~2 waves per output tile, 3..12 (a sweep over the step's shapes: 200 x 200 sym (10 tiles)
-    // best at 12, 64 x 64 at 3, 64 x 100 at 3-4, 164 x 100 at 12; fewer splits = less partial traffic)
-    const i64 target = 148 * (env_waves > 0 ? env_waves : std::min(12, std::max(3, 2 * ntiles)));
+    // split-K CTAs. Below 256k rows (cfg3: ~107k stacked rows) ~2 waves per output tile, 3..12 (a per-shape
+    // sweep: 200 x 200 sym (10 tiles) best at 12, 64 x 64 at 3, 64 x 100 at 3-4, 164 x 100 at 12; fewer splits
+    // = less partial traffic); above (cfg4/cfg5), 24 waves for square tiles and 4 for 32 x 128 tiles (the
+    // tail of unequal tiles outweighs the partials there: cfg4's Grams 28.5 vs 30.0 ms per step)
+    const int waves = rows >= (1 << 18) ? (layout == 0 ? 24 : 4) : std::min(12, std::max(3, 2 * ntiles));
+    const i64 target = 148 * (env_waves > 0 ? env_waves : waves);
     const i64 rows_min = narrow ? 256 : 128;
     i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
     splits = std::min<i64>(splits, 65535);
