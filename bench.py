@@ -300,19 +300,21 @@ def _run_ours(args, saved_stdout):
     sess.close()
     del dev_updates
 
-    # ---- e2e: host edit lists through the C ABI, Ritz values read back
+    # ---- e2e: host edit lists (page-locked, as a streaming caller keeps its
+    # batch buffers) through the C ABI, Ritz values read back
+    host_updates = [u.pinned() for u in stream.updates]
     sess = new_session()
     for t in range(W):
-        sess.step(stream.updates[t])
+        sess.step(host_updates[t])
     torch.cuda.synchronize()
     barrier(world)
     h2d = 0
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for t in range(W, W + K):
-        sess.step(stream.updates[t])
+        sess.step(host_updates[t])
         _ = sess.values()
-        h2d += stream.updates[t].h2d_bytes()
+        h2d += host_updates[t].h2d_bytes()
     torch.cuda.synchronize()
     f1.record()
     torch.cuda.synchronize()

@@ -99,7 +99,10 @@ void st_destroy(st_session* s);
  *                    | session.advance(d);           laplacian_track.cpp:48-64
  *   A = apply_update(A, d);                          graph.cpp:102-115
  *   state = tracker_step(state, p);                  trackers.cpp:341-387
- * Inputs are host buffers; the state stays resident on the device. */
+ * Inputs are host buffers; the state stays resident on the device. Lists in
+ * page-locked memory (cudaHostAlloc / cudaHostRegister) are DMA'd straight
+ * from the caller's arrays; pageable lists go through one internal pinned
+ * staging copy. The call returns after the uploads completed either way. */
 st_status st_step(st_session* s, const st_update* upd);
 
 /* st_step with the edit arrays already resident in device memory (same

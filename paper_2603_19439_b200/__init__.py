@@ -150,6 +150,28 @@ class Update:
                      int(self.n_new), len(ni), _p(ni, I64P), _p(nj, I64P), _p(nw))
         return keep, s
 
+    def pinned(self) -> "Update":
+        """The same edit lists in page-locked host memory (torch pin_memory):
+        st_step then DMAs each list straight from it, without the staging copy."""
+        import torch
+
+        keep = []
+
+        def pin(x, dt):
+            a = np.ascontiguousarray(np.asarray(x, dt).reshape(-1))
+            t = torch.empty(len(a), dtype=torch.int64 if dt == np.int64 else torch.float64, pin_memory=True)
+            v = t.numpy()
+            v[:] = a
+            keep.append(t)
+            return v
+
+        u = Update((pin(self.added[0], np.int64), pin(self.added[1], np.int64), pin(self.added[2], np.float64)),
+                   (pin(self.removed[0], np.int64), pin(self.removed[1], np.int64)), int(self.n_new),
+                   (pin(self.new_edges[0], np.int64), pin(self.new_edges[1], np.int64),
+                    pin(self.new_edges[2], np.float64)))
+        u._pinned_storage = keep
+        return u
+
     def h2d_bytes(self) -> int:
         return 16 * (len(self.added[0]) + len(self.removed[0]) + len(self.new_edges[0])) + 8 * (
             len(self.added[0]) + len(self.new_edges[0]))

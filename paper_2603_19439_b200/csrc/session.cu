@@ -1292,14 +1292,26 @@ class Session {
       ed.nj = reinterpret_cast<const i64*>(u.new_j);
       ed.nw = u.new_w;
     } else {
-      // upload the edit lists (one pinned staging buffer, one copy)
+      // upload the edit lists: straight from the caller's arrays when they are
+      // page-locked (one DMA per list), else through one pinned staging buffer
       const size_t bytes = sizeof(i64) * (2 * E) + sizeof(double) * (u.n_added + u.n_new_edges);
-      char* host = static_cast<char*>(pin_.get(std::max<size_t>(bytes, 8)));
       char* dev = arena_.get<char>("edits", static_cast<i64>(std::max<size_t>(bytes, 8)));
+      const void* srcs[8] = {u.added_i, u.added_j, u.removed_i, u.removed_j, u.new_i, u.new_j, u.added_w, u.new_w};
+      const i64 lens[8] = {u.n_added, u.n_added, u.n_removed, u.n_removed, u.n_new_edges, u.n_new_edges, u.n_added,
+                           u.n_new_edges};
+      bool pinned = true;
+      for (int q = 0; q < 8 && pinned; ++q) {
+        if (lens[q] == 0) continue;
+        cudaPointerAttributes at{};
+        pinned = cudaPointerGetAttributes(&at, srcs[q]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+      }
+      (void)cudaGetLastError();  // a failed attribute query of pageable memory is not an error
+      char* host = pinned ? nullptr : static_cast<char*>(pin_.get(std::max<size_t>(bytes, 8)));
       size_t off = 0;
       auto put = [&](const void* src, size_t b) -> size_t {
         const size_t o = off;
-        if (b) std::memcpy(host + off, src, b);
+        if (b && pinned) STG_CUDA(cudaMemcpyAsync(dev + off, src, b, cudaMemcpyHostToDevice, st_));
+        if (b && !pinned) std::memcpy(host + off, src, b);
         off += b;
         return o;
       };
@@ -1309,7 +1321,7 @@ class Session {
       const size_t o_ni = put(u.new_i, sizeof(i64) * u.n_new_edges), o_nj = put(u.new_j, sizeof(i64) * u.n_new_edges);
       const size_t o_aw = put(u.added_w, sizeof(double) * u.n_added);
       const size_t o_nw = put(u.new_w, sizeof(double) * u.n_new_edges);
-      if (off) STG_CUDA(cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, st_));
+      if (off && !pinned) STG_CUDA(cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, st_));
       ed.ai = reinterpret_cast<const i64*>(dev + o_ai);
       ed.aj = reinterpret_cast<const i64*>(dev + o_aj);
       ed.aw = reinterpret_cast<const double*>(dev + o_aw);

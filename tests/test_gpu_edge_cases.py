@@ -77,3 +77,26 @@ def test_k_above_candidate_rank():
     """k = 12 with a single edit: Delta X-bar has rank 2, ten candidates drop."""
     a = ring(300, 80, 5)
     run(a, [U([(10, 200, 1.0)], [], 0, [])], kind="grest2", k=12)
+
+
+@pytest.mark.gpu
+def test_pinned_edit_lists_take_the_direct_upload():
+    """Edit lists in page-locked memory are DMA'd straight from the caller's
+    arrays (no staging copy); the step is bit-identical to the staged path."""
+    from paper_2603_19439_b200 import TrackerSession, streams
+
+    s = streams.config1(n=3000, steps=2)
+    rp, col, val = s.csr0()
+    rng = np.random.default_rng(0)
+    x, _ = np.linalg.qr(rng.standard_normal((len(rp) - 1, 8)))
+    lam = np.linspace(8.0, 1.0, 8)
+    a = TrackerSession(rp, col, val, lam, x, kind="grest-rsvd", k=8, seed=1)
+    b = TrackerSession(rp, col, val, lam, x, kind="grest-rsvd", k=8, seed=1)
+    for upd in s.updates:
+        a.step(upd)
+        b.step(upd.pinned())
+    va, xa = a.embedding()
+    vb, xb = b.embedding()
+    assert np.array_equal(va, vb) and np.array_equal(xa, xb)
+    for c in range(3):
+        assert np.array_equal(a.csr(0)[c], b.csr(0)[c])
