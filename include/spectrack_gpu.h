@@ -116,6 +116,13 @@ st_status st_info(const st_session* s, int64_t* n, int64_t* k, uint64_t* steps_t
 
 /* SpectralEmbedding (trackers.hpp:28-34): values[k], vectors n x k column-major. */
 st_status st_get_embedding(const st_session* s, double* values, double* vectors, int64_t ld);
+
+/* norms[i] = ||Op x_i - theta_i x_i||_2 for the k tracked pairs on the current
+ * operator (A, or the shifted Laplacian T): the per-vector residual of the
+ * reference's Lanczos convergence test (lanczos.hpp:85-95), computed on the
+ * device with one full-operator SpMM (Op X) so a caller can monitor tracking
+ * quality at any size without copying X to the host. Unsharded sessions. */
+st_status st_residual_norms(st_session* s, double* norms);
 /* Ritz values only (k doubles), the per-step result read by the e2e benchmark. */
 st_status st_get_values(const st_session* s, double* values);
 

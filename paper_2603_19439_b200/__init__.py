@@ -28,7 +28,7 @@ OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
 ORDER = {"abs_desc": 0, "alg_desc": 1}
 FLAG_FORCE_DENSE, FLAG_TIMING, FLAG_KERNEL_TIMING, FLAG_CUSOLVER_EIG = 1, 2, 4, 8
 KERNEL_CLASSES = ["dmma_gram", "dmma_gemm", "spmm", "cholesky", "tri_inverse", "eigensolver", "csr_merge", "rng",
-                  "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other"]
+                  "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other", "spmm_full"]
 
 
 class StConfig(C.Structure):
@@ -68,6 +68,7 @@ def lib():
         L.st_step.argtypes = [C.c_void_p, C.POINTER(StUpdate)]
         L.st_info.argtypes = [C.c_void_p, I64P, I64P, C.POINTER(C.c_uint64), I64P, I64P, I64P, DP]
         L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
+        L.st_residual_norms.argtypes = [C.c_void_p, DP]
         L.st_get_values.argtypes = [C.c_void_p, DP]
         L.st_get_csr.argtypes = [C.c_void_p, C.c_int32, I32P, I32P, DP]
         L.st_probe_basis.argtypes = [C.c_void_p, C.POINTER(StUpdate), C.c_int32, C.c_uint64, DP, I64, I64, I64P]
@@ -98,7 +99,7 @@ def lib():
         L.st_shard_layout.argtypes = [C.c_int32, I64P, I64, C.c_int32, I64, I64P, I64]
         L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
-                  "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows"):
+                  "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows", "st_residual_norms"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -256,6 +257,12 @@ class TrackerSession:
         vecs = np.zeros((n, self.k), order="F")
         self._check(lib().st_get_embedding(self._h, _p(vals), vecs.ctypes.data_as(DP), n))
         return vals, np.ascontiguousarray(vecs)
+
+    def residual_norms(self) -> np.ndarray:
+        """||Op x_i - theta_i x_i|| per tracked pair, on the device (st_residual_norms)."""
+        out = np.zeros(self.k)
+        self._check(lib().st_residual_norms(self._h, _p(out)))
+        return out
 
     def csr(self, which: int = 0):
         inf = self.info()

@@ -41,7 +41,7 @@ namespace stg {
 // kernel classes for per-class device timing (st_kernel_stats)
 enum KClass : int {
   kGram = 0, kGemm = 1, kSpmm = 2, kChol = 3, kTriinv = 4, kEig = 5, kMerge = 6, kRng = 7, kRotate = 8,
-  kKcGram = 9, kSpmmSketch = 10, kIngestOther = 11
+  kKcGram = 9, kSpmmSketch = 10, kIngestOther = 11, kSpmmFull = 12
 };
 
 struct InvalidArgument : std::invalid_argument {
@@ -50,6 +50,46 @@ struct InvalidArgument : std::invalid_argument {
 struct RuntimeError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+
+// ------------------------------------------------------------------ residual norms
+// Per-column sums of (AX - X diag(theta))^2 over row blocks of 256 rows:
+// thread (c, ry) of a 32 x 8 block walks rows ry, ry + 8, ... of its block for
+// columns c, c + 32, ...; partial[block][c] in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) residual_partial_kernel(const double* AX, int ldax, const double* X, int ldx,
+                                                               const double* theta, i64 n, int k, double* partial) {
+  __shared__ double red[8][33];
+  const int c_l = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const i64 r0 = static_cast<i64>(blockIdx.x) * 256;
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    const int c = c0 + c_l;
+    double acc = 0.0;
+    if (c < k) {
+      const double th = theta[c];
+      for (int i = ry; i < 256; i += 8) {
+        const i64 r = r0 + i;
+        if (r >= n) break;
+        const double d = AX[r * ldax + c] - th * X[r * ldx + c];
+        acc = fma(d, d, acc);
+      }
+    }
+    red[ry][c_l] = acc;
+    __syncthreads();
+    if (ry == 0 && c < k) {
+      double t = 0.0;
+      for (int q = 0; q < 8; ++q) t += red[q][c_l];
+      partial[static_cast<i64>(blockIdx.x) * k + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void residual_reduce_kernel(const double* partial, int nblocks, int k, double* out) {
+  const int c = threadIdx.x;
+  if (c >= k) return;
+  double t = 0.0;
+  for (int b = 0; b < nblocks; ++b) t += partial[static_cast<i64>(b) * k + c];
+  out[c] = sqrt(t);
+}
 
 // ------------------------------------------------------------------ memory
 class Arena {
@@ -198,7 +238,7 @@ class Session {
     double ms = 0, work = 0;
     i64 launches = 0;
   };
-  static constexpr int kClasses = 12;
+  static constexpr int kClasses = 13;
   KStat kstats[kClasses];
 
   struct ShardInit {
@@ -2334,6 +2374,45 @@ class Session {
     }
   }
 
+  // ||Op x_i - theta_i x_i||_2 for the tracked pairs on the current operator
+ public:
+  // (A, or the shifted Laplacian T): the residual the reference's Lanczos
+  // convergence test measures (lanczos.hpp:85-95). One full-operator SpMM
+  // Op X (the north star's A Z with Z = X) on the segment-planned CSR kernel,
+  // then deterministic column sums.
+  void residual_norms(double* out) {
+    if (sh_) throw InvalidArgument("st_residual_norms: not available on sharded sessions");
+    const DevCsr& op = is_laplacian() ? T() : A();
+    const i64 rows = n;
+    const int kk = static_cast<int>(k);
+    double* AX = arena_.get<double>("res_ax", rows * ldx());
+    SpmmArgs sa{};
+    sa.rows = rows;
+    sa.row_off = 0;
+    sa.rowptr = op.rp;
+    sa.col = op.col;
+    sa.val = op.val;
+    sa.col_lo = 0;
+    sa.X = X_;
+    sa.ldx = static_cast<int>(ldx());
+    sa.m = kk;
+    sa.Y = AX;
+    sa.ldy = static_cast<int>(ldx());
+    STG_CUDA(cudaMemsetAsync(AX, 0, sizeof(double) * rows * ldx(), st_));
+    do_spmm(sa, op.nnz, rows, kSpmmFull);
+    const int nb = static_cast<int>(cdiv(rows, 256));
+    double* part = arena_.get<double>("res_part", static_cast<i64>(nb) * kk);
+    double* dout = arena_.get<double>("res_out", kk);
+    launch(residual_partial_kernel, dim3(static_cast<unsigned>(nb)), dim3(256), 0, st_, static_cast<const double*>(AX),
+           static_cast<int>(ldx()), static_cast<const double*>(X_), static_cast<int>(ldx()),
+           static_cast<const double*>(d_values_), rows, kk, part);
+    launch(residual_reduce_kernel, dim3(1), dim3(static_cast<unsigned>(round_up(kk, 32))), 0, st_, static_cast<const double*>(part), nb, kk, dout);
+    STG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    kflush();
+  }
+
+ private:
   // Dense n_total x D column-major expansion of a stacked basis (probes only).
   void expand_dense(const Pert& pt, Blk z, int D, double* out, i64 ldo) {
     const int ldd = ld_for(D);
@@ -2476,6 +2555,13 @@ st_status st_get_embedding(const st_session* s, double* values, double* vectors,
 st_status st_get_values(const st_session* s, double* values) {
   std::memcpy(values, s->impl->values.data(), sizeof(double) * s->impl->values.size());
   return ST_OK;
+}
+
+st_status st_residual_norms(st_session* s, double* norms) {
+  return guarded(s, [&] {
+    if (!norms) throw std::invalid_argument("st_residual_norms: null argument");
+    s->impl->residual_norms(norms);
+  });
 }
 
 st_status st_get_csr(const st_session* s, int32_t which, int32_t* rowptr, int32_t* colidx, double* values) {

@@ -80,3 +80,32 @@ def test_gaussian_stream_matches_reference_sampler(seed, rows, cols):
     rel = np.abs(g - o) / np.maximum(1.0, np.abs(o))
     assert rel.max() <= 4e-16 * 8
     assert (g == o).mean() > 0.5
+
+
+@pytest.mark.gpu
+def test_residual_norms_match_host():
+    """st_residual_norms (one full-operator SpMM on the device) equals the
+    per-pair residual ||A x_i - theta_i x_i|| of the reference's Lanczos test
+    (lanczos.hpp:85-95) computed on the host from the session's own CSR and
+    embedding, for the adjacency and the normalized-Laplacian operator."""
+    import scipy.sparse as sp
+
+    from paper_2603_19439_b200 import TrackerSession, streams
+
+    s = streams.config1(n=3000, steps=2)
+    rp, col, val = s.csr0()
+    rng = np.random.default_rng(0)
+    x, _ = np.linalg.qr(rng.standard_normal((len(rp) - 1, 8)))
+    for op, order in (("adjacency", "abs_desc"), ("normalized-laplacian", "alg_desc")):
+        g = TrackerSession(rp, col, val, np.linspace(8.0, 1.0, 8), x, kind="grest-rsvd", k=8, seed=1,
+                           operator=op, order=order)
+        for upd in s.updates:
+            g.step(upd)
+        lam, X = g.embedding()
+        which = 1 if op != "adjacency" else 0
+        crp, ccol, cval = g.csr(which)
+        n = len(crp) - 1
+        A = sp.csr_matrix((cval, ccol, crp), shape=(n, n))
+        ref = np.linalg.norm(A @ X - X * lam, axis=0)
+        got = g.residual_norms()
+        assert np.allclose(got, ref, rtol=1e-10, atol=1e-12 * np.abs(lam).max()), (op, got, ref)
