@@ -256,11 +256,19 @@ def _run_ours(args, saved_stdout):
         blk = local_block(rp, col, val, vecs0, lo, hi)
         kw_sh = {k_: v for k_, v in kw.items() if k_ != "operator"}
 
+    # capacity for the whole stream (final node count; stored entries bounded by
+    # the inserts), so no step inside a timed region grows a device buffer
+    n_cap = len(rp) - 1 + sum(int(u.n_new) for u in stream.updates)
+    nnz_cap = int(rp[-1]) + 2 * sum(len(u.added[0]) + len(u.new_edges[0]) for u in stream.updates)
+
     def new_session(kernel_timing=False):
         if sharded:
-            return ShardedTrackerSession(comm, len(rp) - 1, lo, hi, blk[0], blk[1], blk[2], vals0, blk[3],
-                                         chunk=1024, kernel_timing=kernel_timing, **kw_sh)
-        return TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, **kw)
+            s_ = ShardedTrackerSession(comm, len(rp) - 1, lo, hi, blk[0], blk[1], blk[2], vals0, blk[3],
+                                       chunk=1024, kernel_timing=kernel_timing, **kw_sh)
+        else:
+            s_ = TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, **kw)
+        s_.reserve(n_cap, nnz_cap)
+        return s_
 
     # ---- value: edit lists resident in HBM (no per-launch timing events)
     dev_updates = [DeviceUpdate(u, device=f"cuda:{local}") for u in stream.updates]
@@ -273,17 +281,20 @@ def _run_ours(args, saved_stdout):
     clocks.start()
     time.sleep(0.3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     launches = 0
     torch.cuda.synchronize()
     e0.record()
     for t in range(W, W + K):
         sess.step_device(dev_updates[t])
+        marks[t - W].record()  # after the step's work on the session stream (no host sync)
         launches += sess.launches()
     torch.cuda.synchronize()  # the session's side streams included
     e1.record()
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = dist_max(e0.elapsed_time(e1), world)
+    step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, K)]
     info = sess.info()
     sess.close()
 
@@ -310,15 +321,18 @@ def _run_ours(args, saved_stdout):
     barrier(world)
     h2d = 0
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fmarks = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     f0.record()
     for t in range(W, W + K):
         sess.step(host_updates[t])
         _ = sess.values()
+        fmarks[t - W].record()
         h2d += host_updates[t].h2d_bytes()
     torch.cuda.synchronize()
     f1.record()
     torch.cuda.synchronize()
     ms_e2e = dist_max(f0.elapsed_time(f1), world)
+    step_ms_e2e = [f0.elapsed_time(fmarks[0])] + [fmarks[i - 1].elapsed_time(fmarks[i]) for i in range(1, K)]
     sess.close()
 
     streams_run = 1 if sharded else world  # one row-sharded stream, or one stream per replica
@@ -384,6 +398,8 @@ def _run_ours(args, saved_stdout):
         "e2e": {"value": e2e, "unit": "steps/s", "ms_per_step": ms_e2e / K, "h2d_bytes_per_step": h2d // K,
                 "d2h_bytes_per_step": 8 * wl["k"]},
         "gpu_launches": launches,
+        "step_ms": [round(x, 3) for x in step_ms],
+        "step_ms_e2e": [round(x, 3) for x in step_ms_e2e],
         "clocks": clk,
     }
     if rank == 0 and world == 1 and args.config == "cfg5" and not args.no_cpu_baseline:

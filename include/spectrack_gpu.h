@@ -92,6 +92,28 @@ st_status st_create(const st_config* cfg, int64_t n, const int32_t* rowptr, cons
                     st_session** out);
 void st_destroy(st_session* s);
 
+/* LanczosOptions (lanczos.hpp:29-36) beyond k / order / seed, which come from
+ * st_config. Defaults: tol 1e-10, max_basis 0 (= max(2k + 20, 40)),
+ * max_restarts 500. The device path limits max_basis to 256. */
+typedef struct {
+  double tol;
+  int64_t max_basis;
+  int64_t max_restarts;
+} st_lanczos_options;
+
+/* tracker_init (trackers.cpp:132-145) on the device: a session whose initial
+ * eigenpairs are the leading k of the tracked operator (A, or the shifted
+ * Laplacian T for Laplacian operators), computed by thick-restart Lanczos with
+ * full reorthogonalization (lanczos.hpp:38-127, seed mix_seed(cfg->seed,
+ * 0x1a2c), residual test ||A x_i - theta_i x_i|| <= tol max|theta|). opts may
+ * be NULL for the reference defaults. Errors as lanczos_topk: "k must satisfy
+ * 1 <= k <= n", "max_basis below k", "no convergence after N restarts (...)". */
+st_status st_tracker_init(const st_config* cfg, const st_lanczos_options* opts, int64_t n, const int32_t* rowptr,
+                          const int32_t* colidx, const double* values_csr, st_session** out);
+/* Restarts and operator products of the session's tracker_init (0 when the
+ * session was created from given eigenpairs). */
+st_status st_init_stats(const st_session* s, int64_t* restarts, int64_t* products);
+
 /* One step of the hot path. Replaces, in one call, the reference loop body
  * (experiment.cpp:169-173, 203):
  *   GraphUpdate d = assemble_update(...);            graph.cpp:45-100
@@ -104,6 +126,13 @@ void st_destroy(st_session* s);
  * from the caller's arrays; pageable lists go through one internal pinned
  * staging copy. The call returns after the uploads completed either way. */
 st_status st_step(st_session* s, const st_update* upd);
+
+/* Capacity hint for a stream that will reach n_nodes nodes and nnz stored
+ * entries of A: the device state and the node- and entry-indexed buffers of
+ * ingestion are sized once, so later steps up to that size allocate nothing
+ * large. Optional; the reference has no counterpart (its CSR is rebuilt by
+ * value each step). Invalidates the last step's Delta export (st_get_csr 2). */
+st_status st_reserve(st_session* s, int64_t n_nodes, int64_t nnz);
 
 /* st_step with the edit arrays already resident in device memory (same
  * layout; every pointer in *upd is a device pointer). Used to time the step

@@ -37,6 +37,10 @@ class StConfig(C.Structure):
                 ("flags", C.c_int32)]
 
 
+class StLanczosOptions(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_basis", C.c_int64), ("max_restarts", C.c_int64)]
+
+
 class StUpdate(C.Structure):
     _fields_ = [("n_added", C.c_int64), ("added_i", I64P), ("added_j", I64P), ("added_w", DP),
                 ("n_removed", C.c_int64), ("removed_i", I64P), ("removed_j", I64P), ("n_new", C.c_int64),
@@ -66,6 +70,10 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.st_create.argtypes = [C.POINTER(StConfig), I64, I32P, I32P, DP, DP, DP, I64, C.POINTER(C.c_void_p)]
         L.st_step.argtypes = [C.c_void_p, C.POINTER(StUpdate)]
+        L.st_tracker_init.argtypes = [C.POINTER(StConfig), C.POINTER(StLanczosOptions), I64, I32P, I32P, DP,
+                                      C.POINTER(C.c_void_p)]
+        L.st_init_stats.argtypes = [C.c_void_p, I64P, I64P]
+        L.st_reserve.argtypes = [C.c_void_p, I64, I64]
         L.st_info.argtypes = [C.c_void_p, I64P, I64P, C.POINTER(C.c_uint64), I64P, I64P, I64P, DP]
         L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
         L.st_residual_norms.argtypes = [C.c_void_p, DP]
@@ -99,7 +107,8 @@ def lib():
         L.st_shard_layout.argtypes = [C.c_int32, I64P, I64, C.c_int32, I64, I64P, I64]
         L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
-                  "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows", "st_residual_norms"):
+                  "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows", "st_residual_norms",
+                  "st_reserve", "st_tracker_init", "st_init_stats"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -204,6 +213,37 @@ class TrackerSession:
         self._h = h.value
         self.k = k
 
+    @classmethod
+    def tracker_init(cls, rowptr, col, val, k, kind="grest-rsvd", order="abs_desc", rsvd_l=100, rsvd_p=100, seed=0,
+                     operator="adjacency", device=0, tol=1e-10, max_basis=0, max_restarts=500, force_dense=False,
+                     timing=False, kernel_timing=False, cusolver_eig=False):
+        """tracker_init (trackers.cpp:132-145) on the device: the session starts
+        from the leading k eigenpairs of the tracked operator, computed by
+        thick-restart Lanczos (lanczos.hpp:38-127) on the GPU."""
+        L = lib()
+        rowptr = np.ascontiguousarray(rowptr, np.int32)
+        col = np.ascontiguousarray(col, np.int32)
+        val = np.ascontiguousarray(val, np.float64)
+        flags = ((FLAG_FORCE_DENSE if force_dense else 0) | (FLAG_TIMING if timing else 0)
+                 | (FLAG_KERNEL_TIMING if kernel_timing else 0) | (FLAG_CUSOLVER_EIG if cusolver_eig else 0))
+        cfg = StConfig(KIND[kind], OPERATOR[operator], k, ORDER[order], rsvd_l, rsvd_p, seed, device, flags)
+        opts = StLanczosOptions(tol, max_basis, max_restarts)
+        h = C.c_void_p()
+        rc = L.st_tracker_init(C.byref(cfg), C.byref(opts), len(rowptr) - 1, _p(rowptr, I32P), _p(col, I32P),
+                               _p(val), C.byref(h))
+        if rc != ST_OK:
+            raise TrackerError(_KINDS.get(rc, "other"), L.st_last_error(None).decode())
+        self = cls.__new__(cls)
+        self._h = h.value
+        self.k = k
+        return self
+
+    def init_stats(self):
+        """(restarts, operator products) of the device tracker_init."""
+        r, p = I64(), I64()
+        self._check(lib().st_init_stats(self._h, C.byref(r), C.byref(p)))
+        return r.value, p.value
+
     def close(self):
         if getattr(self, "_h", None):
             lib().st_destroy(self._h)
@@ -219,6 +259,11 @@ class TrackerSession:
     def step(self, upd: Update) -> None:
         keep, s = upd.struct()
         self._check(lib().st_step(self._h, C.byref(s)))
+
+    def reserve(self, n_nodes: int, nnz: int) -> None:
+        """Size the session for a stream reaching n_nodes nodes and nnz stored
+        entries (st_reserve): later steps up to that size grow no buffer."""
+        self._check(lib().st_reserve(self._h, int(n_nodes), int(nnz)))
 
     def step_device(self, dev_update) -> None:
         """Step with edit arrays already in device memory: `dev_update` is a

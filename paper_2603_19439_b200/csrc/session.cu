@@ -20,6 +20,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
+#include <sstream>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -30,6 +32,7 @@
 #include "dmma.cuh"
 #include "eigsolve.cuh"
 #include "ingest.cuh"
+#include "lanczos.cuh"
 #include "rng.cuh"
 #include "shard.cuh"
 #include "smalllin.cuh"
@@ -83,45 +86,139 @@ __global__ void __launch_bounds__(256) residual_partial_kernel(const double* AX,
   }
 }
 
-__global__ void residual_reduce_kernel(const double* partial, int nblocks, int k, double* out) {
-  const int c = threadIdx.x;
-  if (c >= k) return;
+// out[c] = sqrt(sum_b partial[b][c]): one CTA per column, each thread sums a
+// fixed strided subset of the partials, then a fixed-shape tree (deterministic).
+__global__ void __launch_bounds__(256) residual_reduce_kernel(const double* partial, int nblocks, int k, double* out) {
+  __shared__ double red[256];
+  const int c = blockIdx.x;
   double t = 0.0;
-  for (int b = 0; b < nblocks; ++b) t += partial[static_cast<i64>(b) * k + c];
-  out[c] = sqrt(t);
+  for (int b = threadIdx.x; b < nblocks; b += 256) t += partial[static_cast<i64>(b) * k + c];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[c] = sqrt(red[0]);
 }
 
 // ------------------------------------------------------------------ memory
+// Named device buffers that only grow. Allocations come from a session-owned
+// stream-ordered memory pool that never releases to the driver, on the main
+// stream: a buffer outgrown as n and |P| creep up each step is freed and
+// re-allocated in stream order (no device-wide synchronization, unlike
+// cudaFree/cudaMalloc), and the freed block is reused by later growth.
+// Ordering: a buffer's old block is only ever used on the main stream when it
+// is outgrown (side-stream users of the previous block are joined by then:
+// the merge at commit, the sketch eigensolve before the Rayleigh-Ritz step,
+// the RNG by ensure_raw), so the free needs no extra dependency; a buffer a
+// side stream uses after its allocation (`side_use`) makes the side streams
+// wait for the allocation point.
 class Arena {
  public:
-  ~Arena() {
+  ~Arena() { reset(); }
+  // frees every buffer and the pool (the session calls this before it
+  // destroys the streams)
+  void reset() {
+    if (!pool_) return;
     for (auto& kv : bufs_)
-      if (kv.second.ptr) cudaFree(kv.second.ptr);
+      if (kv.second.ptr) cudaFreeAsync(kv.second.ptr, main_);
+    bufs_.clear();
+    cudaStreamSynchronize(main_);
+    cudaMemPoolDestroy(pool_);
+    pool_ = nullptr;
+    if (ev_) cudaEventDestroy(ev_);
+    ev_ = nullptr;
+  }
+  void init(int device, cudaStream_t main, std::vector<cudaStream_t> sides) {
+    main_ = main;
+    sides_ = std::move(sides);
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    STG_CUDA(cudaMemPoolCreate(&pool_, &props));
+    unsigned long long keep = ~0ULL;
+    STG_CUDA(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
   }
   template <class T>
-  T* get(const std::string& name, i64 count) {
+  T* get(const std::string& name, i64 count, bool side_use = false) {
     Buf& b = bufs_[name];
     const size_t bytes = static_cast<size_t>(std::max<i64>(count, 1)) * sizeof(T);
     if (b.bytes < bytes) {
-      if (b.ptr) STG_CUDA(cudaFree(b.ptr));
       const size_t nb = bytes + bytes / 4 + 256;
-      STG_CUDA(cudaMalloc(&b.ptr, nb));
+      if (b.ptr) STG_CUDA(cudaFreeAsync(b.ptr, main_));
+      STG_CUDA(cudaMallocFromPoolAsync(&b.ptr, nb, pool_, main_));
+      if (side_use) join_main_into_sides();
       b.bytes = nb;
+      ++grows_;
     }
     return static_cast<T*>(b.ptr);
+  }
+  // get() that keeps the first keep_bytes of the old contents on growth
+  template <class T>
+  T* get_keep(const std::string& name, i64 count, size_t keep_bytes) {
+    Buf& b = bufs_[name];
+    const size_t bytes = static_cast<size_t>(std::max<i64>(count, 1)) * sizeof(T);
+    if (b.bytes < bytes && b.ptr) {
+      void* old = b.ptr;
+      const size_t nb = bytes + bytes / 4 + 256;
+      STG_CUDA(cudaMallocFromPoolAsync(&b.ptr, nb, pool_, main_));
+      if (keep_bytes) STG_CUDA(cudaMemcpyAsync(b.ptr, old, std::min(keep_bytes, b.bytes), cudaMemcpyDeviceToDevice, main_));
+      STG_CUDA(cudaFreeAsync(old, main_));
+      join_main_into_sides();  // the live CSR is read by the merge stream
+      b.bytes = nb;
+      ++grows_;
+      return static_cast<T*>(b.ptr);
+    }
+    return get<T>(name, count);
+  }
+  // stream-ordered allocation outside the named buffers (X and temporaries
+  // used on the main stream only)
+  void* alloc(size_t bytes) {
+    void* p = nullptr;
+    STG_CUDA(cudaMallocFromPoolAsync(&p, bytes, pool_, main_));
+    return p;
+  }
+  void release(void* p) {
+    if (p) STG_CUDA(cudaFreeAsync(p, main_));
   }
   size_t total() const {
     size_t s = 0;
     for (auto& kv : bufs_) s += kv.second.bytes;
     return s;
   }
+  i64 grows() const { return grows_; }
+  // Keeps `bytes` of free memory in the pool (allocated once, then freed:
+  // the pool never releases it), so later growth sub-allocates instead of
+  // mapping new device memory in the middle of a step.
+  void prewarm(size_t bytes) {
+    if (!bytes) return;
+    void* p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, bytes, pool_, main_) != cudaSuccess) {
+      (void)cudaGetLastError();  // not enough memory for the headroom: skip it
+      return;
+    }
+    STG_CUDA(cudaFreeAsync(p, main_));
+    STG_CUDA(cudaStreamSynchronize(main_));
+  }
 
  private:
+  void join_main_into_sides() {
+    STG_CUDA(cudaEventRecord(ev_, main_));
+    for (cudaStream_t s : sides_) STG_CUDA(cudaStreamWaitEvent(s, ev_, 0));
+  }
   struct Buf {
     void* ptr = nullptr;
     size_t bytes = 0;
   };
   std::unordered_map<std::string, Buf> bufs_;
+  cudaMemPool_t pool_ = nullptr;
+  cudaStream_t main_ = nullptr;
+  std::vector<cudaStream_t> sides_;
+  cudaEvent_t ev_ = nullptr;
+  i64 grows_ = 0;
 };
 
 class Pinned {
@@ -246,8 +343,19 @@ class Session {
     i64 n_global, lo, hi, chunk;
   };
 
+  // LanczosOptions (lanczos.hpp:29-36) beyond the tracker's k / order / seed
+  struct LzOpts {
+    double tol = 1e-10;
+    i64 max_basis = 0;
+    i64 max_restarts = 500;
+  };
+  i64 lz_restarts = 0, lz_products = 0;  // tracker_init statistics
+  bool prewarmed_ = false;
+
+  // ev == nullptr: tracker_init (trackers.cpp:132-145) on the device, i.e. the
+  // leading eigenpairs of the tracked operator by thick-restart Lanczos.
   Session(const st_config& c, i64 n0, const int* rp, const int* col, const double* val, const double* ev,
-          const double* evec, i64 ld, const ShardInit* shard = nullptr)
+          const double* evec, i64 ld, const ShardInit* shard = nullptr, const LzOpts* lz = nullptr)
       : cfg(c) {
     STG_CUDA(cudaSetDevice(cfg.device));
     {  // priorities: the eigensolve's CTAs take SMs ahead of the wide kernels it
@@ -259,6 +367,7 @@ class Session {
       STG_CUDA(cudaStreamCreateWithPriority(&st_mg_, cudaStreamNonBlocking, lo));
     }
     STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
+    arena_.init(cfg.device, st_, {st_eig_, st_mg_, st_rng_});
     STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
     STG_CUDA(cudaEventCreateWithFlags(&ev_mg_fork_, cudaEventDisableTiming));
     STG_CUDA(cudaEventCreateWithFlags(&ev_mg_, cudaEventDisableTiming));
@@ -292,6 +401,12 @@ class Session {
                                   static_cast<int>(dm::kNNTmaSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNTmaSmem)));
+    // function attributes are per device: set for this session's device here
+    STG_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(chol_smem_bytes(kCholMaxW))));
+    STG_CUDA(cudaFuncSetAttribute(triinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(triinv_smem_bytes(kCholMaxW))));
+    eig_set_attributes();
     d_scal_ = arena_.get<u64>("scalars", 32);
     k = cfg.k;
     n = n0;
@@ -316,6 +431,16 @@ class Session {
     acur_ = 0;
     ensure_node_capacity(n, n0);
     nloc_ = n0;
+    d_values_ = arena_.get<double>("values", k);
+    if (!ev) {
+      if (shard) throw InvalidArgument("st_tracker_init: sharded sessions take their initial eigenpairs");
+      if (is_laplacian()) init_laplacian();
+      const LzOpts o = lz ? *lz : LzOpts{};
+      lanczos(is_laplacian() ? T() : A(), n0, o);
+      STG_CUDA(cudaMemcpyAsync(d_values_, values.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      return;
+    }
     // eigenpairs: column-major host -> row-major device
     values.assign(ev, ev + k);
     std::vector<double> xr(static_cast<size_t>(n0 * k));
@@ -323,7 +448,6 @@ class Session {
       for (i64 i = 0; i < n0; ++i) xr[static_cast<size_t>(i * k + c)] = evec[c * ld + i];
     STG_CUDA(cudaMemcpy2DAsync(X_, sizeof(double) * ldx(), xr.data(), sizeof(double) * k, sizeof(double) * k, n0,
                                cudaMemcpyHostToDevice, st_));
-    d_values_ = arena_.get<double>("values", k);
     STG_CUDA(cudaMemcpyAsync(d_values_, values.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st_));
     if (is_laplacian()) init_laplacian();
     STG_CUDA(cudaStreamSynchronize(st_));
@@ -332,7 +456,11 @@ class Session {
   ~Session() {
     cudaStreamSynchronize(st_);
     cudaStreamSynchronize(st_rng_);
-    if (X_) cudaFree(X_);
+    cudaStreamSynchronize(st_eig_);
+    cudaStreamSynchronize(st_mg_);
+    if (X_) cudaFreeAsync(X_, st_);
+    X_ = nullptr;
+    arena_.reset();  // pool blocks are freed on st_ before the streams go
     if (solver_) cusolverDnDestroy(solver_);
     if (hs_) cudaFreeHost(hs_);
     for (auto& e : tev_) cudaEventDestroy(e);
@@ -384,7 +512,8 @@ class Session {
     }
     if (bounds_[R] != si.n_global) throw InvalidArgument("st_create_sharded: row blocks must tile [0, n_global) in rank order");
     i64* db = arena_.get<i64>("shard_bounds", R + 1);
-    STG_CUDA(cudaMemcpy(db, bounds_.data(), sizeof(i64) * (R + 1), cudaMemcpyHostToDevice));
+    STG_CUDA(cudaMemcpyAsync(db, bounds_.data(), sizeof(i64) * (R + 1), cudaMemcpyHostToDevice, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
     map_.n0 = si.n_global;
     map_.chunk = si.chunk;
     map_.size = R;
@@ -460,8 +589,56 @@ class Session {
     values = newvals;
     n = pt.n_total;
     steps_taken += 1;
+    if (!prewarmed_) {
+      // after the first full step the working set is known: keep 1.6x of it
+      // free in the pool, so the buffers that outgrow their 1.25x headroom as
+      // the graph grows (at 1%/step, ~every 22 steps) are re-carved from
+      // memory the pool already holds
+      prewarmed_ = true;
+      size_t fr = 0, tot = 0;
+      STG_CUDA(cudaMemGetInfo(&fr, &tot));
+      arena_.prewarm(std::min<size_t>(arena_.total() + arena_.total() * 6 / 10, fr / 2));
+    }
     timing_end(5);
     kflush();
+  }
+
+  // Capacity for a stream that will reach n_nodes nodes and nnz stored
+  // entries: X, the node marks and the node- and entry-indexed buffers of
+  // ingestion and the CSR merge are sized once, so steps up to that size never
+  // grow a buffer (st_reserve).
+  void reserve(i64 n_nodes, i64 nnz) {
+    if (n_nodes < n || nnz < 0) throw InvalidArgument("st_reserve: capacity below the current graph");
+    if (n_nodes >= (1LL << 31)) throw InvalidArgument("st_step: node count exceeds int32 CSR indexing");
+    ensure_node_capacity(n_nodes, sh_ ? rows_at(comm_.rank, n_nodes) : n_nodes);
+    const i64 rows = (sh_ ? rows_at(comm_.rank, n_nodes) : n_nodes) + 1;
+    for (const char* name : {"m_ncnt", "sh_lcnt", "sh_ldrp", "sh_pflag", "sh_ppos"}) arena_.get<int>(name, rows);
+    if (!sh_)
+      for (const char* name : {"dcnt", "drp", "p_flag", "p_pos", "P", "t_cnt", "dt_cnt", "dt_rp"})
+        arena_.get<int>(name, n_nodes + 1);
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_mg_, 0));
+    for (int slot = 0; slot < 2; ++slot) {  // the live slot keeps its contents
+      DevCsr& a = A_[slot];
+      const bool live = slot == acur_;
+      const std::string nm = "A" + std::to_string(slot);
+      int* rp = arena_.get_keep<int>(nm + ".rp", rows, live ? sizeof(int) * (a.n + 1) : 0);
+      int* col = arena_.get_keep<int>(nm + ".col", nnz, live ? sizeof(int) * a.nnz : 0);
+      double* val = arena_.get_keep<double>(nm + ".val", nnz, live ? sizeof(double) * a.nnz : 0);
+      if (live) {
+        a.rp = rp;
+        a.col = col;
+        a.val = val;
+      }
+    }
+    if (is_laplacian()) {
+      DevCsr& t = T_[tcur_];
+      const std::string nm = "T" + std::to_string(tcur_);
+      t.rp = arena_.get_keep<int>(nm + ".rp", n_nodes + 1, sizeof(int) * (t.n + 1));
+      arena_.get<int>("T" + std::to_string(1 - tcur_) + ".rp", n_nodes + 1);
+    }
+    last_delta_ = DevCsr{};  // its buffers may have moved: the Delta export restarts at the next step
+    last_delta_nnz_ = 0;
+    STG_CUDA(cudaStreamSynchronize(st_));
   }
 
   i64 probe_basis(const st_update& u, int basis_kind, u64 seed, double* z, i64 ldz, i64 max_cols) {
@@ -797,12 +974,10 @@ class Session {
     if (need_x < 0) need_x = need;
     if (need_x > xcap_ || !X_) {
       const i64 cap = std::max<i64>(need_x + need_x / 4, 1024);
-      double* nx = nullptr;
-      STG_CUDA(cudaMalloc(&nx, sizeof(double) * cap * ldx()));
-      if (X_) {
+      double* nx = static_cast<double*>(arena_.alloc(sizeof(double) * cap * ldx()));
+      if (X_) {  // stream-ordered copy and free (no host or device-wide sync)
         STG_CUDA(cudaMemcpyAsync(nx, X_, sizeof(double) * xcap_ * ldx(), cudaMemcpyDeviceToDevice, st_));
-        STG_CUDA(cudaStreamSynchronize(st_));
-        STG_CUDA(cudaFree(X_));
+        arena_.release(X_);
       }
       X_ = nx;
       if (sh_) {
@@ -1059,14 +1234,28 @@ class Session {
     return *e;
   }
 
-  void do_spmm(const SpmmArgs& a, i64 nnz, i64 distinct_cols, int cls = kSpmm) {
+  // transient: size the segment scratch from the plan's real long-row segment
+  // count (one read-back) in a stream-ordered allocation freed after the
+  // product, instead of the step's worst-case persistent buffer (monitoring
+  // calls over the full operator).
+  void do_spmm(const SpmmArgs& a, i64 nnz, i64 distinct_cols, int cls = kSpmm, bool transient = false) {
     if (a.rows <= 0 || a.m <= 0) return;
     PlanEntry& pe = spmm_plan(a, nnz);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "spmm %lld rows m=%d", a.rows, a.m);
-    kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
     SpmmPlan pl = pe.pl;
     pl.lds = static_cast<int>(round_up(std::min(a.m, 256), 2));
-    pl.scratch = arena_.get<double>("spmm_scratch", pe.smax * pl.lds);
+    double* tscratch = nullptr;
+    if (transient) {
+      int segs = 0;
+      STG_CUDA(cudaMemcpyAsync(&segs, pe.pl.sstart + a.rows, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      STG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tscratch),
+                               sizeof(double) * std::max<i64>(segs, 1) * pl.lds, st_));
+      pl.scratch = tscratch;
+    } else {
+      pl.scratch = arena_.get<double>("spmm_scratch", pe.smax * pl.lds);
+    }
+    kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
     for (int c0 = 0; c0 < a.m; c0 += 256) {  // dense blocks wider than 256 columns: 256-column slabs
       SpmmArgs b = a;
       b.X = a.X + c0;
@@ -1076,6 +1265,7 @@ class Session {
       launches += pe.split_max > 0 ? 3 : 1;
     }
     kend();
+    if (tscratch) STG_CUDA(cudaFreeAsync(tscratch, st_));
   }
 
   // Cholesky G = R'R; with Ri also R^-1 (triinv_kernel on R', written by chol).
@@ -1084,14 +1274,6 @@ class Session {
     if (w > kCholMaxW) throw RuntimeError("chol: block wider than 238 columns");
     if (klog_) snprintf(ktag_, sizeof(ktag_), "chol w=%d", w);
     kbegin(kChol, static_cast<double>(w) * w * w / 3.0);
-    static bool attr = false;
-    if (!attr) {
-      STG_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(chol_smem_bytes(kCholMaxW))));
-      STG_CUDA(cudaFuncSetAttribute(triinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(triinv_smem_bytes(kCholMaxW))));
-      attr = true;
-    }
     const int ldt = ld_for(w);
     double* Rt = Ri ? arena_.get<double>("chol_Rt", static_cast<i64>(w) * ldt) : nullptr;
     launch(chol_kernel, dim3(1), dim3(kCholThreads), chol_smem_bytes(w), st_, G, ldg, w, R, ldr, Rt, ldt, orig2, tau2,
@@ -1150,14 +1332,9 @@ class Session {
     // tridiagonalization's shared-memory limit
     if (cfg.flags & ST_FLAG_CUSOLVER_EIG) return false;
     if (D > kEigMaxN || want > kEigMaxWant) return false;
-    static bool attr = false;
-    if (!attr) {
-      eig_set_attributes();
-      attr = true;
-    }
     const int wv = std::max(want, 1);
-    double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(D, wv)));
-    int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(D, wv)));
+    double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(D, wv)), /*side_use*/ true);
+    int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(D, wv)), /*side_use*/ true);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "device syev D=%d want=%d", D, want);
     cudaStream_t es = s ? s : st_;
     kbegin(kEig, 4.0 * D * D * D / 3.0, es);
@@ -2146,12 +2323,12 @@ class Session {
     if (words <= raw_cap_) return;
     STG_CUDA(cudaStreamSynchronize(st_rng_));
     raw_cap_ = round_up(words + words / 2, kMtM);
-    raw_ = arena_.get<u64>("mt_raw", raw_cap_);
+    raw_ = arena_.get<u64>("mt_raw", raw_cap_, /*side_use*/ true);
     pre_blocks_ = -1;  // contents lost
   }
 
   void generate_raw(u64 rseed, i64 blocks_needed) {
-    if (!ring_state_) ring_state_ = arena_.get<u64>("mt_ring", kMtRing);
+    if (!ring_state_) ring_state_ = arena_.get<u64>("mt_ring", kMtRing, /*side_use*/ true);
     ensure_raw(blocks_needed * kMtM);
     if (pre_seed_ == rseed && pre_blocks_ >= 0) {
       if (pre_blocks_ >= blocks_needed) return;
@@ -2166,7 +2343,7 @@ class Session {
 
   void prepare_omega(u64 seed, i64 S, int q, double** omega, int* ldo_out) {
     const int ldo = ld_for(q);
-    double* om = arena_.get<double>("omega", S * ldo);
+    double* om = arena_.get<double>("omega", S * ldo, /*side_use*/ true);
     if (!(omega_seed_ == seed && omega_S_ == S && omega_q_ == q)) {
       const i64 npairs = cdiv(S * q, 2);
       const u64 rseed = mix_seed(seed, 0x5bdULL);
@@ -2375,6 +2552,295 @@ class Session {
   }
 
   // ||Op x_i - theta_i x_i||_2 for the tracked pairs on the current operator
+  // ---------------------------------------------------------------- tracker_init
+  // Row classes of a full operator for the SpMV (lanczos.cuh), stream-ordered
+  // temporaries released with the plan.
+  struct SpvBufs {
+    SpvPlan pl;
+    std::vector<void*> mem;
+  };
+  SpvBufs spv_plan(const int* rp, i64 rows) {
+    SpvBufs b;
+    auto tmp = [&](size_t bytes) {
+      void* p = arena_.alloc(std::max<size_t>(bytes, 16));
+      b.mem.push_back(p);
+      return p;
+    };
+    const size_t ni = sizeof(int) * (rows + 1);
+    int* fs = static_cast<int*>(tmp(ni));
+    int* fm = static_cast<int*>(tmp(ni));
+    int* fl = static_cast<int*>(tmp(ni));
+    int* sg = static_cast<int*>(tmp(ni));
+    int* ps = static_cast<int*>(tmp(ni));
+    int* pm = static_cast<int*>(tmp(ni));
+    int* pl = static_cast<int*>(tmp(ni));
+    int* pg = static_cast<int*>(tmp(ni));
+    launch(spv_classify_kernel, dim3(blocks(rows + 1)), dim3(256), 0, st_, rp, rows, fs, fm, fl, sg);
+    scan_int(fs, ps, rows + 1);
+    scan_int(fm, pm, rows + 1);
+    scan_int(fl, pl, rows + 1);
+    scan_int(sg, pg, rows + 1);
+    int cnt[4];
+    STG_CUDA(cudaMemcpyAsync(&cnt[0], ps + rows, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&cnt[1], pm + rows, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&cnt[2], pl + rows, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(&cnt[3], pg + rows, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    int* ls = static_cast<int*>(tmp(sizeof(int) * cnt[0]));
+    int* lm = static_cast<int*>(tmp(sizeof(int) * cnt[1]));
+    int* ll = static_cast<int*>(tmp(sizeof(int) * cnt[2]));
+    int* sr = static_cast<int*>(tmp(sizeof(int) * cnt[3]));
+    int* si = static_cast<int*>(tmp(sizeof(int) * cnt[3]));
+    double* part = static_cast<double*>(tmp(sizeof(double) * cnt[3]));
+    if (rows > 0)
+      launch(spv_scatter_kernel, dim3(blocks(rows)), dim3(256), 0, st_, static_cast<const int*>(fs),
+             static_cast<const int*>(ps), static_cast<const int*>(fm), static_cast<const int*>(pm),
+             static_cast<const int*>(fl), static_cast<const int*>(pl), static_cast<const int*>(sg),
+             static_cast<const int*>(pg), rows, ls, lm, ll, sr, si);
+    b.pl = SpvPlan{ls, lm, ll, sr, si, pg, cnt[0], cnt[1], cnt[2], cnt[3], part};
+    return b;
+  }
+  void spv_release(SpvBufs& b) {
+    for (void* p : b.mem) arena_.release(p);
+    b.mem.clear();
+  }
+  // y = Op x (matvec, sparse.cpp:79-82); y also stored at out2[r * ld2]
+  void spmv(const DevCsr& op, const SpvPlan& pl, const double* x, double* y, double* out2, int ld2) {
+    int* fl = flags_ptr();
+    if (pl.n_short)
+      launch(spv_short_kernel, dim3(blocks(static_cast<i64>(pl.n_short) * 8)), dim3(256), 0, st_,
+             static_cast<const int*>(op.rp), static_cast<const int*>(op.col), static_cast<const double*>(op.val), x,
+             pl.l_short, pl.n_short, y, out2, ld2, fl);
+    if (pl.n_med)
+      launch(spv_med_kernel, dim3(blocks(static_cast<i64>(pl.n_med) * 32)), dim3(256), 0, st_,
+             static_cast<const int*>(op.rp), static_cast<const int*>(op.col), static_cast<const double*>(op.val), x,
+             pl.l_med, pl.n_med, y, out2, ld2, fl);
+    if (pl.n_seg) {
+      launch(spv_seg_kernel, dim3(blocks(static_cast<i64>(pl.n_seg) * 32)), dim3(256), 0, st_,
+             static_cast<const int*>(op.rp), static_cast<const int*>(op.col), static_cast<const double*>(op.val), x,
+             pl.seg_row, pl.seg_idx, pl.n_seg, pl.seg_part);
+      launch(spv_fix_kernel, dim3(blocks(pl.n_long)), dim3(256), 0, st_, static_cast<const int*>(op.rp), pl.l_long,
+             pl.n_long, pl.p_seg, static_cast<const double*>(pl.seg_part), y, out2, ld2, fl);
+    }
+  }
+
+  // lz_dot / lz_update with the accumulator count for j columns
+  template <bool NORM>
+  void lz_launch(int which, const double* V, int ldv, int j, const double* coef, const double* vi, double* vo, i64 N,
+                 double* partial, int ldp, int G) {
+    const int na = std::max(1, static_cast<int>(cdiv(j, 32)));
+#define STG_LZ(NA)                                                                                                  \
+  case NA:                                                                                                          \
+    if (which == 0)                                                                                                 \
+      launch(lz_dot_kernel<NA>, dim3(G), dim3(kLzThreads), 0, st_, V, ldv, j, vi, N, partial, ldp);                 \
+    else if (which == 2)                                                                                            \
+      launch(lz_colsq_kernel<NA>, dim3(G), dim3(kLzThreads), 0, st_, V, ldv, j, N, partial, ldp);                   \
+    else                                                                                                            \
+      launch(lz_update_kernel<NA, NORM>, dim3(G), dim3(kLzThreads), 0, st_, V, ldv, j, coef, vi, vo, N, partial, ldp); \
+    break;
+    switch (na) {
+      STG_LZ(1) STG_LZ(2) STG_LZ(3) STG_LZ(4) STG_LZ(5) STG_LZ(6) STG_LZ(7) STG_LZ(8)
+      default: throw InvalidArgument("lanczos_topk: max_basis above the device limit (256)");
+    }
+#undef STG_LZ
+  }
+
+  // GaussianSampler(rseed) draws [pos, pos + count) into out (device)
+  void gauss_draws(u64 rseed, i64 pos, i64 count, double* out) {
+    const i64 words = 2 * cdiv(pos + count, 2);
+    const i64 nb = cdiv(words, kMtM);
+    u64* raw = static_cast<u64*>(arena_.alloc(sizeof(u64) * nb * kMtM));
+    u64* ring = static_cast<u64*>(arena_.alloc(sizeof(u64) * kMtRing));
+    launch(mt19937_64_kernel, dim3(1), dim3(160), 0, st_, rseed, static_cast<i64>(0), nb, 1, ring, raw);
+    launch(gauss_range_kernel, dim3(blocks(count)), dim3(256), 0, st_, static_cast<const u64*>(raw), pos, count, out);
+    arena_.release(raw);
+    arena_.release(ring);
+  }
+
+  // lanczos_topk (lanczos.hpp:38-127) on the tracked operator; the leading
+  // k eigenpairs go to X (rows [0, N)) and `values`.
+  void lanczos(const DevCsr& op, i64 N, const LzOpts& o) {
+    const i64 kq = k;
+    if (N < 1) throw InvalidArgument("lanczos_topk: empty operator");
+    if (kq < 1 || kq > N) throw InvalidArgument("lanczos_topk: k must satisfy 1 <= k <= n");
+    i64 m = o.max_basis > 0 ? o.max_basis : std::max<i64>(2 * kq + 20, 40);
+    if (m < kq) throw InvalidArgument("lanczos_topk: max_basis below k");
+    m = std::min(m, N);
+    if (m > kLzMaxCols) throw InvalidArgument("lanczos_topk: max_basis above the device limit (256)");
+    const int mm = static_cast<int>(m);
+    const int ldv = ld_for(mm);
+    const int keep_max = static_cast<int>(std::min<i64>(m, kq + std::min<i64>(kq, 10) + 2));
+    const int ldt = ld_for(std::max<i64>(keep_max, kq));
+    const int G = static_cast<int>(std::min<i64>(cdiv(N, 64), 148 * 8));
+    double* V = static_cast<double*>(arena_.alloc(sizeof(double) * N * ldv));
+    double* W = static_cast<double*>(arena_.alloc(sizeof(double) * N * ldv));
+    double* T = static_cast<double*>(arena_.alloc(sizeof(double) * N * ldt));
+    double* vb[2] = {static_cast<double*>(arena_.alloc(sizeof(double) * N)),
+                     static_cast<double*>(arena_.alloc(sizeof(double) * N))};
+    double* part = static_cast<double*>(arena_.alloc(sizeof(double) * G * kLzMaxCols));
+    double* small = static_cast<double*>(arena_.alloc(sizeof(double) * (4 * kLzMaxCols + 8)));
+    double* c1 = small;
+    double* c2 = small + kLzMaxCols;
+    double* nrm = small + 2 * kLzMaxCols;      // [0] ||v||^2 -> ||v||
+    double* rn = small + 2 * kLzMaxCols + 8;   // residual norms^2 (kk)
+    const int ldh = ld_for(mm);
+    double* H = static_cast<double*>(arena_.alloc(sizeof(double) * mm * ldh));
+    double* F = static_cast<double*>(arena_.alloc(sizeof(double) * mm * ldt));
+    double* wsort = static_cast<double*>(arena_.alloc(sizeof(double) * mm));
+    SpvBufs sp = spv_plan(op.rp, N);
+    struct Free {
+      Session* s;
+      std::vector<void*> p;
+      SpvBufs* sp;
+      ~Free() {
+        for (void* q : p) s->arena_.release(q);
+        s->spv_release(*sp);
+        cudaStreamSynchronize(s->st_);
+      }
+    } fr{this, {V, W, T, vb[0], vb[1], part, small, H, F, wsort}, &sp};
+    const u64 rseed = mix_seed(cfg.seed, 0x1a2cULL);
+    i64 draw_pos = 0;
+    int cur = 0;
+    auto fresh_vector = [&]() {
+      gauss_draws(rseed, draw_pos, N, vb[cur]);
+      draw_pos += N;
+    };
+    // ||v||^2 (+ the non-finite flag of the last product) on the host
+    std::vector<double> hbuf(static_cast<size_t>(2 * kLzMaxCols + 8));
+    auto norm2_of = [&](const double* v) {
+      lz_launch<true>(1, V, ldv, 0, c1, v, const_cast<double*>(v), N, part, kLzMaxCols, G);
+      launch(lz_colsum_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(part), G, kLzMaxCols, 1, nrm);
+      STG_CUDA(cudaMemcpyAsync(hbuf.data(), nrm, sizeof(double), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(&hs_->flags, flags_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      if (hs_->flags & 1) throw RuntimeError("lanczos_topk: operator produced non-finite values");
+      return hbuf[0];
+    };
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    fresh_vector();
+    int j = 0;
+    double a_norm = 0.0;
+    double best_worst = std::numeric_limits<double>::infinity();
+    std::vector<double> wv(static_cast<size_t>(mm)), res(static_cast<size_t>(kq));
+    lz_restarts = lz_products = 0;
+    for (i64 restart = 0;; ++restart) {
+      int fresh = 0;
+      while (j < mm) {
+        double* v = vb[cur];
+        double* v1 = vb[1 - cur];
+        double n2;
+        if (j > 0) {  // two Gram-Schmidt passes against the basis (lanczos.hpp:59-60)
+          lz_launch<false>(0, V, ldv, j, nullptr, v, nullptr, N, part, kLzMaxCols, G);
+          launch(lz_colsum_kernel, dim3(j), dim3(256), 0, st_, static_cast<const double*>(part), G, kLzMaxCols, j, c1);
+          lz_launch<false>(1, V, ldv, j, c1, v, v1, N, part, kLzMaxCols, G);
+          launch(lz_colsum_kernel, dim3(j), dim3(256), 0, st_, static_cast<const double*>(part), G, kLzMaxCols, j, c2);
+          lz_launch<true>(1, V, ldv, j, c2, v1, v, N, part, kLzMaxCols, G);
+          launch(lz_colsum_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(part), G, kLzMaxCols, 1, nrm);
+          STG_CUDA(cudaMemcpyAsync(hbuf.data(), nrm, sizeof(double), cudaMemcpyDeviceToHost, st_));
+          STG_CUDA(cudaMemcpyAsync(&hs_->flags, flags_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+          STG_CUDA(cudaStreamSynchronize(st_));
+          if (hs_->flags & 1) throw RuntimeError("lanczos_topk: operator produced non-finite values");
+          n2 = hbuf[0];
+        } else {
+          n2 = norm2_of(v);
+        }
+        const double nr = std::sqrt(n2);
+        if (!(nr > 1e-12)) {
+          if (++fresh > 4) break;  // invariant subspace; solve with what we have
+          fresh_vector();
+          continue;
+        }
+        fresh = 0;
+        launch(lz_sqrt_kernel, dim3(1), dim3(1), 0, st_, nrm);
+        launch(lz_store_kernel, dim3(blocks(N)), dim3(256), 0, st_, v, N, static_cast<const double*>(nrm), V, ldv, j);
+        spmv(op, sp.pl, v, v1, W + j, ldv);  // w = A v, stored as column j of W; v <- w
+        ++lz_products;
+        cur = 1 - cur;
+        ++j;
+      }
+      if (j == 0) throw RuntimeError("lanczos_topk: could not build a starting basis");
+      // Rayleigh-Ritz on the retained basis (lanczos.hpp:80-84)
+      const int kk = static_cast<int>(std::min<i64>(kq, j));
+      const int keep = static_cast<int>(std::min<i64>(j - 1 > 0 ? j - 1 : j, kq + std::min<i64>(kq, 10) + 2));
+      const int want = std::max(kk, keep);
+      gram(V, ldv, W, ldv, N, j, j, false, H, ldh);
+      ritz(H, ldh, j, want, wsort, F, ldt);
+      nn(V, ldv, N, j, F, ldt, kk, X_, ldx(), 1.0, 0.0, nullptr, 0);  // x = V F_k
+      nn(W, ldv, N, j, F, ldt, kk, T, ldt, 1.0, 0.0, nullptr, 0);     // W F_k
+      launch(lz_residual_kernel, dim3(blocks(N * kk)), dim3(256), 0, st_, T, ldt, static_cast<const double*>(X_),
+             ldx(), static_cast<const double*>(wsort), N, kk);
+      lz_launch<false>(2, T, ldt, kk, nullptr, nullptr, nullptr, N, part, kLzMaxCols, G);
+      launch(lz_colsum_kernel, dim3(kk), dim3(256), 0, st_, static_cast<const double*>(part), G, kLzMaxCols, kk, rn);
+      STG_CUDA(cudaMemcpyAsync(wv.data(), wsort, sizeof(double) * j, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(res.data(), rn, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(&hs_->flags, flags_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaMemcpyAsync(&hs_->info, info_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      if (hs_->flags & 1) throw RuntimeError("lanczos_topk: operator produced non-finite values");
+      if (hs_->flags & kNonFinite) throw InvalidArgument("sym_eig_dense: non-finite entries");
+      if (hs_->info != 0) throw RuntimeError("sym_eig_dense: factorization did not converge");
+      for (int i = 0; i < j; ++i) a_norm = std::max(a_norm, std::fabs(wv[static_cast<size_t>(i)]));
+      const double scale = std::max(a_norm, 1e-300);
+      int first_unconverged = -1;
+      double worst = 0.0;
+      for (int i = 0; i < kk; ++i) {
+        const double r = std::sqrt(res[static_cast<size_t>(i)]);
+        worst = std::max(worst, r);
+        if (first_unconverged < 0 && r > o.tol * scale) first_unconverged = i;
+      }
+      best_worst = std::min(best_worst, worst);
+      lz_restarts = restart;
+      if ((first_unconverged < 0 && kk == kq) || j >= N) {
+        values.assign(wv.begin(), wv.begin() + kk);
+        values.resize(static_cast<size_t>(kq), 0.0);
+        return;
+      }
+      if (restart >= o.max_restarts) {
+        std::ostringstream msg;
+        msg << "lanczos_topk: no convergence after " << o.max_restarts << " restarts (best worst-case residual "
+            << best_worst << ", tol " << o.tol * scale << ")";
+        throw RuntimeError(msg.str());
+      }
+      // thick restart (lanczos.hpp:116-125): the next direction is the first
+      // unconverged residual, then V, W <- V F_keep, W F_keep
+      const int pick = first_unconverged >= 0 ? first_unconverged : kk - 1;
+      launch(lz_column_kernel, dim3(blocks(N)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, pick, N,
+             vb[cur]);
+      nn(V, ldv, N, j, F, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
+      launch(copy2d_kernel, dim3(blocks(N * keep)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, V, ldv, N,
+             keep);
+      nn(W, ldv, N, j, F, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
+      launch(copy2d_kernel, dim3(blocks(N * keep)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, W, ldv, N,
+             keep);
+      j = keep;
+      if (!(std::sqrt(norm2_of(vb[cur])) > 0.0)) fresh_vector();
+    }
+  }
+
+  // sym_eig_dense of a j x j Lanczos projection (symmetrized (H + H')/2 as
+  // eig.hpp:39): all values in spectral order, `want` leading vectors
+  // (row-major j x want, ldf).
+  void ritz(const double* H, int ldh, int j, int want, double* wsort, double* F, int ldf) {
+    STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
+    if (!(cfg.flags & ST_FLAG_CUSOLVER_EIG) && j <= kEigMaxN) {
+      double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(j, want)));
+      int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(j, want)));
+      kbegin(kEig, 4.0 * j * j * j / 3.0);
+      syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, st_, args...); },
+                  H, ldh, j, /*sym_input*/ 0, static_cast<int>(cfg.order), want, 1e-3, wsort, F, ldf, dbuf, ibuf,
+                  flags_ptr());
+      kend();
+      return;
+    }
+    double *w = nullptr, *Vc = nullptr;
+    eig(H, ldh, j, &w, &Vc, "lz");
+    int* perm = arena_.get<int>("lz_perm", j);
+    launch(sort_perm_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(w), j,
+           static_cast<int>(cfg.order), perm);
+    launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(j) * j)), dim3(256), 0, st_, static_cast<const double*>(Vc),
+           j, static_cast<const double*>(w), static_cast<const int*>(perm), j, F, ldf, wsort);
+  }
+
  public:
   // (A, or the shifted Laplacian T): the residual the reference's Lanczos
   // convergence test measures (lanczos.hpp:85-95). One full-operator SpMM
@@ -2385,7 +2851,19 @@ class Session {
     const DevCsr& op = is_laplacian() ? T() : A();
     const i64 rows = n;
     const int kk = static_cast<int>(k);
-    double* AX = arena_.get<double>("res_ax", rows * ldx());
+    if (rows == 0) {
+      std::fill(out, out + kk, 0.0);
+      return;
+    }
+    // stream-ordered temporaries: a monitoring call leaves the session's
+    // persistent footprint unchanged
+    double* AX = nullptr;
+    const int nb = static_cast<int>(cdiv(rows, 256));
+    double* part = nullptr;
+    double* dout = nullptr;
+    STG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&AX), sizeof(double) * rows * ldx(), st_));
+    STG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(double) * nb * kk, st_));
+    STG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(double) * kk, st_));
     SpmmArgs sa{};
     sa.rows = rows;
     sa.row_off = 0;
@@ -2399,15 +2877,16 @@ class Session {
     sa.Y = AX;
     sa.ldy = static_cast<int>(ldx());
     STG_CUDA(cudaMemsetAsync(AX, 0, sizeof(double) * rows * ldx(), st_));
-    do_spmm(sa, op.nnz, rows, kSpmmFull);
-    const int nb = static_cast<int>(cdiv(rows, 256));
-    double* part = arena_.get<double>("res_part", static_cast<i64>(nb) * kk);
-    double* dout = arena_.get<double>("res_out", kk);
+    do_spmm(sa, op.nnz, rows, kSpmmFull, /*transient*/ true);
     launch(residual_partial_kernel, dim3(static_cast<unsigned>(nb)), dim3(256), 0, st_, static_cast<const double*>(AX),
            static_cast<int>(ldx()), static_cast<const double*>(X_), static_cast<int>(ldx()),
            static_cast<const double*>(d_values_), rows, kk, part);
-    launch(residual_reduce_kernel, dim3(1), dim3(static_cast<unsigned>(round_up(kk, 32))), 0, st_, static_cast<const double*>(part), nb, kk, dout);
+    launch(residual_reduce_kernel, dim3(static_cast<unsigned>(kk)), dim3(256), 0, st_, static_cast<const double*>(part),
+           nb, kk, dout);
     STG_CUDA(cudaMemcpyAsync(out, dout, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaFreeAsync(AX, st_));
+    STG_CUDA(cudaFreeAsync(part, st_));
+    STG_CUDA(cudaFreeAsync(dout, st_));
     STG_CUDA(cudaStreamSynchronize(st_));
     kflush();
   }
@@ -2443,10 +2922,26 @@ struct st_session {
 namespace {
 thread_local std::string g_create_error;
 
+// Selects a session's device for the duration of one ABI call and restores the
+// caller's current device afterwards (sessions on different GPUs may share a
+// process and a host thread).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) (void)cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) (void)cudaSetDevice(prev);
+  }
+};
+
 template <class F>
 st_status guarded(st_session* s, F&& f) {
   std::string* err = s ? &s->err : &g_create_error;
   try {
+    std::unique_ptr<DeviceGuard> dg;
+    if (s && s->impl) dg = std::make_unique<DeviceGuard>(s->impl->cfg.device);
     f();
     return ST_OK;
   } catch (const std::invalid_argument& e) {
@@ -2474,13 +2969,42 @@ st_status st_create(const st_config* cfg, int64_t n, const int32_t* rowptr, cons
     if (!cfg || !out || !rowptr || !eig_values || !eig_vectors) throw std::invalid_argument("st_create: null argument");
     if (n < 1) throw std::invalid_argument("st_create: empty graph");
     if (ld < n) throw std::invalid_argument("st_create: leading dimension below n");
+    DeviceGuard dg(cfg->device);
     auto s = std::make_unique<st_session>();
     s->impl = std::make_unique<stg::Session>(*cfg, n, rowptr, colidx, values_csr, eig_values, eig_vectors, ld);
     *out = s.release();
   });
 }
 
-void st_destroy(st_session* s) { delete s; }
+st_status st_tracker_init(const st_config* cfg, const st_lanczos_options* opts, int64_t n, const int32_t* rowptr,
+                          const int32_t* colidx, const double* values_csr, st_session** out) {
+  return guarded(nullptr, [&] {
+    if (!cfg || !out || !rowptr) throw std::invalid_argument("st_tracker_init: null argument");
+    if (n < 1) throw std::invalid_argument("lanczos_topk: empty operator");
+    stg::Session::LzOpts lz;
+    if (opts) {
+      lz.tol = opts->tol;
+      lz.max_basis = opts->max_basis;
+      lz.max_restarts = opts->max_restarts;
+    }
+    DeviceGuard dg(cfg->device);
+    auto s = std::make_unique<st_session>();
+    s->impl = std::make_unique<stg::Session>(*cfg, n, rowptr, colidx, values_csr, nullptr, nullptr, n, nullptr, &lz);
+    *out = s.release();
+  });
+}
+
+st_status st_init_stats(const st_session* s, int64_t* restarts, int64_t* products) {
+  if (restarts) *restarts = s->impl->lz_restarts;
+  if (products) *products = s->impl->lz_products;
+  return ST_OK;
+}
+
+void st_destroy(st_session* s) {
+  if (!s) return;
+  DeviceGuard dg(s->impl ? s->impl->cfg.device : 0);
+  delete s;
+}
 
 st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n_global, int64_t row_lo,
                             int64_t row_hi, int64_t chunk, const int32_t* rowptr, const int32_t* colidx,
@@ -2492,6 +3016,7 @@ st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n
     if (n_global < 1) throw std::invalid_argument("st_create: empty graph");
     if (ld < row_hi - row_lo) throw std::invalid_argument("st_create: leading dimension below n");
     stg::Session::ShardInit si{*comm, n_global, row_lo, row_hi, chunk};
+    DeviceGuard dg(cfg->device);
     auto s = std::make_unique<st_session>();
     s->impl = std::make_unique<stg::Session>(*cfg, row_hi - row_lo, rowptr, colidx, values_csr, eig_values,
                                              eig_vectors, ld, &si);
@@ -2522,6 +3047,10 @@ int64_t st_shard_layout(int32_t size, const int64_t* bounds, int64_t chunk, int3
   const int64_t rows = stg::sm_rows(m, rank, n_total, b);
   for (int64_t l = 0; l < rows && l < cap; ++l) global_ids[l] = stg::sm_global(m, l);
   return rows;
+}
+
+st_status st_reserve(st_session* s, int64_t n_nodes, int64_t nnz) {
+  return guarded(s, [&] { s->impl->reserve(n_nodes, nnz); });
 }
 
 st_status st_step(st_session* s, const st_update* upd) {
@@ -2601,7 +3130,7 @@ st_status st_sym_eig_dense(int32_t device, int64_t n, const double* s_colmajor, 
       if (!std::isfinite(s_colmajor[i])) throw std::invalid_argument("sym_eig_dense: non-finite entries");
     if (n == 0) return;
     if (n > stg::kEigMaxN) throw std::invalid_argument("st_sym_eig_dense: order above the on-device solver limit");
-    STG_CUDA(cudaSetDevice(device));
+    DeviceGuard dg(device);
     stg::eig_set_attributes();
     // row-major copy of S' (the solver symmetrizes (S + S')/2 itself)
     std::vector<double> rm(static_cast<size_t>(n * n));
@@ -2660,7 +3189,7 @@ st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_
   return guarded(nullptr, [&] {
     if (rows < 0 || cols < 0) throw std::invalid_argument("gaussian_matrix: negative size");
     if (rows * cols == 0) return;
-    STG_CUDA(cudaSetDevice(device));
+    DeviceGuard dg(device);
     const int64_t npairs = (rows * cols + 1) / 2;
     const int64_t nblocks = (2 * npairs + stg::kMtM - 1) / stg::kMtM;
     stg::u64 *raw, *ring;

@@ -194,6 +194,7 @@ class ShardedTrackerSession:
     _check = _T._check
     step = _T.step
     step_device = _T.step_device
+    reserve = _T.reserve
     info = _T.info
     values = _T.values
     launches = _T.launches
