@@ -134,6 +134,42 @@ st_status st_step(st_session* s, const st_update* upd);
  * value each step). Invalidates the last step's Delta export (st_get_csr 2). */
 st_status st_reserve(st_session* s, int64_t n_nodes, int64_t nnz);
 
+/* A CSR block (int32 row offsets rows + 1, int32 column ids, fp64 values). */
+typedef struct {
+  int64_t rows, cols, nnz;
+  const int32_t* rowptr;
+  const int32_t* colidx;
+  const double* values;
+} st_csr_block;
+
+/* GraphUpdate (graph.hpp:23-37): the step from n_old to n_old + n_new nodes as
+ * the symmetric block perturbation [K G; G' C] (K n_old x n_old symmetric, G
+ * n_old x n_new, C n_new x n_new symmetric). */
+typedef struct {
+  int64_t n_old, n_new;
+  st_csr_block k_block, g_block, c_block;
+} st_graph_update;
+
+/* One step from a GraphUpdate. Replaces, for a caller that holds blocks
+ * instead of edit lists (experiment.cpp:166-173):
+ *   A = apply_update(A, d);                graph.cpp:102-115
+ *   state = tracker_step(state, d);        trackers.cpp:384-387 -> to_perturbation
+ * Delta is assembled on the device exactly as GraphUpdate::to_delta +
+ * SymSparseMatrix::from_triplets (graph.cpp:17-32, sparse.cpp:17-23):
+ * duplicates summed in insertion order, exact zeros pruned, symmetry
+ * validated ("SymSparseMatrix: matrix is not symmetric"). Blocks may carry
+ * any nonzero weights (partial deletions, diagonal entries). Host arrays;
+ * st_step_blocks_device takes device arrays. */
+st_status st_step_blocks(st_session* s, const st_graph_update* upd);
+st_status st_step_blocks_device(st_session* s, const st_graph_update* upd);
+
+/* tracker_step(state, Perturbation) (trackers.cpp:341-382; Perturbation =
+ * {n_old, n_new, delta}, trackers.hpp:78-86) on an adjacency session: delta is
+ * the (n_old + n_new)-square symmetric perturbation, also applied to the
+ * session's A (pad(A) + delta with apply_update's checks). Laplacian sessions
+ * derive Delta_T themselves and reject this call. */
+st_status st_step_perturbation(st_session* s, int64_t n_old, int64_t n_new, const st_csr_block* delta);
+
 /* st_step with the edit arrays already resident in device memory (same
  * layout; every pointer in *upd is a device pointer). Used to time the step
  * with its inputs in HBM. */

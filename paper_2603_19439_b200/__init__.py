@@ -41,6 +41,16 @@ class StLanczosOptions(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_basis", C.c_int64), ("max_restarts", C.c_int64)]
 
 
+class StCsrBlock(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64), ("rowptr", I32P), ("colidx", I32P),
+                ("values", DP)]
+
+
+class StGraphUpdate(C.Structure):
+    _fields_ = [("n_old", C.c_int64), ("n_new", C.c_int64), ("k_block", StCsrBlock), ("g_block", StCsrBlock),
+                ("c_block", StCsrBlock)]
+
+
 class StUpdate(C.Structure):
     _fields_ = [("n_added", C.c_int64), ("added_i", I64P), ("added_j", I64P), ("added_w", DP),
                 ("n_removed", C.c_int64), ("removed_i", I64P), ("removed_j", I64P), ("n_new", C.c_int64),
@@ -74,6 +84,8 @@ def lib():
                                       C.POINTER(C.c_void_p)]
         L.st_init_stats.argtypes = [C.c_void_p, I64P, I64P]
         L.st_reserve.argtypes = [C.c_void_p, I64, I64]
+        L.st_step_blocks.argtypes = [C.c_void_p, C.POINTER(StGraphUpdate)]
+        L.st_step_perturbation.argtypes = [C.c_void_p, I64, I64, C.POINTER(StCsrBlock)]
         L.st_info.argtypes = [C.c_void_p, I64P, I64P, C.POINTER(C.c_uint64), I64P, I64P, I64P, DP]
         L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
         L.st_residual_norms.argtypes = [C.c_void_p, DP]
@@ -108,7 +120,7 @@ def lib():
         L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
                   "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows", "st_residual_norms",
-                  "st_reserve", "st_tracker_init", "st_init_stats"):
+                  "st_reserve", "st_tracker_init", "st_init_stats", "st_step_blocks", "st_step_perturbation"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -187,6 +199,65 @@ class Update:
             len(self.added[0]) + len(self.new_edges[0]))
 
 
+def _csr_block(rows, cols, rp, col, val):
+    rp = np.ascontiguousarray(rp, np.int32)
+    col = np.ascontiguousarray(col, np.int32)
+    val = np.ascontiguousarray(val, np.float64)
+    return (rp, col, val), StCsrBlock(rows, cols, len(col), _p(rp, I32P), _p(col, I32P), _p(val))
+
+
+def csr_from_coo(n_rows, rows, cols, vals):
+    """Canonical CSR (sorted, duplicates summed in input order) of COO triplets."""
+    rows, cols, vals = np.asarray(rows, np.int64), np.asarray(cols, np.int64), np.asarray(vals, np.float64)
+    o = np.lexsort((cols, rows))
+    rows, cols, vals = rows[o], cols[o], vals[o]
+    if len(rows):
+        head = np.ones(len(rows), bool)
+        head[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
+        idx = np.flatnonzero(head)
+        sums = np.add.reduceat(vals, idx) if len(idx) else vals
+        rows, cols, vals = rows[idx], cols[idx], sums
+    rp = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n_rows), out=rp[1:])
+    return rp.astype(np.int32), cols.astype(np.int32), vals
+
+
+@dataclass
+class GraphUpdate:
+    """GraphUpdate (graph.hpp:23-37): blocks K (n_old^2), G (n_old x n_new),
+    C (n_new^2) as canonical CSR triples (rowptr, col, val)."""
+    n_old: int
+    n_new: int
+    k_block: tuple
+    g_block: tuple
+    c_block: tuple
+
+    @staticmethod
+    def from_edits(n_old: int, upd: "Update") -> "GraphUpdate":
+        """assemble_update (graph.cpp:45-100) block placement, without its
+        validation: added/removed -> K (both triangles), old-new -> G,
+        new-new -> C (both triangles)."""
+        ai, aj, aw = (np.asarray(x) for x in upd.added)
+        ri, rj = (np.asarray(x, np.int64) for x in upd.removed)
+        ki = np.concatenate([ai, aj, ri, rj]).astype(np.int64)
+        kj = np.concatenate([aj, ai, rj, ri]).astype(np.int64)
+        kv = np.concatenate([aw, aw, -np.ones(len(ri)), -np.ones(len(ri))])
+        ni, nj, nw = (np.asarray(x) for x in upd.new_edges)
+        lo, hi = np.minimum(ni, nj).astype(np.int64), np.maximum(ni, nj).astype(np.int64)
+        g = lo < n_old
+        S = int(upd.n_new)
+        gb = csr_from_coo(n_old, lo[g], hi[g] - n_old, nw[g])
+        cl, ch, cw = lo[~g] - n_old, hi[~g] - n_old, nw[~g]
+        cb = csr_from_coo(S, np.concatenate([cl, ch]), np.concatenate([ch, cl]), np.concatenate([cw, cw]))
+        return GraphUpdate(n_old, S, csr_from_coo(n_old, ki, kj, kv), gb, cb)
+
+    def struct(self):
+        kk, kbs = _csr_block(self.n_old, self.n_old, *self.k_block)
+        gk, gbs = _csr_block(self.n_old, self.n_new, *self.g_block)
+        ck, cbs = _csr_block(self.n_new, self.n_new, *self.c_block)
+        return (kk, gk, ck), StGraphUpdate(self.n_old, self.n_new, kbs, gbs, cbs)
+
+
 class TrackerSession:
     """One tracker lane on one GPU: the adjacency CSR (and shifted operator for
     Laplacian operators) plus the TrackerState, resident in HBM."""
@@ -259,6 +330,17 @@ class TrackerSession:
     def step(self, upd: Update) -> None:
         keep, s = upd.struct()
         self._check(lib().st_step(self._h, C.byref(s)))
+
+    def step_blocks(self, g: GraphUpdate) -> None:
+        """One step from a GraphUpdate's blocks (st_step_blocks)."""
+        keep, st = g.struct()
+        self._check(lib().st_step_blocks(self._h, C.byref(st)))
+
+    def step_perturbation(self, n_old: int, n_new: int, rowptr, col, val) -> None:
+        """tracker_step(state, Perturbation{n_old, n_new, delta}) (st_step_perturbation)."""
+        n = n_old + n_new
+        keep, b = _csr_block(n, n, rowptr, col, val)
+        self._check(lib().st_step_perturbation(self._h, n_old, n_new, C.byref(b)))
 
     def reserve(self, n_nodes: int, nnz: int) -> None:
         """Size the session for a stream reaching n_nodes nodes and nnz stored

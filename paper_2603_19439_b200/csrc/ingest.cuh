@@ -22,6 +22,8 @@ enum EditError : int {
   kErrNewRange = 5,
   kErrNewWeight = 6,
   kErrNewOldOnly = 7,
+  kErrNotSymmetric = 8,  // from_triplets validation (sparse.cpp:55-63)
+  kErrBlockShape = 9,    // malformed caller CSR block (st_step_blocks / st_step_perturbation)
 };
 
 constexpr u64 kSentinel = ~0ULL;
@@ -225,6 +227,95 @@ __global__ void delta_rows_kernel(const u64* skey, i64 n2, int* drow, int* dcol,
   atomicAdd(rowcnt + r, 1);
   mark[r] = stamp;
 }
+
+// ---- GraphUpdate blocks / Perturbation CSR -> Delta entries ---------------
+// GraphUpdate::to_delta (graph.cpp:17-32) then from_triplets (sparse.cpp:
+// 17-23): the K, G (+ mirror) and C entries in that insertion order,
+// duplicates summed in insertion order (stable radix sort, sequential run
+// sums), exact zeros pruned, symmetry validated.
+struct BlockIn {
+  const int* rp;
+  const int* col;
+  const double* val;
+  i64 rows, cols, nnz;
+  i64 row_off, col_off;
+  int mirror;  // G: also emit the transposed entry
+  i64 out0;    // first output slot
+};
+
+__global__ void block_check_kernel(BlockIn b, u64* err) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (t == 0) bad = b.rp[0] != 0 || b.rp[b.rows] != b.nnz;
+  if (t < b.rows) bad = bad || b.rp[t + 1] < b.rp[t];
+  if (t < b.nnz) bad = bad || b.col[t] < 0 || b.col[t] >= b.cols;
+  if (bad) atomicMin(err, static_cast<u64>(kErrBlockShape));
+}
+
+__global__ void block_emit_kernel(BlockIn b, int kb, u64* key, double* val) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= b.nnz) return;
+  i64 lo = 0, hi = b.rows;  // row of entry e: last r with rp[r] <= e
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (b.rp[mid] <= e) lo = mid; else hi = mid;
+  }
+  const u64 r = static_cast<u64>(lo + b.row_off), c = static_cast<u64>(b.col[e] + b.col_off);
+  const double v = b.val[e];
+  const i64 o = b.out0 + (b.mirror ? 2 * e : e);
+  key[o] = (r << kb) | c;
+  val[o] = v;
+  if (b.mirror) {
+    key[o + 1] = (c << kb) | r;
+    val[o + 1] = v;
+  }
+}
+
+// heads of equal-key runs take the run's sum (insertion order); keep the
+// nonzero sums
+__global__ void run_sum_kernel(const u64* skey, const double* sval, i64 n, int* keep, double* sum) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e > n) return;
+  if (e == n) {
+    keep[e] = 0;
+    return;
+  }
+  const u64 k = skey[e];
+  const bool head = e == 0 || skey[e - 1] != k;
+  double s = 0.0;
+  if (head) {
+    s = sval[e];
+    for (i64 q = e + 1; q < n && skey[q] == k; ++q) s += sval[q];
+  }
+  keep[e] = head && s != 0.0;
+  sum[e] = s;
+}
+
+__global__ void run_compact_kernel(const u64* skey, const double* sum, const int* keep, const int* pos, i64 n,
+                                   u64* okey, double* oval) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n || !keep[e]) return;
+  okey[pos[e]] = skey[e];
+  oval[pos[e]] = sum[e];
+}
+
+// is_symmetric (sparse.cpp:65-77): every (r, c, v) has (c, r, v) exactly
+__global__ void sym_check_kernel(const u64* key, const double* val, const int* count, int kb, u64* err) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 cnt = *count;
+  if (e >= cnt) return;
+  const u64 k = key[e];
+  const u64 mask = (1ULL << kb) - 1;
+  const u64 t = ((k & mask) << kb) | (k >> kb);
+  i64 lo = 0, hi = cnt;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (key[mid] < t) lo = mid + 1; else hi = mid;
+  }
+  if (lo >= cnt || key[lo] != t || val[lo] != val[e]) atomicMin(err, static_cast<u64>(kErrNotSymmetric));
+}
+
+__global__ void count_to_u64_kernel(const int* count, unsigned long long* out) { *out = static_cast<unsigned long long>(*count); }
 
 __global__ void mark_range_kernel(int* mark, i64 lo, i64 hi, int stamp) {
   const i64 r = lo + static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;

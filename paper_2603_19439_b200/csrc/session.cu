@@ -22,6 +22,7 @@
 #include <cstring>
 #include <limits>
 #include <sstream>
+#include <functional>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -277,6 +278,8 @@ static const char* edit_message(int code) {
     case kErrNewRange: return "assemble_update: new edge endpoint out of range";
     case kErrNewWeight: return "assemble_update: new edges need positive weight";
     case kErrNewOldOnly: return "assemble_update: new edge addresses only existing nodes";
+    case kErrNotSymmetric: return "SymSparseMatrix: matrix is not symmetric";
+    case kErrBlockShape: return "st_step_blocks: malformed block CSR";
     default: return "assemble_update: invalid edit";
   }
 }
@@ -551,21 +554,54 @@ class Session {
 
   // ---------------------------------------------------------------- public ops
   void step(const st_update& u, bool device_ptrs = false) {
+    run_step(u.n_new, [&]() { return ingest(u, /*commit_slot*/ true, device_ptrs); });
+  }
+
+  // tracker_step(state, GraphUpdate) (trackers.cpp:384-387) with the session's
+  // apply_update: the blocks K, G, C of graph.hpp:23-37
+  void step_blocks(const st_graph_update& g, bool device_ptrs) {
+    if (g.n_old != n) throw InvalidArgument("apply_update: matrix size != d.n_old");
+    if (g.n_new < 0) throw InvalidArgument("make_empty_update: negative size");
+    const st_csr_block& K = g.k_block;
+    const st_csr_block& G = g.g_block;
+    const st_csr_block& Cb = g.c_block;
+    if (K.rows != g.n_old || K.cols != g.n_old || G.rows != g.n_old || G.cols != g.n_new || Cb.rows != g.n_new ||
+        Cb.cols != g.n_new)
+      throw InvalidArgument("st_step_blocks: block shape mismatch");
+    std::vector<HostBlock> hb{{K, 0, 0, 0}, {G, 0, g.n_old, 1}, {Cb, g.n_old, g.n_old, 0}};
+    run_step(g.n_new, [&]() { return ingest_blocks(g.n_new, hb, true, device_ptrs); });
+  }
+
+  // tracker_step(state, Perturbation) (trackers.cpp:341-382) on an adjacency
+  // session: Delta (n_old + n_new square) is also applied to the session's A
+  void step_perturbation(i64 n_old, i64 n_new, const st_csr_block& delta, bool device_ptrs) {
+    if (is_laplacian())
+      throw InvalidArgument("st_step_perturbation: Laplacian sessions derive Delta_T from graph updates");
+    if (n_old != n) throw InvalidArgument("build_projection_basis: perturbation dimension mismatch");
+    if (n_new < 0) throw InvalidArgument("build_projection_basis: negative expansion");
+    if (delta.rows != n_old + n_new || delta.cols != n_old + n_new)
+      throw InvalidArgument("build_projection_basis: delta size != n_old + n_new");
+    std::vector<HostBlock> hb{{delta, 0, 0, 0}};
+    run_step(n_new, [&]() { return ingest_blocks(n_new, hb, true, device_ptrs); });
+  }
+
+  template <class F>
+  void run_step(i64 n_new, F&& front) {
     launches = 0;
     rr_pre_.valid = false;
     kdiscard();  // a failed or probe call may have left unflushed entries
     timing_begin();
     const u64 basis_seed = mix_seed(mix_seed(cfg.seed, 0x6b7aULL), steps_taken);
     omega_S_ = -1;  // a sketch from an earlier call is never reused
-    if (cfg.kind == ST_GREST_RSVD && u.n_new > cfg.rsvd_l && u.n_new > 0) {
+    if (cfg.kind == ST_GREST_RSVD && n_new > cfg.rsvd_l && n_new > 0) {
       // the sketch's seed and shape are known before ingestion: overlap the
       // sequential mt19937_64 recurrence with it (trackers.cpp:362, rsvd.hpp:42-44)
-      const int q = static_cast<int>(std::min<i64>(u.n_new, cfg.rsvd_l + cfg.rsvd_p));
+      const int q = static_cast<int>(std::min<i64>(n_new, cfg.rsvd_l + cfg.rsvd_p));
       double* om;
       int ldo;
-      prepare_omega(basis_seed, u.n_new, q, &om, &ldo);
+      prepare_omega(basis_seed, n_new, q, &om, &ldo);
     }
-    Pert pt = ingest(u, /*commit_slot*/ true, device_ptrs);
+    Pert pt = front();
     timing_mark(0);
     if (pt.empty()) {
       commit_graph(pt);
@@ -1559,7 +1595,6 @@ class Session {
     while ((1LL << ed.kb) <= n_total) ++ed.kb;
     const int key_bits = 2 * ed.kb;
     u64* err_edit = d_scal_;
-    u64* err_apply = d_scal_ + 1;
     unsigned long long* nvalid = reinterpret_cast<unsigned long long*>(d_scal_ + 2);
     const i64 n2 = 2 * E;
     // ---- validation + Delta entries -> Delta (global CSR over n_total rows)
@@ -1625,12 +1660,161 @@ class Session {
       scan_int(dcnt, drp, n_total + 1);
     }
     kend();
-    if (sh_) return ingest_shard_tail(pt, u, device_ptrs, sort_path, ed, ekey_s, eval_s, dcol, drp, n2);
+    TailIn in{keep_delta, ed.kb, ekey_s, eval_s, n2, drow, dcol, drp, sort_path,
+              [&]() { return ingest(u, keep_delta, device_ptrs, true); }};
+    return ingest_tail(pt, in);
+  }
+
+  // ---- GraphUpdate blocks (graph.hpp:23-37) or a Perturbation's Delta
+  // (trackers.hpp:78-86) as the front of ingestion: `blocks` are CSRs with
+  // their offsets in the n_total square (K at (0,0), G at (0,n_old) mirrored,
+  // C at (n_old,n_old); or Delta alone at (0,0)).
+  struct HostBlock {
+    st_csr_block b;
+    i64 row_off, col_off;
+    int mirror;
+  };
+  Pert ingest_blocks(i64 S, const std::vector<HostBlock>& hb, bool keep_delta, bool device_ptrs) {
+    const i64 n_old = n, n_total = n_old + S;
+    if (S < 0) throw InvalidArgument("make_empty_update: negative size");
+    if (n_total >= (1LL << 31)) throw InvalidArgument("st_step: node count exceeds int32 CSR indexing");
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_mg_, 0));
+    if (sh_ && !keep_delta) throw InvalidArgument("st_probe: not available on sharded sessions");
+    ensure_node_capacity(n_total, sh_ ? rows_at(comm_.rank, n_total) : n_total);
+    ++stamp_;
+    if (stamp_ == 0x7fffffff) stamp_ = 1;
+    ++plan_epoch_;
+    Pert pt;
+    pt.n_old = n_old;
+    pt.S = S;
+    pt.n_total = n_total;
+    pt.stamp = stamp_;
+    STG_CUDA(cudaMemsetAsync(d_scal_, 0xff, sizeof(u64) * 2, st_));
+    STG_CUDA(cudaMemsetAsync(d_scal_ + 2, 0, sizeof(u64) * 3, st_));
+    kbegin(kIngestOther, 0.0);
+    int kb = 1;
+    while ((1LL << kb) <= n_total) ++kb;
+    u64* err_edit = d_scal_;
+    // upload (host blocks) and shape checks
+    std::vector<BlockIn> bins;
+    i64 n2 = 0;
+    for (size_t q = 0; q < hb.size(); ++q) {
+      const st_csr_block& b = hb[q].b;
+      if (b.nnz < 0 || b.rows < 0) throw InvalidArgument("st_step_blocks: malformed block CSR");
+      BlockIn bi{};
+      bi.rows = b.rows;
+      bi.cols = b.cols;
+      bi.nnz = b.nnz;
+      bi.row_off = hb[q].row_off;
+      bi.col_off = hb[q].col_off;
+      bi.mirror = hb[q].mirror;
+      bi.out0 = n2;
+      if (device_ptrs) {
+        bi.rp = b.rowptr;
+        bi.col = b.colidx;
+        bi.val = b.values;
+      } else {
+        const std::string nm = "blk" + std::to_string(q);
+        int* rp = arena_.get<int>(nm + ".rp", b.rows + 1);
+        int* col = arena_.get<int>(nm + ".col", b.nnz);
+        double* val = arena_.get<double>(nm + ".val", b.nnz);
+        if (!b.rowptr || (b.nnz && (!b.colidx || !b.values))) throw InvalidArgument("st_step_blocks: null block array");
+        STG_CUDA(cudaMemcpyAsync(rp, b.rowptr, sizeof(int) * (b.rows + 1), cudaMemcpyHostToDevice, st_));
+        if (b.nnz) {
+          STG_CUDA(cudaMemcpyAsync(col, b.colidx, sizeof(int) * b.nnz, cudaMemcpyHostToDevice, st_));
+          STG_CUDA(cudaMemcpyAsync(val, b.values, sizeof(double) * b.nnz, cudaMemcpyHostToDevice, st_));
+        }
+        bi.rp = rp;
+        bi.col = col;
+        bi.val = val;
+      }
+      launch(block_check_kernel, dim3(blocks(std::max(b.rows, b.nnz) + 1)), dim3(256), 0, st_, bi, err_edit);
+      n2 += bi.mirror ? 2 * b.nnz : b.nnz;
+      bins.push_back(bi);
+    }
+    STG_CUDA(cudaMemcpyAsync(&hs_->err_edit, err_edit, sizeof(u64), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
+    // entries -> stable sort -> run sums (duplicates in insertion order) -> prune zeros
+    const std::string sfx = keep_delta ? "" : "_probe";
+    u64* ekey = arena_.get<u64>("ekey", n2);
+    double* eval = arena_.get<double>("eval", n2);
+    u64* skey = arena_.get<u64>("b_skey", n2);
+    double* sval = arena_.get<double>("b_sval", n2);
+    for (const BlockIn& bi : bins)
+      if (bi.nnz) launch(block_emit_kernel, dim3(blocks(bi.nnz)), dim3(256), 0, st_, bi, kb, ekey, eval);
+    if (n2 > 0) {
+      size_t tmp = 0;
+      cub::DeviceRadixSort::SortPairs(nullptr, tmp, ekey, skey, eval, sval, static_cast<int>(n2), 0, 2 * kb, st_);
+      void* t = arena_.get<char>("cub_tmp", static_cast<i64>(tmp));
+      cub::DeviceRadixSort::SortPairs(t, tmp, ekey, skey, eval, sval, static_cast<int>(n2), 0, 2 * kb, st_);
+    }
+    int* keep = arena_.get<int>("b_keep", n2 + 1);
+    int* kpos = arena_.get<int>("b_kpos", n2 + 1);
+    double* rsum = arena_.get<double>("b_rsum", n2);
+    u64* ekey_s = arena_.get<u64>(keep_delta ? "ekey_s" : "ekey_s_probe", n2);
+    double* eval_s = arena_.get<double>(keep_delta ? "eval_s" : "eval_s_probe", n2);
+    int* drow = arena_.get<int>("drow" + sfx, n2);
+    int* dcol = arena_.get<int>("dcol" + sfx, n2);
+    int* dcnt = arena_.get<int>("dcnt", n_total + 1);
+    int* drp = arena_.get<int>("drp" + sfx, n_total + 1);
+    STG_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(int) * (n_total + 1), st_));
+    STG_CUDA(cudaMemsetAsync(ekey_s, 0xff, sizeof(u64) * std::max<i64>(n2, 1), st_));
+    launch(run_sum_kernel, dim3(blocks(n2 + 1)), dim3(256), 0, st_, static_cast<const u64*>(skey),
+           static_cast<const double*>(sval), n2, keep, rsum);
+    scan_int(keep, kpos, n2 + 1);
+    if (n2 > 0) {
+      launch(run_compact_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(skey),
+             static_cast<const double*>(rsum), static_cast<const int*>(keep), static_cast<const int*>(kpos), n2,
+             ekey_s, eval_s);
+      launch(sym_check_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s),
+             static_cast<const double*>(eval_s), static_cast<const int*>(kpos + n2), kb, err_edit);
+      launch(delta_rows_kernel, dim3(blocks(n2)), dim3(256), 0, st_, static_cast<const u64*>(ekey_s), n2, drow, dcol,
+             dcnt, mark_delta_, stamp_, kb);
+    }
+    launch(count_to_u64_kernel, dim3(1), dim3(1), 0, st_, static_cast<const int*>(kpos + n2),
+           reinterpret_cast<unsigned long long*>(d_scal_ + 2));
+    scan_int(dcnt, drp, n_total + 1);
+    kend();
+    TailIn in{keep_delta, kb, ekey_s, eval_s, n2, drow, dcol, drp, true, nullptr};
+    return ingest_tail(pt, in);
+  }
+
+  // What the validation / Delta-assembly front hands to the shared tail: the
+  // sorted Delta entries (keys (row << kb | col), sentinels last), their CSR
+  // over n_total rows, and how to redo the front on the sorting path.
+  struct TailIn {
+    bool keep_delta;
+    int kb;
+    u64* ekey_s;
+    double* eval_s;
+    i64 n2;
+    int* drow;
+    int* dcol;
+    int* drp;
+    bool sort_path;
+    std::function<Pert()> redo;
+  };
+
+  // apply_update (graph.cpp:102-115) or ShiftedLaplacianSession::advance
+  // (laplacian_track.cpp:48-64), then P and the compressed CSR.
+  Pert ingest_tail(Pert pt, const TailIn& in) {
+    const bool keep_delta = in.keep_delta;
+    const i64 n_old = pt.n_old, S = pt.S, n_total = pt.n_total, n2 = in.n2;
+    u64* ekey_s = in.ekey_s;
+    double* eval_s = in.eval_s;
+    int* drow = in.drow;
+    int* dcol = in.dcol;
+    int* drp = in.drp;
+    const std::string sfx = keep_delta ? "" : "_probe";
+    u64* err_edit = d_scal_;
+    u64* err_apply = d_scal_ + 1;
+    if (sh_) return ingest_shard_tail(pt, in);
     // ---- apply_update merge (A_next in the spare slot)
     const DevCsr& a = A();
     const int slot = keep_delta ? 1 - acur_ : 2;  // probes never touch the live buffers
     size_t merge_pend = 0;
-    DevCsr an = merge_launch(a, n_old, n_total, ekey_s, eval_s, n2, drow, dcol, drp, mark_delta_, ed.kb, slot,
+    DevCsr an = merge_launch(a, n_old, n_total, ekey_s, eval_s, n2, drow, dcol, drp, mark_delta_, in.kb, slot,
                              keep_delta && !is_laplacian(), err_apply, &merge_pend);
     const bool kt_p = !is_laplacian();  // (the Laplacian path syncs inside)
     if (kt_p && klog_) snprintf(ktag_, sizeof(ktag_), "ingest: P, sizes");
@@ -1654,10 +1838,10 @@ class Session {
         pend_[merge_pend].work = 12.0 * a.nnz + 4.0 * (n_old + 1) + 12.0 * an.nnz + 4.0 * (n_total + 1);
     };
     // a Delta row too long for the counting path: redo on the sorting path
-    auto redo = [&]() { return !sort_path && hs_->err_edit == 0; };
+    auto redo = [&]() { return !in.sort_path && hs_->err_edit == 0; };
     if (is_laplacian()) {
       STG_CUDA(cudaStreamSynchronize(st_));
-      if (redo()) return ingest(u, keep_delta, device_ptrs, true);
+      if (redo()) return in.redo();
       check_validation();
     }
     // ---- the tracked operator's perturbation
@@ -1728,7 +1912,7 @@ class Session {
     if (kt_p) kend();
     STG_CUDA(cudaStreamSynchronize(st_));
     if (!is_laplacian()) {
-      if (redo()) return ingest(u, keep_delta, device_ptrs, true);
+      if (redo()) return in.redo();
       check_validation();
     }
     pt.p = hs_->p;
@@ -1759,10 +1943,14 @@ class Session {
   // owned rows of Delta are compressed. Errors are decided identically on
   // every rank (edit errors are replicated; apply errors are gathered and the
   // one at the smallest global (row, col) is reported, as on one GPU).
-  Pert ingest_shard_tail(Pert pt, const st_update& u, bool device_ptrs, bool sort_path, const EditsDev& ed,
-                         const u64* ekey_s, const double* eval_s, const int* dcol, const int* drp, i64 n2) {
+  Pert ingest_shard_tail(Pert pt, const TailIn& in) {
+    const u64* ekey_s = in.ekey_s;
+    const double* eval_s = in.eval_s;
+    const int* dcol = in.dcol;
+    const int* drp = in.drp;
+    const i64 n2 = in.n2;
     const i64 n_old = pt.n_old, n_total = pt.n_total;
-    const int R = comm_.size, rank = comm_.rank, kb = ed.kb;
+    const int R = comm_.size, rank = comm_.rank, kb = in.kb;
     const i64 xo = nloc_, xt = rows_at(rank, n_total);
     u64* err_edit = d_scal_;
     u64* err_apply = d_scal_ + 1;
@@ -1804,7 +1992,7 @@ class Session {
     STG_CUDA(cudaMemcpyAsync(&hs_->nnz_new, an.rp + xt, sizeof(int), cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaMemcpyAsync(&hs_->p, pp + xt, sizeof(int), cudaMemcpyDeviceToHost, st_));
     STG_CUDA(cudaStreamSynchronize(st_));
-    if (!sort_path && hs_->err_edit == 0) return ingest(u, true, device_ptrs, true);  // replicated decision
+    if (!in.sort_path && hs_->err_edit == 0) return in.redo();  // replicated decision
     if (hs_->err_edit != kSentinel) throw InvalidArgument(edit_message(static_cast<int>(hs_->err_edit & 0xff)));
     u64 mine = hs_->err_apply;
     if (mine != kSentinel) {  // local row -> global row in the error key
@@ -3216,6 +3404,27 @@ st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_
 st_status st_debug_bench(st_session* s, int32_t which, int64_t N, int32_t m1, int32_t m2, int32_t flag,
                          int32_t iters, double* ms) {
   return guarded(s, [&] { *ms = s->impl->bench_kernel(which, N, m1, m2, flag, iters); });
+}
+
+st_status st_step_blocks(st_session* s, const st_graph_update* upd) {
+  return guarded(s, [&] {
+    if (!upd) throw std::invalid_argument("st_step_blocks: null update");
+    s->impl->step_blocks(*upd, false);
+  });
+}
+
+st_status st_step_blocks_device(st_session* s, const st_graph_update* upd) {
+  return guarded(s, [&] {
+    if (!upd) throw std::invalid_argument("st_step_blocks: null update");
+    s->impl->step_blocks(*upd, true);
+  });
+}
+
+st_status st_step_perturbation(st_session* s, int64_t n_old, int64_t n_new, const st_csr_block* delta) {
+  return guarded(s, [&] {
+    if (!delta) throw std::invalid_argument("st_step_perturbation: null delta");
+    s->impl->step_perturbation(n_old, n_new, *delta, false);
+  });
 }
 
 st_status st_step_device(st_session* s, const st_update* upd) {
