@@ -35,6 +35,7 @@ HBM_PEAK_FALLBACK = 6650.0
 # FP64 tensor (DMMA) peak: not in MEASURED_PEAKS.json; measured by us on this
 # pool with cuBLAS DGEMM 8192^3 (profiles/fp64_peaks_r01.txt).
 FP64_PEAK_MEASURED = 35.46
+FLOP_CLASSES = ("dmma_gram", "dmma_gemm", "masked_gram_x", "dmma_gram_narrow", "dmma_gemm_narrow")
 
 
 def measured_peaks():
@@ -224,6 +225,9 @@ def _run_ours(args, saved_stdout):
     t_setup = time.time()
     replicas = world > 1 and args.replicas
     stream, wl = make_workload(args.config, W + K, seed_offset=rank if replicas else 0, scale=args.scale)
+    if args.k:
+        wl["k"] = args.k
+        wl["workload"] = wl["workload"].replace("k=32", f"k={args.k}").replace("k=64", f"k={args.k}")
     if hasattr(stream, "csr0_torch"):  # config 5: the start graph is already on the device
         trp, tcol, tval = stream.csr0_torch()
         n_ = trp.numel() - 1
@@ -246,11 +250,14 @@ def _run_ours(args, saved_stdout):
     if sharded:
         import torch.distributed as dist
 
-        from paper_2603_19439_b200.shard import ShardedTrackerSession, TorchComm, local_block, shard_bounds
+        from paper_2603_19439_b200.shard import (NcclComm, ShardedTrackerSession, TorchComm, local_block,
+                                                 shard_bounds)
 
         if not dist.is_initialized():  # --sharded on one GPU: a one-rank NCCL group
             dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1)
-        comm = TorchComm("nccl")
+        # the library's own NCCL communicator (collectives enqueued by the
+        # library on the session stream); --torch-comm: torch.distributed callbacks
+        comm = TorchComm("nccl") if args.torch_comm else NcclComm(device=local)
         bounds = shard_bounds(rp, world)
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         blk = local_block(rp, col, val, vecs0, lo, hi)
@@ -266,7 +273,7 @@ def _run_ours(args, saved_stdout):
             s_ = ShardedTrackerSession(comm, len(rp) - 1, lo, hi, blk[0], blk[1], blk[2], vals0, blk[3],
                                        chunk=1024, kernel_timing=kernel_timing, **kw_sh)
         else:
-            s_ = TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, **kw)
+            s_ = TrackerSession(rp, col, val, vals0, vecs0, kernel_timing=kernel_timing, timing=kernel_timing, **kw)
         s_.reserve(n_cap, nnz_cap)
         return s_
 
@@ -283,6 +290,7 @@ def _run_ours(args, saved_stdout):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     launches = 0
+    halo0 = sess.halo_stats() if sharded else None
     torch.cuda.synchronize()
     e0.record()
     for t in range(W, W + K):
@@ -296,16 +304,22 @@ def _run_ours(args, saved_stdout):
     ms = dist_max(e0.elapsed_time(e1), world)
     step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, K)]
     info = sess.info()
+    halo = ({k_: v - halo0[k_] for k_, v in sess.halo_stats().items()} if sharded else None)
     sess.close()
 
     # ---- per-kernel-class device time: the same steps again, CUDA events
     # around every launch (ST_FLAG_KERNEL_TIMING), outside the timed region
     sess = new_session(kernel_timing=True)
+    sess.set_peaks(FP64_PEAK_MEASURED, measured_peaks()[0])
     for t in range(W):
         sess.step_device(dev_updates[t])
     sess.reset_kernel_stats()
+    tracker_ms = []
     for t in range(W, W + K):
         sess.step_device(dev_updates[t])
+        ph = sess.timings() if not sharded else []
+        if len(ph) >= 6:  # [ingest, basis, rr_gram, eig, rotate, total]: the step after ingestion
+            tracker_ms.append(ph[5] - ph[0])
     torch.cuda.synchronize()
     kstats = sess.kernel_stats()
     sess.close()
@@ -346,15 +360,19 @@ def _run_ours(args, saved_stdout):
         st = kstats[name]
         if st["launches"] == 0:
             continue
-        flops_class = name in ("dmma_gram", "dmma_gemm", "masked_gram_x")
+        flops_class = name in FLOP_CLASSES
         byte_class = name in ("spmm", "spmm_sketch", "csr_merge", "rotate_x")
         ach = st["work"] / (st["ms"] / 1e3) if st["ms"] > 0 else 0.0
         row = dict(ms_per_step=st["ms"] / K, launches_per_step=st["launches"] / K,
                    share=st["ms"] / ms if ms > 0 else 0.0)
         if flops_class:
-            row.update(achieved_tflops=ach / 1e12, frac_fp64_peak=ach / 1e12 / FP64_PEAK_MEASURED)
+            row.update(achieved_tflops=ach / 1e12, frac_fp64_peak=ach / 1e12 / FP64_PEAK_MEASURED,
+                       achieved_gbs=st["work2"] / (st["ms"] / 1e3) / 1e9 if st["ms"] > 0 else 0.0)
         elif byte_class:
             row.update(achieved_gbs=ach / 1e9, frac_hbm=ach / 1e9 / hbm_peak)
+        if (flops_class or byte_class) and st["ms"] > 0:
+            # per-launch roofline time max(flops / F, bytes / B) summed, over the measured time
+            row["frac_of_roofline_bound"] = st["bound_ms"] / st["ms"]
         classes[name] = row
     # the roofline kernel: the largest class on the step's critical stream (the eigensolver is latency-bound;
     # the CSR merge builds the NEXT step's A on a low-priority side stream, its event time includes starvation)
@@ -370,17 +388,19 @@ def _run_ours(args, saved_stdout):
     if dom is not None:
         st = kstats[dom]
         ach = st["work"] / (st["ms"] / 1e3)
-        if dom in ("dmma_gram", "dmma_gemm", "masked_gram_x"):
-            tr = traffic.get(dom)
+        if dom in FLOP_CLASSES:
+            tr = traffic.get(args.config, {}).get(dom)  # measured for this config, else null
             roof = dict(kernel=dom, bound="tensor", achieved=ach / 1e12, peak=FP64_PEAK_MEASURED, unit="TFLOP/s",
                         frac=ach / 1e12 / FP64_PEAK_MEASURED, traffic=tr["bytes_per_launch"] if tr else None,
                         traffic_launch=tr, 
                         peak_source="measured cuBLAS DGEMM 8192^3 on this pool (FP64 not in MEASURED_PEAKS.json)",
-                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="flop")
+                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="flop",
+                        frac_of_roofline_bound=classes[dom].get("frac_of_roofline_bound"))
         else:
             roof = dict(kernel=dom, bound="hbm", achieved=ach / 1e9, peak=hbm_peak, unit="GB/s",
                         frac=ach / 1e9 / hbm_peak, traffic=None, peak_source=hbm_src,
-                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="byte")
+                        algorithmic_work_per_launch=st["work"] / st["launches"], unit_work="byte",
+                        frac_of_roofline_bound=classes[dom].get("frac_of_roofline_bound"))
     out = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
@@ -388,7 +408,7 @@ def _run_ours(args, saved_stdout):
         "data": f"synthetic (seeded stream, BASELINE {args.config} shapes)",
         "config": {"workload": wl["workload"], "n0": int(len(rp) - 1), "nnz0": int(rp[-1]), "k": wl["k"],
                    "kind": wl["kind"], "rsvd_l": 100, "rsvd_p": 100, "n_final": info["n"],
-                   "parallelism": (f"row-sharded over {world} GPU(s) (NCCL allreduce of Grams, allgather halo)"
+                   "parallelism": (f"row-sharded over {world} GPU(s) (NCCL allreduce of Grams, boundary-row alltoallv halo)"
                                    if sharded else "single GPU" if world == 1 else f"{world} independent replicas"),
                    "l2": f"inputs larger than L2 (CSR {12 * int(rp[-1]) / 1e9:.2f} GB + X "
                          f"{8 * wl['k'] * (len(rp) - 1) / 1e9:.2f} GB per stream)",
@@ -397,6 +417,12 @@ def _run_ours(args, saved_stdout):
         "kernel_classes": classes,
         "e2e": {"value": e2e, "unit": "steps/s", "ms_per_step": ms_e2e / K, "h2d_bytes_per_step": h2d // K,
                 "d2h_bytes_per_step": 8 * wl["k"]},
+        "tracker_step_only": ({"value": 1e3 / float(np.mean(tracker_ms)), "unit": "steps/s",
+                               "ms_per_step": float(np.mean(tracker_ms)),
+                               "what": "device time from the end of ingestion (validation, Delta, CSR merge "
+                                       "launch, P) to the end of the step: the reference's step_seconds "
+                                       "(experiment.cpp:202-204, tracker_step only); measured in the kernel-timing "
+                                       "session, per-phase events"} if tracker_ms else None),
         "gpu_launches": launches,
         "step_ms": [round(x, 3) for x in step_ms],
         "step_ms_e2e": [round(x, 3) for x in step_ms_e2e],
@@ -407,7 +433,7 @@ def _run_ours(args, saved_stdout):
                                "sample": "not run: one oracle step at R-MAT s25 is hours of CPU work and ~150 GB "
                                          "of host RAM (SURVEY.md 8(d)); see the cfg3 line for the CPU baseline"}
     elif rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
+        threads = args.cpu_threads or os.cpu_count() or 1
         dt, dt_tracker = cpu_baseline(stream, vals0, vecs0, wl, threads)
         out["cpu_baseline"] = {"value": 1.0 / dt, "unit": "steps/s", "cores": threads, "kind": "port",
                                "sample": f"1 step (step {0}) of the same stream: assemble_update + apply_update + "
@@ -415,7 +441,9 @@ def _run_ours(args, saved_stdout):
                                          f"tracker_step alone {dt_tracker:.2f} s",
                                "seconds_per_step": dt}
     if comm is not None:
-        out["comm"] = {"calls_per_step": {k_: v / (2 * (W + K)) for k_, v in comm.calls.items()}}
+        out["comm"] = {"kind": "torch.distributed callbacks" if args.torch_comm else "library NCCL (st_comm_nccl)",
+                       "halo_bytes_recv_per_step": halo["halo_bytes_recv"] / max(K, 1),
+                       "halo_bytes_local_per_step": halo["halo_bytes_local"] / max(K, 1)}
     if rank == 0:
         sys.stdout.flush()
         os.write(saved_stdout, (json.dumps(out) + "\n").encode())
@@ -432,7 +460,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
+    threads = args.cpu_threads or os.cpu_count() or 1
     os.environ["OMP_NUM_THREADS"] = str(threads)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
@@ -479,8 +507,13 @@ def main():
     ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--scale", type=int, default=None, help="R-MAT scale override (development)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--k", type=int, default=None, help="tracked pairs override (the cfg5 k sweep {16, 32, 64})")
+    ap.add_argument("--cpu-threads", type=int, default=None,
+                    help="threads of the CPU legs (default: all host threads; 1 = the reference's serial build)")
     ap.add_argument("--sharded", action="store_true", help="row-sharded sessions even on one GPU (NCCL group of 1)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of row sharding")
+    ap.add_argument("--torch-comm", action="store_true", help="sharded: torch.distributed callbacks instead of the "
+                                                               "library's NCCL communicator")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

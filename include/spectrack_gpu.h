@@ -224,6 +224,13 @@ typedef struct {
   int32_t (*allreduce_sum_f64)(void* ctx, double* buf, int64_t count, void* stream);
   /* recv[r * bytes .. (r + 1) * bytes) = send of rank r, for every rank r */
   int32_t (*allgather)(void* ctx, const void* send, void* recv, int64_t bytes, void* stream);
+  /* personalized exchange: the send buffer holds send_bytes[r] bytes for rank
+   * r, the chunks contiguous in rank order; the recv buffer receives
+   * recv_bytes[r] bytes from rank r, contiguous in rank order (the byte
+   * counts are host arrays of `size` entries; ncclSend/ncclRecv in a group,
+   * MPI_Alltoallv). Carries the boundary-row halo of the sharded SpMMs. */
+  int32_t (*alltoallv)(void* ctx, const void* send, const int64_t* send_bytes, void* recv, const int64_t* recv_bytes,
+                       void* stream);
 } st_comm;
 
 /* Sharded counterpart of st_create. Every rank passes the same cfg and
@@ -242,6 +249,19 @@ st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n
                             int64_t row_hi, int64_t chunk, const int32_t* rowptr, const int32_t* colidx,
                             const double* values_csr, const double* eig_values, const double* eig_vectors,
                             int64_t ld, st_session** out);
+
+/* The library's own st_comm over NCCL (NVLink / NVSwitch): every collective
+ * is enqueued on the session stream with no host callback. Rank 0 calls
+ * st_nccl_unique_id and shares the 128 bytes with the other ranks (any
+ * transport); each rank then calls st_comm_nccl_create on its device.
+ * NCCL is resolved at run time (libnccl.so.2). */
+st_status st_nccl_unique_id(void* out128);
+st_status st_comm_nccl_create(const void* unique_id, int32_t rank, int32_t size, int32_t device, st_comm* out);
+void st_comm_nccl_destroy(st_comm* c);
+
+/* Halo traffic of a sharded session since creation: bytes received from
+ * other ranks, bytes of own rows copied locally, and the number of halos. */
+st_status st_shard_stats(const st_session* s, int64_t* halo_bytes_recv, int64_t* halo_bytes_local, int64_t* halos);
 
 /* Owned rows of a (sharded) session: *n_local, and their global ids when
  * global_ids is not NULL. An unsharded session owns every row. */
@@ -281,6 +301,15 @@ st_status st_gaussian_matrix(int32_t device, uint64_t seed, int64_t rows, int64_
  * unknown class. */
 int32_t st_kernel_stats(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work);
 void st_reset_kernel_stats(st_session* s);
+/* st_kernel_stats plus the second work measure (bytes of the DMMA classes,
+ * flops of the memory classes) and the summed per-launch roofline time
+ * max(flops / peak_flops, bytes / peak_bw) (peaks from st_set_peaks;
+ * defaults 35.46 TFLOP/s FP64, 6465.8 GB/s). Classes 13 (DMMA Gram with both
+ * sides <= 32 columns) and 14 (row-local GEMM with <= 32 output columns)
+ * separate the narrow, memory-bound shapes from classes 0 and 1. */
+int32_t st_kernel_stats2(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work, double* work2,
+                         double* bound_ms);
+void st_set_peaks(st_session* s, double fp64_tflops, double hbm_gbs);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,8 @@ OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
 ORDER = {"abs_desc": 0, "alg_desc": 1}
 FLAG_FORCE_DENSE, FLAG_TIMING, FLAG_KERNEL_TIMING, FLAG_CUSOLVER_EIG = 1, 2, 4, 8
 KERNEL_CLASSES = ["dmma_gram", "dmma_gemm", "spmm", "cholesky", "tri_inverse", "eigensolver", "csr_merge", "rng",
-                  "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other", "spmm_full"]
+                  "rotate_x", "masked_gram_x", "spmm_sketch", "ingest_other", "spmm_full", "dmma_gram_narrow",
+                  "dmma_gemm_narrow"]
 
 
 class StConfig(C.Structure):
@@ -105,6 +106,10 @@ def lib():
         L.st_step_device.restype = C.c_int
         L.st_kernel_stats.argtypes = [C.c_void_p, C.c_int32, DP, I64P, DP]
         L.st_kernel_stats.restype = C.c_int32
+        L.st_kernel_stats2.argtypes = [C.c_void_p, C.c_int32, DP, I64P, DP, DP, DP]
+        L.st_kernel_stats2.restype = C.c_int32
+        L.st_set_peaks.argtypes = [C.c_void_p, C.c_double, C.c_double]
+        L.st_set_peaks.restype = None
         L.st_reset_kernel_stats.argtypes = [C.c_void_p]
         L.st_reset_kernel_stats.restype = None
         L.st_sym_eig_dense.argtypes = [C.c_int32, I64, DP, C.c_int32, I64, DP, DP]
@@ -116,6 +121,14 @@ def lib():
         L.st_create_sharded.argtypes = [C.POINTER(StConfig), C.POINTER(_shard.StComm), I64, I64, I64, I64, I32P,
                                         I32P, DP, DP, DP, I64, C.POINTER(C.c_void_p)]
         L.st_shard_rows.argtypes = [C.c_void_p, I64P, I64P]
+        L.st_nccl_unique_id.argtypes = [C.c_void_p]
+        L.st_nccl_unique_id.restype = C.c_int
+        L.st_comm_nccl_create.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(_shard.StComm)]
+        L.st_comm_nccl_create.restype = C.c_int
+        L.st_comm_nccl_destroy.argtypes = [C.POINTER(_shard.StComm)]
+        L.st_comm_nccl_destroy.restype = None
+        L.st_shard_stats.argtypes = [C.c_void_p, I64P, I64P, I64P]
+        L.st_shard_stats.restype = C.c_int
         L.st_shard_layout.argtypes = [C.c_int32, I64P, I64, C.c_int32, I64, I64P, I64]
         L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
@@ -355,11 +368,16 @@ class TrackerSession:
     def kernel_stats(self) -> dict:
         out = {}
         for i, name in enumerate(KERNEL_CLASSES):
-            ms, work = C.c_double(), C.c_double()
+            ms, work, work2, bound = C.c_double(), C.c_double(), C.c_double(), C.c_double()
             cnt = I64()
-            lib().st_kernel_stats(self._h, i, C.byref(ms), C.byref(cnt), C.byref(work))
-            out[name] = dict(ms=ms.value, launches=cnt.value, work=work.value)
+            lib().st_kernel_stats2(self._h, i, C.byref(ms), C.byref(cnt), C.byref(work), C.byref(work2),
+                                   C.byref(bound))
+            out[name] = dict(ms=ms.value, launches=cnt.value, work=work.value, work2=work2.value,
+                             bound_ms=bound.value)
         return out
+
+    def set_peaks(self, fp64_tflops: float, hbm_gbs: float) -> None:
+        lib().st_set_peaks(self._h, fp64_tflops, hbm_gbs)
 
     def reset_kernel_stats(self) -> None:
         lib().st_reset_kernel_stats(self._h)

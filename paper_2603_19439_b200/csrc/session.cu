@@ -34,6 +34,7 @@
 #include "eigsolve.cuh"
 #include "ingest.cuh"
 #include "lanczos.cuh"
+#include "nccl_comm.cuh"
 #include "rng.cuh"
 #include "shard.cuh"
 #include "smalllin.cuh"
@@ -45,7 +46,7 @@ namespace stg {
 // kernel classes for per-class device timing (st_kernel_stats)
 enum KClass : int {
   kGram = 0, kGemm = 1, kSpmm = 2, kChol = 3, kTriinv = 4, kEig = 5, kMerge = 6, kRng = 7, kRotate = 8,
-  kKcGram = 9, kSpmmSketch = 10, kIngestOther = 11, kSpmmFull = 12
+  kKcGram = 9, kSpmmSketch = 10, kIngestOther = 11, kSpmmFull = 12, kGramNarrow = 13, kGemmNarrow = 14
 };
 
 struct InvalidArgument : std::invalid_argument {
@@ -305,7 +306,11 @@ struct Pert {
   i64 G = 0;                 // p + k (unsharded)
   i64 S_loc = 0;             // appended rows in P here (= S unsharded)
   i64 x_old = 0, x_total = 0;  // rows of the X storage before / after the step
-  i64 pmax = 0;              // halo rows per rank (sharded)
+  i64 pmax = 0;              // P-id exchange rows per rank (sharded)
+  // boundary-row halo (sharded): rows sent to / received from each rank
+  const int* hsend = nullptr;  // own P indices to send, grouped by destination
+  i64 nsend = 0, nrecv = 0;
+  std::vector<i64> send_rows, recv_rows;
   const int* Ploc = nullptr;   // X storage row of each row of P (= P unsharded)
   const int* Pglob = nullptr;  // global id of each row of P (= P unsharded)
   const double* gval = nullptr;  // values of the global Delta CSR (grp/gcol)
@@ -334,11 +339,15 @@ class Session {
   i64 launches = 0;
   // per-kernel-class device time (CUDA events on the launching stream) and
   // algorithmic work (flops for DMMA classes, bytes for memory-bound classes)
+  // work: flops (DMMA classes) or bytes (memory classes); work2 the other
+  // measure; bound_ms the per-launch roofline time max(flops / F, bytes / B)
+  // summed (peaks from st_set_peaks)
   struct KStat {
-    double ms = 0, work = 0;
+    double ms = 0, work = 0, work2 = 0, bound_ms = 0;
     i64 launches = 0;
   };
-  static constexpr int kClasses = 13;
+  static constexpr int kClasses = 15;
+  double peak_tflops_ = 35.46, peak_gbs_ = 6465.8;
   KStat kstats[kClasses];
 
   struct ShardInit {
@@ -496,7 +505,7 @@ class Session {
 
   void init_shard(const ShardInit& si) {
     if (si.comm.size < 1 || si.comm.rank < 0 || si.comm.rank >= si.comm.size || !si.comm.allreduce_sum_f64 ||
-        !si.comm.allgather)
+        !si.comm.allgather || !si.comm.alltoallv)
       throw InvalidArgument("st_create_sharded: invalid communicator");
     if (si.chunk < 1) throw InvalidArgument("st_create_sharded: chunk must be positive");
     if (si.lo < 0 || si.hi < si.lo || si.hi > si.n_global)
@@ -540,6 +549,13 @@ class Session {
   void allgather(const void* send, void* recv, i64 bytes) {
     if (comm_.allgather(comm_.ctx, send, recv, bytes, st_) != 0) throw RuntimeError("st_comm: allgather failed");
   }
+  void alltoallv(const void* send, const std::vector<i64>& sb, void* recv, const std::vector<i64>& rb) {
+    if (comm_.alltoallv(comm_.ctx, send, reinterpret_cast<const int64_t*>(sb.data()), recv,
+                        reinterpret_cast<const int64_t*>(rb.data()), st_) != 0)
+      throw RuntimeError("st_comm: alltoallv failed");
+  }
+  // bytes the sharded SpMM halos received (diagnostics: st_shard_stats)
+  i64 halo_bytes_recv_ = 0, halo_bytes_local_ = 0, halo_calls_ = 0;
   // small host values of every rank (rank-major), through device staging
   std::vector<u64> allgather_u64(const std::vector<u64>& mine) {
     const i64 m = static_cast<i64>(mine.size());
@@ -883,7 +899,7 @@ class Session {
   struct PendingK {
     int cls;
     cudaEvent_t a, b;
-    double work;
+    double work, work2;
     char tag[48];
   };
   char ktag_[48] = {0};  // optional shape tag for the next kbegin (STG_KLOG)
@@ -901,9 +917,9 @@ class Session {
     return evpool_[evnext_++];
   }
   std::vector<size_t> open_;  // kbegin/kend nest (e.g. the rotation contains a GEMM)
-  void kbegin(int cls, double work, cudaStream_t s = nullptr) {
+  void kbegin(int cls, double work, cudaStream_t s = nullptr, double work2 = 0.0) {
     if (!ktiming()) return;
-    PendingK p{cls, next_event(), next_event(), work, {0}};
+    PendingK p{cls, next_event(), next_event(), work, work2, {0}};
     std::memcpy(p.tag, ktag_, sizeof(p.tag));
     ktag_[0] = 0;
     STG_CUDA(cudaEventRecord(p.a, s ? s : st_));
@@ -924,7 +940,14 @@ class Session {
       STG_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
       kstats[p.cls].ms += ms;
       kstats[p.cls].work += p.work;
+      kstats[p.cls].work2 += p.work2;
       kstats[p.cls].launches += 1;
+      const bool flop_cls = p.cls == kGram || p.cls == kGemm || p.cls == kKcGram || p.cls == kGramNarrow ||
+                            p.cls == kGemmNarrow;
+      const bool byte_cls = p.cls == kSpmm || p.cls == kSpmmSketch || p.cls == kMerge || p.cls == kRotate ||
+                            p.cls == kSpmmFull;
+      if (flop_cls) kstats[p.cls].bound_ms += 1e3 * std::max(p.work / (peak_tflops_ * 1e12), p.work2 / (peak_gbs_ * 1e9));
+      if (byte_cls) kstats[p.cls].bound_ms += 1e3 * std::max(p.work / (peak_gbs_ * 1e9), p.work2 / (peak_tflops_ * 1e12));
       if (klog_) {
         float t0 = 0;  // start offset from the step's first timed launch (timeline across streams)
         cudaEventElapsedTime(&t0, pend_.front().a, p.a);
@@ -1073,7 +1096,9 @@ class Session {
     const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * TB;
     a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "gram %lldx%dx%d%s", rows, m1, m2, sym ? " sym" : "");
-    kbegin(mask ? kKcGram : kGram, sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
+    kbegin(mask ? kKcGram : narrow ? kGramNarrow : kGram,
+           sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2, nullptr,
+           8.0 * rows * (sym ? m1 : m1 + m2) + 8.0 * m1 * m2);
     const dim3 grid(ntiles, static_cast<unsigned>(splits));
     const bool bulk = !mask && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
                       lda % 2 == 0 && ldb % 2 == 0;
@@ -1143,22 +1168,30 @@ class Session {
   }
 
   // Dense SpMM operand over the rows of P: the stacked block itself, or in a
-  // sharded session the halo of every rank's owned rows (rank-major, pmax
-  // rows per rank; the compressed columns are positions in it).
+  // sharded session [own rows of P | the remote rows the owned Delta rows
+  // reference] (the boundary-row halo planned in ingest_shard_tail).
   const double* halo(const Pert& pt, const double* X, int ldx, int m, int* ld_out) {
     if (!sh_) {
       *ld_out = ldx;
       return X;
     }
     const int ldh = ld_for(m);
-    const i64 rows = std::max<i64>(pt.pmax, 1);
-    double* send = arena_.get<double>("halo_send", rows * ldh);
-    double* recv = arena_.get<double>("halo_recv", rows * ldh * comm_.size);
-    if (pt.p > 0)
-      launch(copy2d_kernel, dim3(blocks(pt.p * m)), dim3(256), 0, st_, X, ldx, send, ldh, pt.p, m);
-    allgather(send, recv, static_cast<i64>(sizeof(double)) * rows * ldh);
+    double* buf = arena_.get<double>("halo_buf", std::max<i64>(pt.p + pt.nrecv, 1) * ldh);
+    double* send = arena_.get<double>("halo_send", std::max<i64>(pt.nsend, 1) * ldh);
+    if (pt.p > 0) launch(copy2d_kernel, dim3(blocks(pt.p * m)), dim3(256), 0, st_, X, ldx, buf, ldh, pt.p, m);
+    if (pt.nsend > 0)
+      launch(gather_rows_kernel, dim3(blocks(pt.nsend * m)), dim3(256), 0, st_, X, ldx, pt.hsend, pt.nsend, m, send,
+             ldh);
+    std::vector<i64> sb(pt.send_rows.size()), rb(pt.recv_rows.size());
+    const i64 rowb = static_cast<i64>(sizeof(double)) * ldh;
+    for (size_t r = 0; r < sb.size(); ++r) sb[r] = pt.send_rows[r] * rowb;
+    for (size_t r = 0; r < rb.size(); ++r) rb[r] = pt.recv_rows[r] * rowb;
+    alltoallv(send, sb, buf + pt.p * ldh, rb);
+    halo_bytes_recv_ += pt.nrecv * rowb;
+    halo_bytes_local_ += pt.p * rowb;
+    ++halo_calls_;
     *ld_out = ldh;
-    return recv;
+    return buf;
   }
 
   void nn(const double* A, int lda, i64 rows, int m1, const double* C, int ldc, int m2, double* Out, int ldo,
@@ -1185,7 +1218,8 @@ class Session {
       a.skip_info = info_ptr();
     }
     if (klog_) snprintf(ktag_, sizeof(ktag_), "nn %lldx%dx%d%s", rows, m1, m2, tri ? " tri" : "");
-    kbegin(kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2);
+    kbegin(m2 <= 32 ? kGemmNarrow : kGemm, tri ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2,
+           nullptr, 8.0 * rows * (m1 + m2 + (beta != 0.0 ? m2 : 0)) + 8.0 * m1 * m2);
     if (m2 <= 32)
     {
       const bool stream = m1 <= 32 && beta == 0.0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && lda % 2 == 0 &&
@@ -1291,7 +1325,7 @@ class Session {
     } else {
       pl.scratch = arena_.get<double>("spmm_scratch", pe.smax * pl.lds);
     }
-    kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols));
+    kbegin(cls, 12.0 * nnz + 4.0 * (a.rows + 1) + 8.0 * a.m * (a.rows + distinct_cols), nullptr, 2.0 * nnz * a.m);
     for (int c0 = 0; c0 < a.m; c0 += 256) {  // dense blocks wider than 256 columns: 256-column slabs
       SpmmArgs b = a;
       b.X = a.X + c0;
@@ -2060,6 +2094,56 @@ class Session {
       launch(own_compress_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, drp, dcol, eval_s,
              static_cast<const int*>(pglob), p, static_cast<const int*>(lrp), static_cast<const int*>(posmap_), lcol,
              scol, val);
+    // ---- boundary-row halo plan: the remote rows of P the owned Delta rows
+    // reference, requested from their owners; columns renumbered to
+    // [own rows | received rows]
+    {
+      const i64 total = pmax * R;
+      int* need = arena_.get<int>("sh_need", total + 1);
+      int* npos = arena_.get<int>("sh_npos", total + 1);
+      int* slot = arena_.get<int>("sh_slot", total);
+      STG_CUDA(cudaMemsetAsync(need, 0, sizeof(int) * (total + 1), st_));
+      if (pt.nnz > 0)
+        launch(halo_need_kernel, dim3(blocks(pt.nnz)), dim3(256), 0, st_, static_cast<const int*>(lcol), pt.nnz, pmax,
+               rank, need);
+      scan_int(need, npos, total + 1);
+      // requests per owner: positions [r pmax, (r + 1) pmax) of the scan
+      std::vector<int> cut(static_cast<size_t>(R) + 1);
+      for (int r = 0; r <= R; ++r)
+        STG_CUDA(cudaMemcpyAsync(&cut[r], npos + std::min<i64>(static_cast<i64>(r) * pmax, total), sizeof(int),
+                                 cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      const i64 nreq = cut[R];
+      int* req = arena_.get<int>("sh_req", std::max<i64>(nreq, 1));
+      launch(halo_req_kernel, dim3(blocks(total)), dim3(256), 0, st_, static_cast<const int*>(need),
+             static_cast<const int*>(npos), total, pmax, p, req, slot);
+      if (pt.nnz > 0)
+        launch(halo_remap_kernel, dim3(blocks(pt.nnz)), dim3(256), 0, st_, lcol, pt.nnz, pmax, rank,
+               static_cast<const int*>(slot));
+      // everyone's request counts (R x R, host) -> what this rank sends to whom
+      std::vector<u64> mine(static_cast<size_t>(R));
+      for (int r = 0; r < R; ++r) mine[r] = static_cast<u64>(cut[r + 1] - cut[r]);
+      const std::vector<u64> all = allgather_u64(mine);  // all[src * R + owner]
+      pt.recv_rows.assign(static_cast<size_t>(R), 0);
+      pt.send_rows.assign(static_cast<size_t>(R), 0);
+      for (int r = 0; r < R; ++r) {
+        pt.recv_rows[r] = static_cast<i64>(mine[r]);
+        pt.send_rows[r] = static_cast<i64>(all[static_cast<size_t>(r) * R + rank]);
+      }
+      pt.recv_rows[rank] = pt.send_rows[rank] = 0;
+      pt.nrecv = nreq;
+      pt.nsend = 0;
+      for (int r = 0; r < R; ++r) pt.nsend += pt.send_rows[r];
+      int* hsend = arena_.get<int>("sh_hsend", std::max<i64>(pt.nsend, 1));
+      // the requests travel to the owners (request lists out, send lists in)
+      std::vector<i64> sb(static_cast<size_t>(R)), rb(static_cast<size_t>(R));
+      for (int r = 0; r < R; ++r) {
+        sb[r] = pt.recv_rows[r] * static_cast<i64>(sizeof(int));
+        rb[r] = pt.send_rows[r] * static_cast<i64>(sizeof(int));
+      }
+      alltoallv(req, sb, hsend, rb);
+      pt.hsend = hsend;
+    }
     pt.p = p;
     pt.p_old = p - pt.S_loc;
     pt.pmax = pmax;
@@ -3212,6 +3296,52 @@ st_status st_create_sharded(const st_config* cfg, const st_comm* comm, int64_t n
   });
 }
 
+st_status st_nccl_unique_id(void* out128) {
+  return guarded(nullptr, [&] {
+    if (!out128) throw std::invalid_argument("st_nccl_unique_id: null argument");
+    ncclUniqueId id;
+    if (stg::nccl_api().GetUniqueId(&id) != ncclSuccess) throw stg::CudaError("ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+st_status st_comm_nccl_create(const void* unique_id, int32_t rank, int32_t size, int32_t device, st_comm* out) {
+  return guarded(nullptr, [&] {
+    if (!unique_id || !out) throw std::invalid_argument("st_comm_nccl_create: null argument");
+    if (size < 1 || rank < 0 || rank >= size) throw std::invalid_argument("st_comm_nccl_create: bad rank / size");
+    DeviceGuard dg(device);
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    auto ctx = std::make_unique<stg::NcclCtx>();
+    ctx->rank = rank;
+    ctx->size = size;
+    const ncclResult_t r = stg::nccl_api().CommInitRank(&ctx->comm, size, id, rank);
+    if (r != ncclSuccess)
+      throw stg::CudaError(std::string("ncclCommInitRank failed: ") + stg::nccl_api().GetErrorString(r));
+    out->rank = rank;
+    out->size = size;
+    out->ctx = ctx.release();
+    out->allreduce_sum_f64 = stg::nccl_allreduce_cb;
+    out->allgather = stg::nccl_allgather_cb;
+    out->alltoallv = stg::nccl_alltoallv_cb;
+  });
+}
+
+void st_comm_nccl_destroy(st_comm* c) {
+  if (!c || !c->ctx) return;
+  auto* ctx = static_cast<stg::NcclCtx*>(c->ctx);
+  if (ctx->comm) stg::nccl_api().CommDestroy(ctx->comm);
+  delete ctx;
+  c->ctx = nullptr;
+}
+
+st_status st_shard_stats(const st_session* s, int64_t* halo_bytes_recv, int64_t* halo_bytes_local, int64_t* halos) {
+  if (halo_bytes_recv) *halo_bytes_recv = s->impl->halo_bytes_recv_;
+  if (halo_bytes_local) *halo_bytes_local = s->impl->halo_bytes_local_;
+  if (halos) *halos = s->impl->halo_calls_;
+  return ST_OK;
+}
+
 st_status st_shard_rows(const st_session* s, int64_t* n_local, int64_t* global_ids) {
   auto* ms = const_cast<st_session*>(s);
   return guarded(ms, [&] {
@@ -3444,5 +3574,22 @@ int32_t st_kernel_stats(const st_session* s, int32_t cls, double* ms, int64_t* l
 }
 
 void st_reset_kernel_stats(st_session* s) { s->impl->kreset(); }
+
+int32_t st_kernel_stats2(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work, double* work2,
+                         double* bound_ms) {
+  if (cls < 0 || cls >= stg::Session::kClasses) return 0;
+  const auto& k = s->impl->kstats[cls];
+  *ms = k.ms;
+  *launches = k.launches;
+  *work = k.work;
+  *work2 = k.work2;
+  *bound_ms = k.bound_ms;
+  return 1;
+}
+
+void st_set_peaks(st_session* s, double fp64_tflops, double hbm_gbs) {
+  if (fp64_tflops > 0) s->impl->peak_tflops_ = fp64_tflops;
+  if (hbm_gbs > 0) s->impl->peak_gbs_ = hbm_gbs;
+}
 
 }  // extern "C"

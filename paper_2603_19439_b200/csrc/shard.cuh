@@ -12,9 +12,15 @@
 // Per step each rank holds the full (small) perturbation Delta — every rank
 // validates and assembles the same edit lists, O(edits) — and keeps the rows
 // it owns: the CSR merge, the rows of P, the stacked coordinates, the Delta
-// SpMMs and the rotation of X are row-local. Dense operands of the SpMMs are
-// exchanged as a halo of the rows of P (allgather, padded per rank), and every
-// Gram is a local split-K partial followed by one allreduce (st_comm).
+// SpMMs and the rotation of X are row-local. Dense operands of the SpMMs need
+// the rows their owned Delta rows reference on other ranks: a boundary-row
+// halo. Once per step (Delta changes every step) each rank lists the distinct
+// remote rows of P its compressed Delta references, the lists are exchanged
+// (counts by allgather, ids by alltoallv), and the compressed columns are
+// renumbered into [own rows of P | received rows, grouped by source rank]. An
+// SpMM then copies its own rows, gathers the rows peers asked for and runs one
+// alltoallv of exactly the referenced rows (no rank receives rows it does not
+// read). Every Gram is a local split-K partial followed by one allreduce.
 #pragma once
 
 #include "common.cuh"
@@ -141,6 +147,43 @@ __global__ void __launch_bounds__(256) own_compress_kernel(const int* grp, const
     scol[o + q - s] = c;
     val[o + q - s] = gval[q];
   }
+}
+
+// ---- boundary-row halo plan ----------------------------------------------
+// need[h] = 1 for every remote halo position (owner != rank) an owned Delta
+// entry references (h = owner * pmax + index in the owner's rows of P).
+__global__ void halo_need_kernel(const int* lcol, i64 nnz, i64 pmax, int rank, int* need) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const int h = lcol[e];
+  if (h / pmax != rank) need[h] = 1;
+}
+
+// requested positions in halo order (owner-major, then index) and, per
+// position, its slot after the own rows
+__global__ void halo_req_kernel(const int* need, const int* pos, i64 total, i64 pmax, i64 p, int* req_idx,
+                                int* slot) {
+  const i64 h = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (h >= total || !need[h]) return;
+  req_idx[pos[h]] = static_cast<int>(h % pmax);  // the owner's local index
+  slot[h] = static_cast<int>(p + pos[h]);
+}
+
+// compressed columns: own position -> index in the own rows, remote -> slot
+__global__ void halo_remap_kernel(int* lcol, i64 nnz, i64 pmax, int rank, const int* slot) {
+  const i64 e = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const int h = lcol[e];
+  lcol[e] = (h / pmax == rank) ? static_cast<int>(h % pmax) : slot[h];
+}
+
+// rows a peer asked for, in the order it asked (send buffer of one SpMM halo)
+__global__ void gather_rows_kernel(const double* X, int ldx, const int* idx, i64 rows, int m, double* out, int ldo) {
+  const i64 t = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= rows * m) return;
+  const i64 r = t / m;
+  const int c = static_cast<int>(t % m);
+  out[r * ldo + c] = X[static_cast<i64>(idx[r]) * ldx + c];
 }
 
 // grest3 trailing block on owned rows: entry (i, n_old + j) of Delta -> column j.

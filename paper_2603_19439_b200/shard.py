@@ -21,11 +21,13 @@ import numpy as np
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64), C.c_void_p)
 
 
 class StComm(C.Structure):
     _fields_ = [("rank", C.c_int32), ("size", C.c_int32), ("ctx", C.c_void_p),
-                ("allreduce_sum_f64", ALLREDUCE_FN), ("allgather", ALLGATHER_FN)]
+                ("allreduce_sum_f64", ALLREDUCE_FN), ("allgather", ALLGATHER_FN), ("alltoallv", ALLTOALLV_FN)]
 
 
 class _DevBuf:
@@ -55,10 +57,11 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.size = dist.get_world_size(group)
-        self.calls = {"allreduce": 0, "allgather": 0, "bytes": 0, "host_s": 0.0}
+        self.calls = {"allreduce": 0, "allgather": 0, "alltoallv": 0, "bytes": 0, "host_s": 0.0}
         self._ar = ALLREDUCE_FN(self._allreduce)
         self._ag = ALLGATHER_FN(self._allgather)
-        self.struct = StComm(self.rank, self.size, None, self._ar, self._ag)
+        self._a2a = ALLTOALLV_FN(self._alltoallv)
+        self.struct = StComm(self.rank, self.size, None, self._ar, self._ag, self._a2a)
 
     def _allreduce(self, ctx, buf, count, stream):
         t0 = time.perf_counter()
@@ -118,6 +121,78 @@ class TorchComm:
         except Exception as e:
             print(f"[rank {self.rank}] st_comm allgather failed: {e!r}", flush=True)
             return 1
+
+
+    def _alltoallv(self, ctx, send, send_bytes, recv, recv_bytes, stream):
+        t0 = time.perf_counter()
+        try:
+            import torch
+            import torch.distributed as dist
+
+            sb = [int(send_bytes[r]) for r in range(self.size)]
+            rb = [int(recv_bytes[r]) for r in range(self.size)]
+            if sum(sb) == 0 and sum(rb) == 0 and self.mode == "nccl":
+                return 0
+            s = _view(send, max(sum(sb), 1), torch.uint8)[: sum(sb)] if sum(sb) else torch.empty(
+                0, dtype=torch.uint8, device="cuda")
+            r = _view(recv, max(sum(rb), 1), torch.uint8)[: sum(rb)] if sum(rb) else torch.empty(
+                0, dtype=torch.uint8, device="cuda")
+            ext = torch.cuda.ExternalStream(stream)
+            self.calls["alltoallv"] += 1
+            self.calls["bytes"] += sum(rb)
+            if self.mode == "nccl":
+                with torch.cuda.stream(ext):
+                    dist.all_to_all_single(r, s, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+            else:
+                ext.synchronize()
+                hs = s.cpu()
+                hr = torch.empty(sum(rb), dtype=torch.uint8)
+                dist.all_to_all_single(hr, hs, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+                if sum(rb):
+                    with torch.cuda.stream(ext):
+                        r.copy_(hr)
+                    ext.synchronize()
+            self.calls["host_s"] += time.perf_counter() - t0
+            return 0
+        except Exception as e:
+            print(f"[rank {self.rank}] st_comm alltoallv failed: {e!r}", flush=True)
+            return 1
+
+
+class NcclComm:
+    """The library's own st_comm over NCCL (st_comm_nccl_create): rank 0 draws
+    the unique id, torch.distributed carries it to the other ranks, and every
+    collective of the sharded step is then enqueued by the library itself on
+    the session stream (no Python on the data path)."""
+
+    def __init__(self, device: int = 0, group=None):
+        import torch.distributed as dist
+
+        from . import ST_OK, TrackerError, _KINDS, lib
+
+        L = lib()
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        uid = C.create_string_buffer(128)
+        if self.rank == 0 and L.st_nccl_unique_id(uid) != ST_OK:
+            raise TrackerError("cuda", L.st_last_error(None).decode())
+        box = [bytes(uid.raw)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = C.create_string_buffer(box[0], 128)
+        self.struct = StComm()
+        rc = L.st_comm_nccl_create(uid, self.rank, self.size, device, C.byref(self.struct))
+        if rc != ST_OK:
+            raise TrackerError(_KINDS.get(rc, "other"), L.st_last_error(None).decode())
+        self.calls = {"native": 1}
+
+    def close(self):
+        from . import lib
+
+        if getattr(self, "struct", None) is not None and self.struct.ctx:
+            lib().st_comm_nccl_destroy(C.byref(self.struct))
+
+    def __del__(self):
+        self.close()
 
 
 def shard_bounds(rowptr, size: int) -> np.ndarray:
@@ -199,8 +274,17 @@ class ShardedTrackerSession:
     values = _T.values
     launches = _T.launches
     kernel_stats = _T.kernel_stats
+    set_peaks = _T.set_peaks
     reset_kernel_stats = _T.reset_kernel_stats
     del _T
+
+    def halo_stats(self) -> dict:
+        """Boundary-row halo traffic since creation (st_shard_stats)."""
+        from . import I64P, lib
+
+        r, l_, h = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().st_shard_stats(self._h, C.byref(r), C.byref(l_), C.byref(h))
+        return {"halo_bytes_recv": r.value, "halo_bytes_local": l_.value, "halos": h.value}
 
     def rows(self) -> np.ndarray:
         from . import I64P, lib

@@ -55,7 +55,7 @@ def _cases():
     }
 
 
-def run(rank, world, port, case, chunk, q):
+def run(rank, world, port, case, chunk, q, comm_kind="staged"):
     try:
         os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
                           MASTER_PORT=str(port))
@@ -67,7 +67,7 @@ def run(rank, world, port, case, chunk, q):
         import pyoracle as po
         from harness import SIN_TOL, VALUE_RTOL, edges_of, random_update, sin_angle, value_err
         from paper_2603_19439_b200 import TrackerError
-        from paper_2603_19439_b200.shard import ShardedTrackerSession, TorchComm, local_block, shard_bounds
+        from paper_2603_19439_b200.shard import NcclComm, ShardedTrackerSession, TorchComm, local_block, shard_bounds
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
         rp, col, val, cfg, stream, *init = _cases()[case]()
@@ -89,7 +89,9 @@ def run(rank, world, port, case, chunk, q):
         bounds = shard_bounds(a.rowptr, world)
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         lrp, lcol, lval, lx = local_block(a.rowptr, a.col, a.val, vecs, lo, hi)
-        comm = TorchComm("staged")
+        # "staged": collectives through host memory over gloo (several ranks on
+        # one GPU); "nccl": the library's own NCCL communicator (one rank per GPU)
+        comm = TorchComm("staged") if comm_kind == "staged" else NcclComm(device=0)
         g = ShardedTrackerSession(comm, n, lo, hi, lrp, lcol, lval, vals, lx, chunk=chunk, **cfg)
         rng = stream[1] if stream[0] == "random" else None
         nsteps = stream[2] if stream[0] == "random" else len(stream[1])
@@ -148,7 +150,7 @@ def run(rank, world, port, case, chunk, q):
         after = g.embedding()
         assert msg == "apply_update: invalid deletion (no such edge)", msg
         assert np.array_equal(before[1], after[1]) and g.info()["n"] == cur
-        q.put((rank, "ok", report, comm.calls))
+        q.put((rank, "ok", report, dict(comm.calls, **g.halo_stats())))
         dist.destroy_process_group()
     except Exception:
         q.put((rank, "fail", traceback.format_exc(), None))

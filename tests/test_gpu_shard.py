@@ -13,7 +13,7 @@ import pytest
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(world, case, chunk=4):
+def _run(world, case, chunk=4, comm="staged"):
     import torch.multiprocessing as mp
 
     sys.path.insert(0, HERE)
@@ -24,7 +24,7 @@ def _run(world, case, chunk=4):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=shard_worker.run, args=(r, world, port, case, chunk, q)) for r in range(world)]
+    procs = [ctx.Process(target=shard_worker.run, args=(r, world, port, case, chunk, q, comm)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
@@ -63,3 +63,10 @@ def test_sharded_config3_shape_two_ranks():
     """Config 3's shapes (R-MAT s15, k = 32, L = P = 100: q = 200 sketch, D = 164)
     row-sharded over two ranks."""
     _run(2, "cfg3_s15", chunk=64)
+
+
+@pytest.mark.gpu
+def test_sharded_native_nccl_comm_one_rank():
+    """The library's own NCCL communicator (st_comm_nccl_create): allreduce,
+    allgather and the alltoallv halo enqueued on the session stream."""
+    _run(1, "cfg3_s15", chunk=64, comm="nccl")
