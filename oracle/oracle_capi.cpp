@@ -76,13 +76,8 @@ struct Session {
 };
 
 TrackerKind kind_of(int k) {
-  switch (k) {
-    case 3: return TrackerKind::iasc;
-    case 4: return TrackerKind::grest2;
-    case 5: return TrackerKind::grest3;
-    case 6: return TrackerKind::grest_rsvd;
-    default: throw std::invalid_argument("oracle: tracker kind outside the G-REST path");
-  }
+  if (k < 0 || k > 7) throw std::invalid_argument("unknown tracker kind");
+  return static_cast<TrackerKind>(k);  // trackers.hpp:36-45 order
 }
 
 }  // namespace
@@ -264,6 +259,9 @@ int or_session_create(int kind, int op, std::int64_t k, int order, std::int64_t 
       s->state.values.assign(values, values + k);
       s->state.vectors = mat_in(n, k, vectors);
       s->state.n = n;
+      double sq = 0.0;  // restart_scale = ||Lambda||_2 as tracker_init sets it (trackers.cpp:143)
+      for (double v : s->state.values) sq += v * v;
+      s->state.restart_scale = std::sqrt(sq);
     } else {
       s->state = tracker_init(opmat, tk, o);
     }
@@ -272,6 +270,31 @@ int or_session_create(int kind, int op, std::int64_t k, int order, std::int64_t 
 }
 
 void or_session_destroy(void* h) { delete static_cast<Session*>(h); }
+
+// TrackerOptions fields of the perturbation trackers and TIMERS (trackers.hpp:52-63)
+int or_session_set_options(void* h, double mu, int trip_replace_span, double theta, std::int64_t min_restart_gap,
+                           int restart_inner, char* err, int errlen) {
+  Session* s = static_cast<Session*>(h);
+  return guarded(err, errlen, [&] {
+    if (s->state.kind == TrackerKind::timers && restart_inner == static_cast<int>(TrackerKind::timers))
+      throw std::invalid_argument("tracker_init: timers cannot delegate to itself");
+    (void)kind_of(restart_inner);
+    s->state.opts.mu = mu;
+    s->state.opts.trip_replace_span = trip_replace_span != 0;
+    s->state.opts.theta = theta;
+    s->state.opts.min_restart_gap = min_restart_gap;
+    s->state.opts.restart_inner = restart_inner;
+  });
+}
+
+void or_session_tracker_stats(void* h, double* accumulated_change, std::int64_t* steps_since_restart,
+                              double* restart_scale, int* ridge_used) {
+  Session* s = static_cast<Session*>(h);
+  *accumulated_change = s->state.accumulated_change;
+  *steps_since_restart = s->state.steps_since_restart;
+  *restart_scale = s->state.restart_scale;
+  *ridge_used = s->state.ridge_used ? 1 : 0;
+}
 
 int or_session_step(void* h, std::int64_t n_add, const std::int64_t* ai, const std::int64_t* aj, const double* aw,
                     std::int64_t n_rem, const std::int64_t* ri, const std::int64_t* rj, std::int64_t n_new_nodes,
@@ -292,7 +315,8 @@ int or_session_step(void* h, std::int64_t n_add, const std::int64_t* ai, const s
       p = lap_next->advance(d);
     }
     const auto t0 = std::chrono::steady_clock::now();
-    TrackerState next = tracker_step(s->state, p);
+    const Csr* provider = s->op == 0 ? &*a_next : &lap_next->shifted();  // the MatrixProvider
+    TrackerState next = tracker_step(s->state, p, provider);
     const auto t1 = std::chrono::steady_clock::now();
     if (tracker_seconds) *tracker_seconds = std::chrono::duration<double>(t1 - t0).count();
     s->state = std::move(next);

@@ -298,7 +298,7 @@ def shifted_laplacian(a: Csr, kind: int, alpha: float):
 
 
 # ------------------------------------------------------------------ sessions
-KIND = {"iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6}
+KIND = {"trip-basic": 0, "trip": 1, "rm": 2, "iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6, "timers": 7}
 OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
 ORDER = {"abs_desc": 0, "alg_desc": 1}
 
@@ -309,7 +309,8 @@ class Session:
     tracker_step, transactional on error like the reference's value semantics."""
 
     def __init__(self, a: Csr, kind="grest-rsvd", k=8, order="abs_desc", rsvd_l=100, rsvd_p=100, seed=0,
-                 operator="adjacency", values=None, vectors=None):
+                 operator="adjacency", values=None, vectors=None, mu=0.0, trip_replace_span=False, theta=0.01,
+                 min_restart_gap=5, restart_inner="iasc"):
         err = C.create_string_buffer(ERRLEN)
         h = C.c_void_p()
         vals = None if values is None else _d(values)
@@ -320,6 +321,19 @@ class Session:
                                        C.byref(h), err, ERRLEN), err)
         self._h = h.value
         self.last_tracker_seconds = 0.0
+        L = lib()
+        L.or_session_set_options.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_double, I64, C.c_int,
+                                             C.c_char_p, C.c_int]
+        _check(L.or_session_set_options(C.c_void_p(self._h), C.c_double(mu), C.c_int(int(trip_replace_span)),
+                                        C.c_double(theta), I64(min_restart_gap), C.c_int(KIND[restart_inner]),
+                                        err, ERRLEN), err)
+
+    def tracker_stats(self):
+        """(accumulated_change, steps_since_restart, restart_scale, ridge_used) of the TrackerState."""
+        L = lib()
+        acc, gap, scale, ridge = C.c_double(), I64(), C.c_double(), C.c_int()
+        L.or_session_tracker_stats(C.c_void_p(self._h), C.byref(acc), C.byref(gap), C.byref(scale), C.byref(ridge))
+        return acc.value, gap.value, scale.value, bool(ridge.value)
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -1004,21 +1004,228 @@ Mat trailing_adjoint(const TrailingBlock& b, const Mat& y) {
 
 Perturbation to_perturbation(const GraphUpdate& d) { return {d.n_old, d.n_new, d.to_delta()}; }
 
-TrackerState tracker_init(const Csr& a0, TrackerKind kind, const TrackerOptions& opts) {
-  // trackers.cpp:132-145 (projection trackers; timers fields not restated)
-  if (opts.k < 1 || opts.k > a0.rows) throw std::invalid_argument("tracker_init: k must satisfy 1 <= k <= n");
-  TrackerState s;
-  s.kind = kind;
-  s.opts = opts;
+namespace {
+EigResult solve_leading(const Csr& a, const TrackerOptions& opts) {
+  // trackers.cpp:67-75
   LanczosOptions lo;
   lo.k = opts.k;
   lo.order = opts.order;
   lo.seed = opts.seed;
-  const EigResult r = lanczos_topk_csr(a0, lo);
+  return lanczos_topk_csr(a, lo);
+}
+
+double vec_norm(const Vec& v) {  // Eigen Vector::norm (sqrt of the squared sum)
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+}  // namespace
+
+double frobenius_norm(const Csr& a) {
+  double s = 0.0;
+  for (double x : a.val) s += x * x;
+  return std::sqrt(s);
+}
+
+TrackerState tracker_init(const Csr& a0, TrackerKind kind, const TrackerOptions& opts) {
+  // trackers.cpp:132-145
+  if (opts.k < 1 || opts.k > a0.rows) throw std::invalid_argument("tracker_init: k must satisfy 1 <= k <= n");
+  if (kind == TrackerKind::timers && opts.restart_inner == static_cast<int>(TrackerKind::timers))
+    throw std::invalid_argument("tracker_init: timers cannot delegate to itself");
+  TrackerState s;
+  s.kind = kind;
+  s.opts = opts;
+  const EigResult r = solve_leading(a0, opts);
   s.values = r.values;
   s.vectors = r.vectors;
   s.n = a0.rows;
+  s.restart_scale = vec_norm(s.values);
   return s;
+}
+
+// ---------------------------------------------------------------- perturbation trackers
+namespace {
+double gap_clamp(const Vec& values) {  // trackers.cpp:26-31
+  const double lead = values.empty() ? 0.0 : std::abs(values[0]);
+  return 1e-12 * std::max(1.0, lead);
+}
+
+// b_ij = c_ij / (lambda_j - lambda_i), degenerate gaps dropped (trackers.cpp:54-65)
+Mat first_order_coefficients(const Mat& c, const Vec& lam) {
+  const double eps = gap_clamp(lam);
+  const Index k = static_cast<Index>(lam.size());
+  Mat b(k, k);
+  for (Index j = 0; j < k; ++j)
+    for (Index i = 0; i < k; ++i) {
+      if (i == j) continue;
+      const double gap = lam[static_cast<size_t>(j)] - lam[static_cast<size_t>(i)];
+      if (std::abs(gap) < eps) continue;
+      b(i, j) = c(i, j) / gap;
+    }
+  return b;
+}
+
+// renormalize_and_sort (trackers.cpp:43-52)
+void renormalize_and_sort(TrackerState& out, const Vec& values, Mat vectors, SpectralOrder order) {
+  for (Index j = 0; j < vectors.cols; ++j) {
+    const double nrm = norm2(vectors.col(j), vectors.rows);
+    if (nrm > 0.0)
+      for (Index i = 0; i < vectors.rows; ++i) vectors(i, j) /= nrm;
+  }
+  const EigResult r = reorder_eig(values, vectors, order);
+  out.values = r.values;
+  out.vectors = r.vectors;
+}
+
+// xb, dx = Delta xb, c = xb' dx, lambda + diag(c) (trackers.cpp:152-157)
+struct FirstOrder {
+  Mat xb, dx, c;
+  Vec lam_new;
+};
+FirstOrder first_order(const TrackerState& s, const Perturbation& p) {
+  FirstOrder f;
+  f.xb = padded_vectors(s, p.n_new);
+  f.dx = matmat(p.delta, f.xb);
+  f.c = matmul_tn(f.xb, f.dx);
+  f.lam_new = s.values;
+  for (size_t j = 0; j < f.lam_new.size(); ++j) f.lam_new[j] += f.c(static_cast<Index>(j), static_cast<Index>(j));
+  return f;
+}
+}  // namespace
+
+SmallSolve solve_linear_small(const Mat& a, const Vec& b, double ridge) {
+  // solve.hpp:23-45: partial-pivot LU, ridge fallback below a 1e-12 relative pivot
+  if (a.rows != a.cols) throw std::invalid_argument("solve_linear_small: matrix must be square");
+  if (a.rows != static_cast<Index>(b.size())) throw std::invalid_argument("solve_linear_small: rhs size mismatch");
+  for (double x : a.a)
+    if (!std::isfinite(x)) throw std::invalid_argument("solve_linear_small: non-finite entries");
+  for (double x : b)
+    if (!std::isfinite(x)) throw std::invalid_argument("solve_linear_small: non-finite entries");
+  const Index n = a.rows;
+  if (n == 0) return {};
+  double amax = 0.0;
+  for (double x : a.a) amax = std::max(amax, std::abs(x));
+  auto lu_solve = [&](const Mat& m, double* pivot_min) {
+    Mat lu = m;
+    std::vector<Index> perm(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) perm[static_cast<size_t>(i)] = i;
+    double pmin = std::numeric_limits<double>::infinity();
+    for (Index c = 0; c < n; ++c) {
+      Index piv = c;
+      double best = std::abs(lu(c, c));
+      for (Index r = c + 1; r < n; ++r)
+        if (std::abs(lu(r, c)) > best) {
+          best = std::abs(lu(r, c));
+          piv = r;
+        }
+      if (piv != c) {
+        for (Index q = 0; q < n; ++q) std::swap(lu(c, q), lu(piv, q));
+        std::swap(perm[static_cast<size_t>(c)], perm[static_cast<size_t>(piv)]);
+      }
+      const double d = lu(c, c);
+      pmin = std::min(pmin, std::abs(d));
+      if (d != 0.0)
+        for (Index r = c + 1; r < n; ++r) {
+          const double l = lu(r, c) / d;
+          lu(r, c) = l;
+          for (Index q = c + 1; q < n; ++q) lu(r, q) -= l * lu(c, q);
+        }
+    }
+    if (pivot_min) *pivot_min = pmin;
+    Vec x(static_cast<size_t>(n));
+    for (Index i = 0; i < n; ++i) x[static_cast<size_t>(i)] = b[static_cast<size_t>(perm[static_cast<size_t>(i)])];
+    for (Index i = 0; i < n; ++i)
+      for (Index q = 0; q < i; ++q) x[static_cast<size_t>(i)] -= lu(i, q) * x[static_cast<size_t>(q)];
+    for (Index i = n - 1; i >= 0; --i) {
+      for (Index q = i + 1; q < n; ++q) x[static_cast<size_t>(i)] -= lu(i, q) * x[static_cast<size_t>(q)];
+      x[static_cast<size_t>(i)] /= lu(i, i);
+    }
+    return x;
+  };
+  if (amax > 0.0) {
+    double pmin = 0.0;
+    Vec x = lu_solve(a, &pmin);
+    if (pmin >= 1e-12 * amax) return {x, false};
+  }
+  const double eps = ridge * std::max(1.0, amax);
+  Mat reg = a;
+  for (Index i = 0; i < n; ++i) reg(i, i) += eps;
+  return {lu_solve(reg, nullptr), true};
+}
+
+TrackerState trip_basic_step(const TrackerState& s, const Perturbation& p) {
+  // trackers.cpp:147-164
+  check_step("trip_basic_step", s, p);
+  TrackerState out = s;
+  if (p.empty()) return out;
+  const FirstOrder f = first_order(s, p);
+  const Mat b = first_order_coefficients(f.c, s.values);
+  Mat xt = f.xb;
+  const Mat xbb = matmul(f.xb, b);
+  for (size_t e = 0; e < xt.a.size(); ++e) xt.a[e] += xbb.a[e];
+  renormalize_and_sort(out, f.lam_new, std::move(xt), s.opts.order);
+  out.n = p.n_old + p.n_new;
+  return out;
+}
+
+TrackerState trip_step(const TrackerState& s, const Perturbation& p) {
+  // trackers.cpp:166-197
+  check_step("trip_step", s, p);
+  TrackerState out = s;
+  if (p.empty()) return out;
+  const FirstOrder f = first_order(s, p);
+  const Index k = static_cast<Index>(s.values.size());
+  Mat xt(f.xb.rows, k);
+  for (Index j = 0; j < k; ++j) {
+    Vec rhs(static_cast<size_t>(k));
+    double rmax = 0.0;
+    for (Index i = 0; i < k; ++i) {
+      rhs[static_cast<size_t>(i)] = f.c(i, j);
+      rmax = std::max(rmax, std::abs(f.c(i, j)));
+    }
+    Vec bj(static_cast<size_t>(k), 0.0);
+    if (rmax > 0.0) {
+      Mat system(k, k);
+      for (Index q = 0; q < k; ++q)
+        for (Index i = 0; i < k; ++i) system(i, q) = -f.c(i, q);
+      for (Index i = 0; i < k; ++i)
+        system(i, i) += f.lam_new[static_cast<size_t>(j)] - s.values[static_cast<size_t>(i)];
+      const SmallSolve sol = solve_linear_small(system, rhs);
+      bj = sol.x;
+      out.ridge_used = out.ridge_used || sol.ridge_used;
+    }
+    for (Index r = 0; r < f.xb.rows; ++r) {
+      double acc = 0.0;
+      for (Index i = 0; i < k; ++i) acc += f.xb(r, i) * bj[static_cast<size_t>(i)];
+      xt(r, j) = s.opts.trip_replace_span ? acc : f.xb(r, j) + acc;
+    }
+  }
+  renormalize_and_sort(out, f.lam_new, std::move(xt), s.opts.order);
+  out.n = p.n_old + p.n_new;
+  return out;
+}
+
+TrackerState residual_modes_step(const TrackerState& s, const Perturbation& p, double mu) {
+  // trackers.cpp:199-224
+  check_step("residual_modes_step", s, p);
+  TrackerState out = s;
+  if (p.empty()) return out;
+  const double eps = gap_clamp(s.values);
+  for (double l : s.values)
+    if (std::abs(l - mu) < eps) throw std::invalid_argument("residual_modes_step: mu collides with tracked eigenvalue");
+  const FirstOrder f = first_order(s, p);
+  const Mat b = first_order_coefficients(f.c, s.values);
+  const Mat xc = matmul(f.xb, f.c);
+  const Mat xbb = matmul(f.xb, b);
+  Mat xt = f.xb;
+  for (size_t e = 0; e < xt.a.size(); ++e) xt.a[e] += xbb.a[e];
+  for (Index j = 0; j < xt.cols; ++j) {
+    const double den = s.values[static_cast<size_t>(j)] - mu;
+    for (Index r = 0; r < xt.rows; ++r) xt(r, j) += (f.dx(r, j) - xc(r, j)) / den;
+  }
+  renormalize_and_sort(out, f.lam_new, std::move(xt), s.opts.order);
+  out.n = p.n_old + p.n_new;
+  return out;
 }
 
 Mat build_projection_basis(const TrackerState& s, const Perturbation& p, BasisKind kind, std::uint64_t seed) {
@@ -1103,10 +1310,48 @@ TrackerState rayleigh_ritz_step(const TrackerState& s, const Perturbation& p, co
   return out;
 }
 
-TrackerState tracker_step(const TrackerState& s, const Perturbation& p) {
-  // trackers.cpp:341-382 (projection kinds)
+TrackerState tracker_step(const TrackerState& s, const Perturbation& p, const Csr* full_matrix) {
+  // trackers.cpp:341-382
   TrackerState out;
   switch (s.kind) {
+    case TrackerKind::trip_basic:
+      out = trip_basic_step(s, p);
+      break;
+    case TrackerKind::trip:
+      out = trip_step(s, p);
+      break;
+    case TrackerKind::residual_modes:
+      out = residual_modes_step(s, p, s.opts.mu);
+      break;
+    case TrackerKind::timers: {
+      // timers_step (trackers.cpp:310-339) around the inner kind
+      check_step("timers_step", s, p);
+      if (s.opts.theta < 0.0) throw std::invalid_argument("timers_step: theta must be >= 0");
+      TrackerState acc = s;
+      acc.kind = static_cast<TrackerKind>(s.opts.restart_inner);
+      const double denom = s.restart_scale > 0.0 ? s.restart_scale : 1.0;
+      acc.accumulated_change += frobenius_norm(p.delta) / denom;
+      acc.steps_since_restart += 1;
+      if (acc.accumulated_change >= s.opts.theta && acc.steps_since_restart >= s.opts.min_restart_gap) {
+        if (!full_matrix) throw std::invalid_argument("timers_step: restart requires a full-matrix provider");
+        if (full_matrix->rows != p.n_old + p.n_new)
+          throw std::invalid_argument("timers_step: provider matrix has the wrong dimension");
+        const EigResult r = solve_leading(*full_matrix, s.opts);
+        out = acc;
+        out.values = r.values;
+        out.vectors = r.vectors;
+        out.n = full_matrix->rows;
+        out.restart_scale = vec_norm(out.values);
+        out.accumulated_change = 0.0;
+        out.steps_since_restart = 0;
+      } else {
+        out = tracker_step(acc, p, nullptr);
+        out.accumulated_change = acc.accumulated_change;
+        out.steps_since_restart = acc.steps_since_restart;
+      }
+      out.kind = TrackerKind::timers;
+      break;
+    }
     case TrackerKind::iasc:
     case TrackerKind::grest2:
     case TrackerKind::grest3:

@@ -157,18 +157,27 @@ enum class BasisKind { iasc, grest2, grest3, grest_rsvd };
 struct TrackerOptions {  // trackers.hpp:52-63
   Index k = 8;
   SpectralOrder order = SpectralOrder::abs_desc;
+  double mu = 0.0;                 // residual-modes denominator scalar
+  bool trip_replace_span = false;  // x = X b instead of x = x + X b
   Index rsvd_l = 100;
   Index rsvd_p = 100;
+  double theta = 0.01;             // timers restart threshold
+  Index min_restart_gap = 5;       // timers minimum steps between restarts
+  int restart_inner = 3;           // TrackerKind timers delegates to (iasc)
   std::uint64_t seed = 0;
 };
 
-struct TrackerState {  // trackers.hpp:65-75 (projection-tracker fields)
+struct TrackerState {  // trackers.hpp:65-75
   TrackerKind kind = TrackerKind::grest3;
   TrackerOptions opts;
   Vec values;
   Mat vectors;
   Index n = 0;
+  double accumulated_change = 0.0;
+  Index steps_since_restart = 0;
+  double restart_scale = 0.0;
   std::uint64_t steps_taken = 0;
+  bool ridge_used = false;
 };
 
 struct Perturbation {  // trackers.hpp:78-84
@@ -193,7 +202,19 @@ TrackerState tracker_init(const Csr& a0, TrackerKind kind, const TrackerOptions&
 Mat build_projection_basis(const TrackerState& s, const Perturbation& p, BasisKind kind,
                            std::uint64_t seed);  // trackers.cpp:226-280
 TrackerState rayleigh_ritz_step(const TrackerState& s, const Perturbation& p, const Mat& z);  // :282-308
-TrackerState tracker_step(const TrackerState& s, const Perturbation& p);  // trackers.cpp:341-382
+// The perturbation trackers and TIMERS (trackers.cpp:147-224, 310-339)
+struct SmallSolve {  // solve.hpp:17-45
+  Vec x;
+  bool ridge_used = false;
+};
+SmallSolve solve_linear_small(const Mat& a, const Vec& b, double ridge = 1e-10);
+TrackerState trip_basic_step(const TrackerState& s, const Perturbation& p);
+TrackerState trip_step(const TrackerState& s, const Perturbation& p);
+TrackerState residual_modes_step(const TrackerState& s, const Perturbation& p, double mu);
+// full_matrix: the current operator (the reference's MatrixProvider), may be null
+TrackerState tracker_step(const TrackerState& s, const Perturbation& p,
+                          const Csr* full_matrix = nullptr);  // trackers.cpp:341-382
+double frobenius_norm(const Csr& a);  // sparse.hpp:43
 
 // laplacian_track.cpp:35-64
 class ShiftedLaplacianSession {
