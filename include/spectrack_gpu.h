@@ -31,8 +31,27 @@ typedef enum {
   ST_OTHER = 4
 } st_status;
 
-/* TrackerKind (trackers.hpp:36-45); the G-REST path implements the projection kinds. */
-typedef enum { ST_IASC = 3, ST_GREST2 = 4, ST_GREST3 = 5, ST_GREST_RSVD = 6 } st_tracker_kind;
+/* TrackerKind (trackers.hpp:36-45). */
+typedef enum {
+  ST_TRIP_BASIC = 0,
+  ST_TRIP = 1,
+  ST_RESIDUAL_MODES = 2,
+  ST_IASC = 3,
+  ST_GREST2 = 4,
+  ST_GREST3 = 5,
+  ST_GREST_RSVD = 6,
+  ST_TIMERS = 7
+} st_tracker_kind;
+
+/* TrackerOptions fields of the perturbation trackers and TIMERS
+ * (trackers.hpp:52-63); reference defaults {0, 0, 0.01, 5, ST_IASC}. */
+typedef struct {
+  double mu;                /* residual-modes denominator scalar */
+  int32_t trip_replace_span; /* TRIP: x = X b instead of x = x + X b */
+  double theta;             /* TIMERS restart threshold */
+  int64_t min_restart_gap;  /* TIMERS minimum steps between restarts */
+  int32_t restart_inner;    /* the kind TIMERS delegates to */
+} st_tracker_options;
 /* BasisKind (trackers.hpp:104) */
 typedef enum { ST_BASIS_IASC = 0, ST_BASIS_GREST2 = 1, ST_BASIS_GREST3 = 2, ST_BASIS_GREST_RSVD = 3 } st_basis_kind;
 /* SpectralOrder (types.hpp:22) */
@@ -110,6 +129,13 @@ typedef struct {
  * 1 <= k <= n", "max_basis below k", "no convergence after N restarts (...)". */
 st_status st_tracker_init(const st_config* cfg, const st_lanczos_options* opts, int64_t n, const int32_t* rowptr,
                           const int32_t* colidx, const double* values_csr, st_session** out);
+/* Sets the TrackerOptions fields above (before the first step); the session
+ * starts with the reference defaults. */
+st_status st_set_tracker_options(st_session* s, const st_tracker_options* opts);
+/* TrackerState fields of TIMERS and TRIP (trackers.hpp:65-75). */
+st_status st_tracker_state(const st_session* s, double* accumulated_change, int64_t* steps_since_restart,
+                           double* restart_scale, int32_t* ridge_used);
+
 /* Restarts and operator products of the session's tracker_init (0 when the
  * session was created from given eigenpairs). */
 st_status st_init_stats(const st_session* s, int64_t* restarts, int64_t* products);
@@ -188,6 +214,13 @@ st_status st_get_embedding(const st_session* s, double* values, double* vectors,
  * device with one full-operator SpMM (Op X) so a caller can monitor tracking
  * quality at any size without copying X to the host. Unsharded sessions. */
 st_status st_residual_norms(st_session* s, double* norms);
+/* Tracking quality against reference vectors Y (n x k, column-major, leading
+ * dimension ld; e.g. the Lanczos reference of experiment.cpp:177-184), on the
+ * device: psi[i] = principal_angle(x_i, y_i) (metrics.cpp:17-27, the
+ * 2 atan2(||u - v||, ||u + v||) form) and *largest_angle = the largest
+ * principal angle between span(X) and span(Y) (metrics.cpp:243-259), radians.
+ * Either output may be NULL. Unsharded sessions. */
+st_status st_angles(st_session* s, const double* ref_vectors, int64_t ld, double* psi, double* largest_angle);
 /* Ritz values only (k doubles), the per-step result read by the e2e benchmark. */
 st_status st_get_values(const st_session* s, double* values);
 

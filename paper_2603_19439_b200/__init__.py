@@ -22,7 +22,7 @@ I32P = C.POINTER(C.c_int32)
 I64P = C.POINTER(C.c_int64)
 
 ST_OK, ST_INVALID_ARGUMENT, ST_RUNTIME_ERROR, ST_CUDA_ERROR, ST_OTHER = range(5)
-KIND = {"iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6}
+KIND = {"trip-basic": 0, "trip": 1, "rm": 2, "iasc": 3, "grest2": 4, "grest3": 5, "grest-rsvd": 6, "timers": 7}
 BASIS = {"iasc": 0, "grest2": 1, "grest3": 2, "grest-rsvd": 3}
 OPERATOR = {"adjacency": 0, "laplacian": 1, "normalized-laplacian": 2}
 ORDER = {"abs_desc": 0, "alg_desc": 1}
@@ -50,6 +50,11 @@ class StCsrBlock(C.Structure):
 class StGraphUpdate(C.Structure):
     _fields_ = [("n_old", C.c_int64), ("n_new", C.c_int64), ("k_block", StCsrBlock), ("g_block", StCsrBlock),
                 ("c_block", StCsrBlock)]
+
+
+class StTrackerOptions(C.Structure):
+    _fields_ = [("mu", C.c_double), ("trip_replace_span", C.c_int32), ("theta", C.c_double),
+                ("min_restart_gap", C.c_int64), ("restart_inner", C.c_int32)]
 
 
 class StUpdate(C.Structure):
@@ -84,12 +89,15 @@ def lib():
         L.st_tracker_init.argtypes = [C.POINTER(StConfig), C.POINTER(StLanczosOptions), I64, I32P, I32P, DP,
                                       C.POINTER(C.c_void_p)]
         L.st_init_stats.argtypes = [C.c_void_p, I64P, I64P]
+        L.st_set_tracker_options.argtypes = [C.c_void_p, C.POINTER(StTrackerOptions)]
+        L.st_tracker_state.argtypes = [C.c_void_p, DP, I64P, DP, C.POINTER(C.c_int32)]
         L.st_reserve.argtypes = [C.c_void_p, I64, I64]
         L.st_step_blocks.argtypes = [C.c_void_p, C.POINTER(StGraphUpdate)]
         L.st_step_perturbation.argtypes = [C.c_void_p, I64, I64, C.POINTER(StCsrBlock)]
         L.st_info.argtypes = [C.c_void_p, I64P, I64P, C.POINTER(C.c_uint64), I64P, I64P, I64P, DP]
         L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
         L.st_residual_norms.argtypes = [C.c_void_p, DP]
+        L.st_angles.argtypes = [C.c_void_p, DP, I64, DP, DP]
         L.st_get_values.argtypes = [C.c_void_p, DP]
         L.st_get_csr.argtypes = [C.c_void_p, C.c_int32, I32P, I32P, DP]
         L.st_probe_basis.argtypes = [C.c_void_p, C.POINTER(StUpdate), C.c_int32, C.c_uint64, DP, I64, I64, I64P]
@@ -133,7 +141,8 @@ def lib():
         L.st_shard_layout.restype = C.c_int64
         for f in ("st_create", "st_step", "st_info", "st_get_embedding", "st_get_values", "st_get_csr",
                   "st_probe_basis", "st_probe_rr", "st_create_sharded", "st_shard_rows", "st_residual_norms",
-                  "st_reserve", "st_tracker_init", "st_init_stats", "st_step_blocks", "st_step_perturbation"):
+                  "st_reserve", "st_tracker_init", "st_init_stats", "st_step_blocks", "st_step_perturbation",
+                  "st_set_tracker_options", "st_tracker_state", "st_angles"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -322,6 +331,20 @@ class TrackerSession:
         self.k = k
         return self
 
+    def set_tracker_options(self, mu=0.0, trip_replace_span=False, theta=0.01, min_restart_gap=5,
+                            restart_inner="iasc") -> None:
+        """TrackerOptions of the perturbation trackers and TIMERS (trackers.hpp:52-63)."""
+        o = StTrackerOptions(mu, int(trip_replace_span), theta, min_restart_gap, KIND[restart_inner])
+        self._check(lib().st_set_tracker_options(self._h, C.byref(o)))
+
+    def tracker_state(self):
+        """(accumulated_change, steps_since_restart, restart_scale, ridge_used)."""
+        acc, scale = C.c_double(), C.c_double()
+        gap = I64()
+        ridge = C.c_int32()
+        self._check(lib().st_tracker_state(self._h, C.byref(acc), C.byref(gap), C.byref(scale), C.byref(ridge)))
+        return acc.value, gap.value, scale.value, bool(ridge.value)
+
     def init_stats(self):
         """(restarts, operator products) of the device tracker_init."""
         r, p = I64(), I64()
@@ -408,6 +431,15 @@ class TrackerSession:
         out = np.zeros(self.k)
         self._check(lib().st_residual_norms(self._h, _p(out)))
         return out
+
+    def angles(self, ref_vectors):
+        """(psi per vector, largest principal angle) against reference vectors
+        (n x k), computed on the device (st_angles; metrics.cpp:17-27, 243-259)."""
+        y = np.asfortranarray(np.asarray(ref_vectors, np.float64))
+        psi = np.zeros(self.k)
+        big = C.c_double()
+        self._check(lib().st_angles(self._h, y.ctypes.data_as(DP), y.shape[0], _p(psi), C.byref(big)))
+        return psi, big.value
 
     def csr(self, which: int = 0):
         inf = self.info()

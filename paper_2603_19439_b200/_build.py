@@ -7,7 +7,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libspectrack_b200.so")
 SOURCES = ["csrc/session.cu"]
 HEADERS = ["csrc/common.cuh", "csrc/dmma.cuh", "csrc/spmm.cuh", "csrc/smalllin.cuh", "csrc/rng.cuh",
-           "csrc/ingest.cuh", "csrc/stepk.cuh", "csrc/eigsolve.cuh", "csrc/shard.cuh", "csrc/lanczos.cuh", "csrc/nccl_comm.cuh", "../include/spectrack_gpu.h"]
+           "csrc/ingest.cuh", "csrc/stepk.cuh", "csrc/eigsolve.cuh", "csrc/shard.cuh", "csrc/lanczos.cuh", "csrc/nccl_comm.cuh", "csrc/trackers.cuh", "csrc/metrics.cuh", "../include/spectrack_gpu.h"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

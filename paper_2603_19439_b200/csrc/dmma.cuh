@@ -331,11 +331,39 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
     }
 }
 
-// Deterministic split reduction, one warp per output element: lane l sums
-// splits l, l+32, ... in order, then a fixed butterfly combines the lanes. For
-// sym the (min, max) element is read so the result is exactly symmetric.
+// Deterministic split reduction, one thread per output element (consecutive
+// threads on consecutive columns, so every split's partial row is read
+// coalesced), splits summed in order with 8 loads in flight. For sym only the
+// computed upper triangle (i <= j) is read and written to both (i, j) and
+// (j, i): the result is exactly symmetric.
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* partial, int splits, int m1, int m2, int m1p,
                                                           int m2p, int sym, double* out, int ldo, double alpha) {
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<i64>(m1) * m2) return;
+  const int i = static_cast<int>(idx / m2), j = static_cast<int>(idx % m2);
+  if (sym && j < i) return;
+  const i64 stride = static_cast<i64>(m1p) * m2p;
+  const double* src = partial + static_cast<i64>(i) * m2p + j;
+  double s = 0.0;
+  int sp = 0;
+  for (; sp + 8 <= splits; sp += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = __ldcs(src + (sp + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += t[u];
+  }
+  for (; sp < splits; ++sp) s += __ldcs(src + sp * stride);
+  out[static_cast<i64>(i) * ldo + j] = alpha * s;
+  if (sym && i != j) out[static_cast<i64>(j) * ldo + i] = alpha * s;
+}
+
+// (previous layout, one warp per output element, kept for A/B) lane l sums
+// splits l, l+32, ... in order, then a fixed butterfly combines the lanes. For
+// sym the (min, max) element is read so the result is exactly symmetric.
+__global__ void __launch_bounds__(256) gram_reduce_warp_kernel(const double* partial, int splits, int m1, int m2,
+                                                               int m1p, int m2p, int sym, double* out, int ldo,
+                                                               double alpha) {
   const i64 idx = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (idx >= static_cast<i64>(m1) * m2) return;

@@ -95,16 +95,18 @@ __global__ void __launch_bounds__(256) spv_short_kernel(const int* rp, const int
                                                         double* out2, int ld2, int* flags) {
   const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;  // 8-lane group
   const int sub = threadIdx.x & 7;
-  if (g >= cnt) return;
-  const int r = list[g];
-  const int b = rp[r], e = rp[r + 1];
+  // every lane of the warp reaches the shuffles (full mask): lanes of one
+  // group leave the entry loop at different trip counts, so no partial mask
+  // (e.g. __activemask) is guaranteed to hold the whole group
+  const bool valid = g < cnt;
+  const int r = valid ? list[g] : 0;
+  const int b = valid ? rp[r] : 0, e = valid ? rp[r + 1] : 0;
   double acc = 0.0;
   for (int q = b + sub; q < e; q += 8) acc = fma(val[q], x[col[q]], acc);
-  const unsigned mask = __activemask();
-  acc += __shfl_xor_sync(mask, acc, 4, 8);
-  acc += __shfl_xor_sync(mask, acc, 2, 8);
-  acc += __shfl_xor_sync(mask, acc, 1, 8);
-  if (sub == 0) spv_store(acc, r, out, out2, ld2, flags);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4, 8);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2, 8);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1, 8);
+  if (valid && sub == 0) spv_store(acc, r, out, out2, ld2, flags);
 }
 
 __global__ void __launch_bounds__(256) spv_med_kernel(const int* rp, const int* col, const double* val,
@@ -298,6 +300,12 @@ __global__ void lz_residual_kernel(double* R, int ldr, const double* X, int ldx,
   const i64 r = t / k;
   const int c = static_cast<int>(t % k);
   R[r * ldr + c] -= X[r * ldx + c] * theta[c];
+}
+
+// all values of a cuSOLVER solve in spectral order
+__global__ void lz_sorted_vals_kernel(const double* w, const int* perm, int j, double* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < j) out[c] = w[perm[c]];
 }
 
 // Column of a row-major block into a contiguous vector (restart direction).

@@ -34,12 +34,14 @@
 #include "eigsolve.cuh"
 #include "ingest.cuh"
 #include "lanczos.cuh"
+#include "metrics.cuh"
 #include "nccl_comm.cuh"
 #include "rng.cuh"
 #include "shard.cuh"
 #include "smalllin.cuh"
 #include "spmm.cuh"
 #include "stepk.cuh"
+#include "trackers.cuh"
 
 namespace stg {
 
@@ -362,6 +364,17 @@ class Session {
     i64 max_restarts = 500;
   };
   i64 lz_restarts = 0, lz_products = 0;  // tracker_init statistics
+  // TrackerOptions of the perturbation trackers and TIMERS (trackers.hpp:52-63)
+  // and the TrackerState fields they carry (trackers.hpp:65-75)
+  st_tracker_options topt_{0.0, 0, 0.01, 5, ST_IASC};
+  double acc_change_ = 0.0, restart_scale_ = 0.0;
+  i64 steps_since_restart_ = 0;
+  bool ridge_used_ = false;
+  static double l2norm(const std::vector<double>& v) {
+    double s = 0.0;
+    for (double x : v) s += x * x;
+    return std::sqrt(s);
+  }
   bool prewarmed_ = false;
 
   // ev == nullptr: tracker_init (trackers.cpp:132-145) on the device, i.e. the
@@ -427,8 +440,11 @@ class Session {
       n = shard->n_global;
     }
     if (k < 1 || k > n) throw InvalidArgument("tracker_init: k must satisfy 1 <= k <= n");
-    if (cfg.kind < ST_IASC || cfg.kind > ST_GREST_RSVD)
-      throw InvalidArgument("st_create: tracker kind outside the G-REST path");
+    if (cfg.kind < ST_TRIP_BASIC || cfg.kind > ST_TIMERS) throw InvalidArgument("tracker_step: unknown tracker kind");
+    if (shard && (cfg.kind < ST_IASC || cfg.kind > ST_GREST_RSVD))
+      throw InvalidArgument("st_create_sharded: sharded sessions run the projection trackers");
+    if (cfg.kind <= ST_RESIDUAL_MODES && k > kTrkMaxK)
+      throw InvalidArgument("st_create: the perturbation trackers support k <= 128");
     if (cfg.op == ST_NORMALIZED_LAPLACIAN || cfg.op == ST_LAPLACIAN) {
       if (cfg.order != ST_ALG_DESC) {
         // the reference adapter forces alg_desc for shifted operators (laplacian_track.cpp:88)
@@ -451,10 +467,12 @@ class Session {
       lanczos(is_laplacian() ? T() : A(), n0, o);
       STG_CUDA(cudaMemcpyAsync(d_values_, values.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st_));
       STG_CUDA(cudaStreamSynchronize(st_));
+      restart_scale_ = l2norm(values);
       return;
     }
     // eigenpairs: column-major host -> row-major device
     values.assign(ev, ev + k);
+    restart_scale_ = l2norm(values);
     std::vector<double> xr(static_cast<size_t>(n0 * k));
     for (i64 c = 0; c < k; ++c)
       for (i64 i = 0; i < n0; ++i) xr[static_cast<size_t>(i * k + c)] = evec[c * ld + i];
@@ -617,20 +635,63 @@ class Session {
       int ldo;
       prepare_omega(basis_seed, n_new, q, &om, &ldo);
     }
+    // the kind that steps: TIMERS delegates to restart_inner (trackers.cpp:369-377)
+    const int kind = cfg.kind == ST_TIMERS ? topt_.restart_inner : cfg.kind;
+    if (cfg.kind == ST_TIMERS && topt_.theta < 0.0) throw InvalidArgument("timers_step: theta must be >= 0");
+    if (kind == ST_RESIDUAL_MODES) {  // trackers.cpp:204-207
+      const double eps = 1e-12 * std::max(1.0, values.empty() ? 0.0 : std::fabs(values[0]));
+      for (double l : values)
+        if (std::fabs(l - topt_.mu) < eps)
+          throw InvalidArgument("residual_modes_step: mu collides with tracked eigenvalue");
+    }
     Pert pt = front();
     timing_mark(0);
+    // TIMERS proxy (trackers.cpp:317-320): ||Delta||_F / restart_scale accumulated
+    double acc_next = acc_change_;
+    i64 ssr_next = steps_since_restart_;
+    if (cfg.kind == ST_TIMERS) {
+      double* sq = arena_.get<double>("timers_sq", 1);
+      STG_CUDA(cudaMemsetAsync(sq, 0, sizeof(double), st_));
+      if (pt.nnz > 0) launch(sumsq_kernel, dim3(1), dim3(256), 0, st_, pt.gval ? pt.gval : pt.val, pt.nnz, sq);
+      double h = 0.0;
+      STG_CUDA(cudaMemcpyAsync(&h, sq, sizeof(double), cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      acc_next += std::sqrt(h) / (restart_scale_ > 0.0 ? restart_scale_ : 1.0);
+      ssr_next += 1;
+      if (acc_next >= topt_.theta && ssr_next >= topt_.min_restart_gap) {
+        // restart: the leading pairs of the updated operator (trackers.cpp:322-333)
+        commit_graph(pt);
+        n = pt.n_total;
+        lanczos(is_laplacian() ? T() : A(), n, LzOpts{});
+        STG_CUDA(cudaMemcpyAsync(d_values_, values.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st_));
+        STG_CUDA(cudaStreamSynchronize(st_));
+        restart_scale_ = l2norm(values);
+        acc_change_ = 0.0;
+        steps_since_restart_ = 0;
+        steps_taken += 1;
+        timing_end(0);
+        kflush();
+        return;
+      }
+    }
     if (pt.empty()) {
       commit_graph(pt);
       steps_taken += 1;
+      acc_change_ = acc_next;
+      steps_since_restart_ = ssr_next;
       timing_end(0);
       kflush();
       return;
     }
     std::vector<double> newvals;
     try {
-      Basis b = build_basis(pt, cfg.kind - ST_IASC, basis_seed);
-      timing_mark(1);
-      rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+      if (kind >= ST_IASC && kind <= ST_GREST_RSVD) {
+        Basis b = build_basis(pt, kind - ST_IASC, basis_seed);
+        timing_mark(1);
+        rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+      } else {
+        perturbation_step(pt, kind, newvals);
+      }
     } catch (...) {
       restore_x();
       cudaStreamSynchronize(st_);
@@ -641,6 +702,8 @@ class Session {
     values = newvals;
     n = pt.n_total;
     steps_taken += 1;
+    acc_change_ = acc_next;
+    steps_since_restart_ = ssr_next;
     if (!prewarmed_) {
       // after the first full step the working set is known: keep 1.6x of it
       // free in the pool, so the buffers that outgrow their 1.25x headroom as
@@ -1111,7 +1174,7 @@ class Session {
       a.partial = arena_.get<double>("gram_partial", static_cast<i64>(G) * 1024);
       launch(dm::gram_stream_kernel, dim3(static_cast<unsigned>(G)), dim3(dm::NT), dm::gram_stream_smem(same), st_,
              a, ma, mb, same ? 1 : 0, ntl);
-      launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2, 8)), dim3(256), 0, st_,
+      launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
              static_cast<const double*>(a.partial), G, m1, m2, 32, 32, a.sym, out, ldo, alpha);
       kend();
       return;
@@ -1134,7 +1197,7 @@ class Session {
       launch(dm::gram_tn_kernel<4, 1>, grid, dim3(dm::NT), dm::gram_smem(4, 1), st_, a);
     else
       launch(dm::gram_tn_kernel<2, 2>, grid, dim3(dm::NT), dm::gram_smem(2, 2), st_, a);
-    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2, 8)), dim3(256), 0, st_,
+    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
            static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
            static_cast<int>(m2p), a.sym, out, ldo, alpha);
     kend();
@@ -1284,9 +1347,9 @@ class Session {
     e->rows = a.rows;
     e->nnz = nnz;
     e->epoch = plan_epoch_;
-    e->vmax = 2 * cdiv(nnz, kSegNnz) + 1;  // segments of the rows longer than kSegNnz
-    e->split_max = std::min<i64>(a.rows, nnz / (kSegNnz + 1));
-    e->smax = 2 * cdiv(nnz, kSegNnz) + 1;
+    e->vmax = nnz / (kSegNnz + 1) + 1;  // segments of the rows longer than kSegNnz (each >= 33 entries)
+    e->split_max = std::min<i64>(a.rows, nnz / (kLongSeg + 1));  // rows of more than one segment
+    e->smax = 2 * cdiv(nnz, kLongSeg) + 1;
     int* cnt = arena_.get<int>(e->tag + "cnt", a.rows + 1);
     int* cnt2 = arena_.get<int>(e->tag + "cnt2", a.rows + 1);
     int* vstart = arena_.get<int>(e->tag + "vstart", a.rows + 1);
@@ -1331,8 +1394,9 @@ class Session {
       b.X = a.X + c0;
       b.Y = a.Y + c0;
       b.m = std::min(a.m - c0, 256);
-      spmm_launch(b, pl, pe.vmax, pe.split_max, st_);
-      launches += pe.split_max > 0 ? 3 : 1;
+      const bool long_rows = nnz > kSegNnz;
+      spmm_launch(b, pl, pe.vmax, pe.split_max, long_rows, st_);
+      launches += 1 + (long_rows ? 1 : 0) + (pe.split_max > 0 ? 1 : 0);
     }
     kend();
     if (tscratch) STG_CUDA(cudaFreeAsync(tscratch, st_));
@@ -2561,6 +2625,10 @@ class Session {
     int rank = 0;
     while (rank < qm && sv[rank] > cutoff && sv[rank] > 0.0) ++rank;
     const int keep = static_cast<int>(std::min<i64>(cfg.rsvd_l, rank));
+    if (getenv("STG_SKETCH_LOG") && keep > 0 && keep < qm) {  // development: the singular gap at the cut
+      fprintf(stderr, "sketch: qm %d rank %d keep %d  sv[keep-1] %.17g sv[keep] %.17g rel gap %.3e\n", qm, rank, keep,
+              sv[keep - 1], sv[keep], (sv[keep - 1] - sv[keep]) / sv[0]);
+    }
     if (keep == 0) return 0;
     // R = M U_keep; when the caller projected M against its basis meanwhile
     // (pre_pm_ = M - B C1), R's first projection is PM U_keep with
@@ -2722,7 +2790,7 @@ class Session {
 
   void rayleigh_ritz(const Pert& pt, const Basis& b, std::vector<double>& newvals, bool write_state, double* wout,
                      i64 wrows, Blk xbar_override = Blk{}) {
-    const i64 p = pt.p, N = p + 2 * k, G = pt.G;
+    const i64 p = pt.p, G = pt.G;
     const int D = b.D, kk = static_cast<int>(k);
     const Blk xb = xbar_override.p ? xbar_override : b.z;
     const bool pre = rr_pre_.valid && !xbar_override.p && rr_pre_.a <= D;
@@ -2786,6 +2854,83 @@ class Session {
              ldk, nv);
     }
     timing_mark(3);
+    finish_rotation(pt, b.z, D, F, ldk, nv, newvals, write_state, wout, wrows);
+  }
+
+  // TRIP-Basic / TRIP / residual modes (trackers.cpp:147-224) on the stacked
+  // coordinates: Z = [X-bar] or [X-bar | Delta X-bar], C = X-bar'(Delta X-bar),
+  // the coefficient block on the device (trackers.cuh), renormalize_and_sort
+  // through the basis Gram, then the shared rotation.
+  void perturbation_step(const Pert& pt, int kind, std::vector<double>& newvals) {
+    const i64 p = pt.p, N = p + 2 * k, G = pt.G;
+    const int kk = static_cast<int>(k);
+    const bool rm = kind == ST_RESIDUAL_MODES;
+    const int D = rm ? 2 * kk : kk;
+    const int ldz = ld_for(2 * kk);
+    double* Z = arena_.get<double>("trk_Z", N * ldz);
+    STG_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * N * ldz, st_));
+    build_xbar(pt, Blk{Z, ldz});
+    // Delta X-bar on the rows of P (coordinate rows stay 0): columns [k, 2k) of Z
+    SpmmArgs sa{};
+    sa.rows = p;
+    sa.rowptr = pt.lrp;
+    sa.col = pt.lcol;
+    sa.val = pt.val;
+    sa.X = halo(pt, Z, ldz, kk, &sa.ldx);
+    sa.m = kk;
+    sa.Y = Z + kk;
+    sa.ldy = ldz;
+    do_spmm(sa, pt.nnz, p);
+    const int ldc = ld_for(kk);
+    double* C = arena_.get<double>("trk_C", static_cast<i64>(kk) * ldc);
+    pgram(Z, ldz, Z + kk, ldz, G, kk, kk, false, C, ldc);
+    const int ldf = ld_for(kk);
+    double* F = arena_.get<double>("trk_F", static_cast<i64>(D) * ldf);
+    double* F2 = arena_.get<double>("trk_F2", static_cast<i64>(D) * ldf);
+    double* lam_new = arena_.get<double>("trk_lam", kk);
+    double* nv = arena_.get<double>("trk_vals", kk);
+    int* ridge = reinterpret_cast<int*>(d_scal_ + 7);
+    STG_CUDA(cudaMemsetAsync(ridge, 0, sizeof(int), st_));
+    if (kind == ST_TRIP) {
+      STG_CUDA(cudaFuncSetAttribute(trip_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(trip_solve_smem(kk))));
+      launch(trip_solve_kernel, dim3(static_cast<unsigned>(kk)), dim3(128), trip_solve_smem(kk), st_,
+             static_cast<const double*>(C), ldc, static_cast<const double*>(d_values_), kk, topt_.trip_replace_span,
+             F, ldf, ridge);
+      launch(lam_new_kernel, dim3(blocks(kk)), dim3(256), 0, st_, static_cast<const double*>(C), ldc,
+             static_cast<const double*>(d_values_), kk, lam_new);
+    } else {
+      launch(pert_coeff_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(C), ldc,
+             static_cast<const double*>(d_values_), kk, rm ? 2 : 0, topt_.mu, F, ldf, lam_new);
+    }
+    const int ldg = ld_for(D);
+    double* Gz = arena_.get<double>("trk_G", static_cast<i64>(D) * ldg);
+    pgram(Z, ldz, Z, ldz, G, D, D, true, Gz, ldg);
+    launch(renorm_sort_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(F), ldf, D, kk,
+           static_cast<const double*>(Gz), ldg, static_cast<const double*>(lam_new), static_cast<int>(cfg.order), F2,
+           ldf, nv);
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
+    timing_mark(1);
+    finish_rotation(pt, Blk{Z, ldz}, D, F2, ldf, nv, newvals, /*write_state*/ true, nullptr, 0);
+    int hr = 0;
+    STG_CUDA(cudaMemcpyAsync(&hr, ridge, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    ridge_used_ = ridge_used_ || hr != 0;
+  }
+
+  // The new vectors Z F (D columns of the stacked basis Z, F D x k row-major)
+  // and the values nv (device): W = Z F; rows of P -> new rows of X, the
+  // a-rows -> A_new for the rows outside P (trackers.cpp:305 and the
+  // perturbation trackers' xt). Gated on the device error flags.
+  void finish_rotation(const Pert& pt, Blk z, int D, const double* F, int ldk, const double* nv,
+                       std::vector<double>& newvals, bool write_state, double* wout, i64 wrows) {
+    const i64 p = pt.p, N = p + 2 * k;
+    const int kk = static_cast<int>(k);
+    Blk bz = z;
+    struct {
+      Blk z;
+    } b{bz};
     // W = Z F (all stacked rows): rows of P -> new rows of X, a-rows -> A_new
     double* W = arena_.get<double>("rr_W", N * ldk);
     nn(b.z.p, b.z.ld, N, D, F, ldk, kk, W, ldk, 1.0, 0.0, nullptr, 0);
@@ -3036,9 +3181,9 @@ class Session {
       const int keep = static_cast<int>(std::min<i64>(j - 1 > 0 ? j - 1 : j, kq + std::min<i64>(kq, 10) + 2));
       const int want = std::max(kk, keep);
       gram(V, ldv, W, ldv, N, j, j, false, H, ldh);
-      ritz(H, ldh, j, want, wsort, F, ldt);
-      nn(V, ldv, N, j, F, ldt, kk, X_, ldx(), 1.0, 0.0, nullptr, 0);  // x = V F_k
-      nn(W, ldv, N, j, F, ldt, kk, T, ldt, 1.0, 0.0, nullptr, 0);     // W F_k
+      const double* Fr = ritz(H, ldh, j, want, wsort, F, ldt);
+      nn(V, ldv, N, j, Fr, ldt, kk, X_, ldx(), 1.0, 0.0, nullptr, 0);  // x = V F_k
+      nn(W, ldv, N, j, Fr, ldt, kk, T, ldt, 1.0, 0.0, nullptr, 0);     // W F_k
       launch(lz_residual_kernel, dim3(blocks(N * kk)), dim3(256), 0, st_, T, ldt, static_cast<const double*>(X_),
              ldx(), static_cast<const double*>(wsort), N, kk);
       lz_launch<false>(2, T, ldt, kk, nullptr, nullptr, nullptr, N, part, kLzMaxCols, G);
@@ -3078,10 +3223,10 @@ class Session {
       const int pick = first_unconverged >= 0 ? first_unconverged : kk - 1;
       launch(lz_column_kernel, dim3(blocks(N)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, pick, N,
              vb[cur]);
-      nn(V, ldv, N, j, F, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
+      nn(V, ldv, N, j, Fr, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
       launch(copy2d_kernel, dim3(blocks(N * keep)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, V, ldv, N,
              keep);
-      nn(W, ldv, N, j, F, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
+      nn(W, ldv, N, j, Fr, ldt, keep, T, ldt, 1.0, 0.0, nullptr, 0);
       launch(copy2d_kernel, dim3(blocks(N * keep)), dim3(256), 0, st_, static_cast<const double*>(T), ldt, W, ldv, N,
              keep);
       j = keep;
@@ -3092,28 +3237,142 @@ class Session {
   // sym_eig_dense of a j x j Lanczos projection (symmetrized (H + H')/2 as
   // eig.hpp:39): all values in spectral order, `want` leading vectors
   // (row-major j x want, ldf).
-  void ritz(const double* H, int ldh, int j, int want, double* wsort, double* F, int ldf) {
+  // Returns the buffer holding the `want` vectors (F, or its re-orthonormalized
+  // copy). Like the Rayleigh-Ritz solve of the step, inverse iteration groups
+  // only near-degenerate values (gap below kRrOrtol ||H||) and the vectors are
+  // then re-orthonormalized as a block (CholQR), so clusters of close Ritz
+  // values (SBM blocks) cost no serial dstein sweeps and keep eps-accurate
+  // residuals.
+  const double* ritz(const double* H, int ldh, int j, int want, double* wsort, double* F, int ldf) {
     STG_CUDA(cudaMemsetAsync(info_ptr(), 0, sizeof(int), st_));
-    if (!(cfg.flags & ST_FLAG_CUSOLVER_EIG) && j <= kEigMaxN) {
+    if (!(cfg.flags & ST_FLAG_CUSOLVER_EIG) && j <= kEigMaxN && want <= kCholMaxW) {
       double* dbuf = arena_.get<double>("eig_dbuf", static_cast<i64>(eig_scratch_doubles(j, want)));
       int* ibuf = arena_.get<int>("eig_ibuf", static_cast<i64>(eig_scratch_ints(j, want)));
       kbegin(kEig, 4.0 * j * j * j / 3.0);
       syev_launch([&](auto kernel, dim3 g, dim3 bl, size_t sm, auto... args) { launch(kernel, g, bl, sm, st_, args...); },
-                  H, ldh, j, /*sym_input*/ 0, static_cast<int>(cfg.order), want, 1e-3, wsort, F, ldf, dbuf, ibuf,
+                  H, ldh, j, /*sym_input*/ 0, static_cast<int>(cfg.order), want, kRrOrtol, wsort, F, ldf, dbuf, ibuf,
                   flags_ptr());
       kend();
-      return;
+      return orthonormalize_small(F, ldf, j, want);
     }
     double *w = nullptr, *Vc = nullptr;
     eig(H, ldh, j, &w, &Vc, "lz");
     int* perm = arena_.get<int>("lz_perm", j);
     launch(sort_perm_kernel, dim3(1), dim3(256), 0, st_, static_cast<const double*>(w), j,
            static_cast<int>(cfg.order), perm);
-    launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(j) * j)), dim3(256), 0, st_, static_cast<const double*>(Vc),
-           j, static_cast<const double*>(w), static_cast<const int*>(perm), j, F, ldf, wsort);
+    launch(gather_ritz_kernel, dim3(blocks(static_cast<i64>(j) * want)), dim3(256), 0, st_,
+           static_cast<const double*>(Vc), j, static_cast<const double*>(w), static_cast<const int*>(perm), want, F, ldf,
+           wsort);
+    launch(lz_sorted_vals_kernel, dim3(blocks(j)), dim3(256), 0, st_, static_cast<const double*>(w),
+           static_cast<const int*>(perm), j, wsort);
+    return F;
   }
 
  public:
+  // Tracking quality against reference vectors Y (n x k, column-major, e.g. a
+  // Lanczos reference of the current operator as experiment.cpp:177-184
+  // computes): psi_i = principal_angle(x_i, y_i) (metrics.cpp:17-27) and the
+  // largest principal angle between span(X) and span(Y) (metrics.cpp:243-259),
+  // both on the device. The spans are orthonormalized by CholeskyQR2 (the
+  // reference's MGS gives the same span for full-rank inputs).
+  void angles(const double* y, i64 ld, double* psi, double* largest) {
+    if (sh_) throw InvalidArgument("st_angles: not available on sharded sessions");
+    const i64 rows = n;
+    const int kk = static_cast<int>(k), ldq = ldx();
+    if (ld < rows) throw InvalidArgument("st_angles: leading dimension below n");
+    std::vector<void*> tmp;
+    auto alloc = [&](size_t b) {
+      void* p = arena_.alloc(std::max<size_t>(b, 16));
+      tmp.push_back(p);
+      return static_cast<double*>(p);
+    };
+    struct Free {
+      Session* s;
+      std::vector<void*>* t;
+      ~Free() {
+        for (void* p : *t) s->arena_.release(p);
+        cudaStreamSynchronize(s->st_);
+      }
+    } fr{this, &tmp};
+    double* Y = alloc(sizeof(double) * rows * ldq);
+    {
+      std::vector<double> yr(static_cast<size_t>(rows * kk));
+      for (int c = 0; c < kk; ++c)
+        for (i64 i = 0; i < rows; ++i) yr[static_cast<size_t>(i * kk + c)] = y[c * ld + i];
+      STG_CUDA(cudaMemcpy2DAsync(Y, sizeof(double) * ldq, yr.data(), sizeof(double) * kk, sizeof(double) * kk, rows,
+                                 cudaMemcpyHostToDevice, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+    }
+    // ---- psi (two column-statistic passes)
+    const int G = static_cast<int>(std::max<i64>(1, std::min<i64>(cdiv(rows, 256), 148 * 4)));
+    const int ldp = 3 * kk;
+    double* part = alloc(sizeof(double) * G * ldp);
+    double* stats = alloc(sizeof(double) * 3 * kk);
+    double* diffs = alloc(sizeof(double) * 2 * kk);
+    const size_t sm3 = sizeof(double) * (kMetThreads / 32) * 3 * kk, sm2 = sizeof(double) * (kMetThreads / 32) * 2 * kk;
+    STG_CUDA(cudaFuncSetAttribute(angle_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm3)));
+    STG_CUDA(cudaFuncSetAttribute(angle_diff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm2)));
+    launch(angle_stats_kernel, dim3(G), dim3(kMetThreads), sm3, st_, static_cast<const double*>(X_), ldq,
+           static_cast<const double*>(Y), ldq, rows, kk, part, ldp);
+    launch(lz_colsum_kernel, dim3(3 * kk), dim3(256), 0, st_, static_cast<const double*>(part), G, ldp, 3 * kk, stats);
+    launch(angle_diff_kernel, dim3(G), dim3(kMetThreads), sm2, st_, static_cast<const double*>(X_), ldq,
+           static_cast<const double*>(Y), ldq, rows, kk, static_cast<const double*>(stats), part, ldp);
+    launch(lz_colsum_kernel, dim3(2 * kk), dim3(256), 0, st_, static_cast<const double*>(part), G, ldp, 2 * kk, diffs);
+    std::vector<double> hs(static_cast<size_t>(3 * kk)), hd(static_cast<size_t>(2 * kk));
+    STG_CUDA(cudaMemcpyAsync(hs.data(), stats, sizeof(double) * 3 * kk, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaMemcpyAsync(hd.data(), diffs, sizeof(double) * 2 * kk, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    for (int c = 0; c < kk; ++c) {
+      if (hs[3 * c] == 0.0 || hs[3 * c + 1] == 0.0) throw InvalidArgument("zero vector has no angle");
+      if (psi) psi[c] = 2.0 * std::atan2(std::sqrt(hd[2 * c]), std::sqrt(hd[2 * c + 1]));
+    }
+    if (!largest) return;
+    // ---- largest principal angle: Qa, Qb by CholeskyQR2, G = Qa'Qb, R = Qa - Qb G'
+    const int ldk = ld_for(kk);
+    double* Gm = alloc(sizeof(double) * kk * ldk);
+    double* Rk = alloc(sizeof(double) * kk * ldk);
+    double* Ri = alloc(sizeof(double) * kk * ldk);
+    double* Qa = alloc(sizeof(double) * rows * ldq);
+    double* Qb = alloc(sizeof(double) * rows * ldq);
+    double* T1 = alloc(sizeof(double) * rows * ldq);
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    auto cholqr2 = [&](const double* A, double* Q) {
+      const double* src = A;
+      for (int pass = 0; pass < 2; ++pass) {
+        gram(src, ldq, src, ldq, rows, kk, kk, true, Gm, ldk);
+        chol(Gm, ldk, kk, Rk, ldk, Ri, ldk, nullptr, 0.0, true);
+        double* dst = pass == 0 ? T1 : Q;
+        nn(src, ldq, rows, kk, Ri, ldk, kk, dst, ldq, 1.0, 0.0, nullptr, 0, /*tri*/ true);
+        src = dst;
+      }
+    };
+    cholqr2(X_, Qa);
+    cholqr2(Y, Qb);
+    double* Gt = alloc(sizeof(double) * kk * ldk);
+    double* GtG = alloc(sizeof(double) * kk * ldk);
+    double* RtR = alloc(sizeof(double) * kk * ldk);
+    gram(Qb, ldq, Qa, ldq, rows, kk, kk, false, Gt, ldk);             // G' = Qb'Qa
+    nn(Qb, ldq, rows, kk, Gt, ldk, kk, T1, ldq, -1.0, 1.0, Qa, ldq);  // R = Qa - Qb G'
+    gram(T1, ldq, T1, ldq, rows, kk, kk, true, RtR, ldk);             // R'R
+    gram(Gt, ldk, Gt, ldk, kk, kk, kk, true, GtG, ldk);               // G G' (same singular values as G)
+    double* wv = alloc(sizeof(double) * 2 * kk);
+    double* fv = alloc(sizeof(double) * kk * ldk);
+    read_scalars();
+    if (hs_->flags & kBreakdown) throw InvalidArgument("st_angles: rank-deficient vectors");
+    const bool dev = eig_fast(GtG, ldk, kk, /*alg_desc*/ 1, 1, wv, fv, ldk) &&
+                     eig_fast(RtR, ldk, kk, /*alg_desc*/ 1, 1, wv + kk, fv, ldk);
+    std::vector<double> hw(static_cast<size_t>(2 * kk));
+    if (dev) {
+      STG_CUDA(cudaMemcpyAsync(hw.data(), wv, sizeof(double) * 2 * kk, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+    } else {
+      throw InvalidArgument("st_angles: k above the on-device eigensolver limit");
+    }
+    const double c = std::sqrt(std::max(hw[static_cast<size_t>(kk - 1)], 0.0));  // smallest singular value of G
+    const double sres = std::sqrt(std::max(hw[static_cast<size_t>(kk)], 0.0));   // largest of the residual
+    *largest = std::atan2(sres, std::max(c, 0.0));
+  }
+
   // (A, or the shifted Laplacian T): the residual the reference's Lanczos
   // convergence test measures (lanczos.hpp:85-95). One full-operator SpMM
   // Op X (the north star's A Z with Z = X) on the segment-planned CSR kernel,
@@ -3266,6 +3525,27 @@ st_status st_tracker_init(const st_config* cfg, const st_lanczos_options* opts, 
   });
 }
 
+st_status st_set_tracker_options(st_session* s, const st_tracker_options* o) {
+  return guarded(s, [&] {
+    if (!o) throw std::invalid_argument("st_set_tracker_options: null options");
+    if (o->restart_inner < ST_TRIP_BASIC || o->restart_inner > ST_TIMERS)
+      throw std::invalid_argument("unknown tracker kind");
+    if (s->impl->cfg.kind == ST_TIMERS && o->restart_inner == ST_TIMERS)
+      throw std::invalid_argument("tracker_init: timers cannot delegate to itself");
+    s->impl->topt_ = *o;
+  });
+}
+
+st_status st_tracker_state(const st_session* s, double* accumulated_change, int64_t* steps_since_restart,
+                           double* restart_scale, int32_t* ridge_used) {
+  const auto& m = *s->impl;
+  if (accumulated_change) *accumulated_change = m.acc_change_;
+  if (steps_since_restart) *steps_since_restart = m.steps_since_restart_;
+  if (restart_scale) *restart_scale = m.restart_scale_;
+  if (ridge_used) *ridge_used = m.ridge_used_ ? 1 : 0;
+  return ST_OK;
+}
+
 st_status st_init_stats(const st_session* s, int64_t* restarts, int64_t* products) {
   if (restarts) *restarts = s->impl->lz_restarts;
   if (products) *products = s->impl->lz_products;
@@ -3408,6 +3688,13 @@ st_status st_residual_norms(st_session* s, double* norms) {
   return guarded(s, [&] {
     if (!norms) throw std::invalid_argument("st_residual_norms: null argument");
     s->impl->residual_norms(norms);
+  });
+}
+
+st_status st_angles(st_session* s, const double* ref_vectors, int64_t ld, double* psi, double* largest_angle) {
+  return guarded(s, [&] {
+    if (!ref_vectors) throw std::invalid_argument("st_angles: null argument");
+    s->impl->angles(ref_vectors, ld, psi, largest_angle);
   });
 }
 

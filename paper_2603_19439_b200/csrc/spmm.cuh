@@ -8,9 +8,16 @@
 // (proj/src/sparse.cpp:84-87) bit for bit.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace stg {
+
+inline bool getenv_flag(const char* name) {  // development A/B switches, read once
+  const char* v = std::getenv(name);
+  return v && v[0] && v[0] != '0';
+}
 
 struct SpmmArgs {
   i64 rows;             // output rows
@@ -32,7 +39,9 @@ struct SpmmArgs {
 // above and written directly; the segments of a longer row write partial
 // sums, which spmm_fixup_kernel adds in segment order (deterministic; the
 // association differs from Eigen's only within those rows, at rounding level).
-constexpr int kSegNnz = 32;
+constexpr int kSegNnz = 32;    // rows up to this length: the row-group kernels
+constexpr int kLongSeg = 512;  // longer rows: one warp per 512-entry segment (most
+                               // Delta hub rows are a single segment: no fix-up)
 
 struct SpmmPlan {
   const int* vrow;        // virtual row (segment) -> row
@@ -53,8 +62,13 @@ __global__ void __launch_bounds__(256) spmm_kernel(SpmmArgs a, SpmmPlan pl) {
   const int s = static_cast<int>(v - pl.vstart[r]);
   const int nseg = pl.vstart[r + 1] - pl.vstart[r];
   const i64 gr = r + a.row_off;
-  const int rs = a.rowptr[gr] + s * kSegNnz;
-  const int cnt = min(kSegNnz, a.rowptr[gr + 1] - rs);
+  const int seg0 = a.rowptr[gr] + s * kLongSeg;
+  const int seg_end = min(seg0 + kLongSeg, a.rowptr[gr + 1]);
+  double acc[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) acc[t] = 0.0;
+  for (int rs = seg0; rs < seg_end; rs += 32) {  // 32-entry windows, sums in column order
+  const int cnt = min(32, seg_end - rs);
   int c_l = 0;
   double v_l = 0.0;
   if (lane < cnt) {
@@ -63,9 +77,6 @@ __global__ void __launch_bounds__(256) spmm_kernel(SpmmArgs a, SpmmPlan pl) {
   }
   // trailing-column view: the (sorted) columns below col_lo are a prefix
   int q = a.col_lo > 0 ? __popc(__ballot_sync(0xffffffffu, lane < cnt && c_l < a.col_lo)) : 0;
-  double acc[T];
-#pragma unroll
-  for (int t = 0; t < T; ++t) acc[t] = 0.0;
   // four nonzeros per pass: their row loads are issued together, the sums
   // still run in column order
   for (; q + 4 <= cnt; q += 4) {
@@ -95,6 +106,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(SpmmArgs a, SpmmPlan pl) {
       const int cc = lane + 32 * t;
       if (cc < a.m) acc[t] = __dadd_rn(acc[t], __dmul_rn(vq, __ldg(xr + cc)));
     }
+  }
   }
   double* yr = nseg == 1 ? a.Y + static_cast<i64>(r) * a.ldy
                          : pl.scratch + static_cast<i64>(pl.sstart[r] + s) * pl.lds;
@@ -283,6 +295,144 @@ __global__ void __launch_bounds__(32 * kGroupWarps) spmm_group_kernel(SpmmArgs a
   }
 }
 
+// Rows of at most kSegNnz nonzeros, kGroupRows consecutive rows per warp, ALL
+// dense columns per warp: lane l owns columns 64 t + 2l, 2l + 1 of every
+// 64-column slab t < T (128-bit loads and stores), so the group's index work
+// (row pointers, the (col, val) window, row of each entry) is done once for
+// all m columns, and each entry issues T loads. Entries are consumed U at a
+// time with their T x 4 loads in flight together; each row is summed in
+// column order with separate multiply and add roundings (bit-identical to
+// spmm_kernel and to Eigen's row-major product). (U = 2 entries in flight
+// when T >= 3 keeps the kernel at 2 CTAs of 8 warps per SM.) Warps walk the groups
+// grid-stride and fetch the next group's header before gathering the current
+// one. Longer rows are skipped (spmm_kernel over the long-row plan).
+template <int T>
+__global__ void __launch_bounds__(256, 2) spmm_rows_kernel(SpmmArgs a, i64 ngroups) {
+  constexpr int U = T >= 3 ? 2 : 4;  // entries whose T loads are in flight together
+  const int lane = threadIdx.x & 31;
+  const i64 w0 = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  const int* rowp = a.rowptr + a.row_off;
+  bool on[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) on[t] = 64 * t + 2 * lane < a.m;
+  auto header = [&](i64 g, int& rp_l, int& nr) {
+    const i64 r0 = g * kGroupRows;
+    nr = static_cast<int>(min(static_cast<i64>(kGroupRows), a.rows - r0));
+    rp_l = (g < ngroups && lane <= nr) ? __ldg(rowp + r0 + lane) : 0;
+  };
+  int rp_n = 0, nr_n = 0;
+  if (w0 < ngroups) header(w0, rp_n, nr_n);
+  for (i64 g = w0; g < ngroups; g += nw) {
+    const int rp_l = rp_n, nr = nr_n;
+    if (g + nw < ngroups) header(g + nw, rp_n, nr_n);  // next group's row pointers in flight
+    const i64 r0 = g * kGroupRows;
+    const int rp_next = __shfl_down_sync(0xffffffffu, rp_l, 1);
+    double* Yg = a.Y + r0 * static_cast<i64>(a.ldy) + 2 * lane;
+    auto store = [&](int r, const double (&acc)[T][2]) {
+      double* yr = Yg + static_cast<i64>(r) * a.ldy;
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        if (on[t]) *reinterpret_cast<double2*>(yr + 64 * t) = make_double2(acc[t][0], acc[t][1]);
+    };
+    double acc[T][2];
+    const int e_l = lane < nr ? rp_next : 0;  // end of row `lane` of the group
+    // rows of the group one window at a time: rows [ri, last] whose entries fit
+    // 32 lanes; a row longer than kSegNnz is skipped (the long-row plan has it)
+    int ri = 0;
+    while (ri < nr) {
+      const int wb = __shfl_sync(0xffffffffu, rp_l, ri);
+      const unsigned fm = __ballot_sync(0xffffffffu, lane >= ri && lane < nr && e_l <= wb + 32);
+      if (!(fm & (1u << ri))) {  // row ri is long
+        ++ri;
+        continue;
+      }
+      const int last = __ffs(~(fm >> ri)) - 1 + ri - 1;  // end of the contiguous run of fitting rows
+      const int we = __shfl_sync(0xffffffffu, e_l, last);
+      int c_l = 0;
+      double v_l = 0.0;
+      if (wb + lane < we) {
+        c_l = __ldg(a.col + wb + lane);
+        v_l = __ldg(a.val + wb + lane);
+      }
+      int row_l = -1;  // row (within the group) of entry `lane`
+#pragma unroll
+      for (int i = 0; i < kGroupRows; ++i) {
+        const int rs = __shfl_sync(0xffffffffu, rp_l, i);
+        row_l += (i < nr && wb + lane >= rs) ? 1 : 0;
+      }
+      const int q_end = we - wb;
+      unsigned act = __ballot_sync(0xffffffffu, lane < q_end && c_l >= a.col_lo);
+      // rows ri..last with no active entry are zero rows
+      {
+        const bool mine = lane >= ri && lane <= last;
+        bool has = false;
+        if (mine) {
+          const int s = rp_l - wb, e = e_l - wb;
+          const unsigned hi = e >= 32 ? 0xffffffffu : ((1u << e) - 1u);
+          const unsigned lo = s >= 32 ? 0xffffffffu : ((1u << s) - 1u);
+          has = (act & hi & ~lo) != 0;
+        }
+        unsigned empty = __ballot_sync(0xffffffffu, mine && !has);
+        double z[T][2];
+#pragma unroll
+        for (int t = 0; t < T; ++t) z[t][0] = z[t][1] = 0.0;
+        while (empty) {
+          const int r = __ffs(empty) - 1;
+          empty &= empty - 1;
+          store(r, z);
+        }
+      }
+      int cur = -1;
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+      while (act) {
+        int jj[U], nb = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          jj[u] = act ? __ffs(act) - 1 : -1;
+          if (act) {
+            act &= act - 1;
+            ++nb;
+          }
+        }
+        double2 xv[U][T];
+        double vv[U];
+        int rw[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = jj[u] < 0 ? 0 : jj[u];
+          const int c = __shfl_sync(0xffffffffu, c_l, j);
+          vv[u] = __shfl_sync(0xffffffffu, v_l, j);
+          rw[u] = __shfl_sync(0xffffffffu, row_l, j);
+          const double* xr = a.X + static_cast<i64>(c) * a.ldx + 2 * lane;
+#pragma unroll
+          for (int t = 0; t < T; ++t)
+            xv[u][t] = (u < nb && on[t]) ? __ldg(reinterpret_cast<const double2*>(xr + 64 * t))
+                                         : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (u >= nb) break;
+          if (rw[u] != cur) {
+            if (cur >= 0) store(cur, acc);
+            cur = rw[u];
+#pragma unroll
+            for (int t = 0; t < T; ++t) acc[t][0] = acc[t][1] = 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < T; ++t) {
+            acc[t][0] = __dadd_rn(acc[t][0], __dmul_rn(vv[u], xv[u][t].x));
+            acc[t][1] = __dadd_rn(acc[t][1], __dmul_rn(vv[u], xv[u][t].y));
+          }
+        }
+      }
+      if (cur >= 0) store(cur, acc);
+      ri = last + 1;
+    }
+  }
+}
+
 // Rows of several segments: partial sums added in segment order.
 __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl) {
   const int i = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -315,7 +465,7 @@ __global__ void seg_count_kernel(const int* rowptr, i64 row_off, i64 rows, int* 
     return;
   }
   const int len = rowptr[r + row_off + 1] - rowptr[r + row_off];
-  const int c = len > kSegNnz ? (len + kSegNnz - 1) / kSegNnz : 0;  // short rows: spmm_group_kernel
+  const int c = len > kSegNnz ? (len + kLongSeg - 1) / kLongSeg : 0;  // short rows: the row-group kernel
   cnt[r] = c;
   cnt2[r] = c > 1 ? c : 0;
 }
@@ -328,8 +478,23 @@ __global__ void seg_fill_kernel(const int* vstart, i64 rows, int* vrow, int* spl
   if (c > 1) split_rows[atomicAdd(nsplit, 1)] = static_cast<int>(r);
 }
 
-inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 split_max, cudaStream_t st) {
-  {  // rows of at most kSegNnz nonzeros
+// long_rows: a row longer than kSegNnz may exist (nnz > kSegNnz);
+// split_max > 0: a row longer than kLongSeg may exist (segments + fix-up)
+inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 split_max, bool long_rows,
+                        cudaStream_t st) {
+  const bool vec2 = a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 && a.m <= 256 &&
+                    ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
+  if (vec2 && !getenv_flag("STG_SPMM_GROUP")) {  // rows of at most kSegNnz nonzeros, all columns per warp
+    const i64 ng = cdiv(a.rows, kGroupRows);
+    const unsigned grid = static_cast<unsigned>(std::min<i64>(cdiv(ng, 8), 148 * 16));
+    switch (static_cast<int>(cdiv(a.m, 64))) {
+      case 1: spmm_rows_kernel<1><<<grid, 256, 0, st>>>(a, ng); break;
+      case 2: spmm_rows_kernel<2><<<grid, 256, 0, st>>>(a, ng); break;
+      case 3: spmm_rows_kernel<3><<<grid, 256, 0, st>>>(a, ng); break;
+      default: spmm_rows_kernel<4><<<grid, 256, 0, st>>>(a, ng); break;
+    }
+    STG_LAUNCH();
+  } else {  // rows of at most kSegNnz nonzeros
     const bool vec = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 &&
                      ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
     const int w = vec ? 64 : 32;
@@ -338,7 +503,7 @@ inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 spl
     else spmm_group_kernel<false><<<g, 32 * kGroupWarps, spmm_group_smem<false>(), st>>>(a);
     STG_LAUNCH();
   }
-  if (split_max <= 0) return;  // no row longer than kSegNnz can exist
+  if (!long_rows) return;  // no row longer than kSegNnz can exist
   const unsigned grid = static_cast<unsigned>(cdiv(vmax, 8));
   const int T = static_cast<int>(cdiv(a.m < 1 ? 1 : a.m, 32));
   switch (T) {
