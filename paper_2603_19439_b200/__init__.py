@@ -98,6 +98,8 @@ def lib():
         L.st_get_embedding.argtypes = [C.c_void_p, DP, DP, I64]
         L.st_residual_norms.argtypes = [C.c_void_p, DP]
         L.st_angles.argtypes = [C.c_void_p, DP, I64, DP, DP]
+        L.st_debug_determinism.argtypes = [C.c_void_p, C.c_int32, I64, C.c_int32, C.c_int32, C.c_int32, DP, DP]
+        L.st_debug_determinism.restype = C.c_int
         L.st_get_values.argtypes = [C.c_void_p, DP]
         L.st_get_csr.argtypes = [C.c_void_p, C.c_int32, I32P, I32P, DP]
         L.st_probe_basis.argtypes = [C.c_void_p, C.POINTER(StUpdate), C.c_int32, C.c_uint64, DP, I64, I64, I64P]
@@ -431,6 +433,18 @@ class TrackerSession:
         out = np.zeros(self.k)
         self._check(lib().st_residual_norms(self._h, _p(out)))
         return out
+
+    def determinism(self, which: int, N: int, m1: int, m2: int, reps: int = 3, out: bool = False):
+        """Largest run-to-run difference of a kernel on pseudo-random operands
+        (0 Gram, 1 row-local GEMM, 2 SpMV of the session operator, 3 its SpMM);
+        with out=True also the first run's result."""
+        d = C.c_double()
+        rows = m1 if which == 0 else N
+        cols = m2 if which in (0, 1) else 1 if which == 2 else m1
+        buf = np.zeros(rows * cols) if out else None
+        self._check(lib().st_debug_determinism(self._h, which, N, m1, m2, reps, C.byref(d),
+                                               _p(buf) if out else None))
+        return (d.value, buf.reshape(rows, cols)) if out else d.value
 
     def angles(self, ref_vectors):
         """(psi per vector, largest principal angle) against reference vectors

@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT / 32);
+      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
     }
     mbar_fence_init();
   }
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
     else
       warp_mma_dispatch<SA, 8, SB, 8, kBK>(code, acc, pa, pb);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    mbar_arrive(&empty[st]);  // each thread's smem reads ordered before the TMA refill
   }
   if (code == 0) return;
   const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
@@ -623,7 +623,6 @@ template <bool FULL, bool BETA>
 __device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* tmA, const CUtensorMap* tmC, i64 row0,
                                             int tj, unsigned char* smraw) {
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
-  unsigned long long* empty = full + kNNStages;
   double* stage0 = reinterpret_cast<double*>(smraw + 128);
   constexpr int STG = BM * SAR2 + BK2 * SST;
   constexpr unsigned kStageBytes = sizeof(double) * STG;
@@ -634,10 +633,7 @@ __device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* 
   const int nk = static_cast<int>(cdiv(kmax, BK2));
   const int code = FULL ? 16 : warp_code(frags_left(a.nrows, row0 + wm * 32), frags_left(a.m2, tj * BN + wn * 32), false);
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kNNStages; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT / 32);
-    }
+    for (int st = 0; st < kNNStages; ++st) mbar_init(&full[st], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -649,7 +645,7 @@ __device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* 
     tma_load_2d(sa + BM * SAR2, tmC, tj * BN, q * BK2, &full[st]);
   };
   if (threadIdx.x == 0)
-    for (int q = 0; q < min(nk, kNNStages - 1); ++q) produce(q);
+    for (int q = 0; q < min(nk, kNNStages); ++q) produce(q);
   double acc[4][4][2];
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -668,12 +664,10 @@ __device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* 
         bpre[x][y][1] = v.y;
       }
   }
+  // a stage is refilled only after a CTA barrier shows every warp has
+  // finished reading it (the refill of chunk q + kNNStages overlaps the
+  // compute of chunk q + 1)
   for (int q = 0; q < nk; ++q) {
-    if (threadIdx.x == 0 && q + kNNStages - 1 < nk) {
-      const int qq = q + kNNStages - 1;
-      if (qq >= kNNStages) mbar_wait(&empty[qq % kNNStages], static_cast<unsigned>((qq / kNNStages - 1) & 1));
-      produce(qq);
-    }
     const int st = q % kNNStages;
     mbar_wait(&full[st], static_cast<unsigned>((q / kNNStages) & 1));
     const double* sa = stage0 + st * STG;
@@ -683,8 +677,8 @@ __device__ __forceinline__ void nn_tma_tile(const NNArgs& a, const CUtensorMap* 
       warp_mma<4, 4, false, 1, 8 * SAR2, SST, 8>(acc, pa, pc);
     else
       warp_mma_dispatch<1, 8 * SAR2, SST, 8>(code, acc, pa, pc);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    __syncthreads();
+    if (threadIdx.x == 0 && q + kNNStages < nk) produce(q + kNNStages);
   }
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -769,7 +763,7 @@ __global__ void __launch_bounds__(NT, 2)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStreamStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT / 32);
+      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
     }
     mbar_fence_init();
   }
@@ -812,7 +806,7 @@ __global__ void __launch_bounds__(NT, 2)
           if (y < nxw) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);  // A is in registers' products now; the slot may refill
+    mbar_arrive(&empty[st]);  // A is in registers' products now; the slot may refill
     const i64 row0 = static_cast<i64>(b + q * G) * kStreamRows + warp * 32;
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -862,7 +856,7 @@ __global__ void __launch_bounds__(NT, 3)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStreamStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT / 32);
+      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
     }
     mbar_fence_init();
   }
@@ -909,7 +903,7 @@ __global__ void __launch_bounds__(NT, 3)
           if (x < nx && y < ny && (!a.sym || x <= y)) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    mbar_arrive(&empty[st]);  // each thread's smem reads ordered before the TMA refill
   }
   // combine the four warps (fixed order) through the (drained) stage buffers
   __syncthreads();

@@ -57,6 +57,7 @@ struct InvalidArgument : std::invalid_argument {
 struct RuntimeError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct SpecRedo {};  // a speculated decision of the step failed (internal: the step is redone)
 
 // ------------------------------------------------------------------ residual norms
 // Per-column sums of (AX - X diag(theta))^2 over row blocks of 256 rows:
@@ -268,6 +269,7 @@ struct Scalars {  // pinned host mirror of device scalars read at sync points
   int nnz_dt;
   int flags;
   int info;
+  int sticky;
   double alpha;
   double sk_lam[kEigMaxN];  // sketch eigenvalues, copied asynchronously (pageable memory would block the host)
 };
@@ -376,6 +378,10 @@ class Session {
     return std::sqrt(s);
   }
   bool prewarmed_ = false;
+  bool spec_ = false;      // the current step attempt speculates (run_step)
+  i64 spec_redos = 0;      // steps redone on the exact path
+  const bool lz_log_ = getenv("STG_LZ_LOG") != nullptr;
+  const bool lz_log2_ = getenv("STG_LZ_LOG2") != nullptr;
 
   // ev == nullptr: tracker_init (trackers.cpp:132-145) on the device, i.e. the
   // leading eigenpairs of the tracked operator by thick-restart Lanczos.
@@ -684,18 +690,33 @@ class Session {
       return;
     }
     std::vector<double> newvals;
-    try {
-      if (kind >= ST_IASC && kind <= ST_GREST_RSVD) {
-        Basis b = build_basis(pt, kind - ST_IASC, basis_seed);
-        timing_mark(1);
-        rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
-      } else {
-        perturbation_step(pt, kind, newvals);
+    // first attempt speculates the rare host decisions (suspect pivots, sketch
+    // rank) and checks them once at the end; a failed speculation leaves X
+    // untouched (the rotation is gated) and the step is redone exactly
+    for (int attempt = 0;; ++attempt) {
+      spec_ = attempt == 0 && !sh_ && !(cfg.flags & ST_FLAG_CUSOLVER_EIG) && !getenv_flag("STG_NO_SPEC");
+      STG_CUDA(cudaMemsetAsync(sticky_ptr(), 0, sizeof(int), st_));
+      try {
+        if (kind >= ST_IASC && kind <= ST_GREST_RSVD) {
+          Basis b = build_basis(pt, kind - ST_IASC, basis_seed);
+          timing_mark(1);
+          rayleigh_ritz(pt, b, newvals, /*write_state*/ true, nullptr, 0);
+        } else {
+          perturbation_step(pt, kind, newvals);
+        }
+        spec_ = false;
+        break;
+      } catch (const SpecRedo&) {
+        restore_x();
+        rr_pre_.valid = false;
+        ++spec_redos;
+        continue;
+      } catch (...) {
+        spec_ = false;
+        restore_x();
+        cudaStreamSynchronize(st_);
+        throw;
       }
-    } catch (...) {
-      restore_x();
-      cudaStreamSynchronize(st_);
-      throw;
     }
     xrestore_.active = false;  // the rotation rewrote the rows of P
     commit_graph(pt);
@@ -872,6 +893,80 @@ class Session {
     return ms / iters;
   }
 
+  // Run-to-run determinism of a kernel on pseudo-random operands (development
+  // and tests): the largest |difference| between `reps` repeated runs and the
+  // first. which = 0 Gram A'B (N x m1, N x m2), 1 row-local GEMM A C
+  // (N x m1 times m1 x m2), 2 SpMV with the session's operator, 3 SpMM of the
+  // session's operator with an n x m1 block.
+  double det_check(int which, i64 N, int m1, int m2, int reps, double* first_out = nullptr) {
+    const DevCsr& op = is_laplacian() ? T() : A();
+    if (which >= 2) N = n;
+    const int ld1 = ld_for(m1), ld2 = ld_for(m2);
+    double* Aa = arena_.get<double>("dc_A", N * ld1);
+    double* Bb = arena_.get<double>("dc_B", N * ld2);
+    double* Cc = arena_.get<double>("dc_C", static_cast<i64>(m1) * ld2 + 8);
+    const i64 outn = which == 0 ? static_cast<i64>(m1) * ld2 : which == 1 ? N * ld2 : which == 2 ? N : N * ld1;
+    double* O = arena_.get<double>("dc_O", outn);
+    launch(hash_fill_kernel, dim3(blocks(N * ld1)), dim3(256), 0, st_, Aa, N * ld1, 11ULL);
+    launch(hash_fill_kernel, dim3(blocks(N * ld2)), dim3(256), 0, st_, Bb, N * ld2, 22ULL);
+    launch(hash_fill_kernel, dim3(blocks(static_cast<i64>(m1) * ld2)), dim3(256), 0, st_, Cc,
+           static_cast<i64>(m1) * ld2, 33ULL);
+    SpvBufs sp;
+    if (which == 2) sp = spv_plan(op.rp, N);
+    auto run = [&]() {
+      if (which == 0) gram(Aa, ld1, Bb, ld2, N, m1, m2, false, O, ld2);
+      if (which == 1) nn(Aa, ld1, N, m1, Cc, ld2, m2, O, ld2, 1.0, 0.0, nullptr, 0);
+      if (which == 2) spmv(op, sp.pl, Aa, O, nullptr, 0);
+      if (which == 3) {
+        SpmmArgs sa{};
+        sa.rows = N;
+        sa.rowptr = op.rp;
+        sa.col = op.col;
+        sa.val = op.val;
+        sa.X = Aa;
+        sa.ldx = ld1;
+        sa.m = m1;
+        sa.Y = O;
+        sa.ldy = ld1;
+        ++plan_epoch_;
+        do_spmm(sa, op.nnz, N, kSpmmFull, true);
+      }
+    };
+    run();
+    std::vector<double> ref(static_cast<size_t>(outn)), cur(static_cast<size_t>(outn));
+    STG_CUDA(cudaMemcpyAsync(ref.data(), O, sizeof(double) * outn, cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    if (first_out) {  // rows x cols, dense row-major
+      const int cols = which == 0 || which == 1 ? m2 : which == 2 ? 1 : m1;
+      const int ld = which == 0 || which == 1 ? ld2 : which == 2 ? 1 : ld1;
+      const i64 rows = which == 0 ? m1 : N;
+      for (i64 i = 0; i < rows; ++i)
+        for (int c = 0; c < cols; ++c) first_out[i * cols + c] = ref[static_cast<size_t>(i * ld + c)];
+    }
+    double md = 0.0;
+    for (int r = 0; r < reps; ++r) {
+      STG_CUDA(cudaMemsetAsync(O, 0xff, sizeof(double) * outn, st_));  // NaN-poisoned output
+      run();
+      STG_CUDA(cudaMemcpyAsync(cur.data(), O, sizeof(double) * outn, cudaMemcpyDeviceToHost, st_));
+      STG_CUDA(cudaStreamSynchronize(st_));
+      const int cols = which == 0 || which == 1 ? m2 : which == 2 ? 1 : m1;
+      const int ld = which == 0 || which == 1 ? ld2 : which == 2 ? 1 : ld1;
+      const i64 rows = which == 0 ? m1 : N;
+      for (i64 i = 0; i < rows; ++i)
+        for (int c = 0; c < cols; ++c) {
+          const size_t q = static_cast<size_t>(i * ld + c);
+          const double d = std::fabs(cur[q] - ref[q]);
+          if (d != 0.0 && getenv_flag("STG_DET_LOG"))
+            fprintf(stderr, "det which %d rep %d row %lld col %d ref %.17g got %.17g\n", which, r,
+                    static_cast<long long>(i), c, ref[q], cur[q]);
+          md = std::max(md, d == d ? d : 1e300);
+        }
+    }
+    if (which == 2) spv_release(sp);
+    kdiscard();
+    return md;
+  }
+
   void copy_x_colmajor(double* out, i64 rows) {
     std::vector<double> xr(static_cast<size_t>(rows * k));
     STG_CUDA(cudaMemcpy2DAsync(xr.data(), sizeof(double) * k, X_, sizeof(double) * ldx(), sizeof(double) * k, rows,
@@ -1036,6 +1131,7 @@ class Session {
   int* flags_ptr() { return reinterpret_cast<int*>(d_scal_ + 3); }
   int* info_ptr() { return reinterpret_cast<int*>(d_scal_ + 4); }
   int* side_flags_ptr() { return reinterpret_cast<int*>(d_scal_ + 5); }
+  int* sticky_ptr() { return reinterpret_cast<int*>(d_scal_ + 8); }
 
   template <typename K, typename... Args>
   void launch(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
@@ -1277,7 +1373,7 @@ class Session {
     a.upper_tri_c = tri ? 1 : 0;
     if (gated) {  // skip when the step has already failed (keeps a failed step side-effect free)
       a.skip_flags = flags_ptr();
-      a.skip_mask = kNonFinite | kNotOrthonormal;
+      a.skip_mask = kNonFinite | kNotOrthonormal | kSpecFail;
       a.skip_info = info_ptr();
     }
     if (klog_) snprintf(ktag_, sizeof(ktag_), "nn %lldx%dx%d%s", rows, m1, m2, tri ? " tri" : "");
@@ -1300,8 +1396,9 @@ class Session {
     else
     {
       const dim3 grid(static_cast<unsigned>(cdiv(rows, dm::BM) * cdiv(m2, dm::BN)));
-      const bool tma = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 && lda % 2 == 0 &&
-                       ldc % 2 == 0;
+      static const bool no_tma = getenv_flag("STG_NN_NOTMA");  // development A/B
+      const bool tma = !no_tma && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 &&
+                       lda % 2 == 0 && ldc % 2 == 0;
       if (tma) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
@@ -2315,8 +2412,17 @@ class Session {
            (against ? a : 0), w, o2);
     STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
     chol(Gm, ldw, w, R, ldw, Ri, ldw, o2, kSuspectTau2, false);
-    read_scalars();
-    last_ortho_exact_ = (hs_->flags & (kSuspect | kBreakdown)) != 0;
+    if (spec_) {
+      // speculate "no suspect pivot" (the common case): the decision is
+      // checked once at the end of the step, which is redone on the exact
+      // path if any pivot was suspect (no host round trip here)
+      launch(or_sticky_kernel, dim3(1), dim3(1), 0, st_, static_cast<const int*>(flags_ptr()), kSuspect | kBreakdown,
+             sticky_ptr());
+      last_ortho_exact_ = false;
+    } else {
+      read_scalars();
+      last_ortho_exact_ = (hs_->flags & (kSuspect | kBreakdown)) != 0;
+    }
     if (last_ortho_exact_) {
       if (against && a > 0 && Cpre) {  // the replica starts from the unprojected block
         double* W0 = arena_.get<double>("on_W0", N * ldw);
@@ -2599,6 +2705,27 @@ class Session {
     // so clusters are re-orthogonalized only when nearly degenerate
     STG_CUDA(cudaEventRecord(ev_gb_, st_));
     STG_CUDA(cudaStreamWaitEvent(st_eig_, ev_gb_, 0));
+    if (spec_ && eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10, st_eig_, side_flags_ptr())) {
+      // speculate full rank (keep = min(L, qm)); the device checks rsvd.hpp:59-63's
+      // cut beside the solve and the step is redone if it disagrees
+      launch(sketch_keep_kernel, dim3(1), dim3(32), 0, st_eig_, static_cast<const double*>(lamd), qm,
+             static_cast<int>(cfg.rsvd_l), wantu, static_cast<const int*>(nullptr), sticky_ptr());
+      STG_CUDA(cudaEventRecord(ev_eig_, st_eig_));
+      during_eig(static_cast<const double*>(M), ldy, qm);
+      STG_CUDA(cudaStreamWaitEvent(st_, ev_eig_, 0));
+      const int keep = wantu;
+      if (keep == 0) return 0;
+      if (pre_pm_) {
+        nn(pre_pm_, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+        const int ldcp = ld_for(keep);
+        pre_cr_ = arena_.get<double>("pm_CR", static_cast<i64>(pre_a_) * ldcp);
+        pre_ldcr_ = ldcp;
+        nn(pre_c1_, ldy, pre_a_, qm, U, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
+      } else {
+        nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+      }
+      return keep;
+    }
     if (eig_fast(gb, ldy, qm, /*alg_desc*/ 1, wantu, lamd, U, ldu, 1e-10, st_eig_, side_flags_ptr())) {
       STG_CUDA(cudaMemcpyAsync(hs_->sk_lam, lamd, sizeof(double) * qm, cudaMemcpyDeviceToHost, st_eig_));
       STG_CUDA(cudaEventRecord(ev_eig_, st_eig_));
@@ -2936,6 +3063,7 @@ class Session {
     nn(b.z.p, b.z.ld, N, D, F, ldk, kk, W, ldk, 1.0, 0.0, nullptr, 0);
     newvals.assign(static_cast<size_t>(kk), 0.0);
     STG_CUDA(cudaMemcpyAsync(newvals.data(), nv, sizeof(double) * kk, cudaMemcpyDeviceToHost, st_));
+    launch(merge_spec_kernel, dim3(1), dim3(1), 0, st_, static_cast<const int*>(sticky_ptr()), flags_ptr());
     if (write_state) {
       // X <- X A_new on the rows outside P (in place, DMMA, single column tile),
       // then the rows of P take W's rows. Both are skipped if the step failed.
@@ -2953,7 +3081,9 @@ class Session {
                static_cast<const int*>(flags_ptr()), static_cast<const int*>(info_ptr()));
       kend();
     }
+    STG_CUDA(cudaMemcpyAsync(&hs_->sticky, sticky_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
     read_scalars();
+    if (hs_->sticky) throw SpecRedo();  // a speculated decision failed: nothing was written
     if (hs_->flags & kNonFinite) throw InvalidArgument("sym_eig_dense: non-finite entries");
     if (hs_->flags & kNotOrthonormal) throw InvalidArgument("rayleigh_ritz_step: basis is not column-orthonormal");
     if (hs_->info != 0) throw RuntimeError("sym_eig_dense: factorization did not converge");
@@ -3207,6 +3337,22 @@ class Session {
       }
       best_worst = std::min(best_worst, worst);
       lz_restarts = restart;
+      if (lz_log2_) {
+        auto sum = [&](const double* p, i64 rows, int cols, int ld) {
+          std::vector<double> h(static_cast<size_t>(rows * ld));
+          STG_CUDA(cudaMemcpy(h.data(), p, sizeof(double) * rows * ld, cudaMemcpyDeviceToHost));
+          double s = 0.0;
+          for (i64 r = 0; r < rows; ++r)
+            for (int c = 0; c < cols; ++c) s += std::fabs(h[static_cast<size_t>(r * ld + c)]) * (1.0 + 1e-3 * c);
+          return s;
+        };
+        fprintf(stderr, "lzdbg restart %lld H %.17g F %.17g Fr %.17g V %.17g W %.17g X %.17g T %.17g res0 %.17g\n",
+                static_cast<long long>(restart), sum(H, j, j, ldh), sum(F, j, want, ldt), sum(Fr, j, want, ldt),
+                sum(V, N, j, ldv), sum(W, N, j, ldv), sum(X_, N, kk, ldx()), sum(T, N, kk, ldt), res[0]);
+      }
+      if (lz_log_ && (restart < 12 || restart % 50 == 0))
+        fprintf(stderr, "lanczos restart %lld j %d worst %.3e first_unconverged %d a_norm %.6g w0 %.17g w_kk-1 %.17g\n",
+                static_cast<long long>(restart), j, worst, first_unconverged, a_norm, wv[0], wv[static_cast<size_t>(kk - 1)]);
       if ((first_unconverged < 0 && kk == kq) || j >= N) {
         values.assign(wv.begin(), wv.begin() + kk);
         values.resize(static_cast<size_t>(kq), 0.0);
@@ -3842,6 +3988,11 @@ st_status st_step_perturbation(st_session* s, int64_t n_old, int64_t n_new, cons
     if (!delta) throw std::invalid_argument("st_step_perturbation: null delta");
     s->impl->step_perturbation(n_old, n_new, *delta, false);
   });
+}
+
+st_status st_debug_determinism(st_session* s, int32_t which, int64_t N, int32_t m1, int32_t m2, int32_t reps,
+                               double* max_diff, double* first_out) {
+  return guarded(s, [&] { *max_diff = s->impl->det_check(which, N, m1, m2, reps, first_out); });
 }
 
 st_status st_step_device(st_session* s, const st_update* upd) {

@@ -13,7 +13,36 @@ enum StepFlagBits : int {
   kBreakdown = 2,      // non-positive / non-finite Cholesky pivot
   kNonFinite = 4,      // non-finite entry in the projected matrix (sym_eig_dense check)
   kNotOrthonormal = 8, // |Z'Z - I|max > 1e-6 (trackers.cpp:293-295)
+  kSpecFail = 16,      // a speculated decision (no suspect pivot, full sketch rank) failed: redo the step
 };
+
+// sticky |= (flags & mask) != 0 (deferred checks of a speculated step)
+__global__ void or_sticky_kernel(const int* flags, int mask, int* sticky) {
+  if (*flags & mask) *sticky = 1;
+}
+
+// the rank / keep decision of rsvd_basis (rsvd.hpp:59-63) on the device:
+// lam_desc are the eigenvalues of bt_m' bt_m in descending order; the host
+// speculated keep_assumed = min(L, qm).
+__global__ void sketch_keep_kernel(const double* lam_desc, int qm, int L, int keep_assumed, const int* info,
+                                   int* sticky) {
+  if (threadIdx.x != 0) return;
+  const double sv0 = sqrt(fmax(lam_desc[0], 0.0));
+  const double cutoff = 1e-10 * sv0;
+  int rank = 0;
+  while (rank < qm) {
+    const double sv = sqrt(fmax(lam_desc[rank], 0.0));
+    if (!(sv > cutoff && sv > 0.0)) break;
+    ++rank;
+  }
+  const int keep = rank < L ? rank : L;
+  if (keep != keep_assumed || (info && *info != 0)) *sticky = 1;
+}
+
+// flags |= kSpecFail when the step's sticky word is set (gates the rotation)
+__global__ void merge_spec_kernel(const int* sticky, int* flags) {
+  if (*sticky) atomicOr(flags, kSpecFail);
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -403,6 +432,17 @@ __global__ void orig2_kernel(const double* G1, int ldg, const double* Cm, int ld
 __global__ void fill_kernel(double* p, i64 n, double v) {
   const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx < n) p[idx] = v;
+}
+
+// pseudo-random fill in [-0.5, 0.5) (splitmix64 of the index; development checks)
+__global__ void hash_fill_kernel(double* p, i64 n, unsigned long long seed) {
+  const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  unsigned long long z = seed + 0x9e3779b97f4a7c15ULL * static_cast<unsigned long long>(idx + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  z ^= z >> 31;
+  p[idx] = static_cast<double>(z >> 11) * 0x1.0p-53 - 0.5;
 }
 
 // Copy a rows x cols block (row-major) between leading dimensions.

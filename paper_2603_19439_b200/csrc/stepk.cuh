@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256) rotate_x_kernel(double* X, int ldx, i64 n
                                                        const int* mark, int stamp, const int* posmap, const double* W,
                                                        int ldw, const double* Anew, int k, const int* flags,
                                                        const int* info) {
-  if ((*flags & (kNonFinite | kNotOrthonormal)) || *info != 0) return;
+  if ((*flags & (kNonFinite | kNotOrthonormal | kSpecFail)) || *info != 0) return;
   const i64 i = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n_total) return;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(256) rotate_x_kernel(double* X, int ldx, i64 n
 __global__ void __launch_bounds__(256) scatter_rows_kernel(double* X, int ldx, const int* P, int dense, i64 p,
                                                            const double* W, int ldw, int k, const int* flags,
                                                            const int* info) {
-  if ((*flags & (kNonFinite | kNotOrthonormal)) || *info != 0) return;
+  if ((*flags & (kNonFinite | kNotOrthonormal | kSpecFail)) || *info != 0) return;
   const i64 t = static_cast<i64>(blockIdx.x) * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (t >= p) return;

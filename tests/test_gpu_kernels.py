@@ -109,3 +109,31 @@ def test_residual_norms_match_host():
         ref = np.linalg.norm(A @ X - X * lam, axis=0)
         got = g.residual_norms()
         assert np.allclose(got, ref, rtol=1e-10, atol=1e-12 * np.abs(lam).max()), (op, got, ref)
+
+
+@pytest.mark.gpu
+def test_dmma_and_sparse_kernels_are_deterministic():
+    """Repeated runs of the DMMA Gram / row-local GEMM (TMA pipelines) and the
+    full-operator SpMV / SpMM on the same pseudo-random operands give the same
+    bits (a lane-divergent mbarrier wait ahead of mma.sync.aligned once made
+    partial column tiles sporadically wrong)."""
+    from paper_2603_19439_b200 import TrackerSession, streams
+
+    s = streams.config1(n=3000, steps=0)
+    rp, col, val = s.csr0()
+    x = np.linalg.qr(np.random.default_rng(0).standard_normal((len(rp) - 1, 8)))[0]
+    g = TrackerSession(rp, col, val, np.arange(8.0, 0, -1), x, kind="grest-rsvd", k=8)
+    bad = []
+    for m1, m2 in [(148, 76), (128, 76), (148, 65), (100, 100), (200, 100), (164, 164), (64, 76), (32, 20)]:
+        d = g.determinism(1, 20000, m1, m2, 12)
+        if d != 0.0:
+            bad.append(("nn", m1, m2, d))
+    for m1, m2 in [(148, 148), (76, 76), (200, 200), (32, 200), (64, 100), (32, 32)]:
+        d = g.determinism(0, 20000, m1, m2, 12)
+        if d != 0.0:
+            bad.append(("gram", m1, m2, d))
+    for which, m in [(2, 1), (3, 32), (3, 100)]:
+        d = g.determinism(which, 0, m, m, 8)
+        if d != 0.0:
+            bad.append(("sparse", which, m, d))
+    assert not bad, bad

@@ -43,7 +43,12 @@ def test_tracker_kinds_match_oracle(case):
     from paper_2603_19439_b200 import streams
 
     kind = "timers" if case.startswith("timers") else "trip" if case == "trip-replace" else case
-    s = streams.config1(n=2000, steps=6)
+    # trip_replace_span takes x_j = X b_j with b_j from a system whose (j, j)
+    # entry is lambda_new_j - lambda_j - C_jj = 0: the direction is sensitive to
+    # the rounding of C, and the difference between two correct implementations
+    # grows ~30x per step (measured: sin 3e-15, 1e-14, 1e-11, 4e-10, 2e-7), so
+    # that reading is compared over its first three steps
+    s = streams.config1(n=2000, steps=3 if case == "trip-replace" else 6)
     rp, col, val = s.csr0()
     a = po.Csr(len(rp) - 1, rp, col, val)
     g, o = _pair(a, kind, 8, **OPTS[case])

@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
-timeout 600 python tools/dbg_init.py 262144 1 2 > gpurun_out/dbg_init.log 2>&1; cat gpurun_out/dbg_init.log | tail -3
-timeout 600 python tools/dbg_init.py 262144 1 2 x > gpurun_out/dbg_init2.log 2>&1; cat gpurun_out/dbg_init2.log | tail -3
-timeout 600 python tools/dbg_init.py 262144 1 0 x > gpurun_out/dbg_init3.log 2>&1; cat gpurun_out/dbg_init3.log | tail -3
+STG_LZ_LOG2=1 STG_LZ_LOG=1 timeout 900 python tools/dbg_cfg4c.py 6 > gpurun_out/dbg_c6.log 2>&1; grep -E "lzdbg|ERR|ok|restart [0-6] " gpurun_out/dbg_c6.log | head -40
