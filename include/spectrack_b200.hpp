@@ -7,9 +7,16 @@
 //       -> EditLists (the same four arguments, validated on the device with
 //          the reference's rules and messages)
 //   tracker_init(a0, kind, opts)                           trackers.hpp:92
-//       -> GpuTracker(a0, kind, opts, op, initial)  (X0, Lambda0 are an input:
-//          the north-star API takes the initial eigenpairs)
+//       -> tracker_init(a0, kind, opts, op): thick-restart Lanczos on the
+//          device (lanczos.hpp:38-127); or GpuTracker(a0, kind, opts, op,
+//          initial) when the caller already holds X0, Lambda0
 //   tracker_step(state, GraphUpdate)                       trackers.hpp:132-133
+//       -> tracker_step(tracker, GraphUpdate) (blocks K, G, C) or
+//          tracker_step(tracker, EditLists)
+//   tracker_step(state, Perturbation)                      trackers.hpp:130-131
+//       -> tracker_step(tracker, Perturbation) (adjacency lanes)
+//   principal_angle / subspace_largest_angle               metrics.hpp
+//       -> GpuTracker::angles (on the device)
 //   apply_update(A, d)                                     graph.hpp:74
 //   ShiftedLaplacianSession::advance(d)                    laplacian_track.hpp:34
 //       -> tracker_step(tracker, edits): one call performs all three on the
@@ -35,7 +42,16 @@ namespace spectrack_b200 {
 
 using Index = std::int64_t;
 
-enum class TrackerKind { iasc = ST_IASC, grest2 = ST_GREST2, grest3 = ST_GREST3, grest_rsvd = ST_GREST_RSVD };
+enum class TrackerKind {
+  trip_basic = ST_TRIP_BASIC,
+  trip = ST_TRIP,
+  residual_modes = ST_RESIDUAL_MODES,
+  iasc = ST_IASC,
+  grest2 = ST_GREST2,
+  grest3 = ST_GREST3,
+  grest_rsvd = ST_GREST_RSVD,
+  timers = ST_TIMERS
+};
 enum class BasisKind { iasc = 0, grest2 = 1, grest3 = 2, grest_rsvd = 3 };
 enum class SpectralOrder { abs_desc = ST_ABS_DESC, alg_desc = ST_ALG_DESC };
 enum class OperatorKind {
@@ -44,13 +60,25 @@ enum class OperatorKind {
   normalized_laplacian = ST_NORMALIZED_LAPLACIAN
 };
 
-// TrackerOptions (trackers.hpp:52-63), G-REST fields.
+// TrackerOptions (trackers.hpp:52-63).
 struct TrackerOptions {
   Index k = 8;
   SpectralOrder order = SpectralOrder::abs_desc;
+  double mu = 0.0;
+  bool trip_replace_span = false;
   Index rsvd_l = 100;
   Index rsvd_p = 100;
+  double theta = 0.01;
+  Index min_restart_gap = 5;
+  TrackerKind restart_inner = TrackerKind::iasc;
   std::uint64_t seed = 0;
+};
+
+// LanczosOptions (lanczos.hpp:29-36) beyond k / order / seed.
+struct LanczosOptions {
+  double tol = 1e-10;
+  Index max_basis = 0;
+  Index max_restarts = 500;
 };
 
 // Symmetric CSR in the layout of SymSparseMatrix (sparse.hpp:18, 46-48).
@@ -70,6 +98,24 @@ struct SpectralEmbedding {
   Index k() const { return static_cast<Index>(values.size()); }
 };
 
+// GraphUpdate (graph.hpp:23-37): the blocks K (n_old^2), G (n_old x n_new),
+// C (n_new^2) of the step's perturbation, each a CSR.
+struct BlockCsr {
+  Index rows = 0, cols = 0;
+  std::vector<std::int32_t> row_offsets{0};
+  std::vector<std::int32_t> col_indices;
+  std::vector<double> values;
+};
+struct GraphUpdate {
+  Index n_old = 0, n_new = 0;
+  BlockCsr k_block, g_block, c_block;
+};
+// Perturbation (trackers.hpp:78-86): delta is (n_old + n_new) square.
+struct Perturbation {
+  Index n_old = 0, n_new = 0;
+  BlockCsr delta;
+};
+
 // The arguments of assemble_update (graph.cpp:45-100).
 struct EditLists {
   std::vector<std::tuple<Index, Index, double>> added_edges;
@@ -79,6 +125,27 @@ struct EditLists {
 };
 
 namespace detail {
+inline st_csr_block block_of(const BlockCsr& b) {
+  return st_csr_block{b.rows, b.cols, static_cast<std::int64_t>(b.values.size()), b.row_offsets.data(),
+                      b.col_indices.data(), b.values.data()};
+}
+inline st_config config_of(TrackerKind kind, const TrackerOptions& opts, OperatorKind op, int device, int flags) {
+  st_config cfg{};
+  cfg.kind = static_cast<std::int32_t>(kind);
+  cfg.op = static_cast<std::int32_t>(op);
+  cfg.k = opts.k;
+  cfg.order = static_cast<std::int32_t>(opts.order);
+  cfg.rsvd_l = opts.rsvd_l;
+  cfg.rsvd_p = opts.rsvd_p;
+  cfg.seed = opts.seed;
+  cfg.device = device;
+  cfg.flags = flags;
+  return cfg;
+}
+inline st_tracker_options tracker_options_of(const TrackerOptions& o) {
+  return st_tracker_options{o.mu, o.trip_replace_span ? 1 : 0, o.theta, o.min_restart_gap,
+                            static_cast<std::int32_t>(o.restart_inner)};
+}
 // The message is fetched after the call returns (st_last_error's buffer is
 // rewritten by every failing call).
 inline void rethrow(st_status s, const st_session* session) {
@@ -137,21 +204,27 @@ class GpuTracker {
  public:
   GpuTracker(const Csr& a0, TrackerKind kind, const TrackerOptions& opts, OperatorKind op,
              const SpectralEmbedding& initial, int device = 0, int flags = 0) {
-    st_config cfg{};
-    cfg.kind = static_cast<std::int32_t>(kind);
-    cfg.op = static_cast<std::int32_t>(op);
-    cfg.k = opts.k;
-    cfg.order = static_cast<std::int32_t>(opts.order);
-    cfg.rsvd_l = opts.rsvd_l;
-    cfg.rsvd_p = opts.rsvd_p;
-    cfg.seed = opts.seed;
-    cfg.device = device;
-    cfg.flags = flags;
+    const st_config cfg = detail::config_of(kind, opts, op, device, flags);
     if (initial.k() != opts.k || initial.n != a0.n || static_cast<Index>(initial.vectors.size()) != a0.n * opts.k)
       throw std::invalid_argument("tracker_init: initial embedding does not match n x k");
     detail::rethrow(st_create(&cfg, a0.n, a0.row_offsets.data(), a0.col_indices.data(), a0.values.data(),
                               initial.values.data(), initial.vectors.data(), a0.n, &s_),
                     nullptr);
+    set_options(opts);
+  }
+  // tracker_init (trackers.cpp:132-145): Lanczos on the device
+  GpuTracker(const Csr& a0, TrackerKind kind, const TrackerOptions& opts, OperatorKind op,
+             const LanczosOptions& lz, int device = 0, int flags = 0) {
+    const st_config cfg = detail::config_of(kind, opts, op, device, flags);
+    const st_lanczos_options lo{lz.tol, lz.max_basis, lz.max_restarts};
+    detail::rethrow(st_tracker_init(&cfg, &lo, a0.n, a0.row_offsets.data(), a0.col_indices.data(), a0.values.data(),
+                                    &s_),
+                    nullptr);
+    set_options(opts);
+  }
+  void set_options(const TrackerOptions& opts) {
+    const st_tracker_options to = detail::tracker_options_of(opts);
+    detail::rethrow(st_set_tracker_options(s_, &to), s_);
   }
   GpuTracker(const GpuTracker&) = delete;
   GpuTracker& operator=(const GpuTracker&) = delete;
@@ -164,6 +237,27 @@ class GpuTracker {
   void step(const EditLists& edits) {
     detail::PackedUpdate pu(edits);
     detail::rethrow(st_step(s_, &pu.u), s_);
+  }
+
+  // tracker_step(state, GraphUpdate) with apply_update (graph.cpp:17-32, 102-115)
+  void step(const GraphUpdate& d) {
+    st_graph_update g{d.n_old, d.n_new, detail::block_of(d.k_block), detail::block_of(d.g_block),
+                      detail::block_of(d.c_block)};
+    detail::rethrow(st_step_blocks(s_, &g), s_);
+  }
+  // tracker_step(state, Perturbation) (trackers.cpp:341-382); A += delta
+  void step(const Perturbation& p) {
+    const st_csr_block b = detail::block_of(p.delta);
+    detail::rethrow(st_step_perturbation(s_, p.n_old, p.n_new, &b), s_);
+  }
+  // principal_angle per vector and subspace_largest_angle against reference
+  // vectors (column-major n x k), on the device (metrics.cpp:17-27, 243-259)
+  std::pair<std::vector<double>, double> angles(const std::vector<double>& ref) const {
+    const Info in = info();
+    std::vector<double> psi(static_cast<size_t>(in.k));
+    double big = 0.0;
+    detail::rethrow(st_angles(s_, ref.data(), in.n, psi.data(), &big), s_);
+    return {psi, big};
   }
 
   Index n() const { return info().n; }
@@ -244,9 +338,23 @@ class GpuTracker {
   st_session* s_ = nullptr;
 };
 
-// tracker_step (trackers.hpp:132-133) in the reference's call shape.
+// tracker_init (trackers.hpp:92) in the reference's call shape.
+inline GpuTracker tracker_init(const Csr& a0, TrackerKind kind, const TrackerOptions& opts,
+                               OperatorKind op = OperatorKind::adjacency, int device = 0) {
+  return GpuTracker(a0, kind, opts, op, LanczosOptions{}, device);
+}
+
+// tracker_step (trackers.hpp:130-133) in the reference's call shapes.
 inline GpuTracker& tracker_step(GpuTracker& t, const EditLists& edits) {
   t.step(edits);
+  return t;
+}
+inline GpuTracker& tracker_step(GpuTracker& t, const GraphUpdate& d) {
+  t.step(d);
+  return t;
+}
+inline GpuTracker& tracker_step(GpuTracker& t, const Perturbation& p) {
+  t.step(p);
   return t;
 }
 

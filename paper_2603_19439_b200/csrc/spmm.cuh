@@ -40,8 +40,9 @@ struct SpmmArgs {
 // sums, which spmm_fixup_kernel adds in segment order (deterministic; the
 // association differs from Eigen's only within those rows, at rounding level).
 constexpr int kSegNnz = 32;    // rows up to this length: the row-group kernels
-constexpr int kLongSeg = 512;  // longer rows: one warp per 512-entry segment (most
-                               // Delta hub rows are a single segment: no fix-up)
+constexpr int kLongSeg = 32;   // longer rows: one warp per 32-entry segment, partials
+                               // summed by the fix-up (512-entry segments made one
+                               // warp walk a hub row serially: 2x slower at config 3)
 
 struct SpmmPlan {
   const int* vrow;        // virtual row (segment) -> row
@@ -484,7 +485,11 @@ inline void spmm_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 spl
                         cudaStream_t st) {
   const bool vec2 = a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 && a.m <= 256 &&
                     ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y)) & 15) == 0;
-  if (vec2 && !getenv_flag("STG_SPMM_GROUP")) {  // rows of at most kSegNnz nonzeros, all columns per warp
+  // all-column warps for the wide sketch operands (m > 128: 0.245 -> 0.209 ms per
+  // step at config 3); the column-slab kernel, which keeps a group's X rows in
+  // flight through shared memory, for the narrower ones
+  static const bool rows_kernel = !getenv_flag("STG_SPMM_SLABS");  // development A/B
+  if (vec2 && rows_kernel && a.m > 128) {
     const i64 ng = cdiv(a.rows, kGroupRows);
     const unsigned grid = static_cast<unsigned>(std::min<i64>(cdiv(ng, 8), 148 * 16));
     switch (static_cast<int>(cdiv(a.m, 64))) {

@@ -98,6 +98,44 @@ int main() {
   // sym_eig_dense on diag(3, 1, 2) (test_linalg.cpp:30-39)
   auto [w, v] = sym_eig_dense({3, 0, 0, 0, 1, 0, 0, 0, 2}, 3, SpectralOrder::abs_desc, 3);
   CHECK(std::fabs(w[0] - 3) < 1e-14 && std::fabs(w[1] - 2) < 1e-14 && std::fabs(w[2] - 1) < 1e-14);
+  // tracker_init on the device (trackers.cpp:132-145): K3 has eigenvalues 2, -1, -1
+  {
+    const Csr k3 = from_edges(3, {{0, 1}, {1, 2}, {0, 2}});
+    TrackerOptions o3;
+    o3.k = 1;
+    GpuTracker ti = tracker_init(k3, TrackerKind::grest2, o3);
+    const SpectralEmbedding e3 = ti.embedding();
+    CHECK(std::fabs(e3.values[0] - 2.0) < 1e-12);
+  }
+  // the same Fig. 1 update as GraphUpdate blocks (graph.hpp:23-37): identical CSR
+  {
+    GpuTracker tb(a0, TrackerKind::grest2, opts, OperatorKind::adjacency, x0);
+    GraphUpdate g;
+    g.n_old = 6;
+    g.n_new = 2;
+    auto block = [](Index rows, Index cols, std::vector<std::tuple<Index, Index, double>> e) {
+      std::sort(e.begin(), e.end());
+      BlockCsr b;
+      b.rows = rows;
+      b.cols = cols;
+      b.row_offsets.assign(static_cast<size_t>(rows + 1), 0);
+      for (auto& [i, j, w] : e) {
+        b.col_indices.push_back(static_cast<std::int32_t>(j));
+        b.values.push_back(w);
+        ++b.row_offsets[static_cast<size_t>(i + 1)];
+      }
+      for (Index r = 0; r < rows; ++r) b.row_offsets[static_cast<size_t>(r + 1)] += b.row_offsets[static_cast<size_t>(r)];
+      return b;
+    };
+    g.k_block = block(6, 6, {{0, 2, 1.0}, {2, 0, 1.0}, {2, 4, 1.0}, {4, 2, 1.0}, {1, 4, -1.0}, {4, 1, -1.0}});
+    g.g_block = block(6, 2, {{2, 0, 1.0}, {3, 0, 1.0}, {3, 1, 1.0}, {4, 1, 1.0}});
+    g.c_block = block(2, 2, {});
+    tracker_step(tb, g);
+    const Csr b1 = tb.csr(0);
+    CHECK(b1.row_offsets == a1.row_offsets && b1.col_indices == a1.col_indices && b1.values == a1.values);
+    const SpectralEmbedding eb = tb.embedding();
+    CHECK(eb.values == e.values && eb.vectors == e.vectors);
+  }
   std::printf(failures ? "shim_smoke: %d failures\n" : "shim_smoke: ok\n", failures);
   return failures ? 1 : 0;
 }
