@@ -26,8 +26,9 @@ s = streams.config3(scale=args.scale, steps=args.warmup + args.steps)
 rp, col, val = s.csr0()
 n = len(rp) - 1
 if args.real_x0:
-    from paper_2603_19439_b200 import init_eig  # noqa: E402
-    vals, x = init_eig.leading_eigenpairs(rp, col, val, args.k, "abs_desc", device="cuda:0")
+    g0 = TrackerSession.tracker_init(rp, col, val, args.k, kind="grest-rsvd", seed=0)  # device Lanczos
+    vals, x = g0.embedding()
+    g0.close()
 else:
     x, _ = np.linalg.qr(np.random.default_rng(0).standard_normal((n, args.k)))
     vals = np.linspace(100.0, 10.0, args.k)
