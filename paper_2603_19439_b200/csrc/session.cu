@@ -1426,6 +1426,8 @@ class Session {
   };
   std::vector<PlanEntry> plans_;
   int plan_epoch_ = 0;
+  const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
+  const int spmm_fused_min_m_ = getenv("STG_SPMM_FUSED_MIN_M") ? atoi(getenv("STG_SPMM_FUSED_MIN_M")) : 129;
   const int merge_mode_ = getenv("STG_MERGE_MODE") ? atoi(getenv("STG_MERGE_MODE")) : 3;  // development A/B
 
   PlanEntry& spmm_plan(const SpmmArgs& a, i64 nnz) {
@@ -1460,7 +1462,9 @@ class Session {
     STG_CUDA(cudaMemsetAsync(nsplit, 0, sizeof(int), st_));
     launch(seg_fill_kernel, dim3(blocks(a.rows)), dim3(256), 0, st_, static_cast<const int*>(vstart), a.rows, vrow,
            split_rows, nsplit);
-    e->pl = SpmmPlan{vrow, vstart, sstart, split_rows, nsplit, nullptr, 0};
+    int* segcnt = arena_.get<int>(e->tag + "segcnt", e->smax);
+    STG_CUDA(cudaMemsetAsync(segcnt, 0, sizeof(int) * e->smax, st_));  // the fused kernel's arrival counters
+    e->pl = SpmmPlan{vrow, vstart, sstart, split_rows, nsplit, nullptr, 0, segcnt};
     return *e;
   }
 
@@ -1492,8 +1496,13 @@ class Session {
       b.Y = a.Y + c0;
       b.m = std::min(a.m - c0, 256);
       const bool long_rows = nnz > kSegNnz;
-      spmm_launch(b, pl, pe.vmax, pe.split_max, long_rows, st_);
-      launches += 1 + (long_rows ? 1 : 0) + (pe.split_max > 0 ? 1 : 0);
+      if (spmm_fused_ && b.m >= spmm_fused_min_m_) {  // one launch: segments, their ordered fix-up and the row groups
+        spmm_fused_launch(b, pl, long_rows ? pe.vmax : 0, st_);
+        launches += 1;
+      } else {
+        spmm_launch(b, pl, pe.vmax, pe.split_max, long_rows, st_);
+        launches += 1 + (long_rows ? 1 : 0) + (pe.split_max > 0 ? 1 : 0);
+      }
     }
     kend();
     if (tscratch) STG_CUDA(cudaFreeAsync(tscratch, st_));

@@ -52,6 +52,7 @@ struct SpmmPlan {
   const int* nsplit;
   double* scratch;        // [slot][lds]
   int lds;
+  int* segcnt;            // per long row (at its first scratch slot): segments arrived (fused kernel)
 };
 
 template <int T>  // columns per lane = T (m <= 32 T)
@@ -434,6 +435,234 @@ __global__ void __launch_bounds__(256, 2) spmm_rows_kernel(SpmmArgs a, i64 ngrou
   }
 }
 
+// ONE launch per product: long-row segments and short-row groups in the same
+// persistent grid, the segment fix-up folded in. Lane l owns VW consecutive
+// columns of every (32 VW)-column slab t < T (VW = 2: 128-bit loads/stores;
+// VW = 1: 8-byte loads, so a 32-column block keeps all 32 lanes busy). Work
+// items: first the long-row segments (one warp per kLongSeg entries; each
+// writes its partial row to the scratch slot of the segment, then bumps the
+// row's arrival counter; the warp that arrives last adds the row's partials in
+// segment order (fixed order: deterministic) and writes Y, then resets the
+// counter), then the groups of kGroupRows consecutive rows, whose rows of at
+// most kSegNnz entries are summed in column order with separate multiply and
+// add roundings (as spmm_kernel). U entries have their T loads in flight
+// together; each warp prefetches the next group's row pointers.
+template <int VW>
+struct SpV;
+template <>
+struct SpV<1> {
+  using T = double;
+  static __device__ __forceinline__ double zero() { return 0.0; }
+  static __device__ __forceinline__ double ld(const double* p) { return __ldg(p); }
+  static __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+  static __device__ __forceinline__ void st(double* p, double v) { *p = v; }
+  static __device__ __forceinline__ void fma(double& acc, double v, double x) { acc = __dadd_rn(acc, __dmul_rn(v, x)); }
+  static __device__ __forceinline__ void add(double& acc, double x) { acc = __dadd_rn(acc, x); }
+};
+template <>
+struct SpV<2> {
+  using T = double2;
+  static __device__ __forceinline__ double2 zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ double2 ld(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+  static __device__ __forceinline__ double2 ldcg(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+  static __device__ __forceinline__ void st(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+  static __device__ __forceinline__ void fma(double2& acc, double v, double2 x) {
+    acc.x = __dadd_rn(acc.x, __dmul_rn(v, x.x));
+    acc.y = __dadd_rn(acc.y, __dmul_rn(v, x.y));
+  }
+  static __device__ __forceinline__ void add(double2& acc, double2 x) {
+    acc.x = __dadd_rn(acc.x, x.x);
+    acc.y = __dadd_rn(acc.y, x.y);
+  }
+};
+
+constexpr int spmm_fused_minb(int vw, int t) { return vw * t <= 1 ? 2 : 2; }
+
+template <int VW, int T>
+__global__ void __launch_bounds__(256, spmm_fused_minb(VW, T)) spmm_fused_kernel(SpmmArgs a, SpmmPlan pl, i64 ngroups) {
+  using V = SpV<VW>;
+  using VT = typename V::T;
+  constexpr int SW = 32 * VW;
+  constexpr int U = VW * T >= 6 ? 2 : VW * T >= 3 ? 4 : VW * T == 2 ? 8 : 16;  // entries whose T loads are in flight together
+  const int lane = threadIdx.x & 31;
+  const i64 w0 = (static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  const int* rowp = a.rowptr + a.row_off;
+  bool on[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) on[t] = SW * t + VW * lane < a.m;
+  // gathers the rows of the active entries (bitmask over the 32-entry window
+  // held as c_l / v_l) in order, U at a time; a change of row(entry) stores
+  // the finished row through `flush`
+  auto gather = [&](unsigned act, int c_l, double v_l, int row_l, VT (&acc)[T], int& cur, auto&& flush) {
+    while (act) {
+      int jj[U], nb = 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        jj[u] = act ? __ffs(act) - 1 : 0;
+        if (act) {
+          act &= act - 1;
+          ++nb;
+        }
+      }
+      VT xv[U][T];
+      double vv[U];
+      int rw[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = __shfl_sync(0xffffffffu, c_l, jj[u]);
+        vv[u] = __shfl_sync(0xffffffffu, v_l, jj[u]);
+        rw[u] = __shfl_sync(0xffffffffu, row_l, jj[u]);
+        const double* xr = a.X + static_cast<i64>(c) * a.ldx + VW * lane;
+#pragma unroll
+        for (int t = 0; t < T; ++t) xv[u][t] = (u < nb && on[t]) ? V::ld(xr + SW * t) : V::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u >= nb) break;
+        if (rw[u] != cur) {
+          if (cur >= 0) flush(cur, acc);
+          cur = rw[u];
+#pragma unroll
+          for (int t = 0; t < T; ++t) acc[t] = V::zero();
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t) V::fma(acc[t], vv[u], xv[u][t]);
+      }
+    }
+  };
+  VT acc[T];
+  // ---- long-row segments (the rows of more than kSegNnz entries)
+  const i64 nseg = pl.vstart[a.rows];
+  i64 w = w0;
+  for (; w < nseg; w += nw) {
+    const int r = pl.vrow[w];
+    const int vs = pl.vstart[r];
+    const int s = static_cast<int>(w - vs);
+    const int nsg = pl.vstart[r + 1] - vs;
+    const int rs = rowp[r];
+    const int seg0 = rs + s * kLongSeg;
+    const int cnt = min(kLongSeg, rowp[r + 1] - seg0);
+    int c_l = 0;
+    double v_l = 0.0;
+    if (lane < cnt) {
+      c_l = __ldg(a.col + seg0 + lane);
+      v_l = __ldg(a.val + seg0 + lane);
+    }
+    const unsigned act = __ballot_sync(0xffffffffu, lane < cnt && c_l >= a.col_lo);
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[t] = V::zero();
+    int cur = -1;
+    gather(act, c_l, v_l, 0, acc, cur, [](int, const VT(&)[T]) {});
+    const int slot0 = pl.sstart[r];
+    double* part = pl.scratch + static_cast<i64>(slot0 + s) * pl.lds + VW * lane;
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+      if (on[t]) V::st(part + SW * t, acc[t]);
+    __threadfence();
+    int last = 0;
+    if (lane == 0) last = atomicAdd(pl.segcnt + slot0, 1) == nsg - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // every partial of row r is written: add them in segment order
+      __threadfence();
+      const double* p0 = pl.scratch + static_cast<i64>(slot0) * pl.lds + VW * lane;
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[t] = V::zero();
+      int q = 0;
+      for (; q + 4 <= nsg; q += 4) {
+        VT tv[4][T];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int t = 0; t < T; ++t) tv[u][t] = on[t] ? V::ldcg(p0 + static_cast<i64>(q + u) * pl.lds + SW * t) : V::zero();
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int t = 0; t < T; ++t) V::add(acc[t], tv[u][t]);
+      }
+      for (; q < nsg; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          if (on[t]) V::add(acc[t], V::ldcg(p0 + static_cast<i64>(q) * pl.lds + SW * t));
+      double* yr = a.Y + static_cast<i64>(r) * a.ldy + VW * lane;
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        if (on[t]) V::st(yr + SW * t, acc[t]);
+      if (lane == 0) pl.segcnt[slot0] = 0;  // ready for the next product over this plan
+    }
+  }
+  // ---- groups of kGroupRows consecutive rows (long rows skipped)
+  auto header = [&](i64 g, int& rp_l, int& nr) {
+    const i64 r0 = g * kGroupRows;
+    nr = static_cast<int>(min(static_cast<i64>(kGroupRows), a.rows - r0));
+    rp_l = (g < ngroups && lane <= nr) ? __ldg(rowp + r0 + lane) : 0;
+  };
+  i64 g = w - nseg;
+  int rp_n = 0, nr_n = 0;
+  if (g < ngroups) header(g, rp_n, nr_n);
+  for (; g < ngroups; g += nw) {
+    const int rp_l = rp_n, nr = nr_n;
+    if (g + nw < ngroups) header(g + nw, rp_n, nr_n);  // next group's row pointers in flight
+    const i64 r0 = g * kGroupRows;
+    const int rp_next = __shfl_down_sync(0xffffffffu, rp_l, 1);
+    double* Yg = a.Y + r0 * static_cast<i64>(a.ldy) + VW * lane;
+    auto store = [&](int r, const VT(&ac)[T]) {
+      double* yr = Yg + static_cast<i64>(r) * a.ldy;
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        if (on[t]) V::st(yr + SW * t, ac[t]);
+    };
+    const int e_l = lane < nr ? rp_next : 0;  // end of row `lane` of the group
+    int ri = 0;
+    while (ri < nr) {
+      const int wb = __shfl_sync(0xffffffffu, rp_l, ri);
+      const unsigned fm = __ballot_sync(0xffffffffu, lane >= ri && lane < nr && e_l <= wb + 32);
+      if (!(fm & (1u << ri))) {  // row ri is long: the segment items have it
+        ++ri;
+        continue;
+      }
+      const int last = __ffs(~(fm >> ri)) - 1 + ri - 1;  // end of the contiguous run of fitting rows
+      const int we = __shfl_sync(0xffffffffu, e_l, last);
+      int c_l = 0;
+      double v_l = 0.0;
+      if (wb + lane < we) {
+        c_l = __ldg(a.col + wb + lane);
+        v_l = __ldg(a.val + wb + lane);
+      }
+      int row_l = -1;  // row (within the group) of entry `lane`
+#pragma unroll
+      for (int i = 0; i < kGroupRows; ++i) {
+        const int rs = __shfl_sync(0xffffffffu, rp_l, i);
+        row_l += (i < nr && wb + lane >= rs) ? 1 : 0;
+      }
+      const unsigned act = __ballot_sync(0xffffffffu, lane < we - wb && c_l >= a.col_lo);
+      {  // rows ri..last with no active entry are zero rows
+        const bool mine = lane >= ri && lane <= last;
+        bool has = false;
+        if (mine) {
+          const int s = rp_l - wb, e = e_l - wb;
+          const unsigned hi = e >= 32 ? 0xffffffffu : ((1u << e) - 1u);
+          const unsigned lo = s >= 32 ? 0xffffffffu : ((1u << s) - 1u);
+          has = (act & hi & ~lo) != 0;
+        }
+        unsigned empty = __ballot_sync(0xffffffffu, mine && !has);
+        VT z[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) z[t] = V::zero();
+        while (empty) {
+          const int r = __ffs(empty) - 1;
+          empty &= empty - 1;
+          store(r, z);
+        }
+      }
+      int cur = -1;
+      gather(act, c_l, v_l, row_l, acc, cur, store);
+      if (cur >= 0) store(cur, acc);
+      ri = last + 1;
+    }
+  }
+}
+
 // Rows of several segments: partial sums added in segment order.
 __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl) {
   const int i = static_cast<int>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -455,6 +684,41 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl
     for (; s < nseg; ++s) y = __dadd_rn(y, p0[static_cast<i64>(s) * pl.lds + cc]);
     a.Y[static_cast<i64>(r) * a.ldy + cc] = y;
   }
+}
+
+template <int VW, int T>
+inline void spmm_fused_go(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 ngroups, cudaStream_t st) {
+  const i64 items = vmax + ngroups;  // vmax: upper bound of the long-row segments
+  const unsigned grid = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(cdiv(items, 8), 148 * spmm_fused_minb(VW, T))));
+  spmm_fused_kernel<VW, T><<<grid, 256, 0, st>>>(a, pl, ngroups);
+}
+
+// One launch: VW = 2 (128-bit) when the operands allow it and m > 32.
+inline void spmm_fused_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, cudaStream_t st) {
+  const i64 ng = cdiv(a.rows, kGroupRows);
+  const bool vec2 = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 && pl.lds % 2 == 0 &&
+                    ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y) |
+                      reinterpret_cast<uintptr_t>(pl.scratch)) & 15) == 0;
+  if (vec2) {
+    switch (static_cast<int>(cdiv(a.m, 64))) {
+      case 1: spmm_fused_go<2, 1>(a, pl, vmax, ng, st); break;
+      case 2: spmm_fused_go<2, 2>(a, pl, vmax, ng, st); break;
+      case 3: spmm_fused_go<2, 3>(a, pl, vmax, ng, st); break;
+      default: spmm_fused_go<2, 4>(a, pl, vmax, ng, st); break;
+    }
+  } else {
+    switch (static_cast<int>(cdiv(a.m, 32))) {
+      case 1: spmm_fused_go<1, 1>(a, pl, vmax, ng, st); break;
+      case 2: spmm_fused_go<1, 2>(a, pl, vmax, ng, st); break;
+      case 3: spmm_fused_go<1, 3>(a, pl, vmax, ng, st); break;
+      case 4: spmm_fused_go<1, 4>(a, pl, vmax, ng, st); break;
+      case 5: spmm_fused_go<1, 5>(a, pl, vmax, ng, st); break;
+      case 6: spmm_fused_go<1, 6>(a, pl, vmax, ng, st); break;
+      case 7: spmm_fused_go<1, 7>(a, pl, vmax, ng, st); break;
+      default: spmm_fused_go<1, 8>(a, pl, vmax, ng, st); break;
+    }
+  }
+  STG_LAUNCH();
 }
 
 // ---- segment plan of a CSR row range (built once per perturbation)
