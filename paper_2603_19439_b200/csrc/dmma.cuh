@@ -358,6 +358,49 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* partial,
   if (sym && i != j) out[static_cast<i64>(j) * ldo + i] = alpha * s;
 }
 
+// Split reduction with the splits cut into CH consecutive chunks: warp c of a
+// CTA sums chunk c of 32 consecutive output elements (lane = element, so each
+// split's partial row is read coalesced) in split order with 8 loads in
+// flight, then warp 0 adds the CH chunk sums in chunk order. The association
+// is fixed by (splits, CH): deterministic. The latency chain per element is
+// splits / CH loads instead of splits. sym as gram_reduce_kernel.
+__global__ void __launch_bounds__(1024) gram_reduce_chunked_kernel(const double* partial, int splits, int m1, int m2,
+                                                                   int m1p, int m2p, int sym, double* out, int ldo,
+                                                                   double alpha) {
+  __shared__ double red[32][33];
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5, CH = blockDim.x >> 5;
+  const i64 idx = static_cast<i64>(blockIdx.x) * 32 + lane;
+  const bool live = idx < static_cast<i64>(m1) * m2;
+  const int i = live ? static_cast<int>(idx / m2) : 0, j = live ? static_cast<int>(idx % m2) : 0;
+  const bool act = live && !(sym && j < i);
+  double s = 0.0;
+  if (act) {
+    const i64 stride = static_cast<i64>(m1p) * m2p;
+    const int s0 = static_cast<int>(static_cast<i64>(splits) * c / CH);
+    const int s1 = static_cast<int>(static_cast<i64>(splits) * (c + 1) / CH);
+    const double* src = partial + static_cast<i64>(i) * m2p + j;
+    int sp = s0;
+    for (; sp + 8 <= s1; sp += 8) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = __ldcs(src + (sp + u) * stride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += t[u];
+    }
+    for (; sp < s1; ++sp) s += __ldcs(src + sp * stride);
+  }
+  red[c][lane] = s;
+  __syncthreads();
+  if (c != 0 || !act) return;
+  double tot = red[0][lane];
+  for (int q = 1; q < CH; ++q) tot += red[q][lane];
+  out[static_cast<i64>(i) * ldo + j] = alpha * tot;
+  if (sym && i != j) out[static_cast<i64>(j) * ldo + i] = alpha * tot;
+}
+
+// chunk count: ~12 splits per chunk, at most 32 warps
+inline int gram_reduce_chunks(i64 splits) { return static_cast<int>(std::max<i64>(1, std::min<i64>(32, splits / 12))); }
+
 // (previous layout, one warp per output element, kept for A/B) lane l sums
 // splits l, l+32, ... in order, then a fixed butterfly combines the lanes. For
 // sym the (min, max) element is read so the result is exactly symmetric.

@@ -1270,8 +1270,7 @@ class Session {
       a.partial = arena_.get<double>("gram_partial", static_cast<i64>(G) * 1024);
       launch(dm::gram_stream_kernel, dim3(static_cast<unsigned>(G)), dim3(dm::NT), dm::gram_stream_smem(same), st_,
              a, ma, mb, same ? 1 : 0, ntl);
-      launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
-             static_cast<const double*>(a.partial), G, m1, m2, 32, 32, a.sym, out, ldo, alpha);
+      gram_reduce(a.partial, G, m1, m2, 32, 32, a.sym, out, ldo, alpha);
       kend();
       return;
     }
@@ -1293,10 +1292,24 @@ class Session {
       launch(dm::gram_tn_kernel<4, 1>, grid, dim3(dm::NT), dm::gram_smem(4, 1), st_, a);
     else
       launch(dm::gram_tn_kernel<2, 2>, grid, dim3(dm::NT), dm::gram_smem(2, 2), st_, a);
-    launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_,
-           static_cast<const double*>(a.partial), static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
-           static_cast<int>(m2p), a.sym, out, ldo, alpha);
+    gram_reduce(a.partial, splits, m1, m2, m1p, m2p, a.sym, out, ldo, alpha);
     kend();
+  }
+
+  // deterministic split-K reduction of the Gram partials (chunked: the splits
+  // cut into consecutive chunks summed by separate warps, then in chunk order)
+  void gram_reduce(const double* partial, i64 splits, int m1, int m2, i64 m1p, i64 m2p, int sym, double* out, int ldo,
+                   double alpha) {
+    static const bool old = getenv_flag("STG_GRAM_REDUCE_OLD");  // development A/B
+    if (old) {
+      launch(dm::gram_reduce_kernel, dim3(blocks(static_cast<i64>(m1) * m2)), dim3(256), 0, st_, partial,
+             static_cast<int>(splits), m1, m2, static_cast<int>(m1p), static_cast<int>(m2p), sym, out, ldo, alpha);
+      return;
+    }
+    const int ch = dm::gram_reduce_chunks(splits);
+    launch(dm::gram_reduce_chunked_kernel, dim3(static_cast<unsigned>(cdiv(static_cast<i64>(m1) * m2, 32))),
+           dim3(32 * ch), 0, st_, partial, static_cast<int>(splits), m1, m2, static_cast<int>(m1p),
+           static_cast<int>(m2p), sym, out, ldo, alpha);
   }
 
   // Gram over rows partitioned across the ranks of a sharded session: local
