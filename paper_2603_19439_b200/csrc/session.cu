@@ -396,7 +396,10 @@ class Session {
       STG_CUDA(cudaStreamCreateWithPriority(&st_, cudaStreamNonBlocking, (lo + hi) / 2));
       STG_CUDA(cudaStreamCreateWithPriority(&st_eig_, cudaStreamNonBlocking, hi));
       STG_CUDA(cudaStreamCreateWithPriority(&st_mg_, cudaStreamNonBlocking, lo));
+      STG_CUDA(cudaStreamCreateWithPriority(&st_rot_, cudaStreamNonBlocking, (lo + hi) / 2));
     }
+    STG_CUDA(cudaEventCreateWithFlags(&ev_rot_ready_, cudaEventDisableTiming));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_rot_done_, cudaEventDisableTiming));
     STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
     arena_.init(cfg.device, st_, {st_eig_, st_mg_, st_rng_});
     STG_CUDA(cudaEventCreateWithFlags(&ev_rng_, cudaEventDisableTiming));
@@ -490,6 +493,7 @@ class Session {
   }
 
   ~Session() {
+    cudaStreamSynchronize(st_rot_);
     cudaStreamSynchronize(st_);
     cudaStreamSynchronize(st_rng_);
     cudaStreamSynchronize(st_eig_);
@@ -510,7 +514,18 @@ class Session {
     cudaEventDestroy(ev_mg_fork_);
     cudaEventDestroy(ev_mg_);
     cudaStreamDestroy(st_mg_);
+    cudaEventDestroy(ev_rot_ready_);
+    cudaEventDestroy(ev_rot_done_);
+    cudaStreamDestroy(st_rot_);
     cudaStreamDestroy(st_);
+  }
+
+  // The last step's rotation of X (rows outside P) runs on st_rot_ so the next
+  // step's ingestion overlaps it; every later use of X orders after it here.
+  void wait_rotation() {
+    if (!rot_pending_) return;
+    STG_CUDA(cudaStreamWaitEvent(st_, ev_rot_done_, 0));
+    rot_pending_ = false;
   }
 
   bool is_laplacian() const { return cfg.op == ST_LAPLACIAN || cfg.op == ST_NORMALIZED_LAPLACIAN; }
@@ -651,6 +666,7 @@ class Session {
           throw InvalidArgument("residual_modes_step: mu collides with tracked eigenvalue");
     }
     Pert pt = front();
+    wait_rotation();  // the previous step's rotation of X ran beside this ingestion
     timing_mark(0);
     // TIMERS proxy (trackers.cpp:317-320): ||Delta||_F / restart_scale accumulated
     double acc_next = acc_change_;
@@ -1031,6 +1047,10 @@ class Session {
   // reads them) runs beside the basis work; joined before the graph commits
   // and before the next ingest touches the spare slot or the Delta marks
   cudaStream_t st_mg_ = nullptr;
+  cudaStream_t st_rot_ = nullptr;  // the X rotation, overlapped with the next step's ingestion
+  cudaEvent_t ev_rot_ready_ = nullptr, ev_rot_done_ = nullptr;
+  bool rot_pending_ = false;
+  const bool rot_aside_ = !getenv_flag("STG_ROT_INLINE");  // development A/B
   cudaEvent_t ev_mg_fork_ = nullptr, ev_mg_ = nullptr;
   cudaEvent_t tev_[8];
   int tev_n_ = 0;
@@ -1191,6 +1211,7 @@ class Session {
   void ensure_node_capacity(i64 need, i64 need_x = -1) {
     if (need_x < 0) need_x = need;
     if (need_x > xcap_ || !X_) {
+      wait_rotation();  // X is copied and released below
       const i64 cap = std::max<i64>(need_x + need_x / 4, 1024);
       double* nx = static_cast<double*>(arena_.alloc(sizeof(double) * cap * ldx()));
       if (X_) {  // stream-ordered copy and free (no host or device-wide sync)
@@ -2395,8 +2416,13 @@ class Session {
   // With `Cpre` the block was already projected once outside (W = W0 - A Cpre,
   // Cpre = A'W0, a x w with leading dimension ldcpre): pass 1 starts at its
   // Gram, and the exact replica, if needed, rebuilds W0.
+  // defer_ri (no `against` only): the second pass's R^-1 is not applied; `out`
+  // receives Q1 (the first pass's output) and defer_ri the w x w upper-
+  // triangular factor, out_final = Q1 R^-1, for a caller whose every use of the
+  // block is linear from the right (last_ortho_deferred_ tells whether it was).
   int orthonormalize(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out, const double* Cpre = nullptr,
-                     int ldcpre = 0) {
+                     int ldcpre = 0, double* defer_ri = nullptr, int ld_defer = 0) {
+    last_ortho_deferred_ = false;
     if (w == 0) return 0;
     if (w > kCholMaxW) {  // wider than the one-CTA Cholesky: the exact column-by-column replica
       last_ortho_exact_ = true;
@@ -2456,9 +2482,18 @@ class Session {
     // pass 2 input Q1 = P1 R^-1: into `out` when it is re-projected into W1,
     // else straight into W1
     const bool proj = against && a > 0;
-    double* Q1 = proj ? out.p : W1;
-    const int ldq1 = proj ? out.ld : ldw;
+    const bool defer = defer_ri && !proj;
+    double* Q1 = proj || defer ? out.p : W1;
+    const int ldq1 = proj || defer ? out.ld : ldw;
     nn(P1, ldp1, N, w, Ri, ldw, w, Q1, ldq1, 1.0, 0.0, nullptr, 0, true);
+    if (defer) {  // pass 2's Gram and factor only: out = Q1, defer_ri = R^-1
+      pgram(out.p, out.ld, out.p, out.ld, G, w, w, true, Gm, ldw);
+      chol_inverse_near_identity(Gm, ldw, w, R, ldw, Ri, ldw);
+      STG_CUDA(cudaMemcpy2DAsync(defer_ri, sizeof(double) * ld_defer, Ri, sizeof(double) * ldw, sizeof(double) * w, w,
+                                 cudaMemcpyDeviceToDevice, st_));
+      last_ortho_deferred_ = true;
+      return w;
+    }
     // pass 2
     if (proj) {
       pgram(against->p, against->ld, out.p, out.ld, G, a, w, false, C, ldw);
@@ -2471,6 +2506,7 @@ class Session {
   }
 
   bool last_ortho_exact_ = false;  // the last orthonormalize took the column-by-column replica
+  bool last_ortho_deferred_ = false;  // ... and returned Q1 with the second pass's R^-1 unapplied
   // sketch basis projected against [X-bar, first candidate block] while the
   // sketch's eigensolve runs (rsvd_trailing / build_basis)
   const double* pre_pm_ = nullptr;
@@ -2682,9 +2718,23 @@ class Session {
     double* cy = arena_.get<double>("cy", static_cast<i64>(kk) * ldy);
     pgram(z.p, z.ld, Y, ldy, G, kk, q, false, cy, ldy);
     nn(z.p, z.ld, N, kk, cy, ldy, q, Y, ldy, -1.0, 1.0, Y, ldy);
-    // M = orthonormalize(Y)
+    // M = orthonormalize(Y). Every later use of M is linear from the right
+    // (bt_m = d2' M, the projection M - Z (Z'M), R = M U_keep), so CholQR2's
+    // last product Q1 R2^-1 over all N rows is not formed: M holds Q1 and
+    // R2^-1 (q x q, upper triangular) is folded into bt_m and U_keep.
     double* M = arena_.get<double>("Msk", N * ldy);
-    const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy});
+    double* r2i = arena_.get<double>("Msk_R2i", static_cast<i64>(q) * ldy);
+    static const bool no_fold = getenv_flag("STG_NO_SKETCH_FOLD");  // development A/B
+    const int qm = orthonormalize(Blk{Y, ldy}, q, nullptr, 0, N, G, Blk{M, ldy}, nullptr, 0, no_fold ? nullptr : r2i,
+                                  ldy);
+    const bool folded = last_ortho_deferred_;
+    // U_keep -> R2^-1 U_keep (the factor M = Q1 R2^-1 leaves on the right)
+    auto fold_u = [&](const double* Uk, int ldu_, int keep_) -> const double* {
+      if (!folded) return Uk;
+      double* ud = arena_.get<double>("Ukeep_f", static_cast<i64>(qm) * ldu_);
+      nn(r2i, ldy, qm, qm, Uk, ldu_, keep_, ud, ldu_, 1.0, 0.0, nullptr, 0);
+      return ud;
+    };
     if (qm == 0) {
       during_eig(static_cast<const double*>(nullptr), ldy, 0);
       return 0;
@@ -2704,6 +2754,7 @@ class Session {
       Msrc = Mp;
     }
     double* btm = arena_.get<double>("btm", std::max<i64>(pt.S_loc, 1) * ldy);
+    double* btm1 = folded ? arena_.get<double>("btm1", std::max<i64>(pt.S_loc, 1) * ldy) : btm;
     SpmmArgs sb{};
     sb.rows = pt.S_loc;
     sb.row_off = pt.p_old;
@@ -2712,9 +2763,11 @@ class Session {
     sb.val = pt.val;
     sb.X = halo(pt, Msrc, ldy, qm, &sb.ldx);
     sb.m = qm;
-    sb.Y = btm;
+    sb.Y = btm1;
     sb.ldy = ldy;
     do_spmm(sb, pt.nnz, p, kSpmmSketch);
+    if (folded)  // bt_m = (d2' Q1) R2^-1 over the S new rows only
+      nn(btm1, ldy, pt.S_loc, qm, r2i, ldy, qm, btm, ldy, 1.0, 0.0, nullptr, 0, true);
     // thin U of (M'B) = eigenvectors of bt_m' bt_m, singular values descending
     double* gb = arena_.get<double>("gb", static_cast<i64>(qm) * ldy);
     pgram(btm, ldy, btm, ldy, pt.S_loc, qm, qm, true, gb, ldy);
@@ -2737,14 +2790,15 @@ class Session {
       STG_CUDA(cudaStreamWaitEvent(st_, ev_eig_, 0));
       const int keep = wantu;
       if (keep == 0) return 0;
+      const double* Uf = fold_u(U, ldu, keep);
       if (pre_pm_) {
-        nn(pre_pm_, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+        nn(pre_pm_, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
         const int ldcp = ld_for(keep);
         pre_cr_ = arena_.get<double>("pm_CR", static_cast<i64>(pre_a_) * ldcp);
         pre_ldcr_ = ldcp;
-        nn(pre_c1_, ldy, pre_a_, qm, U, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
+        nn(pre_c1_, ldy, pre_a_, qm, Uf, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
       } else {
-        nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+        nn(M, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
       }
       return keep;
     }
@@ -2781,15 +2835,16 @@ class Session {
     if (keep == 0) return 0;
     // R = M U_keep; when the caller projected M against its basis meanwhile
     // (pre_pm_ = M - B C1), R's first projection is PM U_keep with
-    // coefficients C1 U_keep
+    // coefficients C1 U_keep (with the folded factor: U_keep -> R2^-1 U_keep)
+    const double* Uf = fold_u(U, ldu, keep);
     if (pre_pm_) {
-      nn(pre_pm_, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+      nn(pre_pm_, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
       const int ldcp = ld_for(keep);
       pre_cr_ = arena_.get<double>("pm_CR", static_cast<i64>(pre_a_) * ldcp);
       pre_ldcr_ = ldcp;
-      nn(pre_c1_, ldy, pre_a_, qm, U, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
+      nn(pre_c1_, ldy, pre_a_, qm, Uf, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
     } else {
-      nn(M, ldy, N, qm, U, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+      nn(M, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
     }
     return keep;
   }
@@ -2873,6 +2928,7 @@ class Session {
   } xrestore_;
 
   void restore_x() {
+    wait_rotation();
     if (!xrestore_.active) return;
     launch(restore_rows_kernel, dim3(blocks(xrestore_.p_old, 8)), dim3(256), 0, st_, X_, ldx(), xrestore_.P,
            xrestore_.p_old, xrestore_.z, xrestore_.ldz, static_cast<int>(k));
@@ -3089,11 +3145,26 @@ class Session {
     if (write_state) {
       // X <- X A_new on the rows outside P (in place, DMMA, single column tile),
       // then the rows of P take W's rows. Both are skipped if the step failed.
+      // compressed adjacency steps rotate on st_rot_ (the next step waits for
+      // it before its first use of X); the row positions of P are copied
+      // first, since the next ingestion rewrites them
+      const bool aside = rot_aside_ && !sh_ && !pt.dense && k <= 64 &&
+                         !(cfg.flags & (ST_FLAG_TIMING | ST_FLAG_KERNEL_TIMING));  // per-phase timings keep it inline
+      const int* ploc = pt.Ploc;
+      if (aside) {
+        int* rp = arena_.get<int>("rot_ploc", std::max<i64>(p, 1));
+        if (p > 0) STG_CUDA(cudaMemcpyAsync(rp, pt.Ploc, sizeof(int) * p, cudaMemcpyDeviceToDevice, st_));
+        ploc = rp;
+        wait_rotation();
+        STG_CUDA(cudaEventRecord(ev_rot_ready_, st_));
+        STG_CUDA(cudaStreamWaitEvent(st_rot_, ev_rot_ready_, 0));
+        std::swap(st_, st_rot_);  // the launches below go to the rotation stream
+      }
       kbegin(kRotate, 16.0 * k * pt.n_total + 8.0 * pt.n_total);
       if (!pt.dense && k <= 64)
         nn(X_, ldx(), pt.x_old, kk, W + (p + k) * ldk, ldk, kk, X_, ldx(), 1.0, 0.0, nullptr, 0, false, true);
       if (pt.dense || k <= 64)
-        launch(scatter_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, X_, ldx(), pt.Ploc, pt.dense ? 1 : 0, p,
+        launch(scatter_rows_kernel, dim3(blocks(p, 8)), dim3(256), 0, st_, X_, ldx(), ploc, pt.dense ? 1 : 0, p,
                static_cast<const double*>(W), ldk, kk, static_cast<const int*>(flags_ptr()),
                static_cast<const int*>(info_ptr()));
       else
@@ -3102,9 +3173,19 @@ class Session {
                static_cast<const double*>(W), ldk, static_cast<const double*>(W + (p + k) * ldk), kk,
                static_cast<const int*>(flags_ptr()), static_cast<const int*>(info_ptr()));
       kend();
+      if (aside) {
+        std::swap(st_, st_rot_);
+        STG_CUDA(cudaEventRecord(ev_rot_done_, st_rot_));
+        rot_pending_ = true;
+      }
     }
     STG_CUDA(cudaMemcpyAsync(&hs_->sticky, sticky_ptr(), sizeof(int), cudaMemcpyDeviceToHost, st_));
     read_scalars();
+    if (rot_pending_ && (hs_->sticky || (hs_->flags & (kNonFinite | kNotOrthonormal)) || hs_->info != 0)) {
+      // the gated rotation must read these flags before anything resets them
+      STG_CUDA(cudaStreamSynchronize(st_rot_));
+      rot_pending_ = false;
+    }
     if (hs_->sticky) throw SpecRedo();  // a speculated decision failed: nothing was written
     if (hs_->flags & kNonFinite) throw InvalidArgument("sym_eig_dense: non-finite entries");
     if (hs_->flags & kNotOrthonormal) throw InvalidArgument("rayleigh_ritz_step: basis is not column-orthonormal");
@@ -3635,12 +3716,15 @@ struct DeviceGuard {
   }
 };
 
+// Every ABI call except the steps orders after a pending rotation of X (the
+// steps wait for it after their ingestion, Session::run_step).
 template <class F>
-st_status guarded(st_session* s, F&& f) {
+st_status guarded(st_session* s, F&& f, bool step = false) {
   std::string* err = s ? &s->err : &g_create_error;
   try {
     std::unique_ptr<DeviceGuard> dg;
     if (s && s->impl) dg = std::make_unique<DeviceGuard>(s->impl->cfg.device);
+    if (s && s->impl && !step) s->impl->wait_rotation();
     f();
     return ST_OK;
   } catch (const std::invalid_argument& e) {
@@ -3823,7 +3907,7 @@ st_status st_step(st_session* s, const st_update* upd) {
   return guarded(s, [&] {
     if (!upd) throw std::invalid_argument("st_step: null update");
     s->impl->step(*upd);
-  });
+  }, /*step*/ true);
 }
 
 st_status st_info(const st_session* s, int64_t* n, int64_t* k, uint64_t* steps_taken, int64_t* nnz_a,
@@ -3995,21 +4079,21 @@ st_status st_step_blocks(st_session* s, const st_graph_update* upd) {
   return guarded(s, [&] {
     if (!upd) throw std::invalid_argument("st_step_blocks: null update");
     s->impl->step_blocks(*upd, false);
-  });
+  }, /*step*/ true);
 }
 
 st_status st_step_blocks_device(st_session* s, const st_graph_update* upd) {
   return guarded(s, [&] {
     if (!upd) throw std::invalid_argument("st_step_blocks: null update");
     s->impl->step_blocks(*upd, true);
-  });
+  }, /*step*/ true);
 }
 
 st_status st_step_perturbation(st_session* s, int64_t n_old, int64_t n_new, const st_csr_block* delta) {
   return guarded(s, [&] {
     if (!delta) throw std::invalid_argument("st_step_perturbation: null delta");
     s->impl->step_perturbation(n_old, n_new, *delta, false);
-  });
+  }, /*step*/ true);
 }
 
 st_status st_debug_determinism(st_session* s, int32_t which, int64_t N, int32_t m1, int32_t m2, int32_t reps,
@@ -4021,7 +4105,7 @@ st_status st_step_device(st_session* s, const st_update* upd) {
   return guarded(s, [&] {
     if (!upd) throw std::invalid_argument("st_step_device: null update");
     s->impl->step(*upd, true);
-  });
+  }, /*step*/ true);
 }
 
 int32_t st_kernel_stats(const st_session* s, int32_t cls, double* ms, int64_t* launches, double* work) {

@@ -100,3 +100,29 @@ def test_pinned_edit_lists_take_the_direct_upload():
     assert np.array_equal(va, vb) and np.array_equal(xa, xb)
     for c in range(3):
         assert np.array_equal(a.csr(0)[c], b.csr(0)[c])
+
+
+
+def test_failed_step_right_after_a_step_keeps_the_rotated_state():
+    """The rotation of X runs beside the next step's ingestion (st_rot_): a step
+    that fails in its ingestion right after a successful one must leave the
+    rotated state of the successful step, and the next step must see it."""
+    from harness import edges_of, random_update
+    from paper_2603_19439_b200 import TrackerError, Update
+    from support import random_graph
+
+    rng = np.random.default_rng(3)
+    n = 600
+    a = random_graph(n, 0.03, 7)
+    g, o = pair(a.rowptr, a.col, a.val, kind="grest-rsvd", k=6, rsvd_l=4, rsvd_p=4)
+    for t in range(3):
+        present = edges_of(g.csr(0))
+        u = random_update(rng, present, n, 6, 3, 5, 3)  # compressed path: |P| << n
+        g.step(u)
+        o.step(u)
+        n += 5
+        have = set(map(tuple, edges_of(g.csr(0)).tolist()))
+        miss = next((i, j) for i in range(n) for j in range(i + 1, n) if (i, j) not in have)
+        with pytest.raises(TrackerError, match="invalid deletion"):
+            g.step(Update.make(removed=[miss]))
+        check_state(g, o, tag=f"after failed step {t}")
