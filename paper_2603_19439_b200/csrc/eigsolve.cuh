@@ -45,29 +45,6 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   return c;
 }
 
-// The same count at R shifts at once: R independent recurrences interleaved,
-// so the FP64 reciprocal latency of one chain hides behind the others.
-template <int R>
-__device__ __forceinline__ void sturm_count_multi(const double* d, const double* e2, int n, const double (&x)[R],
-                                                  double pivmin, int (&c)[R]) {
-  double q[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    q[r] = d[0] - x[r];
-    if (fabs(q[r]) < pivmin) q[r] = -pivmin;
-    c[r] = q[r] < 0.0;
-  }
-  for (int i = 1; i < n; ++i) {
-    const double di = d[i], ei = e2[i - 1];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      q[r] = di - x[r] - ei * __drcp_rn(q[r]);
-      if (fabs(q[r]) < pivmin) q[r] = -pivmin;
-      c[r] += q[r] < 0.0;
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Multi-kernel pipeline: only the tridiagonalization needs one CTA; the
 // eigenvalues (bisection), the inverse iterations and the back-transformation
@@ -445,10 +422,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTriThreads)
 }
 
 // All eigenvalues of the tridiagonal matrix by bisection on Sturm counts:
-// a warp per eigenvalue multisects (129-way split per step) until the bracket
+// a warp per eigenvalue multisects (33-way split per step) until the bracket
 // is below max(2 eps |lambda|, eps ||T||), the absolute accuracy of QR-based
 // solvers; the returned value is the bracket's lower end (count <= j).
-constexpr int kBisG = 32;  // one warp per eigenvalue (kBisR shifts per lane: a 129-way split per Sturm round)
+constexpr int kBisG = 32;  // one warp per eigenvalue: a 33-way split per Sturm round
 // The Sturm chains are FP64 latency-bound and lose most of their issue slots
 // to co-resident DMMA CTAs when the sketch's solve overlaps the basis work on
 // the side stream (706 vs ~130 us measured at D = 200). Each CTA therefore
@@ -484,33 +461,26 @@ __global__ void __launch_bounds__(kBisThreads) bisect_kernel(EigBufs b, int n) {
   }
   __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = gtid / kBisG, sub = gtid % kBisG;
+  const int j = gtid / kBisG, sub = gtid % kBisG, lane = threadIdx.x & 31;
   const double pivmin = s_piv, atol = DBL_EPSILON * s_tn;
   double lo = s_lo, hi = s_hi;
-  // kBisR shifts per lane: a (32 kBisR + 1)-way split per round (7 bits at
-  // kBisR = 4 instead of 5: ~8 rounds to full accuracy instead of ~11)
-  constexpr int kBisR = 4, kWays = kBisG * kBisR;
-  constexpr double kStep = 1.0 / (kWays + 1);
+  constexpr double kStep = 1.0 / (kBisG + 1);
   for (int it = 0; it < 64; ++it) {
     const double width = hi - lo;
     const bool done = !(width > fmax(2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)), atol) && width > pivmin);
-    double x[kBisR];
-    int cnt[kBisR];
+    const double x = lo + width * (sub + 1) * kStep;
+    const int cnt = (j < n && !done) ? sturm_count(d, e2, n, x, pivmin) : 0;
+    const int gbase = lane & ~(kBisG - 1);
+    int nlo_idx = -1;
 #pragma unroll
-    for (int r = 0; r < kBisR; ++r) {
-      x[r] = lo + width * (kBisR * sub + r + 1) * kStep;
-      cnt[r] = 0;
+    for (int q = 0; q < kBisG; ++q) {
+      const int cq = __shfl_sync(0xffffffffu, cnt, gbase + q);
+      if (cq <= j) nlo_idx = q;
     }
-    if (j < n && !done) sturm_count_multi<kBisR>(d, e2, n, x, pivmin, cnt);
-    int mine = -1;  // the largest shift index with count <= j (as the 33-way search: last such shift)
-#pragma unroll
-    for (int r = 0; r < kBisR; ++r)
-      if (cnt[r] <= j) mine = kBisR * sub + r;
-    const int nlo_idx = __reduce_max_sync(0xffffffffu, mine + 1) - 1;
     const unsigned all_done = __all_sync(0xffffffffu, done || j >= n);
     if (!done) {
       const double nlo = nlo_idx >= 0 ? lo + width * (nlo_idx + 1) * kStep : lo;
-      const double nhi = nlo_idx + 1 < kWays ? lo + width * (nlo_idx + 2) * kStep : hi;
+      const double nhi = nlo_idx + 1 < kBisG ? lo + width * (nlo_idx + 2) * kStep : hi;
       lo = nlo;
       hi = nhi;
     }
