@@ -270,6 +270,7 @@ struct Scalars {  // pinned host mirror of device scalars read at sync points
   int flags;
   int info;
   int sticky;
+  int mgs_r;
   double alpha;
   double sk_lam[kEigMaxN];  // sketch eigenvalues, copied asynchronously (pageable memory would block the host)
 };
@@ -2530,45 +2531,40 @@ class Session {
     return F2;
   }
 
-  double host_norm_g(const double* v, int ldv, i64 G) {
-    double* g1 = arena_.get<double>("mgs_g1", 8);
-    pgram(v, ldv, v, ldv, G, 1, 1, true, g1, 1);
-    double h = 0;
-    STG_CUDA(cudaMemcpyAsync(&h, g1, sizeof(double), cudaMemcpyDeviceToHost, st_));
-    STG_CUDA(cudaStreamSynchronize(st_));
-    return std::sqrt(h);
-  }
-
-  // Exact replica of ortho.hpp:26-37, one column at a time.
+  // Exact replica of ortho.hpp:26-37, one column at a time, without host
+  // round trips: the per-column drop decisions stay on the device (dropped
+  // columns are zero slots until one compaction at the end; one read of the
+  // kept count).
   int mgs2_exact(Blk W, int w, const Blk* against, int a, i64 N, i64 G, Blk out) {
     const int ldv = 8;
     double* v = arena_.get<double>("mgs_v", N * ldv);
     double* t = arena_.get<double>("mgs_t", std::max(a, w) * ldv + 8);
-    int r = 0;
+    double* nrm2 = arena_.get<double>("mgs_n2", 16);
+    int* keep = arena_.get<int>("mgs_keep", w + 8);
     for (int c = 0; c < w; ++c) {
       launch(copy2d_kernel, dim3(blocks(N)), dim3(256), 0, st_, static_cast<const double*>(W.p + c), W.ld, v, ldv, N, 1);
-      const double orig = host_norm_g(v, ldv, G);
-      if (orig == 0.0) continue;
+      pgram(v, ldv, v, ldv, G, 1, 1, true, nrm2, 1);  // the original squared norm
       for (int pass = 0; pass < 2; ++pass) {
         if (against && a > 0) {
           pgram(against->p, against->ld, v, ldv, G, a, 1, false, t, ldv);
           nn(against->p, against->ld, N, a, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
         }
-        if (r > 0) {
-          pgram(out.p, out.ld, v, ldv, G, r, 1, false, t, ldv);
-          nn(out.p, out.ld, N, r, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
+        if (c > 0) {  // earlier columns: kept ones normalized, dropped ones zero
+          pgram(out.p, out.ld, v, ldv, G, c, 1, false, t, ldv);
+          nn(out.p, out.ld, N, c, t, ldv, 1, v, ldv, -1.0, 1.0, v, ldv);
         }
       }
-      const double nrm = host_norm_g(v, ldv, G);
-      if (nrm < 1e-10 * orig) continue;
-      double* sc = arena_.get<double>("mgs_scale", 8);
-      const double inv = 1.0 / nrm;
-      STG_CUDA(cudaMemcpyAsync(sc, &inv, sizeof(double), cudaMemcpyHostToDevice, st_));
-      // out[:, r] = v / nrm  (as a 1x1 "GEMM" so it stays on the stream)
-      nn(v, ldv, N, 1, sc, 8, 1, out.p + r, out.ld, 1.0, 0.0, nullptr, 0);
-      STG_CUDA(cudaStreamSynchronize(st_));
-      ++r;
+      pgram(v, ldv, v, ldv, G, 1, 1, true, nrm2 + 8, 1);
+      launch(mgs_scale_kernel, dim3(blocks(N)), dim3(256), 0, st_, static_cast<const double*>(v), ldv, N,
+             static_cast<const double*>(nrm2), static_cast<const double*>(nrm2 + 8), out.p + c, out.ld, keep + c);
     }
+    int* dr = reinterpret_cast<int*>(nrm2 + 4);
+    launch(mgs_compact_kernel, dim3(blocks(N)), dim3(256), 0, st_, out.p, out.ld, N, static_cast<const int*>(keep), w,
+           dr);
+    int r = 0;
+    STG_CUDA(cudaMemcpyAsync(&hs_->mgs_r, dr, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    STG_CUDA(cudaStreamSynchronize(st_));
+    r = hs_->mgs_r;
     return r;
   }
 
@@ -2618,7 +2614,11 @@ class Session {
     // ---- candidates [(I - XX') Delta X | trailing]
     const int ldc = ld_for(wmax);
     double* cand = arena_.get<double>("cand", N * ldc);
-    STG_CUDA(cudaMemsetAsync(cand, 0, sizeof(double) * N * ldc, st_));
+    if (basis_kind >= 2 && !rsvd && S > 0) {  // the dense d2 columns are scattered: zero the whole block
+      STG_CUDA(cudaMemsetAsync(cand, 0, sizeof(double) * N * ldc, st_));
+    } else {  // the SpMM writes every row of P (zero rows included): only the coordinate rows need zeros
+      STG_CUDA(cudaMemsetAsync(cand + p * ldc, 0, sizeof(double) * (N - p) * ldc, st_));
+    }
     double* ck = arena_.get<double>("ck", static_cast<i64>(kk) * ld_for(std::max(q, std::max(trail_max, kk))));
     // dx = Delta X (rows of P; the coordinate rows stay 0)
     SpmmArgs sa{};
@@ -2700,7 +2700,8 @@ class Session {
     const int kk = static_cast<int>(k);
     const int ldy = ld_for(q);
     double* Y = arena_.get<double>("Y", N * ldy);
-    STG_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * N * ldy, st_));
+    // the sketch SpMM writes every row of P (zero rows included): zero the coordinate rows only
+    STG_CUDA(cudaMemsetAsync(Y + p * ldy, 0, sizeof(double) * (N - p) * ldy, st_));
     STG_CUDA(cudaStreamWaitEvent(st_, ev_rng_, 0));
     // Y0 = d2 * Omega: nonzeros of Delta in the appended-node columns
     SpmmArgs sa{};

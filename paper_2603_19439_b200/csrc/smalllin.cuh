@@ -446,6 +446,38 @@ __global__ void hash_fill_kernel(double* p, i64 n, unsigned long long seed) {
 }
 
 // Copy a rows x cols block (row-major) between leading dimensions.
+// mgs2_exact on the device (ortho.hpp:26-37): column c's drop decision from
+// its squared norms before (o2) and after (n2) the two projection passes,
+// nrm = sqrt(n2) < 1e-10 sqrt(o2) or a zero column drops it; a kept column is
+// out[:, c] = v / nrm (the reference's division and square root, IEEE),
+// a dropped one is zeroed, so later projections against out[:, :c] are the
+// projections against the kept columns (zero columns add exact zeros).
+__global__ void mgs_scale_kernel(const double* v, int ldv, i64 rows, const double* o2, const double* n2,
+                                 double* out, int ldo, int* keep) {
+  const double orig = sqrt(*o2), nrm = sqrt(*n2);
+  const bool kept = orig != 0.0 && !(nrm < 1e-10 * orig);
+  const double inv = kept ? 1.0 / nrm : 0.0;
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) *keep = kept ? 1 : 0;
+  if (i < rows) out[i * ldo] = kept ? v[i * ldv] * inv : 0.0;
+}
+
+// Kept columns to the front, in order (row-parallel, in place: a row's
+// writes only go to slots at or left of the column being read); r = count.
+__global__ void mgs_compact_kernel(double* out, int ldo, i64 rows, const int* keep, int w, int* r) {
+  const i64 i = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    int c = 0;
+    for (int j = 0; j < w; ++j) c += keep[j];
+    *r = c;
+  }
+  if (i >= rows) return;
+  double* row = out + i * ldo;
+  int d = 0;
+  for (int j = 0; j < w; ++j)
+    if (keep[j]) row[d++] = row[j];
+}
+
 __global__ void copy2d_kernel(const double* src, int lds, double* dst, int ldd, i64 rows, int cols) {
   const i64 idx = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= rows * cols) return;

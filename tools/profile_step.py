@@ -15,6 +15,8 @@ from paper_2603_19439_b200 import TrackerSession, streams  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=20)
+ap.add_argument("--config", default="cfg3", choices=["cfg3", "cfg4"])
+ap.add_argument("--n", type=int, default=1 << 22, help="cfg4 node count")
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--k", type=int, default=32)
@@ -22,7 +24,10 @@ ap.add_argument("--real-x0", action="store_true", help="leading eigenpairs (as b
 ap.add_argument("--device-edits", action="store_true", help="edit lists resident in HBM (st_step_device, as bench.py)")
 args = ap.parse_args()
 
-s = streams.config3(scale=args.scale, steps=args.warmup + args.steps)
+if args.config == "cfg4":
+    s = streams.config4(n=args.n, steps=args.warmup + args.steps)
+else:
+    s = streams.config3(scale=args.scale, steps=args.warmup + args.steps)
 rp, col, val = s.csr0()
 n = len(rp) - 1
 if args.real_x0:
