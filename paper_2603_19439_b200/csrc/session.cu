@@ -2515,6 +2515,53 @@ class Session {
   int pre_a_ = 0;
   double* pre_cr_ = nullptr;
   int pre_ldcr_ = 0;
+  // speculative steps: the RSVD block's Grams precomputed beside the sketch
+  // eigensolve (PM'PM and [X-bar, Q1]'PM), and U_keep (the block is PM U_keep)
+  const double* pre_gpm_ = nullptr;
+  const double* pre_c1p_ = nullptr;
+  int pre_ldm_ = 0, pre_qm_ = 0;
+  const double* pre_t0_ = nullptr;
+  int pre_ldt0_ = 0;
+  const bool fold_rsvd_ = !getenv_flag("STG_NO_RSVD_FOLD");  // development A/B
+
+  // orthonormalize(PM U_keep, against [X-bar, Q1]) of the speculative path
+  // from Grams computed while the sketch's eigensolve ran: pass 1's Gram is
+  // U'(PM'PM)U (no n-row Gram), its R^-1 folds into one product Q1 = PM (U R^-1)
+  // (R = PM U is never formed), pass 2's coefficients are ([X-bar,Q1]'PM)(U R^-1).
+  // Same algebra and decisions as orthonormalize's Cpre path (suspect pivots
+  // raise the sticky flag and the step is redone on the exact path).
+  int orthonormalize_rsvd_folded(int w, const Blk* against, int a, i64 N, i64 G, Blk out) {
+    const int qm = pre_qm_, ldm = pre_ldm_;
+    const int ldw = ld_for(w);
+    double* H = arena_.get<double>("rf_H", static_cast<i64>(qm) * ldw);
+    double* T1 = arena_.get<double>("rf_T1", static_cast<i64>(qm) * ldw);
+    double* W1 = arena_.get<double>("on_W1", N * ldw);
+    double* C = arena_.get<double>("on_C", static_cast<i64>(std::max(a, 1)) * ldw);
+    double* Gm = arena_.get<double>("on_G", static_cast<i64>(w) * ldw);
+    double* R = arena_.get<double>("on_R", static_cast<i64>(w) * ldw);
+    double* Ri = arena_.get<double>("on_Ri", static_cast<i64>(w) * ldw);
+    double* o2 = arena_.get<double>("on_o2", w);
+    // pass 1: G1 = U'(PM'PM)U, the original norms from G1 and the first projection's coefficients
+    nn(pre_gpm_, ldm, qm, qm, pre_t0_, pre_ldt0_, w, H, ldw, 1.0, 0.0, nullptr, 0);
+    gram(pre_t0_, pre_ldt0_, H, ldw, qm, w, w, false, Gm, ldw);
+    launch(orig2_kernel, dim3(blocks(w, 128)), dim3(128), 0, st_, static_cast<const double*>(Gm), ldw,
+           static_cast<const double*>(pre_cr_), pre_ldcr_, a, w, o2);
+    STG_CUDA(cudaMemsetAsync(flags_ptr(), 0, sizeof(int), st_));
+    chol(Gm, ldw, w, R, ldw, Ri, ldw, o2, kSuspectTau2, false);
+    launch(or_sticky_kernel, dim3(1), dim3(1), 0, st_, static_cast<const int*>(flags_ptr()), kSuspect | kBreakdown,
+           sticky_ptr());
+    last_ortho_exact_ = false;
+    // Q1 = PM (U R^-1)
+    nn(pre_t0_, pre_ldt0_, qm, w, Ri, ldw, w, T1, ldw, 1.0, 0.0, nullptr, 0, true);
+    nn(pre_pm_, ldm, N, qm, T1, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+    // pass 2: W1 = Q1 - A (A'Q1), A'Q1 = (A'PM)(U R^-1)
+    nn(pre_c1p_, ldm, a, qm, T1, ldw, w, C, ldw, 1.0, 0.0, nullptr, 0);
+    nn(against->p, against->ld, N, a, C, ldw, w, W1, ldw, -1.0, 1.0, out.p, out.ld);
+    pgram(W1, ldw, W1, ldw, G, w, w, true, Gm, ldw);
+    chol_inverse_near_identity(Gm, ldw, w, R, ldw, Ri, ldw);
+    nn(W1, ldw, N, w, Ri, ldw, w, out.p, out.ld, 1.0, 0.0, nullptr, 0, true);
+    return w;
+  }
   static constexpr double kSuspectTau2 = 1e-10;  // residual / original norm below 1e-5
   static constexpr double kRrOrtol = 1e-9;       // eigenvector cluster threshold for the RR solve
 
@@ -2659,6 +2706,7 @@ class Session {
         int q1 = 0;
         pre_pm_ = pre_c1_ = nullptr;
         pre_cr_ = nullptr;
+        pre_gpm_ = pre_c1p_ = pre_t0_ = nullptr;
         const int wt = rsvd_trailing(pt, z, q, omega, ldo, Blk{cand + kk, ldc},
                                      [&](const double* Msk, int ldm, int qm) {
           q1 = orthonormalize(Blk{cand, ldc}, kk, &z, kk, N, G, Blk{Z + kk, ldz});
@@ -2674,15 +2722,30 @@ class Session {
           }
           // the Rayleigh-Ritz products of [X-bar, Q1] do not depend on the sketch
           rr_prefix(pt, z, kk + q1, kk + q1 + static_cast<int>(std::min<i64>(cfg.rsvd_l, q)));
+          if (spec_ && fold_rsvd_ && pre_pm_) {  // the RSVD block's Grams, still beside the eigensolve
+            const int a = pre_a_;
+            double* gpm = arena_.get<double>("pm_GPM", static_cast<i64>(qm) * ldm);
+            double* c1p = arena_.get<double>("pm_C1P", static_cast<i64>(a) * ldm);
+            pgram(pre_pm_, ldm, pre_pm_, ldm, G, qm, qm, true, gpm, ldm);
+            pgram(Z, ldz, pre_pm_, ldm, G, a, qm, false, c1p, ldm);
+            pre_gpm_ = gpm;
+            pre_c1p_ = c1p;
+            pre_ldm_ = ldm;
+            pre_qm_ = qm;
+          }
         });
         int q2 = 0;
         if (wt > 0) {
           const Blk against{Z, ldz};
-          q2 = orthonormalize(Blk{cand + kk, ldc}, wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz}, pre_cr_,
-                              pre_ldcr_);
+          if (pre_t0_)
+            q2 = orthonormalize_rsvd_folded(wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz});
+          else
+            q2 = orthonormalize(Blk{cand + kk, ldc}, wt, &against, kk + q1, N, G, Blk{Z + kk + q1, ldz}, pre_cr_,
+                                pre_ldcr_);
         }
         pre_pm_ = pre_c1_ = nullptr;
         pre_cr_ = nullptr;
+        pre_gpm_ = pre_c1p_ = pre_t0_ = nullptr;
         return Basis{z, kk + q1 + q2};
       }
     }
@@ -2793,11 +2856,16 @@ class Session {
       if (keep == 0) return 0;
       const double* Uf = fold_u(U, ldu, keep);
       if (pre_pm_) {
-        nn(pre_pm_, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
         const int ldcp = ld_for(keep);
         pre_cr_ = arena_.get<double>("pm_CR", static_cast<i64>(pre_a_) * ldcp);
         pre_ldcr_ = ldcp;
         nn(pre_c1_, ldy, pre_a_, qm, Uf, ldu, keep, pre_cr_, ldcp, 1.0, 0.0, nullptr, 0);
+        if (pre_gpm_) {  // R = PM U_keep is not formed (orthonormalize_rsvd_folded)
+          pre_t0_ = Uf;
+          pre_ldt0_ = ldu;
+        } else {
+          nn(pre_pm_, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
+        }
       } else {
         nn(M, ldy, N, qm, Uf, ldu, keep, out.p, out.ld, 1.0, 0.0, nullptr, 0);
       }
