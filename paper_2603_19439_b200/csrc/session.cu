@@ -1463,6 +1463,7 @@ class Session {
   int plan_epoch_ = 0;
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
   const int spmm_fused_min_m_ = getenv("STG_SPMM_FUSED_MIN_M") ? atoi(getenv("STG_SPMM_FUSED_MIN_M")) : 129;
+  const bool spmm_chunked_ = !getenv_flag("STG_SPMM_NOCHUNK");  // development A/B
   const int merge_mode_ = getenv("STG_MERGE_MODE") ? atoi(getenv("STG_MERGE_MODE")) : 3;  // development A/B
 
   PlanEntry& spmm_plan(const SpmmArgs& a, i64 nnz) {
@@ -1486,20 +1487,28 @@ class Session {
     e->smax = 2 * cdiv(nnz, kLongSeg) + 1;
     int* cnt = arena_.get<int>(e->tag + "cnt", a.rows + 1);
     int* cnt2 = arena_.get<int>(e->tag + "cnt2", a.rows + 1);
+    int* slen = arena_.get<int>(e->tag + "slen", a.rows + 1);
+    int* sptr = arena_.get<int>(e->tag + "sptr", a.rows + 1);
+    const int nch = static_cast<int>((nnz + a.rows) / kChunk + 1);
+    int* crow = arena_.get<int>(e->tag + "crow", nch + 1);
     int* vstart = arena_.get<int>(e->tag + "vstart", a.rows + 1);
     int* sstart = arena_.get<int>(e->tag + "sstart", a.rows + 1);
     int* vrow = arena_.get<int>(e->tag + "vrow", e->vmax);
     int* split_rows = arena_.get<int>(e->tag + "split", std::max<i64>(e->split_max, 1));
     int* nsplit = arena_.get<int>(e->tag + "nsplit", 1);
-    launch(seg_count_kernel, dim3(blocks(a.rows + 1)), dim3(256), 0, st_, a.rowptr, a.row_off, a.rows, cnt, cnt2);
+    launch(seg_count_kernel, dim3(blocks(a.rows + 1)), dim3(256), 0, st_, a.rowptr, a.row_off, a.rows, cnt, cnt2,
+           slen);
     scan_int(cnt, vstart, a.rows + 1);
     scan_int(cnt2, sstart, a.rows + 1);
+    scan_int(slen, sptr, a.rows + 1);
+    launch(chunk_start_kernel, dim3(blocks(a.rows + 1)), dim3(256), 0, st_, static_cast<const int*>(sptr), a.rows, nch,
+           crow);
     STG_CUDA(cudaMemsetAsync(nsplit, 0, sizeof(int), st_));
     launch(seg_fill_kernel, dim3(blocks(a.rows)), dim3(256), 0, st_, static_cast<const int*>(vstart), a.rows, vrow,
            split_rows, nsplit);
-    int* segcnt = arena_.get<int>(e->tag + "segcnt", e->smax);
-    STG_CUDA(cudaMemsetAsync(segcnt, 0, sizeof(int) * e->smax, st_));  // the fused kernel's arrival counters
-    e->pl = SpmmPlan{vrow, vstart, sstart, split_rows, nsplit, nullptr, 0, segcnt};
+    int* segcnt = arena_.get<int>(e->tag + "segcnt", 4 * e->smax);  // per long row and column slab (<= 4)
+    STG_CUDA(cudaMemsetAsync(segcnt, 0, sizeof(int) * 4 * e->smax, st_));  // the fused kernels' arrival counters
+    e->pl = SpmmPlan{vrow, vstart, sstart, split_rows, nsplit, nullptr, 0, segcnt, sptr, crow, nch};
     return *e;
   }
 
@@ -1533,6 +1542,9 @@ class Session {
       const bool long_rows = nnz > kSegNnz;
       if (spmm_fused_ && b.m >= spmm_fused_min_m_) {  // one launch: segments, their ordered fix-up and the row groups
         spmm_fused_launch(b, pl, long_rows ? pe.vmax : 0, st_);
+        launches += 1;
+      } else if (spmm_chunked_ && b.col_lo == 0) {  // one launch: segments, then streamed row chunks, per column slab
+        spmm_chunk_launch(b, pl, long_rows ? pe.vmax : 0, st_);
         launches += 1;
       } else {
         spmm_launch(b, pl, pe.vmax, pe.split_max, long_rows, st_);

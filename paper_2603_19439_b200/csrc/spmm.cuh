@@ -40,6 +40,7 @@ struct SpmmArgs {
 // sums, which spmm_fixup_kernel adds in segment order (deterministic; the
 // association differs from Eigen's only within those rows, at rounding level).
 constexpr int kSegNnz = 32;    // rows up to this length: the row-group kernels
+constexpr int kChunk = 128;    // rows + short-row entries per chunk of spmm_chunk_kernel
 constexpr int kLongSeg = 32;   // longer rows: one warp per 32-entry segment, partials
                                // summed by the fix-up (512-entry segments made one
                                // warp walk a hub row serially: 2x slower at config 3)
@@ -52,7 +53,10 @@ struct SpmmPlan {
   const int* nsplit;
   double* scratch;        // [slot][lds]
   int lds;
-  int* segcnt;            // per long row (at its first scratch slot): segments arrived (fused kernel)
+  int* segcnt;            // per long row (at its first scratch slot) and column slab: segments arrived
+  const int* sptr;        // row -> short-row entries before it (chunk kernel)
+  const int* crow;        // chunk -> first row (chunk kernel)
+  int nch;                // chunks
 };
 
 template <int T>  // columns per lane = T (m <= 32 T)
@@ -686,6 +690,178 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl
   }
 }
 
+// Narrow products (m <= 128, one (32 VW)-column slab per warp, blockIdx.y):
+// the long-row segments first (as the fused kernel, counters per row and
+// slab), then chunks of rows (chunk_start_kernel). A warp copies its chunk's
+// short-row entries into shared memory as (row, col, val) triples — one lane
+// per row, so no per-entry search — and then streams them in order, eight
+// entries per batch, the next batch's X rows loaded before the current batch
+// is summed: the gathers of a chunk overlap instead of paying one memory
+// round trip per row or per window. Sums per row in column order with
+// separate multiply and add roundings (bit-identical to the other kernels);
+// rows without entries are written as zeros; long rows are left to their
+// segments. (col_lo must be 0 here: the trailing-column products are wide and
+// take the fused kernel.)
+constexpr int kChunkWarps = 8;
+constexpr int kChunkMax = kChunk + kSegNnz;  // short entries per chunk, upper bound
+struct ChunkSmem {
+  int rp[kChunk + 1];
+  int sp[kChunk + 1];
+  int col[kChunkMax];
+  unsigned char row[kChunkMax];
+  double val[kChunkMax];
+};
+
+template <int VW>
+__global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a, SpmmPlan pl) {
+  using V = SpV<VW>;
+  using VT = typename V::T;
+  constexpr int W = 32 * VW;
+  __shared__ ChunkSmem csm[kChunkWarps];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  ChunkSmem& cs = csm[wib];
+  const int c0 = static_cast<int>(blockIdx.y) * W;
+  const bool on = c0 + VW * lane < a.m;
+  const double* Xs = a.X + c0 + VW * lane;
+  double* Ys = a.Y + c0 + VW * lane;
+  const int* rowp = a.rowptr + a.row_off;
+  const i64 gw = static_cast<i64>(blockIdx.x) * kChunkWarps + wib, nw = static_cast<i64>(gridDim.x) * kChunkWarps;
+  // ---- long-row segments of this slab
+  const i64 nseg = pl.vstart[a.rows];
+  i64 w = gw;
+  for (; w < nseg; w += nw) {
+    const int r = pl.vrow[w];
+    const int vs = pl.vstart[r];
+    const int sg = static_cast<int>(w - vs);
+    const int nsg = pl.vstart[r + 1] - vs;
+    const int seg0 = rowp[r] + sg * kLongSeg;
+    const int cnt = min(kLongSeg, rowp[r + 1] - seg0);
+    int c_l = 0;
+    double v_l = 0.0;
+    if (lane < cnt) {
+      c_l = __ldg(a.col + seg0 + lane);
+      v_l = __ldg(a.val + seg0 + lane);
+    }
+    VT acc = V::zero();
+    for (int q = 0; q < cnt; q += 8) {  // eight entries' loads in flight, sums in column order
+      VT xv[8];
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = __shfl_sync(0xffffffffu, c_l, (q + u) & 31);
+        vv[u] = __shfl_sync(0xffffffffu, v_l, (q + u) & 31);
+        xv[u] = (q + u < cnt && on) ? V::ld(Xs + static_cast<i64>(c) * a.ldx) : V::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q + u < cnt) V::fma(acc, vv[u], xv[u]);
+    }
+    const int slot0 = pl.sstart[r];
+    if (on) V::st(pl.scratch + static_cast<i64>(slot0 + sg) * pl.lds + c0 + VW * lane, acc);
+    __threadfence();
+    int last = 0;
+    int* ctr = pl.segcnt + static_cast<i64>(slot0) * gridDim.y + blockIdx.y;
+    if (lane == 0) last = atomicAdd(ctr, 1) == nsg - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // every partial of row r (this slab) is written: add them in segment order
+      __threadfence();
+      const double* p0 = pl.scratch + static_cast<i64>(slot0) * pl.lds + c0 + VW * lane;
+      VT tot = V::zero();
+      int q = 0;
+      for (; q + 4 <= nsg; q += 4) {
+        VT tv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tv[u] = on ? V::ldcg(p0 + static_cast<i64>(q + u) * pl.lds) : V::zero();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) V::add(tot, tv[u]);
+      }
+      for (; q < nsg; ++q)
+        if (on) V::add(tot, V::ldcg(p0 + static_cast<i64>(q) * pl.lds));
+      if (on) V::st(Ys + static_cast<i64>(r) * a.ldy, tot);
+      if (lane == 0) *ctr = 0;
+    }
+  }
+  // ---- chunks
+  for (i64 c = w - nseg; c < pl.nch; c += nw) {
+    const int r0 = pl.crow[c], r1 = pl.crow[c + 1];
+    if (r0 >= r1) continue;
+    const int nr = r1 - r0;
+    __syncwarp();  // the previous chunk's readers are done
+    for (int i = lane; i <= nr; i += 32) {
+      cs.rp[i] = __ldg(rowp + r0 + i);
+      cs.sp[i] = __ldg(pl.sptr + r0 + i);
+    }
+    __syncwarp();
+    const int q0 = cs.sp[0], ns = cs.sp[nr] - q0;
+    // entries of the short rows -> (row, col, val), one lane per row; empty rows -> zeros
+    for (int i0 = 0; i0 < nr; i0 += 32) {
+      const int i = i0 + lane;
+      bool zero = false;
+      if (i < nr) {
+        const int s = cs.rp[i], len = cs.rp[i + 1] - s;
+        zero = len == 0;
+        if (len > 0 && len <= kSegNnz) {
+          const int q = cs.sp[i] - q0;
+          for (int t = 0; t < len; ++t) {
+            cs.col[q + t] = __ldg(a.col + s + t);
+            cs.val[q + t] = __ldg(a.val + s + t);
+            cs.row[q + t] = static_cast<unsigned char>(i);
+          }
+        }
+      }
+      unsigned zm = __ballot_sync(0xffffffffu, zero);
+      while (zm) {
+        const int j = __ffs(zm) - 1;
+        zm &= zm - 1;
+        if (on) V::st(Ys + static_cast<i64>(r0 + i0 + j) * a.ldy, V::zero());
+      }
+    }
+    __syncwarp();
+    // stream the entries: batch b + 1's X rows in flight while batch b is summed
+    int cur = -1;
+    VT acc = V::zero();
+    VT xn[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xn[u] = (u < ns && on) ? V::ld(Xs + static_cast<i64>(cs.col[u]) * a.ldx) : V::zero();
+    for (int b = 0; b < ns; b += 8) {
+      VT xc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xc[u] = xn[u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = b + 8 + u;
+        xn[u] = (j < ns && on) ? V::ld(Xs + static_cast<i64>(cs.col[j]) * a.ldx) : V::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = b + u;
+        if (j >= ns) break;
+        const int rw = cs.row[j];
+        if (rw != cur) {
+          if (cur >= 0 && on) V::st(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
+          cur = rw;
+          acc = V::zero();
+        }
+        V::fma(acc, cs.val[j], xc[u]);
+      }
+    }
+    if (cur >= 0 && on) V::st(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
+  }
+}
+
+inline void spmm_chunk_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, cudaStream_t st) {
+  const bool vec2 = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 && pl.lds % 2 == 0 &&
+                    ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y) |
+                      reinterpret_cast<uintptr_t>(pl.scratch)) & 15) == 0;
+  const int W = vec2 ? 64 : 32;
+  const i64 items = vmax + pl.nch;
+  const unsigned gx = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(cdiv(items, kChunkWarps), 148 * (vec2 ? 2 : 3))));
+  const dim3 grid(gx, static_cast<unsigned>(cdiv(a.m, W)));
+  if (vec2) spmm_chunk_kernel<2><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  else spmm_chunk_kernel<1><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  STG_LAUNCH();
+}
+
 template <int VW, int T>
 inline void spmm_fused_go(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, i64 ngroups, cudaStream_t st) {
   const i64 items = vmax + ngroups;  // vmax: upper bound of the long-row segments
@@ -722,17 +898,32 @@ inline void spmm_fused_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, c
 }
 
 // ---- segment plan of a CSR row range (built once per perturbation)
-__global__ void seg_count_kernel(const int* rowptr, i64 row_off, i64 rows, int* cnt, int* cnt2) {
+__global__ void seg_count_kernel(const int* rowptr, i64 row_off, i64 rows, int* cnt, int* cnt2, int* slen) {
   const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r > rows) return;
   if (r == rows) {
-    cnt[r] = cnt2[r] = 0;
+    cnt[r] = cnt2[r] = slen[r] = 0;
     return;
   }
   const int len = rowptr[r + row_off + 1] - rowptr[r + row_off];
   const int c = len > kSegNnz ? (len + kLongSeg - 1) / kLongSeg : 0;  // short rows: the row-group kernel
   cnt[r] = c;
   cnt2[r] = c > 1 ? c : 0;
+  slen[r] = c > 0 ? 0 : len;  // entries of short rows (the chunk kernel's positions)
+}
+
+// Chunks of the chunk kernel: row r sits at position r + sptr[r] (rows and
+// short-row entries before it); chunk c owns the rows with positions in
+// [c kChunk, (c + 1) kChunk): <= kChunk rows and < kChunk + kSegNnz short
+// entries. One thread per row writes crow[c] for the chunks that start at it.
+__global__ void chunk_start_kernel(const int* sptr, i64 rows, int nch, int* crow) {
+  const i64 r = static_cast<i64>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r > rows) return;
+  const i64 pos = r == rows ? static_cast<i64>(nch) * kChunk : r + sptr[r];
+  const i64 prev = r == 0 ? -1 : (r - 1) + sptr[r - 1];
+  const i64 c_hi = r == rows ? nch : pos / kChunk;            // chunks whose first position is <= pos
+  const i64 c_lo = r == 0 ? 0 : prev / kChunk + 1;            // ... and > prev
+  for (i64 c = c_lo; c <= c_hi && c <= nch; ++c) crow[c] = static_cast<int>(r);
 }
 
 __global__ void seg_fill_kernel(const int* vstart, i64 rows, int* vrow, int* split_rows, int* nsplit) {
