@@ -1543,7 +1543,7 @@ class Session {
       if (spmm_fused_ && b.m >= spmm_fused_min_m_) {  // one launch: segments, their ordered fix-up and the row groups
         spmm_fused_launch(b, pl, long_rows ? pe.vmax : 0, st_);
         launches += 1;
-      } else if (spmm_chunked_ && b.col_lo == 0) {  // one launch: segments, then streamed row chunks, per column slab
+      } else if (spmm_chunked_) {  // one launch: segments, then streamed row chunks, per column slab
         spmm_chunk_launch(b, pl, long_rows ? pe.vmax : 0, st_);
         launches += 1;
       } else {

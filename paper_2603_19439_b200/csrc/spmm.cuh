@@ -700,8 +700,8 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(SpmmArgs a, SpmmPlan pl
 // round trip per row or per window. Sums per row in column order with
 // separate multiply and add roundings (bit-identical to the other kernels);
 // rows without entries are written as zeros; long rows are left to their
-// segments. (col_lo must be 0 here: the trailing-column products are wide and
-// take the fused kernel.)
+// segments. Entries left of a trailing-column view (col < col_lo) are staged
+// as exact zeros.
 constexpr int kChunkWarps = 8;
 constexpr int kChunkMax = kChunk + kSegNnz;  // short entries per chunk, upper bound
 struct ChunkSmem {
@@ -741,6 +741,10 @@ __global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a
     if (lane < cnt) {
       c_l = __ldg(a.col + seg0 + lane);
       v_l = __ldg(a.val + seg0 + lane);
+      if (c_l < a.col_lo) {  // trailing-column view: an exact zero
+        c_l = a.col_lo;
+        v_l = 0.0;
+      }
     }
     VT acc = V::zero();
     for (int q = 0; q < cnt; q += 8) {  // eight entries' loads in flight, sums in column order
@@ -803,8 +807,10 @@ __global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a
         if (len > 0 && len <= kSegNnz) {
           const int q = cs.sp[i] - q0;
           for (int t = 0; t < len; ++t) {
-            cs.col[q + t] = __ldg(a.col + s + t);
-            cs.val[q + t] = __ldg(a.val + s + t);
+            const int cc = __ldg(a.col + s + t);
+            const bool act = cc >= a.col_lo;  // trailing-column view: inactive entries add exact zeros
+            cs.col[q + t] = act ? cc : a.col_lo;
+            cs.val[q + t] = act ? __ldg(a.val + s + t) : 0.0;
             cs.row[q + t] = static_cast<unsigned char>(i);
           }
         }
