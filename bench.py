@@ -81,65 +81,6 @@ def make_workload(name: str, steps: int, seed_offset: int = 0, scale: int | None
     raise SystemExit(f"unknown config {name}")
 
 
-def operator_csr(rp, col, val, operator):
-    """The tracked operator at t=0 (adjacency, or T = 2I - L_n for the
-    normalized Laplacian, graph.cpp:139-150) for computing X0."""
-    if operator == "adjacency":
-        return rp, col, val
-    n = len(rp) - 1
-    rows = np.repeat(np.arange(n), np.diff(rp))
-    deg = np.bincount(rows, weights=val, minlength=n)
-    s = np.where(deg > 0, 1.0 / np.sqrt(np.maximum(deg, 1e-300)), 0.0)
-    offv = (s[rows] * s[col]) * val
-    diag = np.where(deg > 0, 1.0, 2.0)
-    r2 = np.concatenate([rows, np.arange(n)])
-    c2 = np.concatenate([col, np.arange(n)])
-    v2 = np.concatenate([offv, diag])
-    o = np.lexsort((c2, r2))
-    rp2 = np.zeros(n + 1, np.int64)
-    np.cumsum(np.bincount(r2, minlength=n), out=rp2[1:])
-    return rp2.astype(np.int32), c2[o].astype(np.int32), v2[o]
-
-
-class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, index: int):
-        self.index = index
-        self.rows = []
-        self.proc = None
-
-    def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
-        except FileNotFoundError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
-    def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
-
-
 def dist_setup(backend: str | None = None):
     """One process per GPU (torchrun env); NCCL on GPUs, gloo for CPU tests."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -470,34 +411,49 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
 
-    W = min(args.warmup, 1)
     budget_s = 150.0
-    stream, wl = make_workload(args.config, W + args.steps, scale=args.scale)
-    rp, col, val = stream.csr0()
-    orp, ocol, oval = operator_csr(rp, col, val, wl["operator"])
+    stream, wl = make_workload(args.config, args.warmup + args.steps, scale=args.scale)
+    # the GPU arm times steps [warmup, warmup + steps): start the CPU port at the
+    # same graph (the first `warmup` batches applied to the edge set on the host,
+    # set algebra, no tracking), one untimed step, then the same window
+    skip = args.warmup if hasattr(stream, "keys0") else 0
+    if skip:
+        from paper_2603_19439_b200.streams import _EdgeSet, csr_from_keys
+
+        es = _EdgeSet(stream.n0, stream.keys0)
+        for t in range(skip):
+            u = stream.updates[t]
+            rk = np.minimum(u.removed[0], u.removed[1]) * (1 << 32) + np.maximum(u.removed[0], u.removed[1])
+            ak = np.minimum(u.added[0], u.added[1]) * (1 << 32) + np.maximum(u.added[0], u.added[1])
+            nk = np.minimum(u.new_edges[0], u.new_edges[1]) * (1 << 32) + np.maximum(u.new_edges[0], u.new_edges[1])
+            es.apply(np.asarray(ak, np.int64), np.sort(np.asarray(rk, np.int64)), int(u.n_new), np.asarray(nk, np.int64))
+        rp, col, val = csr_from_keys(es.n, es.keys)
+    else:
+        rp, col, val = stream.csr0()
     n = len(rp) - 1
     rng = np.random.default_rng(0)
     x, _ = np.linalg.qr(rng.standard_normal((n, wl["k"])))  # X0 quality does not change the step cost
     a = po.Csr(n, rp, col, val)
     o = po.Session(a, kind=wl["kind"], k=wl["k"], order=wl["order"], operator=wl["operator"], seed=0,
                    values=np.linspace(wl["k"], 1, wl["k"]), vectors=x)
-    for t in range(W):
-        o.step(stream.updates[t])
     times = []
-    for t in range(W, W + args.steps):
+    for t in range(skip, skip + args.steps):
         t0 = time.perf_counter()
         o.step(stream.updates[t])
         times.append(time.perf_counter() - t0)
         if sum(times) > budget_s:
             break
     value = len(times) / sum(times)
-    sample = (f"{len(times)} of {args.steps} requested timed steps (budget {budget_s:.0f} s) after {W} warm-up, "
-              f"oracle restatement with OpenMP {threads} threads")
+    sample = (f"steps {skip}..{skip + len(times) - 1} of the stream ({len(times)} of {args.steps} requested, budget "
+              f"{budget_s:.0f} s; the GPU arm's timed window starts at step {args.warmup}), the graph fast-forwarded "
+              f"through the first {skip} batches on the host, oracle restatement with OpenMP {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
-        "steps": len(times), "warmup": W, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["workload"], "n0": n, "nnz0": int(rp[-1]), "k": wl["k"]},
+        "config": {"workload": wl["workload"], "n0": int(stream.n0), "nnz0": int(stream.nnz0() if hasattr(stream, "nnz0") else 2 * len(stream.keys0)),
+                   "k": wl["k"], "kind": wl["kind"], "rsvd_l": 100, "rsvd_p": 100,
+                   "timed_from": {"step": skip, "n": n, "nnz": int(rp[-1])}},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
