@@ -1464,6 +1464,7 @@ class Session {
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
   const int spmm_fused_min_m_ = getenv("STG_SPMM_FUSED_MIN_M") ? atoi(getenv("STG_SPMM_FUSED_MIN_M")) : 129;
   const bool spmm_chunked_ = !getenv_flag("STG_SPMM_NOCHUNK");  // development A/B
+  const int spmm_chunk_tmax_ = getenv("STG_SPMM_TMAX") ? atoi(getenv("STG_SPMM_TMAX")) : 2;  // development A/B
   const int merge_mode_ = getenv("STG_MERGE_MODE") ? atoi(getenv("STG_MERGE_MODE")) : 3;  // development A/B
 
   PlanEntry& spmm_plan(const SpmmArgs& a, i64 nnz) {
@@ -1544,7 +1545,7 @@ class Session {
         spmm_fused_launch(b, pl, long_rows ? pe.vmax : 0, st_);
         launches += 1;
       } else if (spmm_chunked_) {  // one launch: segments, then streamed row chunks, per column slab
-        spmm_chunk_launch(b, pl, long_rows ? pe.vmax : 0, st_);
+        spmm_chunk_launch(b, pl, long_rows ? pe.vmax : 0, spmm_chunk_tmax_, st_);
         launches += 1;
       } else {
         spmm_launch(b, pl, pe.vmax, pe.split_max, long_rows, st_);

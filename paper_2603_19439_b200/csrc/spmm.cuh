@@ -712,21 +712,29 @@ struct ChunkSmem {
   double val[kChunkMax];
 };
 
-template <int VW>
+template <int VW, int T>  // T slabs of 32 VW columns per warp
 __global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a, SpmmPlan pl) {
   using V = SpV<VW>;
   using VT = typename V::T;
-  constexpr int W = 32 * VW;
+  constexpr int SW = 32 * VW, W = SW * T;
+  constexpr int U = 8 / T;  // entries per batch (U x T loads in flight per lane)
   __shared__ ChunkSmem csm[kChunkWarps];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   ChunkSmem& cs = csm[wib];
   const int c0 = static_cast<int>(blockIdx.y) * W;
-  const bool on = c0 + VW * lane < a.m;
+  bool on[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t) on[t] = c0 + SW * t + VW * lane < a.m;
   const double* Xs = a.X + c0 + VW * lane;
   double* Ys = a.Y + c0 + VW * lane;
   const int* rowp = a.rowptr + a.row_off;
   const i64 gw = static_cast<i64>(blockIdx.x) * kChunkWarps + wib, nw = static_cast<i64>(gridDim.x) * kChunkWarps;
-  // ---- long-row segments of this slab
+  auto store = [&](double* yr, const VT (&v)[T]) {
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+      if (on[t]) V::st(yr + SW * t, v[t]);
+  };
+  // ---- long-row segments of this column block
   const i64 nseg = pl.vstart[a.rows];
   i64 w = gw;
   for (; w < nseg; w += nw) {
@@ -746,42 +754,43 @@ __global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a
         v_l = 0.0;
       }
     }
-    VT acc = V::zero();
-    for (int q = 0; q < cnt; q += 8) {  // eight entries' loads in flight, sums in column order
-      VT xv[8];
-      double vv[8];
+    VT acc[T];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+    for (int t = 0; t < T; ++t) acc[t] = V::zero();
+    for (int q = 0; q < cnt; q += U) {  // U entries' loads in flight, sums in column order
+      VT xv[U][T];
+      double vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         const int c = __shfl_sync(0xffffffffu, c_l, (q + u) & 31);
         vv[u] = __shfl_sync(0xffffffffu, v_l, (q + u) & 31);
-        xv[u] = (q + u < cnt && on) ? V::ld(Xs + static_cast<i64>(c) * a.ldx) : V::zero();
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          xv[u][t] = (q + u < cnt && on[t]) ? V::ld(Xs + static_cast<i64>(c) * a.ldx + SW * t) : V::zero();
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q + u < cnt) V::fma(acc, vv[u], xv[u]);
+      for (int u = 0; u < U; ++u)
+        if (q + u < cnt)
+#pragma unroll
+          for (int t = 0; t < T; ++t) V::fma(acc[t], vv[u], xv[u][t]);
     }
     const int slot0 = pl.sstart[r];
-    if (on) V::st(pl.scratch + static_cast<i64>(slot0 + sg) * pl.lds + c0 + VW * lane, acc);
+    store(pl.scratch + static_cast<i64>(slot0 + sg) * pl.lds + c0 + VW * lane, acc);
     __threadfence();
     int last = 0;
     int* ctr = pl.segcnt + static_cast<i64>(slot0) * gridDim.y + blockIdx.y;
     if (lane == 0) last = atomicAdd(ctr, 1) == nsg - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {  // every partial of row r (this slab) is written: add them in segment order
+    if (last) {  // every partial of row r (this column block) is written: add them in segment order
       __threadfence();
       const double* p0 = pl.scratch + static_cast<i64>(slot0) * pl.lds + c0 + VW * lane;
-      VT tot = V::zero();
-      int q = 0;
-      for (; q + 4 <= nsg; q += 4) {
-        VT tv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) tv[u] = on ? V::ldcg(p0 + static_cast<i64>(q + u) * pl.lds) : V::zero();
+      for (int t = 0; t < T; ++t) acc[t] = V::zero();
+      for (int q = 0; q < nsg; ++q)
 #pragma unroll
-        for (int u = 0; u < 4; ++u) V::add(tot, tv[u]);
-      }
-      for (; q < nsg; ++q)
-        if (on) V::add(tot, V::ldcg(p0 + static_cast<i64>(q) * pl.lds));
-      if (on) V::st(Ys + static_cast<i64>(r) * a.ldy, tot);
+        for (int t = 0; t < T; ++t)
+          if (on[t]) V::add(acc[t], V::ldcg(p0 + static_cast<i64>(q) * pl.lds + SW * t));
+      store(Ys + static_cast<i64>(r) * a.ldy, acc);
       if (lane == 0) *ctr = 0;
     }
   }
@@ -816,55 +825,75 @@ __global__ void __launch_bounds__(32 * kChunkWarps) spmm_chunk_kernel(SpmmArgs a
         }
       }
       unsigned zm = __ballot_sync(0xffffffffu, zero);
+      VT z[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) z[t] = V::zero();
       while (zm) {
         const int j = __ffs(zm) - 1;
         zm &= zm - 1;
-        if (on) V::st(Ys + static_cast<i64>(r0 + i0 + j) * a.ldy, V::zero());
+        store(Ys + static_cast<i64>(r0 + i0 + j) * a.ldy, z);
       }
     }
     __syncwarp();
     // stream the entries: batch b + 1's X rows in flight while batch b is summed
     int cur = -1;
-    VT acc = V::zero();
-    VT xn[8];
+    VT acc[T];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) xn[u] = (u < ns && on) ? V::ld(Xs + static_cast<i64>(cs.col[u]) * a.ldx) : V::zero();
-    for (int b = 0; b < ns; b += 8) {
-      VT xc[8];
+    for (int t = 0; t < T; ++t) acc[t] = V::zero();
+    VT xn[U][T];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) xc[u] = xn[u];
+    for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = b + 8 + u;
-        xn[u] = (j < ns && on) ? V::ld(Xs + static_cast<i64>(cs.col[j]) * a.ldx) : V::zero();
+      for (int t = 0; t < T; ++t)
+        xn[u][t] = (u < ns && on[t]) ? V::ld(Xs + static_cast<i64>(cs.col[u]) * a.ldx + SW * t) : V::zero();
+    for (int b = 0; b < ns; b += U) {
+      VT xc[U][T];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int t = 0; t < T; ++t) xc[u][t] = xn[u][t];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = b + U + u;
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          xn[u][t] = (j < ns && on[t]) ? V::ld(Xs + static_cast<i64>(cs.col[j]) * a.ldx + SW * t) : V::zero();
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int j = b + u;
         if (j >= ns) break;
         const int rw = cs.row[j];
         if (rw != cur) {
-          if (cur >= 0 && on) V::st(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
+          if (cur >= 0) store(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
           cur = rw;
-          acc = V::zero();
+#pragma unroll
+          for (int t = 0; t < T; ++t) acc[t] = V::zero();
         }
-        V::fma(acc, cs.val[j], xc[u]);
+        const double vj = cs.val[j];
+#pragma unroll
+        for (int t = 0; t < T; ++t) V::fma(acc[t], vj, xc[u][t]);
       }
     }
-    if (cur >= 0 && on) V::st(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
+    if (cur >= 0) store(Ys + static_cast<i64>(r0 + cur) * a.ldy, acc);
   }
 }
 
-inline void spmm_chunk_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, cudaStream_t st) {
+inline void spmm_chunk_launch(const SpmmArgs& a, const SpmmPlan& pl, i64 vmax, int tmax, cudaStream_t st) {
   const bool vec2 = a.m > 32 && a.m % 2 == 0 && a.ldx % 2 == 0 && a.ldy % 2 == 0 && pl.lds % 2 == 0 &&
                     ((reinterpret_cast<uintptr_t>(a.X) | reinterpret_cast<uintptr_t>(a.Y) |
                       reinterpret_cast<uintptr_t>(pl.scratch)) & 15) == 0;
-  const int W = vec2 ? 64 : 32;
+  // columns per warp: one 32-column slab (m <= 32), else 64-column slabs, up to tmax per warp
+  const int T = vec2 ? static_cast<int>(std::min<i64>(tmax, cdiv(a.m, 64))) : 1;
+  const int W = vec2 ? 64 * (T >= 4 ? 4 : T >= 2 ? 2 : 1) : 32;
   const i64 items = vmax + pl.nch;
-  const unsigned gx = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(cdiv(items, kChunkWarps), 148 * (vec2 ? 2 : 3))));
+  const int per_sm = !vec2 ? 3 : T >= 2 ? 1 : 2;
+  const unsigned gx = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(cdiv(items, kChunkWarps), 148 * per_sm)));
   const dim3 grid(gx, static_cast<unsigned>(cdiv(a.m, W)));
-  if (vec2) spmm_chunk_kernel<2><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
-  else spmm_chunk_kernel<1><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  if (!vec2) spmm_chunk_kernel<1, 1><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  else if (W == 64) spmm_chunk_kernel<2, 1><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  else if (W == 128) spmm_chunk_kernel<2, 2><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
+  else spmm_chunk_kernel<2, 4><<<grid, 32 * kChunkWarps, 0, st>>>(a, pl);
   STG_LAUNCH();
 }
 
