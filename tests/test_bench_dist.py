@@ -54,3 +54,19 @@ def test_reference_arm_nonzero_ranks_exit_quietly(capsys, monkeypatch):
 
     bench.run_reference(A())
     assert capsys.readouterr().out == ""
+
+
+def test_bench_module_defines_every_leg():
+    """bench.py's legs import and the clock sampler degrades without nvidia-smi
+    (a broken module would only show up on the GPU box)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    for name in ("ClockSampler", "run_ours", "run_reference", "cpu_baseline", "make_workload", "dist_max", "main"):
+        assert hasattr(m, name), name
+    c = m.ClockSampler(0)
+    c.proc = None
+    out = c.stop()
+    assert set(out) == {"sm_mhz", "sm_max_mhz", "reasons", "samples"}
