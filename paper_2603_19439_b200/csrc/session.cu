@@ -1464,7 +1464,7 @@ class Session {
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
   const int spmm_fused_min_m_ = getenv("STG_SPMM_FUSED_MIN_M") ? atoi(getenv("STG_SPMM_FUSED_MIN_M")) : 129;
   const bool spmm_chunked_ = !getenv_flag("STG_SPMM_NOCHUNK");  // development A/B
-  const int spmm_chunk_tmax_ = getenv("STG_SPMM_TMAX") ? atoi(getenv("STG_SPMM_TMAX")) : 2;  // development A/B
+  const int spmm_chunk_tmax_ = getenv("STG_SPMM_TMAX") ? atoi(getenv("STG_SPMM_TMAX")) : 1;  // development A/B (1 measured best)
   const int merge_mode_ = getenv("STG_MERGE_MODE") ? atoi(getenv("STG_MERGE_MODE")) : 3;  // development A/B
 
   PlanEntry& spmm_plan(const SpmmArgs& a, i64 nnz) {
