@@ -410,6 +410,190 @@ __device__ void tridiag_body(const double* M, int ldm, int n, int sym_input, int
   }
 }
 
+// One-CTA tridiagonalization with the rank-2 update fused into the next
+// column's sums (n <= kEig1N, full square in shared memory). Reflector i is
+// applied lazily: column i + 1 gets it in a short pre-pass (P), and the pass
+// that forms column i + 1's sums (F) reads each trailing element, applies
+// reflector i (the same fma order as tri_update_rows), writes it back and
+// accumulates it into the sums in the same visit — one read-modify-write of
+// the trailing square per column instead of a read (sums) plus a read-modify-
+// write (update). Warps split the trailing columns into 32-column blocks and
+// the rows G ways (as the two-pass kernel's sums); the last warp derives the
+// reflector while the others run F. Three barriers per column.
+constexpr int kTri1fThreads = 512;  // 16 warps (1024 measured slower: 842 vs 765 us at n = 164)
+constexpr int kTri1fW = kTri1fThreads / 32;
+inline size_t tridiag1f_smem_bytes(int n, int gmax) {
+  return sizeof(double) * (static_cast<size_t>(n) * n + 5 * static_cast<size_t>(n) + static_cast<size_t>(gmax) * n +
+                           kTri1fW * 4 + 8);
+}
+inline int tridiag1f_gmax(int n) {
+  int g = 4;
+  while (g > 1 && tridiag1f_smem_bytes(n, g) > 232448) --g;
+  return g;
+}
+
+__global__ void __launch_bounds__(kTri1fThreads) tridiag1f_kernel(const double* M, int ldm, int n, int sym_input,
+                                                                int gmax, EigBufs b, int* flags) {
+  extern __shared__ double sm[];
+  double* A = sm;                                  // n x n
+  double* col = A + static_cast<i64>(n) * n;       // [n] column i (rows > i) with every reflector applied
+  double* a0 = col + n;                            // [n] row i + 1 (columns >= i + 1) with every reflector applied
+  double* Pv = a0 + n;                             // [n] the pending reflector: p
+  double* Vv = Pv + n;                             //                            v
+  double* Wv = Vv + n;                             //                            w = p - b2 v
+  double* acc = Wv + n;                            // [gmax][n] partial column sums
+  double* pvs = acc + static_cast<i64>(gmax) * n;  // [kTri1fW][4]: (Av)'v pieces, squared-norm share
+  double* scl = pvs + kTri1fW * 4;                   // {tau, scal, beta, alpha}
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (sym_input) {
+    for (int r = warp; r < n; r += kTri1fW)
+      for (int c = lane; c < n; c += 32) cp_async8(A + static_cast<i64>(r) * n + c, M + static_cast<i64>(r) * ldm + c);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    int bad = 0;
+    for (int r = warp; r < n; r += kTri1fW)
+      for (int c = lane; c < n; c += 32) bad |= !isfinite(A[static_cast<i64>(r) * n + c]);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, kNonFinite);
+  } else {
+    for (int r = warp; r < n; r += kTri1fW)
+      for (int c = lane; c < n; c += 32) {
+        const double x = M[static_cast<i64>(r) * ldm + c];
+        const double y = M[static_cast<i64>(c) * ldm + r];
+        if (!isfinite(x) || !isfinite(y)) atomicOr(flags, kNonFinite);
+        A[static_cast<i64>(r) * n + c] = 0.5 * (x + y);
+      }
+  }
+  for (int r = tid; r < n; r += kTri1fThreads) Pv[r] = Vv[r] = Wv[r] = 0.0;  // no reflector pending
+  __syncthreads();
+  for (int i = 0; i + 1 < n; ++i) {
+    const int r0 = i + 1;
+    // P: column i with the pending reflector (rows >= i); its squared norm below r0 and alpha
+    {
+      const double vi = Vv[i], wi = Wv[i];
+      double sg = 0.0;
+      for (int c = i + tid; c < n; c += kTri1fThreads) {
+        const double x = fma(-Vv[c], wi, fma(-Pv[c], vi, A[static_cast<i64>(c) * n + i]));
+        if (c == i) {
+          b.d[i] = x;
+        } else {
+          col[c] = x;
+          if (c == r0) scl[3] = x;
+          else sg = fma(x, x, sg);
+        }
+      }
+      sg = warp_sum(sg);
+      if (lane == 0) pvs[warp * 4 + 3] = sg;
+    }
+    __syncthreads();
+    const int nblk = (n - r0 + 31) >> 5;
+    const int G = min(gmax, (kTri1fW - 1) / nblk);
+    const int nsw = nblk * G;
+    if (warp < nsw) {
+      // F: reflector i-1 applied to the trailing square, the sums of column i formed on the way
+      const int blk = warp % nblk, g = warp / nblk;
+      const int r = r0 + 32 * blk + lane;
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (r < n) {
+        const double vr = Vv[r], wr = Wv[r];
+        if (g == 0) {  // row r0 -> a0
+          double* Ar = A + static_cast<i64>(r0) * n + r;
+          const double x = fma(-Vv[r0], wr, fma(-Pv[r0], vr, *Ar));
+          *Ar = x;
+          a0[r] = x;
+          if (r != r0) s1 = x * col[r];
+        }
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = r0 + 1 + g;  // rows c > r0, every G-th
+        for (; c + 3 * G < n; c += 4 * G) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int cu = c + u * G;
+            double* Ar = A + static_cast<i64>(cu) * n + r;
+            const double x = fma(-Vv[cu], wr, fma(-Pv[cu], vr, *Ar));
+            *Ar = x;
+            a4[u] = fma(x, col[cu], a4[u]);
+          }
+        }
+        for (; c < n; c += G) {
+          double* Ar = A + static_cast<i64>(c) * n + r;
+          const double x = fma(-Vv[c], wr, fma(-Pv[c], vr, *Ar));
+          *Ar = x;
+          a4[0] = fma(x, col[c], a4[0]);
+        }
+        const double ac = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        acc[static_cast<i64>(g) * n + r] = ac;
+        if (r == r0) s3 = ac;
+        else s2 = ac * col[r];
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      s3 = warp_sum(s3);
+      if (lane == 0) {
+        pvs[warp * 4 + 0] = s1;
+        pvs[warp * 4 + 1] = s2;
+        pvs[warp * 4 + 2] = s3;
+      }
+    } else if (warp == kTri1fW - 1) {
+      // reflector i from column i (beside F)
+      const double sigma = warp_sum(lane < kTri1fW ? pvs[lane * 4 + 3] : 0.0);
+      const double alpha = scl[3];
+      double t = 0.0, scal = 0.0, beta = alpha;
+      if (sigma > 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + sigma), alpha);
+        t = (beta - alpha) * __drcp_rn(beta);
+        scal = __drcp_rn(alpha - beta);
+      }
+      if (lane == 0) {
+        scl[0] = t;
+        scl[1] = scal;
+        scl[2] = beta;
+        b.tau[i] = t;
+        b.e[i] = beta;
+        b.e2[i] = beta * beta;
+      }
+      for (int c = r0 + lane; c < n; c += 32) b.V[static_cast<i64>(i) * n + c] = c == r0 ? 1.0 : col[c] * scal;
+    }
+    __syncthreads();
+    // the pending reflector becomes reflector i
+    {
+      const double t = scl[0], scal = scl[1];
+      double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (lane < nsw) {
+        s1 = pvs[lane * 4 + 0];
+        s2 = pvs[lane * 4 + 1];
+        s3 = pvs[lane * 4 + 2];
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      s3 = warp_sum(s3);
+      const double avv = a0[r0] + scal * (s3 + s1) + scal * scal * s2;  // (Av)'v
+      const double b2 = t * t * avv;
+      for (int r = r0 + tid; r < n; r += kTri1fThreads) {
+        if (t == 0.0) {
+          Pv[r] = Vv[r] = Wv[r] = 0.0;
+          continue;
+        }
+        double sa = 0.0;
+        for (int q = 0; q < G; ++q) sa += acc[static_cast<i64>(q) * n + r];
+        const double pr = t * fma(scal, sa, a0[r]);
+        const double vr = r == r0 ? 1.0 : scal * col[r];
+        Pv[r] = pr;
+        Vv[r] = vr;
+        Wv[r] = pr - b2 * vr;
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const int l = n - 1;
+    b.d[l] = fma(-Vv[l], Wv[l], fma(-Pv[l], Vv[l], A[static_cast<i64>(l) * n + l]));
+    b.e[l] = 0.0;
+    b.e2[l] = 0.0;
+    b.tau[l] = 0.0;
+  }
+}
+
 __global__ void __launch_bounds__(kTriThreads) tridiag1_kernel(const double* M, int ldm, int n, int sym_input,
                                                                int gmax, EigBufs b, int* flags) {
   tridiag_body<1>(M, ldm, n, sym_input, gmax, b, flags, 0);
@@ -746,6 +930,8 @@ inline void eig_set_attributes() {
                                 232448));
   STG_CUDA(cudaFuncSetAttribute(tridiag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 232448));
+  STG_CUDA(cudaFuncSetAttribute(tridiag1f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                232448));
   STG_CUDA(cudaFuncSetAttribute(backtransform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(sizeof(double) * 2 * kBtRows * kEigMaxN)));
   STG_CUDA(cudaFuncSetAttribute(invit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -760,7 +946,11 @@ void syev_launch(Launch&& L, const double* M, int ldm, int n, int sym_input, int
                  double* F, int ldf, double* dbuf, int* ibuf, int* flags) {
   const EigBufs b = eig_carve(dbuf, ibuf, n, want);
   static const int one_cta_max = getenv("STG_EIG1N") ? atoi(getenv("STG_EIG1N")) : kEig1N;  // development A/B
-  if (n <= one_cta_max) {
+  static const bool two_pass = getenv("STG_TRI_TWOPASS") && atoi(getenv("STG_TRI_TWOPASS")) != 0;  // development A/B
+  if (n <= one_cta_max && !two_pass) {
+    const int g = tridiag1f_gmax(n);
+    L(tridiag1f_kernel, dim3(1), dim3(kTri1fThreads), tridiag1f_smem_bytes(n, g), M, ldm, n, sym_input, g, b, flags);
+  } else if (n <= one_cta_max) {
     const int g = tridiag_gmax(n, 1);
     L(tridiag1_kernel, dim3(1), dim3(kTriThreads), tridiag_smem_bytes(n, 1, g), M, ldm, n, sym_input, g, b, flags);
   } else {
