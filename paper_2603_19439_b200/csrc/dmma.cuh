@@ -931,12 +931,21 @@ __global__ void __launch_bounds__(NT, 3)
     const double* sb = same ? sa : sa + STG;
     const double* pa = sa + t * kStreamPitch + g;
     const double* pb = sb + t * kStreamPitch + g;
+    // optional row mask: rows with mask[r] == mask_val contribute nothing (their A fragments read as 0)
+    unsigned mk = 0;
+    if (a.mask) {
+      const i64 rb = static_cast<i64>(b + q * G) * kGsRows + warp * 16 + t;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (rb + 4 * u < a.nrows && a.mask[rb + 4 * u] == a.mask_val) mk |= 1u << u;
+    }
 #pragma unroll
     for (int kk = 0; kk < 16; kk += 4) {
       double fa[4], fb[4];
+      const bool z = (mk >> (kk >> 2)) & 1u;
 #pragma unroll
       for (int x = 0; x < 4; ++x) {
-        fa[x] = pa[kk * kStreamPitch + x * 8];
+        fa[x] = z ? 0.0 : pa[kk * kStreamPitch + x * 8];
         fb[x] = pb[kk * kStreamPitch + x * 8];
       }
 #pragma unroll

@@ -400,6 +400,7 @@ class Session {
       STG_CUDA(cudaStreamCreateWithPriority(&st_rot_, cudaStreamNonBlocking, (lo + hi) / 2));
     }
     STG_CUDA(cudaEventCreateWithFlags(&ev_rot_ready_, cudaEventDisableTiming));
+    STG_CUDA(cudaEventCreateWithFlags(&ev_k_, cudaEventDisableTiming));
     STG_CUDA(cudaEventCreateWithFlags(&ev_rot_done_, cudaEventDisableTiming));
     STG_CUDA(cudaStreamCreateWithFlags(&st_rng_, cudaStreamNonBlocking));
     arena_.init(cfg.device, st_, {st_eig_, st_mg_, st_rng_});
@@ -516,6 +517,7 @@ class Session {
     cudaEventDestroy(ev_mg_);
     cudaStreamDestroy(st_mg_);
     cudaEventDestroy(ev_rot_ready_);
+    cudaEventDestroy(ev_k_);
     cudaEventDestroy(ev_rot_done_);
     cudaStreamDestroy(st_rot_);
     cudaStreamDestroy(st_);
@@ -1275,21 +1277,22 @@ class Session {
     splits = std::max<i64>(1, cdiv(std::max<i64>(rows, 1), a.rows_per_split));
     const i64 m1p = narrow ? 32 : static_cast<i64>(a.tiles_i) * TA;
     const i64 m2p = narrow ? 32 : static_cast<i64>(a.tiles_j) * TB;
-    a.partial = arena_.get<double>("gram_partial", splits * m1p * m2p);
+    a.partial = arena_.get<double>(gram_partial_tag_, splits * m1p * m2p);
     if (klog_) snprintf(ktag_, sizeof(ktag_), "gram %lldx%dx%d%s", rows, m1, m2, sym ? " sym" : "");
     kbegin(mask ? kKcGram : narrow ? kGramNarrow : kGram,
            sym ? static_cast<double>(rows) * m1 * (m1 + 1) : 2.0 * rows * m1 * m2, nullptr,
            8.0 * rows * (sym ? m1 : m1 + m2) + 8.0 * m1 * m2);
     const dim3 grid(ntiles, static_cast<unsigned>(splits));
-    const bool bulk = !mask && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
-                      lda % 2 == 0 && ldb % 2 == 0;
-    if (narrow && bulk) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                         lda % 2 == 0 && ldb % 2 == 0;
+    const bool bulk = !mask && aligned;
+    if (narrow && aligned) {  // the streaming kernel (a row mask zeroes the masked rows' fragments)
       const bool same = A == B && lda == ldb;
       const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::kStreamPitch, dm::kGsRows);
       const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, dm::kStreamPitch, dm::kGsRows);
       const int ntl = static_cast<int>(cdiv(std::max<i64>(rows, 1), dm::kGsRows));
       const int G = std::min(ntl, 148 * (same ? 3 : 1));
-      a.partial = arena_.get<double>("gram_partial", static_cast<i64>(G) * 1024);
+      a.partial = arena_.get<double>(gram_partial_tag_, static_cast<i64>(G) * 1024);
       launch(dm::gram_stream_kernel, dim3(static_cast<unsigned>(G)), dim3(dm::NT), dm::gram_stream_smem(same), st_,
              a, ma, mb, same ? 1 : 0, ntl);
       gram_reduce(a.partial, G, m1, m2, 32, 32, a.sym, out, ldo, alpha);
@@ -1462,6 +1465,12 @@ class Session {
   std::vector<PlanEntry> plans_;
   int plan_epoch_ = 0;
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
+  const char* gram_partial_tag_ = "gram_partial";  // the side stream's Grams use their own split-K buffer
+  // K = X_out'X_out and its Cholesky computed on st_eig_ right after P's marks,
+  // while the host waits for |P| (the rows of P masked instead of zeroed)
+  const bool k_early_ = !getenv_flag("STG_NO_K_EARLY");  // development A/B
+  cudaEvent_t ev_k_ = nullptr;
+  bool k_ready_ = false;
   const int spmm_fused_min_m_ = getenv("STG_SPMM_FUSED_MIN_M") ? atoi(getenv("STG_SPMM_FUSED_MIN_M")) : 129;
   const bool spmm_chunked_ = !getenv_flag("STG_SPMM_NOCHUNK");  // development A/B
   const int spmm_chunk_tmax_ = getenv("STG_SPMM_TMAX") ? atoi(getenv("STG_SPMM_TMAX")) : 1;  // development A/B (1 measured best)
@@ -2160,6 +2169,8 @@ class Session {
     scan_int(flag, pos, n_total + 1);
     launch(scatter_p_kernel, dim3(blocks(n_total)), dim3(256), 0, st_, static_cast<const int*>(flag),
            static_cast<const int*>(pos), n_total, P, posmap_);
+    k_ready_ = false;
+    if (k_early_ && keep_delta && !is_laplacian()) early_k(n_old);
     STG_CUDA(cudaMemcpyAsync(&hs_->p, pos + n_total, sizeof(int), cudaMemcpyDeviceToHost, st_));
     if (kt_p) kend();
     STG_CUDA(cudaStreamSynchronize(st_));
@@ -3017,6 +3028,29 @@ class Session {
     xrestore_.active = false;
   }
 
+  // K = sum over the rows of X outside P of x x' (the marks of P masked) and
+  // its Cholesky R_c, on st_eig_ (the previous step's rotation of X first);
+  // build_xbar waits for ev_k_. In dense mode K is not used.
+  void early_k(i64 x_rows) {
+    const int kk = static_cast<int>(k);
+    const int ldr = ld_for(kk);
+    double* kc = arena_.get<double>("Kc", static_cast<i64>(kk) * ldr, /*side_use*/ true);
+    double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ldr, /*side_use*/ true);
+    arena_.get<double>("gram_partial_k", 148 * 3 * 1024, /*side_use*/ true);
+    STG_CUDA(cudaEventRecord(ev_k_, st_));
+    STG_CUDA(cudaStreamWaitEvent(st_eig_, ev_k_, 0));
+    if (rot_pending_) STG_CUDA(cudaStreamWaitEvent(st_eig_, ev_rot_done_, 0));  // X's rotation; st_ keeps its own wait
+    std::swap(st_, st_eig_);
+    const char* saved = gram_partial_tag_;
+    gram_partial_tag_ = "gram_partial_k";
+    gram(X_, ldx(), X_, ldx(), x_rows, kk, kk, true, kc, ldr, 1.0, mark_p_, stamp_);
+    chol(kc, ldr, kk, rc, ldr, nullptr, 0, nullptr, 0.0, true);
+    gram_partial_tag_ = saved;
+    std::swap(st_, st_eig_);
+    STG_CUDA(cudaEventRecord(ev_k_, st_eig_));
+    k_ready_ = true;
+  }
+
   void build_xbar(const Pert& pt, Blk z) {
     const i64 p = pt.p;
     const int kk = static_cast<int>(k);
@@ -3024,7 +3058,11 @@ class Session {
     double* rc = arena_.get<double>("Rc", static_cast<i64>(kk) * ldr);
     launch(gather_xbar_kernel, dim3(blocks((p + 2 * k) * k)), dim3(256), 0, st_, static_cast<const double*>(X_), ldx(),
            pt.Ploc, pt.dense ? 1 : 0, p, pt.p_old, kk, static_cast<const double*>(nullptr), ldr, z.p, z.ld);
-    if (!pt.dense) {
+    if (!pt.dense && k_ready_ && !sh_) {  // K and R_c came from early_k (X untouched)
+      STG_CUDA(cudaStreamWaitEvent(st_, ev_k_, 0));
+      launch(copy2d_kernel, dim3(blocks(k * k)), dim3(256), 0, st_, static_cast<const double*>(rc), ldr, z.p + p * z.ld,
+             z.ld, k, kk);
+    } else if (!pt.dense) {
       if (pt.p_old > 0) {
         launch(zero_rows_kernel, dim3(blocks(pt.p_old, 8)), dim3(256), 0, st_, X_, ldx(), pt.Ploc, pt.p_old, kk);
         xrestore_ = XRestore{true, pt.Ploc, pt.p_old, z.p, z.ld};
