@@ -13,6 +13,8 @@
 // All blocks are row-major with even leading dimensions.
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace stg {
@@ -36,6 +38,10 @@ struct GramArgs {
   int sym;
   const int* mask;  // optional: rows with mask[r] == mask_val contribute nothing
   int mask_val;
+  // persistent kernels: item i is (tile order[i / splits], split i % splits) when `ordered` (the host sorts
+  // the tiles by DMMA work, heaviest first, so the light edge tiles fill the tail), else (i % ntiles, i / ntiles)
+  int ordered;
+  unsigned char order[64];
 };
 
 // Loads rows [r, r+BK) x cols [c0, c0+64) of a row-major block into s[BK][SST],
@@ -232,7 +238,22 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2) gram_tn_kernel(GramArgs 
 // row pitch; columns/rows outside the matrix arrive as zeros). kStages stages
 // form a ring with full (transaction-counted) and empty mbarriers: the four
 // warps never meet at a CTA barrier and no thread computes load addresses.
-constexpr int kBK = 16, kStages = 4;
+#ifndef STG_GRAM_STAGES
+#define STG_GRAM_STAGES 4
+#endif
+#ifndef STG_GRAM_MINB
+#define STG_GRAM_MINB 3
+#endif
+#ifndef STG_EMPTY_PER_WARP
+#define STG_EMPTY_PER_WARP 0
+#endif
+constexpr int kBK = 16, kStages = STG_GRAM_STAGES;
+// consumers release a stage per thread (NT arrivals) or, after __syncwarp, through one lane per warp
+constexpr unsigned kEmptyCount = STG_EMPTY_PER_WARP ? NT / 32 : NT;
+__device__ __forceinline__ void release_stage(unsigned long long* bar) {
+  __syncwarp();
+  if (!STG_EMPTY_PER_WARP || (threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
 
 template <int WM, int WN>
 constexpr size_t gram_tma_smem() {
@@ -240,7 +261,7 @@ constexpr size_t gram_tma_smem() {
 }
 
 template <int WM, int WN>
-__global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
+__global__ void __launch_bounds__(NT, WM == WN ? STG_GRAM_MINB : 2)
     gram_tma_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
+      mbar_init(&empty[st], kEmptyCount);
     }
     mbar_fence_init();
   }
@@ -315,8 +336,7 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
       warp_mma<4, 4, false, SA, 8, SB, 8, kBK>(acc, pa, pb);
     else
       warp_mma_dispatch<SA, 8, SB, 8, kBK>(code, acc, pa, pb);
-    __syncwarp();
-    mbar_arrive(&empty[st]);  // each thread's smem reads ordered before the TMA refill
+    release_stage(&empty[st]);  // the warp's smem reads ordered before the TMA refill
   }
   if (code == 0) return;
   const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
@@ -329,6 +349,381 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2)
       const i64 i = ibase + x * 8 + g, j = jbase + y * 8 + 2 * t;
       *reinterpret_cast<double2*>(out + i * m2p + j) = make_double2(acc[x][y][0], acc[x][y][1]);
     }
+}
+
+// ---- row-split warp layout for 64 x 64 CTA tiles. Each of the four warps
+// owns two 8-row fragment rows (xr0, xr1) and every live 8-column fragment of
+// the tile, so a tile with F <= 8 live fragment columns costs 2 F DMMA per
+// k-step in every warp: a narrow edge tile costs what it computes (the 2 x 2
+// layout of 32 x 32 warp tiles pays for a full quadrant as soon as one warp
+// has one), and on the diagonal tile of a symmetric Gram the rows are dealt
+// (w, 7 - w), 9 upper-triangle fragments per warp instead of 16 in the busiest
+// one. Fragment arithmetic and its k order are unchanged: same bits.
+template <int NX, int NY, int KA, int KB, int KR>
+__device__ __forceinline__ void rs_mma(double (&acc)[2][8][2], const double* pa0, const double* pa1,
+                                       const double* pb) {
+#pragma unroll
+  for (int kk = 0; kk < KR; kk += 4) {
+    double fa[2], fb[NY];
+    fa[0] = pa0[kk * KA];
+    fa[1] = NX == 2 ? pa1[kk * KA] : 0.0;
+#pragma unroll
+    for (int y = 0; y < NY; ++y) fb[y] = pb[kk * KB + y * 8];
+#pragma unroll
+    for (int x = 0; x < NX; ++x)
+#pragma unroll
+      for (int y = 0; y < NY; ++y) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
+  }
+}
+
+// full diagonal tile, warp W: fragment rows W (columns >= W) and 7 - W (columns >= 7 - W)
+template <int W, int KA, int KB, int KR>
+__device__ __forceinline__ void rs_mma_tri(double (&acc)[2][8][2], const double* pa0, const double* pa1,
+                                           const double* pb) {
+#pragma unroll
+  for (int kk = 0; kk < KR; kk += 4) {
+    double fb[8];
+    const double fa0 = pa0[kk * KA], fa1 = pa1[kk * KA];
+#pragma unroll
+    for (int y = W; y < 8; ++y) fb[y] = pb[kk * KB + y * 8];
+#pragma unroll
+    for (int y = W; y < 8; ++y) dmma(acc[0][y][0], acc[0][y][1], fa0, fb[y]);
+#pragma unroll
+    for (int y = 7 - W; y < 8; ++y) dmma(acc[1][y][0], acc[1][y][1], fa1, fb[y]);
+  }
+}
+
+// any shape (ragged diagonal tiles): warp-uniform guards at run time
+template <int KA, int KB, int KR>
+__device__ __forceinline__ void rs_mma_any(double (&acc)[2][8][2], const double* pa0, const double* pa1,
+                                           const double* pb, int nx, int ylo0, int ylo1, int F) {
+#pragma unroll
+  for (int kk = 0; kk < KR; kk += 4) {
+    const double fa0 = pa0[kk * KA], fa1 = pa1[kk * KA];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      if (y >= F) break;
+      const double fb = pb[kk * KB + y * 8];
+      if (nx > 0 && y >= ylo0) dmma(acc[0][y][0], acc[0][y][1], fa0, fb);
+      if (nx > 1 && y >= ylo1) dmma(acc[1][y][0], acc[1][y][1], fa1, fb);
+    }
+  }
+}
+
+// code: 0 none; 1..16 = (nx - 1) * 8 + F; 17..20 = full diagonal tile, warp code - 17; 21 = rs_mma_any
+template <int KA, int KB, int KR>
+__device__ __forceinline__ void rs_dispatch(int code, double (&acc)[2][8][2], const double* pa0, const double* pa1,
+                                            const double* pb, int nx, int ylo0, int ylo1, int F) {
+  switch (code) {
+#define STG_RS_CASE(NX, NY) \
+  case (NX - 1) * 8 + NY: rs_mma<NX, NY, KA, KB, KR>(acc, pa0, pa1, pb); break;
+    STG_RS_CASE(1, 1) STG_RS_CASE(1, 2) STG_RS_CASE(1, 3) STG_RS_CASE(1, 4)
+    STG_RS_CASE(1, 5) STG_RS_CASE(1, 6) STG_RS_CASE(1, 7) STG_RS_CASE(1, 8)
+    STG_RS_CASE(2, 1) STG_RS_CASE(2, 2) STG_RS_CASE(2, 3) STG_RS_CASE(2, 4)
+    STG_RS_CASE(2, 5) STG_RS_CASE(2, 6) STG_RS_CASE(2, 7) STG_RS_CASE(2, 8)
+#undef STG_RS_CASE
+    case 17: rs_mma_tri<0, KA, KB, KR>(acc, pa0, pa1, pb); break;
+    case 18: rs_mma_tri<1, KA, KB, KR>(acc, pa0, pa1, pb); break;
+    case 19: rs_mma_tri<2, KA, KB, KR>(acc, pa0, pa1, pb); break;
+    case 20: rs_mma_tri<3, KA, KB, KR>(acc, pa0, pa1, pb); break;
+    case 21: rs_mma_any<KA, KB, KR>(acc, pa0, pa1, pb, nx, ylo0, ylo1, F); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ int frags8_left(i64 extent, i64 base) {
+  const i64 f = (extent - base + 7) / 8;
+  return f < 0 ? 0 : f > 8 ? 8 : static_cast<int>(f);
+}
+
+// Persistent split-K Gram on 64 x 64 tiles in the row-split layout (the
+// scheduling of gram_persist_kernel below; same partial format).
+__global__ void __launch_bounds__(NT, STG_GRAM_MINB)
+    gram_persist_rs_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           int ntiles, int splits, int* ctr) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
+  unsigned long long* empty = full + kStages;
+  int2* meta = reinterpret_cast<int2*>(smraw + 64);
+  double* stage0 = reinterpret_cast<double*>(smraw + 128);
+  constexpr int SA = 68, SB = 68, STG = kBK * (SA + SB);
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int total = ntiles * splits;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kEmptyCount);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto tile_of = [&](int tile, int& ti, int& tj) {
+    if (a.sym) {
+      int r = tile;
+      ti = 0;
+      while (r >= a.tiles_i - ti) {
+        r -= a.tiles_i - ti;
+        ++ti;
+      }
+      tj = ti + r;
+    } else {
+      ti = tile / a.tiles_j;
+      tj = tile % a.tiles_j;
+    }
+  };
+  auto chunks_of = [&](int split) {
+    const i64 r0 = static_cast<i64>(split) * a.rows_per_split;
+    const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
+    return r1 > r0 ? static_cast<int>(cdiv(r1 - r0, kBK)) : 0;
+  };
+  int p_item = -1, p_q = 0, p_nch = 0, p_ca = 0, p_cb = 0, p_row0 = 0;
+  bool p_done = false, p_one = false;  // p_one: diagonal tile of a symmetric Gram, both operands are one box
+  auto produce = [&](int i) {
+    const int st = i % kStages;
+    if (i >= kStages) mbar_wait(&empty[st], static_cast<unsigned>((i / kStages - 1) & 1));
+    if (p_q == p_nch) {
+      const int item = atomicAdd(&ctr[0], 1);
+      if (item >= total) {
+        p_done = true;
+        if (atomicAdd(&ctr[1], 1) == static_cast<int>(gridDim.x) - 1) {
+          ctr[0] = 0;
+          ctr[1] = 0;
+        }
+        meta[st] = make_int2(-1, 0);
+        mbar_arrive(&full[st]);
+        return;
+      }
+      int ti, tj;
+      const int p_split = a.ordered ? item % splits : item / ntiles;
+      tile_of(a.ordered ? a.order[item / splits] : item % ntiles, ti, tj);
+      p_item = item;
+      p_q = 0;
+      p_ca = ti * 64;
+      p_cb = tj * 64;
+      p_one = a.sym && ti == tj;
+      p_row0 = static_cast<int>(static_cast<i64>(p_split) * a.rows_per_split);
+      p_nch = chunks_of(p_split);
+    }
+    meta[st] = make_int2(p_item, p_q);
+    double* sa = stage0 + st * STG;
+    mbar_arrive_expect_tx(&full[st], p_one ? kStageBytes / 2 : kStageBytes);
+    tma_load_2d(sa, &tmA, p_ca, p_row0 + p_q * kBK, &full[st]);
+    if (!p_one) tma_load_2d(sa + kBK * SA, &tmB, p_cb, p_row0 + p_q * kBK, &full[st]);
+    ++p_q;
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kStages - 1 && !p_done; ++i) produce(i);
+  double acc[2][8][2];
+  int nx = 0, F = 0, code = 0, nch = 0, split = 0, xr0 = 0, xr1 = 0, ylo0 = 0, ylo1 = 0, ti = 0, tj = 0, boff = 0;
+  for (int i = 0;; ++i) {
+    if (threadIdx.x == 0 && !p_done) produce(i + kStages - 1);
+    const int st = i % kStages;
+    mbar_wait(&full[st], static_cast<unsigned>((i / kStages) & 1));
+    const int2 m = meta[st];
+    if (m.x < 0) break;
+    if (m.y == 0) {  // a new item
+      tile_of(a.ordered ? a.order[m.x / splits] : m.x % ntiles, ti, tj);
+      split = a.ordered ? m.x % splits : m.x / ntiles;
+      nch = chunks_of(split);
+      const int R = frags8_left(a.m1, ti * 64);  // live fragment rows / columns of this tile
+      F = frags8_left(a.m2, tj * 64);
+      const bool diag = a.sym && ti == tj;
+      boff = diag ? 0 : kBK * SA;  // the diagonal tile's B operand is its A box
+      xr0 = warp;
+      xr1 = diag ? 7 - warp : warp + 4;
+      nx = (xr0 < R ? 1 : 0) + (xr1 < R ? 1 : 0);  // xr0 < xr1, so nx == 1 means row xr0 only
+      ylo0 = diag ? xr0 : 0;
+      ylo1 = diag ? xr1 : 0;
+      code = nx == 0 || F == 0 ? 0 : !diag ? (nx - 1) * 8 + F : (R == 8 && F == 8) ? 17 + warp : 21;
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    }
+    const double* sa = stage0 + st * STG;
+    const double* pa0 = sa + t * SA + xr0 * 8 + g;
+    const double* pa1 = sa + t * SA + xr1 * 8 + g;
+    const double* pb = sa + boff + t * SB + g;
+#ifndef STG_SKIP_MMA  // (development: the operand pipeline alone)
+    if (code == 16)
+      rs_mma<2, 8, SA, SB, kBK>(acc, pa0, pa1, pb);
+    else
+      rs_dispatch<SA, SB, kBK>(code, acc, pa0, pa1, pb, nx, ylo0, ylo1, F);
+#else
+    acc[0][0][0] += pa0[0] + pa1[0] + pb[0];
+#endif
+    release_stage(&empty[st]);
+    if (m.y != nch - 1 || code == 0) continue;
+    const i64 m1p = static_cast<i64>(a.tiles_i) * 64, m2p = static_cast<i64>(a.tiles_j) * 64;
+    double* out = a.partial + static_cast<i64>(split) * m1p * m2p;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x >= nx) continue;
+      const i64 ii = ti * 64 + (x ? xr1 : xr0) * 8 + g;
+      const int ylo = x ? ylo1 : ylo0;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        if (y >= F || y < ylo) continue;
+        const i64 jj = tj * 64 + y * 8 + 2 * t;
+        *reinterpret_cast<double2*>(out + ii * m2p + jj) = make_double2(acc[x][y][0], acc[x][y][1]);
+      }
+    }
+  }
+}
+
+// Host: a.order = the 64 x 64 tiles sorted by DMMA fragments (heaviest first, ties in tile order).
+inline void gram_tile_order(GramArgs& a, int ntiles) {
+  a.ordered = 0;
+  if (ntiles > 64) return;
+  int w[64], idx = 0;
+  for (int ti = 0; ti < a.tiles_i; ++ti)
+    for (int tj = a.sym ? ti : 0; tj < a.tiles_j; ++tj) {
+      const int R = static_cast<int>(std::min<i64>(8, cdiv(a.m1 - ti * 64, 8)));
+      const int F = static_cast<int>(std::min<i64>(8, cdiv(a.m2 - tj * 64, 8)));
+      w[idx++] = a.sym && ti == tj ? R * (R + 1) / 2 : R * F;
+    }
+  for (int i = 0; i < ntiles; ++i) a.order[i] = static_cast<unsigned char>(i);
+  std::stable_sort(a.order, a.order + ntiles, [&](unsigned char x, unsigned char y) { return w[x] > w[y]; });
+  a.ordered = 1;
+}
+
+// Persistent variant of gram_tma_kernel: a fixed grid pulls (split, tile) items
+// from a device counter (split major: the tiles of one row range run side by
+// side and share its rows in L2) and streams their 16-row chunks through one
+// TMA ring that keeps running across items, so the next item's rows are in
+// flight while this item's partial tile is stored, and light edge / diagonal
+// tiles balance themselves against full ones. Item (split, tile) writes the
+// same partial slot whichever CTA computes it: the reduction order and the
+// result do not depend on the schedule. ctr as in gemm_nn_persist_kernel.
+template <int WM, int WN>
+__global__ void __launch_bounds__(NT, WM == WN ? STG_GRAM_MINB : 2)
+    gram_persist_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        int ntiles, int splits, int* ctr) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
+  unsigned long long* empty = full + kStages;
+  int2* meta = reinterpret_cast<int2*>(smraw + 64);  // per stage: (item, chunk); item < 0 ends the CTA
+  static_assert(kStages * 16 <= 64 && kStages * 8 <= 64, "barriers and item tags share the 128-byte header");
+  double* stage0 = reinterpret_cast<double*>(smraw + 128);
+  constexpr int TA = 32 * WM, TB = 32 * WN, SA = TA + 4, SB = TB + 4, STG = kBK * (SA + SB);
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % WM, wn = warp / WM;
+  const int total = ntiles * splits;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kEmptyCount);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto tile_of = [&](int tile, int& ti, int& tj) {
+    if (a.sym) {
+      int r = tile;
+      ti = 0;
+      while (r >= a.tiles_i - ti) {
+        r -= a.tiles_i - ti;
+        ++ti;
+      }
+      tj = ti + r;
+    } else {
+      ti = tile / a.tiles_j;
+      tj = tile % a.tiles_j;
+    }
+  };
+  auto chunks_of = [&](int split) {
+    const i64 r0 = static_cast<i64>(split) * a.rows_per_split;
+    const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
+    return r1 > r0 ? static_cast<int>(cdiv(r1 - r0, kBK)) : 0;
+  };
+  // ---- producer state (thread 0)
+  int p_item = -1, p_q = 0, p_nch = 0, p_ca = 0, p_cb = 0, p_row0 = 0;
+  bool p_done = false;
+  auto produce = [&](int i) {
+    const int st = i % kStages;
+    if (i >= kStages) mbar_wait(&empty[st], static_cast<unsigned>((i / kStages - 1) & 1));
+    if (p_q == p_nch) {
+      const int item = atomicAdd(&ctr[0], 1);
+      if (item >= total) {
+        p_done = true;
+        if (atomicAdd(&ctr[1], 1) == static_cast<int>(gridDim.x) - 1) {
+          ctr[0] = 0;
+          ctr[1] = 0;
+        }
+        meta[st] = make_int2(-1, 0);
+        mbar_arrive(&full[st]);
+        return;
+      }
+      int ti, tj;
+      tile_of(item % ntiles, ti, tj);
+      p_item = item;
+      p_q = 0;
+      p_ca = ti * TA;
+      p_cb = tj * TB;
+      p_row0 = static_cast<int>(static_cast<i64>(item / ntiles) * a.rows_per_split);
+      p_nch = chunks_of(item / ntiles);  // >= 1: the host sizes the splits from the row count
+    }
+    meta[st] = make_int2(p_item, p_q);
+    double* sa = stage0 + st * STG;
+    mbar_arrive_expect_tx(&full[st], kStageBytes);
+    tma_load_2d(sa, &tmA, p_ca, p_row0 + p_q * kBK, &full[st]);
+    tma_load_2d(sa + kBK * SA, &tmB, p_cb, p_row0 + p_q * kBK, &full[st]);
+    ++p_q;
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kStages - 1 && !p_done; ++i) produce(i);
+  double acc[4][4][2];
+  int nx = 0, ny = 0, code = 0, nch = 0, ibase = 0, jbase = 0, split = 0;
+  for (int i = 0;; ++i) {
+    if (threadIdx.x == 0 && !p_done) produce(i + kStages - 1);
+    const int st = i % kStages;
+    mbar_wait(&full[st], static_cast<unsigned>((i / kStages) & 1));
+    const int2 m = meta[st];
+    if (m.x < 0) break;
+    if (m.y == 0) {  // a new item
+      int ti, tj;
+      tile_of(m.x % ntiles, ti, tj);
+      split = m.x / ntiles;
+      nch = chunks_of(split);
+      ibase = ti * TA + wm * 32;
+      jbase = tj * TB + wn * 32;
+      nx = frags_left(a.m1, ibase);
+      ny = frags_left(a.m2, jbase);
+      bool tri = false;
+      if (a.sym) {
+        if (ibase >= jbase + 32) nx = 0;
+        tri = ibase == jbase;
+      }
+      code = warp_code(nx, ny, tri);
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    }
+    const double* sa = stage0 + st * STG;
+    const double* pa = sa + t * SA + wm * 32 + g;
+    const double* pb = sa + kBK * SA + t * SB + wn * 32 + g;
+    if (code == 16)
+      warp_mma<4, 4, false, SA, 8, SB, 8, kBK>(acc, pa, pb);
+    else
+      warp_mma_dispatch<SA, 8, SB, 8, kBK>(code, acc, pa, pb);
+    release_stage(&empty[st]);
+    if (m.y != nch - 1 || code == 0) continue;
+    const i64 m1p = static_cast<i64>(a.tiles_i) * TA, m2p = static_cast<i64>(a.tiles_j) * TB;
+    double* out = a.partial + static_cast<i64>(split) * m1p * m2p;
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        if (x >= nx || y >= ny) continue;
+        const i64 ii = ibase + x * 8 + g, jj = jbase + y * 8 + 2 * t;
+        *reinterpret_cast<double2*>(out + ii * m2p + jj) = make_double2(acc[x][y][0], acc[x][y][1]);
+      }
+  }
 }
 
 // Deterministic split reduction, one thread per output element (consecutive
@@ -763,6 +1158,162 @@ __global__ void __launch_bounds__(NT, BETA ? 2 : 3)
     nn_tma_tile<false, BETA>(a, &tmA, &tmC, row0, tj, nsm);
 }
 
+// Persistent variant of gemm_nn_tma_kernel. A fixed grid of CTAs (a multiple
+// of the SM count) pulls 64 x 64 output tiles from a device counter (row tile
+// major, so the column tiles of one row block run side by side and share the A
+// rows in L2) and streams their K chunks through ONE TMA ring that keeps
+// running across tile boundaries: the next tile's first chunks are already in
+// flight while this tile's epilogue stores, no CTA pays a pipeline fill per
+// tile, and uneven tiles (upper-triangular C, narrow edge tiles) balance
+// themselves. Every tile's result is independent of which CTA computes it, so
+// the output is deterministic. ctr = {next tile, CTAs that saw the end}: the
+// last CTA to see the end re-arms both for the next launch on this stream.
+// (BETA: 176+ registers allow two CTAs per SM, which leaves room for a third stage)
+constexpr int nnp_stages(bool beta) { return beta ? 3 : 2; }
+constexpr size_t nnp_smem(bool beta) { return 128 + sizeof(double) * nnp_stages(beta) * (BM * SAR2 + BK2 * SST); }
+
+template <bool BETA>
+__global__ void __launch_bounds__(NT, BETA ? 2 : 3)
+    gemm_nn_persist_kernel(NNArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                           int ntr, int* ctr) {
+  if (nn_skipped(a)) return;
+  extern __shared__ __align__(128) unsigned char psm[];
+  constexpr int kNNPStages = BETA ? 3 : 2;  // nnp_stages(BETA)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(psm);
+  unsigned long long* empty = full + kNNPStages;
+  int2* meta = reinterpret_cast<int2*>(psm + 64);  // per stage: (tile, K chunk); tile < 0 ends the CTA
+  double* stage0 = reinterpret_cast<double*>(psm + 128);
+  static_assert(kNNPStages * 16 <= 64 && kNNPStages * 8 <= 64, "barriers and tile tags share the 128-byte header");
+  constexpr int STG = BM * SAR2 + BK2 * SST;
+  constexpr unsigned kStageBytes = sizeof(double) * STG;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int xr0 = 2 * warp, xr1 = 2 * warp + 1;  // row-split layout: 16 rows x every live column fragment
+  const int tiles_j = static_cast<int>(cdiv(a.m2, BN));
+  const int total = ntr * tiles_j;
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kNNPStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kEmptyCount);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto chunks_of = [&](int tj) {
+    const int kmax = a.upper_tri_c ? min(a.m1, (tj + 1) * BN) : a.m1;
+    return static_cast<int>(cdiv(kmax, BK2));
+  };
+  // ---- producer state (thread 0)
+  int p_tile = -1, p_q = 0, p_nk = 0, p_tj = 0, p_row0 = 0;
+  bool p_done = false;
+  auto produce = [&](int i) {
+    const int st = i % kNNPStages;
+    if (i >= kNNPStages) mbar_wait(&empty[st], static_cast<unsigned>((i / kNNPStages - 1) & 1));
+    if (p_q == p_nk) {
+      const int tile = atomicAdd(&ctr[0], 1);
+      if (tile >= total) {
+        p_done = true;
+        if (atomicAdd(&ctr[1], 1) == static_cast<int>(gridDim.x) - 1) {  // every CTA has seen the end
+          ctr[0] = 0;
+          ctr[1] = 0;
+        }
+        meta[st] = make_int2(-1, 0);
+        mbar_arrive(&full[st]);
+        return;
+      }
+      p_tile = tile;
+      p_q = 0;
+      p_tj = tiles_j - 1 - tile % tiles_j;  // the widest-K column tile of a row block first
+      p_row0 = (tile / tiles_j) * BM;
+      p_nk = chunks_of(p_tj);
+    }
+    meta[st] = make_int2(p_tile, p_q);
+    double* sa = stage0 + st * STG;
+    mbar_arrive_expect_tx(&full[st], kStageBytes);
+    tma_load_2d(sa, &tmA, p_q * BK2, p_row0, &full[st]);
+    tma_load_2d(sa + BM * SAR2, &tmC, p_tj * BN, p_q * BK2, &full[st]);
+    ++p_q;
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kNNPStages - 1 && !p_done; ++i) produce(i);
+  double acc[2][8][2];
+  double bpre[BETA ? 2 : 1][8][2];
+  int tj = 0, nk = 0, code = 0, nx = 0, F = 0;
+  i64 row0 = 0;
+  bool whole = false;
+  for (int i = 0;; ++i) {
+    if (threadIdx.x == 0 && !p_done) produce(i + kNNPStages - 1);
+    const int st = i % kNNPStages;
+    mbar_wait(&full[st], static_cast<unsigned>((i / kNNPStages) & 1));
+    const int2 m = meta[st];
+    if (m.x < 0) break;
+    if (m.y == 0) {  // a new tile
+      tj = tiles_j - 1 - m.x % tiles_j;
+      row0 = static_cast<i64>(m.x / tiles_j) * BM;
+      nk = chunks_of(tj);
+      whole = row0 + BM <= a.nrows && (tj + 1) * BN <= a.m2;
+      const int R = frags8_left(a.nrows, row0);
+      F = frags8_left(a.m2, tj * BN);
+      nx = (xr0 < R ? 1 : 0) + (xr1 < R ? 1 : 0);
+      code = nx == 0 || F == 0 ? 0 : (nx - 1) * 8 + F;
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+      if (BETA && whole) {  // beta * B for the epilogue, in flight during the K loop
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 8; ++y) {
+            const i64 r = row0 + (2 * warp + x) * 8 + g;
+            const int col = tj * BN + y * 8 + 2 * t;
+            const double2 v = *reinterpret_cast<const double2*>(a.Bm + r * a.ldb + col);
+            bpre[BETA ? x : 0][y][0] = v.x;
+            bpre[BETA ? x : 0][y][1] = v.y;
+          }
+      }
+    }
+    const double* sa = stage0 + st * STG;
+    const double* pa0 = sa + (xr0 * 8 + g) * SAR2 + t;
+    const double* pa1 = sa + (xr1 * 8 + g) * SAR2 + t;
+    const double* pc = sa + BM * SAR2 + t * SST + g;
+#ifndef STG_SKIP_MMA
+    if (code == 16)
+      rs_mma<2, 8, 1, SST, BK2>(acc, pa0, pa1, pc);
+    else
+      rs_dispatch<1, SST, BK2>(code, acc, pa0, pa1, pc, nx, 0, 0, F);
+#else
+    acc[0][0][0] += pa0[0] + pa1[0] + pc[0];
+#endif
+    release_stage(&empty[st]);
+    if (m.y != nk - 1) continue;
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        const i64 r = row0 + (2 * warp + x) * 8 + g;
+        const int col = tj * BN + y * 8 + 2 * t;
+        if (whole) {
+          double2 v = make_double2(a.alpha * acc[x][y][0], a.alpha * acc[x][y][1]);
+          if (BETA) {
+            v.x += a.beta * bpre[BETA ? x : 0][y][0];
+            v.y += a.beta * bpre[BETA ? x : 0][y][1];
+          }
+          *reinterpret_cast<double2*>(a.Out + r * a.ldo + col) = v;
+          continue;
+        }
+        if (r >= a.nrows) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (col + h >= a.m2) continue;
+          double v = a.alpha * acc[x][y][h];
+          if (a.beta != 0.0) v += a.beta * a.Bm[r * a.ldb + col + h];
+          a.Out[r * a.ldo + col + h] = v;
+        }
+      }
+  }
+}
+
 template <bool BETA>  // the beta*B prefetch needs 64 more registers: 2 CTAs per SM
 __global__ void __launch_bounds__(NT, BETA ? 2 : 3) gemm_nn_kernel(NNArgs a) {
   if (nn_skipped(a)) return;
@@ -806,7 +1357,7 @@ __global__ void __launch_bounds__(NT, 2)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStreamStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
+      mbar_init(&empty[st], kEmptyCount);
     }
     mbar_fence_init();
   }
@@ -848,8 +1399,7 @@ __global__ void __launch_bounds__(NT, 2)
         for (int y = 0; y < 4; ++y)
           if (y < nxw) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
     }
-    __syncwarp();
-    mbar_arrive(&empty[st]);  // A is in registers' products now; the slot may refill
+    release_stage(&empty[st]);  // A is in registers' products now; the slot may refill
     const i64 row0 = static_cast<i64>(b + q * G) * kStreamRows + warp * 32;
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -899,7 +1449,7 @@ __global__ void __launch_bounds__(NT, 3)
   if (threadIdx.x == 0) {
     for (int st = 0; st < kStreamStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], NT);  // every consumer thread releases its own reads
+      mbar_init(&empty[st], kEmptyCount);
     }
     mbar_fence_init();
   }
@@ -954,8 +1504,7 @@ __global__ void __launch_bounds__(NT, 3)
         for (int y = 0; y < 4; ++y)
           if (x < nx && y < ny && (!a.sym || x <= y)) dmma(acc[x][y][0], acc[x][y][1], fa[x], fb[y]);
     }
-    __syncwarp();
-    mbar_arrive(&empty[st]);  // each thread's smem reads ordered before the TMA refill
+    release_stage(&empty[st]);  // the warp's smem reads ordered before the TMA refill
   }
   // combine the four warps (fixed order) through the (drained) stage buffers
   __syncthreads();

@@ -419,6 +419,12 @@ class Session {
                                   static_cast<int>(dm::gram_smem(1, 4))));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_tn_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::gram_smem(4, 1))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_persist_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<2, 2>())));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_persist_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<1, 4>())));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_persist_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<4, 1>())));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_tma_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::gram_tma_smem<2, 2>())));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_tma_kernel<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -433,6 +439,12 @@ class Session {
                                   static_cast<int>(dm::gram_stream_smem(false))));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kStreamSmem)));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_persist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::nnp_smem(true))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_persist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::nnp_smem(false))));
+    STG_CUDA(cudaFuncSetAttribute(dm::gram_persist_rs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dm::gram_tma_smem<2, 2>())));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNTmaSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -444,6 +456,10 @@ class Session {
                                   static_cast<int>(triinv_smem_bytes(kCholMaxW))));
     eig_set_attributes();
     d_scal_ = arena_.get<u64>("scalars", 32);
+    // tile counters of the persistent DMMA kernels: a {next, ended} pair per stream that launches them
+    // (sched_slot_); each launch leaves its pair at zero
+    sched_ctr_ = arena_.get<int>("sched_ctr", 64, /*side_use=*/true);
+    STG_CUDA(cudaMemsetAsync(sched_ctr_, 0, sizeof(int) * 64, st_));
     k = cfg.k;
     n = n0;
     if (shard) {  // n0 = rows of this rank's block; n = the global node count
@@ -1059,6 +1075,9 @@ class Session {
   int tev_n_ = 0;
   cusolverDnHandle_t solver_ = nullptr;
   Scalars* hs_ = nullptr;
+  int* sched_ctr_ = nullptr;
+  int sched_slot_ = 0;  // 0 main stream, 1 the K Gram's side stream, 2 the rotation stream
+  int* sched_ctr() { return sched_ctr_ + 16 * sched_slot_; }
   u64* d_scal_ = nullptr;  // [0] err_edit [1] err_apply [2] nvalid [3] flags(int) [4] info(int)
   DevCsr A_[2], T_[2];
   int acur_ = 0, tcur_ = 0;
@@ -1301,6 +1320,27 @@ class Session {
     }
     if (narrow)
       launch(dm::gram_tn_small_kernel, grid, dim3(dm::NT), 0, st_, a);
+    else if (bulk && gram_persist_ && rows > 0 && rows < (1LL << 31) &&
+             static_cast<i64>(ntiles) * splits > 148 * (layout == 0 ? STG_GRAM_MINB : 2) &&
+             static_cast<i64>(ntiles) * splits < (1LL << 30)) {
+      const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, dm::kBK);
+      const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, dm::kBK);
+      const dim3 pg(148 * (layout == 0 ? STG_GRAM_MINB : 2));
+      const int nsp = static_cast<int>(splits);
+      if (layout == 0 && gram_rs_ && gram_order_) dm::gram_tile_order(a, ntiles);
+      if (layout == 1)
+        launch(dm::gram_persist_kernel<1, 4>, pg, dim3(dm::NT), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb, ntiles, nsp,
+               sched_ctr());
+      else if (layout == 2)
+        launch(dm::gram_persist_kernel<4, 1>, pg, dim3(dm::NT), dm::gram_tma_smem<4, 1>(), st_, a, ma, mb, ntiles, nsp,
+               sched_ctr());
+      else if (gram_rs_)
+        launch(dm::gram_persist_rs_kernel, pg, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles, nsp,
+               sched_ctr());
+      else
+        launch(dm::gram_persist_kernel<2, 2>, pg, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles, nsp,
+               sched_ctr());
+    }
     else if (bulk) {
       const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, dm::kBK);
       const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, dm::kBK);
@@ -1437,7 +1477,15 @@ class Session {
       static const bool no_tma = getenv_flag("STG_NN_NOTMA");  // development A/B
       const bool tma = !no_tma && ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 &&
                        lda % 2 == 0 && ldc % 2 == 0;
-      if (tma) {
+      static const bool no_persist = getenv_flag("STG_NN_NOPERSIST");  // development A/B
+      const i64 ntr = cdiv(rows, dm::BM), tiles_j = cdiv(m2, dm::BN);
+      const int Gp = 148 * (beta != 0.0 ? 2 : 3);
+      if (tma && !no_persist && m1 > 0 && ntr * tiles_j > Gp && ntr * tiles_j < (1LL << 30)) {
+        const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
+        const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
+        launch(beta != 0.0 ? dm::gemm_nn_persist_kernel<true> : dm::gemm_nn_persist_kernel<false>, dim3(Gp),
+               dim3(dm::NT), dm::nnp_smem(beta != 0.0), st_, a, ma, mc, static_cast<int>(ntr), sched_ctr());
+      } else if (tma) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
         launch(beta != 0.0 ? dm::gemm_nn_tma_kernel<true> : dm::gemm_nn_tma_kernel<false>, grid, dim3(dm::NT),
@@ -1465,6 +1513,9 @@ class Session {
   std::vector<PlanEntry> plans_;
   int plan_epoch_ = 0;
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
+  const bool gram_persist_ = !getenv_flag("STG_GRAM_NOPERSIST");  // development A/B
+  const bool gram_rs_ = !getenv_flag("STG_GRAM_NORS");  // development A/B
+  const bool gram_order_ = !getenv_flag("STG_GRAM_NOORDER");  // development A/B
   const char* gram_partial_tag_ = "gram_partial";  // the side stream's Grams use their own split-K buffer
   // K = X_out'X_out and its Cholesky computed on st_eig_ right after P's marks,
   // while the host waits for |P| (the rows of P masked instead of zeroed)
@@ -3043,8 +3094,10 @@ class Session {
     std::swap(st_, st_eig_);
     const char* saved = gram_partial_tag_;
     gram_partial_tag_ = "gram_partial_k";
+    sched_slot_ = 1;
     gram(X_, ldx(), X_, ldx(), x_rows, kk, kk, true, kc, ldr, 1.0, mark_p_, stamp_);
     chol(kc, ldr, kk, rc, ldr, nullptr, 0, nullptr, 0.0, true);
+    sched_slot_ = 0;
     gram_partial_tag_ = saved;
     std::swap(st_, st_eig_);
     STG_CUDA(cudaEventRecord(ev_k_, st_eig_));
@@ -3279,6 +3332,7 @@ class Session {
         STG_CUDA(cudaEventRecord(ev_rot_ready_, st_));
         STG_CUDA(cudaStreamWaitEvent(st_rot_, ev_rot_ready_, 0));
         std::swap(st_, st_rot_);  // the launches below go to the rotation stream
+        sched_slot_ = 2;
       }
       kbegin(kRotate, 16.0 * k * pt.n_total + 8.0 * pt.n_total);
       if (!pt.dense && k <= 64)
@@ -3295,6 +3349,7 @@ class Session {
       kend();
       if (aside) {
         std::swap(st_, st_rot_);
+        sched_slot_ = 0;
         STG_CUDA(cudaEventRecord(ev_rot_done_, st_rot_));
         rot_pending_ = true;
       }
