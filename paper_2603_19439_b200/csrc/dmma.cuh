@@ -247,7 +247,27 @@ __global__ void __launch_bounds__(NT, WM == WN ? 3 : 2) gram_tn_kernel(GramArgs 
 #ifndef STG_EMPTY_PER_WARP
 #define STG_EMPTY_PER_WARP 0
 #endif
-constexpr int kBK = 16, kStages = STG_GRAM_STAGES;
+#ifndef STG_GRAM_KBK
+#define STG_GRAM_KBK 16
+#endif
+#ifndef STG_GRAM_PW
+#define STG_GRAM_PW 0
+#endif
+constexpr int kBK = STG_GRAM_KBK, kStages = STG_GRAM_STAGES;
+// gram_persist_rs_kernel: a fifth warp only issues the TMA loads (the DMMA warps never wait on a stage
+// release), 32-row stages, two of them (tools/microbench/gram_pipe.cu: 200 x 200 sym 177 -> 158 us)
+#ifndef STG_RS_KBK
+#define STG_RS_KBK 32
+#endif
+#ifndef STG_RS_STAGES
+#define STG_RS_STAGES 2
+#endif
+#ifndef STG_RS_PW
+#define STG_RS_PW 1
+#endif
+constexpr int kRsBK = STG_RS_KBK, kRsStages = STG_RS_STAGES, kGramPW = STG_RS_PW;
+constexpr int kRsThreads = NT + 32 * kGramPW;
+constexpr size_t kRsSmem = 128 + sizeof(double) * kRsStages * kRsBK * 2 * 68;
 // consumers release a stage per thread (NT arrivals) or, after __syncwarp, through one lane per warp
 constexpr unsigned kEmptyCount = STG_EMPTY_PER_WARP ? NT / 32 : NT;
 __device__ __forceinline__ void release_stage(unsigned long long* bar) {
@@ -438,21 +458,21 @@ __device__ __forceinline__ int frags8_left(i64 extent, i64 base) {
 
 // Persistent split-K Gram on 64 x 64 tiles in the row-split layout (the
 // scheduling of gram_persist_kernel below; same partial format).
-__global__ void __launch_bounds__(NT, STG_GRAM_MINB)
+__global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
     gram_persist_rs_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                            int ntiles, int splits, int* ctr) {
   extern __shared__ __align__(128) unsigned char smraw[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smraw);
-  unsigned long long* empty = full + kStages;
+  unsigned long long* empty = full + kRsStages;
   int2* meta = reinterpret_cast<int2*>(smraw + 64);
   double* stage0 = reinterpret_cast<double*>(smraw + 128);
-  constexpr int SA = 68, SB = 68, STG = kBK * (SA + SB);
+  constexpr int SA = 68, SB = 68, STG = kRsBK * (SA + SB);
   constexpr unsigned kStageBytes = sizeof(double) * STG;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int total = ntiles * splits;
   if (threadIdx.x == 0) {
-    for (int st = 0; st < kStages; ++st) {
+    for (int st = 0; st < kRsStages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kEmptyCount);
     }
@@ -476,13 +496,13 @@ __global__ void __launch_bounds__(NT, STG_GRAM_MINB)
   auto chunks_of = [&](int split) {
     const i64 r0 = static_cast<i64>(split) * a.rows_per_split;
     const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
-    return r1 > r0 ? static_cast<int>(cdiv(r1 - r0, kBK)) : 0;
+    return r1 > r0 ? static_cast<int>(cdiv(r1 - r0, kRsBK)) : 0;
   };
   int p_item = -1, p_q = 0, p_nch = 0, p_ca = 0, p_cb = 0, p_row0 = 0;
   bool p_done = false, p_one = false;  // p_one: diagonal tile of a symmetric Gram, both operands are one box
   auto produce = [&](int i) {
-    const int st = i % kStages;
-    if (i >= kStages) mbar_wait(&empty[st], static_cast<unsigned>((i / kStages - 1) & 1));
+    const int st = i % kRsStages;
+    if (i >= kRsStages) mbar_wait(&empty[st], static_cast<unsigned>((i / kRsStages - 1) & 1));
     if (p_q == p_nch) {
       const int item = atomicAdd(&ctr[0], 1);
       if (item >= total) {
@@ -509,18 +529,25 @@ __global__ void __launch_bounds__(NT, STG_GRAM_MINB)
     meta[st] = make_int2(p_item, p_q);
     double* sa = stage0 + st * STG;
     mbar_arrive_expect_tx(&full[st], p_one ? kStageBytes / 2 : kStageBytes);
-    tma_load_2d(sa, &tmA, p_ca, p_row0 + p_q * kBK, &full[st]);
-    if (!p_one) tma_load_2d(sa + kBK * SA, &tmB, p_cb, p_row0 + p_q * kBK, &full[st]);
+    tma_load_2d(sa, &tmA, p_ca, p_row0 + p_q * kRsBK, &full[st]);
+    if (!p_one) tma_load_2d(sa + kRsBK * SA, &tmB, p_cb, p_row0 + p_q * kRsBK, &full[st]);
     ++p_q;
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < kStages - 1 && !p_done; ++i) produce(i);
+  if (kGramPW) {
+    if (warp == 4) {
+      if (lane == 0)
+        for (int i = 0; !p_done; ++i) produce(i);
+      return;
+    }
+  } else if (threadIdx.x == 0) {
+    for (int i = 0; i < kRsStages - 1 && !p_done; ++i) produce(i);
+  }
   double acc[2][8][2];
   int nx = 0, F = 0, code = 0, nch = 0, split = 0, xr0 = 0, xr1 = 0, ylo0 = 0, ylo1 = 0, ti = 0, tj = 0, boff = 0;
   for (int i = 0;; ++i) {
-    if (threadIdx.x == 0 && !p_done) produce(i + kStages - 1);
-    const int st = i % kStages;
-    mbar_wait(&full[st], static_cast<unsigned>((i / kStages) & 1));
+    if (!kGramPW && threadIdx.x == 0 && !p_done) produce(i + kRsStages - 1);
+    const int st = i % kRsStages;
+    mbar_wait(&full[st], static_cast<unsigned>((i / kRsStages) & 1));
     const int2 m = meta[st];
     if (m.x < 0) break;
     if (m.y == 0) {  // a new item
@@ -530,7 +557,7 @@ __global__ void __launch_bounds__(NT, STG_GRAM_MINB)
       const int R = frags8_left(a.m1, ti * 64);  // live fragment rows / columns of this tile
       F = frags8_left(a.m2, tj * 64);
       const bool diag = a.sym && ti == tj;
-      boff = diag ? 0 : kBK * SA;  // the diagonal tile's B operand is its A box
+      boff = diag ? 0 : kRsBK * SA;  // the diagonal tile's B operand is its A box
       xr0 = warp;
       xr1 = diag ? 7 - warp : warp + 4;
       nx = (xr0 < R ? 1 : 0) + (xr1 < R ? 1 : 0);  // xr0 < xr1, so nx == 1 means row xr0 only
@@ -548,9 +575,9 @@ __global__ void __launch_bounds__(NT, STG_GRAM_MINB)
     const double* pb = sa + boff + t * SB + g;
 #ifndef STG_SKIP_MMA  // (development: the operand pipeline alone)
     if (code == 16)
-      rs_mma<2, 8, SA, SB, kBK>(acc, pa0, pa1, pb);
+      rs_mma<2, 8, SA, SB, kRsBK>(acc, pa0, pa1, pb);
     else
-      rs_dispatch<SA, SB, kBK>(code, acc, pa0, pa1, pb, nx, ylo0, ylo1, F);
+      rs_dispatch<SA, SB, kRsBK>(code, acc, pa0, pa1, pb, nx, ylo0, ylo1, F);
 #else
     acc[0][0][0] += pa0[0] + pa1[0] + pb[0];
 #endif
@@ -1173,7 +1200,7 @@ constexpr int nnp_stages(bool beta) { return beta ? 3 : 2; }
 constexpr size_t nnp_smem(bool beta) { return 128 + sizeof(double) * nnp_stages(beta) * (BM * SAR2 + BK2 * SST); }
 
 template <bool BETA>
-__global__ void __launch_bounds__(NT, BETA ? 2 : 3)
+__global__ void __launch_bounds__(kRsThreads, BETA ? 2 : 3)
     gemm_nn_persist_kernel(NNArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                            int ntr, int* ctr) {
   if (nn_skipped(a)) return;
@@ -1234,15 +1261,41 @@ __global__ void __launch_bounds__(NT, BETA ? 2 : 3)
     tma_load_2d(sa + BM * SAR2, &tmC, p_tj * BN, p_q * BK2, &full[st]);
     ++p_q;
   };
-  if (threadIdx.x == 0)
+  if (kGramPW) {
+    // the fifth warp only issues the loads; with beta != 0 its lanes also pull each new tile of B into L2
+    // (the DMMA warps read it straight from global memory at the tile's start, one to two tiles later)
+    if (warp == 4) {
+      for (int i = 0;; ++i) {
+        int fresh = 0;
+        if (lane == 0) {
+          const int before = p_tile;
+          produce(i);
+          fresh = !p_done && p_tile != before;
+        }
+        fresh = __shfl_sync(0xffffffffu, fresh, 0);
+        if (BETA && fresh) {
+          const int row0 = __shfl_sync(0xffffffffu, p_row0, 0), c0 = __shfl_sync(0xffffffffu, p_tj, 0) * BN;
+          for (int l = lane; l < BM * 4; l += 32) {  // 128-byte lines of the 64 x 64 tile
+            const i64 r = row0 + (l >> 2);
+            const int c = c0 + (l & 3) * 16;
+            if (r < a.nrows && c < a.m2)
+              asm volatile("prefetch.global.L2 [%0];\n" ::"l"(a.Bm + r * a.ldb + c));
+          }
+        }
+        if (__shfl_sync(0xffffffffu, p_done ? 1 : 0, 0)) break;
+      }
+      return;
+    }
+  } else if (threadIdx.x == 0) {
     for (int i = 0; i < kNNPStages - 1 && !p_done; ++i) produce(i);
+  }
   double acc[2][8][2];
   double bpre[BETA ? 2 : 1][8][2];
   int tj = 0, nk = 0, code = 0, nx = 0, F = 0;
   i64 row0 = 0;
   bool whole = false;
   for (int i = 0;; ++i) {
-    if (threadIdx.x == 0 && !p_done) produce(i + kNNPStages - 1);
+    if (!kGramPW && threadIdx.x == 0 && !p_done) produce(i + kNNPStages - 1);
     const int st = i % kNNPStages;
     mbar_wait(&full[st], static_cast<unsigned>((i / kNNPStages) & 1));
     const int2 m = meta[st];

@@ -444,7 +444,7 @@ class Session {
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_persist_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::nnp_smem(false))));
     STG_CUDA(cudaFuncSetAttribute(dm::gram_persist_rs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(dm::gram_tma_smem<2, 2>())));
+                                  static_cast<int>(dm::kRsSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dm::kNNTmaSmem)));
     STG_CUDA(cudaFuncSetAttribute(dm::gemm_nn_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1287,7 +1287,9 @@ class Session {
     // sweep: 200 x 200 sym (10 tiles) best at 12, 64 x 64 at 3, 64 x 100 at 3-4, 164 x 100 at 12; fewer splits
     // = less partial traffic); above (cfg4/cfg5), 24 waves for square tiles and 4 for 32 x 128 tiles (the
     // tail of unequal tiles outweighs the partials there: cfg4's Grams 28.5 vs 30.0 ms per step)
-    const int waves = rows >= (1 << 18) ? (layout == 0 ? 24 : 4) : std::min(12, std::max(3, 2 * ntiles));
+    // (the persistent row-split kernel balances its tiles itself: 8 waves measured best, fewer partials)
+    const int wcap = layout == 0 && gram_rs_ && gram_persist_ && !mask ? 8 : 12;
+    const int waves = rows >= (1 << 18) ? (layout == 0 ? 24 : 4) : std::min(wcap, std::max(3, 2 * ntiles));
     const i64 target = 148 * (env_waves > 0 ? env_waves : waves);
     const i64 rows_min = narrow ? 256 : 128;
     i64 splits = std::max<i64>(1, std::min<i64>(cdiv(std::max<i64>(rows, 1), rows_min), cdiv(target, ntiles)));
@@ -1323,19 +1325,20 @@ class Session {
     else if (bulk && gram_persist_ && rows > 0 && rows < (1LL << 31) &&
              static_cast<i64>(ntiles) * splits > 148 * (layout == 0 ? STG_GRAM_MINB : 2) &&
              static_cast<i64>(ntiles) * splits < (1LL << 30)) {
-      const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, dm::kBK);
-      const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, dm::kBK);
+      const bool rs = layout == 0 && gram_rs_;
+      const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, rs ? dm::kRsBK : dm::kBK);
+      const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, rs ? dm::kRsBK : dm::kBK);
       const dim3 pg(148 * (layout == 0 ? STG_GRAM_MINB : 2));
       const int nsp = static_cast<int>(splits);
-      if (layout == 0 && gram_rs_ && gram_order_) dm::gram_tile_order(a, ntiles);
+      if (rs && gram_order_) dm::gram_tile_order(a, ntiles);
       if (layout == 1)
         launch(dm::gram_persist_kernel<1, 4>, pg, dim3(dm::NT), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb, ntiles, nsp,
                sched_ctr());
       else if (layout == 2)
         launch(dm::gram_persist_kernel<4, 1>, pg, dim3(dm::NT), dm::gram_tma_smem<4, 1>(), st_, a, ma, mb, ntiles, nsp,
                sched_ctr());
-      else if (gram_rs_)
-        launch(dm::gram_persist_rs_kernel, pg, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles, nsp,
+      else if (rs)
+        launch(dm::gram_persist_rs_kernel, pg, dim3(dm::kRsThreads), dm::kRsSmem, st_, a, ma, mb, ntiles, nsp,
                sched_ctr());
       else
         launch(dm::gram_persist_kernel<2, 2>, pg, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles, nsp,
@@ -1484,7 +1487,7 @@ class Session {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
         launch(beta != 0.0 ? dm::gemm_nn_persist_kernel<true> : dm::gemm_nn_persist_kernel<false>, dim3(Gp),
-               dim3(dm::NT), dm::nnp_smem(beta != 0.0), st_, a, ma, mc, static_cast<int>(ntr), sched_ctr());
+               dim3(dm::kRsThreads), dm::nnp_smem(beta != 0.0), st_, a, ma, mc, static_cast<int>(ntr), sched_ctr());
       } else if (tma) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);

@@ -161,9 +161,11 @@ void real(const double* A, i64 rows, int m1, int m2, bool sym, int waves, double
   a.partial = partial;
   const CUtensorMap ma = make_tmap_2d(a.A, rows, m1, a.lda, 68, kBK);
   const CUtensorMap mb = make_tmap_2d(a.B, rows, m2, a.ldb, 68, kBK);
+  const CUtensorMap ra = make_tmap_2d(a.A, rows, m1, a.lda, 68, kRsBK);
+  const CUtensorMap rb = make_tmap_2d(a.B, rows, m2, a.ldb, 68, kRsBK);
   const size_t smem = gram_tma_smem<2, 2>();
   STG_CUDA(cudaFuncSetAttribute(gram_tma_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  STG_CUDA(cudaFuncSetAttribute(gram_persist_rs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  STG_CUDA(cudaFuncSetAttribute(gram_persist_rs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRsSmem));
   STG_CUDA(cudaFuncSetAttribute(gram_persist_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -172,6 +174,7 @@ void real(const double* A, i64 rows, int m1, int m2, bool sym, int waves, double
   // tiles by DMMA work, heaviest first (as Session::gram)
   gram_tile_order(a, ntiles);
   for (int v = 0; v < 4; ++v) {
+    if (v == 1 || v == 2) continue;
     a.ordered = v == 3 && ntiles <= 64;
     float best = 1e9f;
     for (int rep = 0; rep < 6; ++rep) {
@@ -179,9 +182,9 @@ void real(const double* A, i64 rows, int m1, int m2, bool sym, int waves, double
       if (v == 0)
         gram_tma_kernel<2, 2><<<dim3(ntiles, (unsigned)splits), NT, smem>>>(a, ma, mb);
       else if (v == 1)
-        gram_persist_kernel<2, 2><<<148 * 3, NT, smem>>>(a, ma, mb, ntiles, (int)splits, ctr);
+        gram_persist_kernel<2, 2><<<148 * STG_GRAM_MINB, NT, smem>>>(a, ma, mb, ntiles, (int)splits, ctr);
       else
-        gram_persist_rs_kernel<<<148 * 3, NT, smem>>>(a, ma, mb, ntiles, (int)splits, ctr);
+        gram_persist_rs_kernel<<<148 * STG_GRAM_MINB, kRsThreads, kRsSmem>>>(a, ra, rb, ntiles, (int)splits, ctr);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -207,6 +210,7 @@ int main() {
   for (size_t i = 0; i < h.size(); ++i) h[i] = 1e-3 * static_cast<double>(i % 1013);
   cudaMemcpy(A, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
   printf("Gram %lld x %d x %d (all tiles full), ideal %.1f us at 37.1 TF\n", rows, m, m, 2.0 * rows * m * m / 37.1e6);
+  if (getenv("PROBE_SYNTH")) {
   run<1, 4, 16, 3>(A, rows, m, 3, out, clk);
   run<1, 4, 16, 5>(A, rows, m, 3, out, clk);
   run<1, 4, 16, 3>(A, rows, m, 1, out, clk);
@@ -223,6 +227,8 @@ int main() {
   run<0, 4, 16, 0>(A, rows, m, 2, out, clk);
   run<1, 4, 16, 0>(A, rows, m, 2, out, clk);
   run<1, 4, 16, 0>(A, rows, m, 1, out, clk);
+  }
+  printf("variant: PW %d rows/stage %d stages %d CTAs/SM %d\n", kGramPW, kRsBK, kRsStages, STG_GRAM_MINB);
   double* partial;
   int* ctr;
   cudaMalloc(&partial, sizeof(double) * 256 * 256 * 2048);
