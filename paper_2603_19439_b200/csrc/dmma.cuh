@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
       p_q = 0;
       p_ca = ti * 64;
       p_cb = tj * 64;
-      p_one = a.sym && ti == tj;
+      p_one = a.sym && ti == tj && a.A == a.B && a.lda == a.ldb;  // (a symmetric product Z'(AZ) has two operands)
       p_row0 = static_cast<int>(static_cast<i64>(p_split) * a.rows_per_split);
       p_nch = chunks_of(p_split);
     }
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
       const int R = frags8_left(a.m1, ti * 64);  // live fragment rows / columns of this tile
       F = frags8_left(a.m2, tj * 64);
       const bool diag = a.sym && ti == tj;
-      boff = diag ? 0 : kRsBK * SA;  // the diagonal tile's B operand is its A box
+      boff = diag && a.A == a.B && a.lda == a.ldb ? 0 : kRsBK * SA;  // one operand: the diagonal tile's B box is its A box
       xr0 = warp;
       xr1 = diag ? 7 - warp : warp + 4;
       nx = (xr0 < R ? 1 : 0) + (xr1 < R ? 1 : 0);  // xr0 < xr1, so nx == 1 means row xr0 only

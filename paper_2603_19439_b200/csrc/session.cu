@@ -1323,7 +1323,7 @@ class Session {
     if (narrow)
       launch(dm::gram_tn_small_kernel, grid, dim3(dm::NT), 0, st_, a);
     else if (bulk && gram_persist_ && rows > 0 && rows < (1LL << 31) &&
-             static_cast<i64>(ntiles) * splits > 148 * (layout == 0 ? STG_GRAM_MINB : 2) &&
+             (persist_always_ || static_cast<i64>(ntiles) * splits > 148 * (layout == 0 ? STG_GRAM_MINB : 2)) &&
              static_cast<i64>(ntiles) * splits < (1LL << 30)) {
       const bool rs = layout == 0 && gram_rs_;
       const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, TA + 4, rs ? dm::kRsBK : dm::kBK);
@@ -1483,7 +1483,7 @@ class Session {
       static const bool no_persist = getenv_flag("STG_NN_NOPERSIST");  // development A/B
       const i64 ntr = cdiv(rows, dm::BM), tiles_j = cdiv(m2, dm::BN);
       const int Gp = 148 * (beta != 0.0 ? 2 : 3);
-      if (tma && !no_persist && m1 > 0 && ntr * tiles_j > Gp && ntr * tiles_j < (1LL << 30)) {
+      if (tma && !no_persist && m1 > 0 && (persist_always_ || ntr * tiles_j > Gp) && ntr * tiles_j < (1LL << 30)) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
         launch(beta != 0.0 ? dm::gemm_nn_persist_kernel<true> : dm::gemm_nn_persist_kernel<false>, dim3(Gp),
@@ -1518,6 +1518,8 @@ class Session {
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
   const bool gram_persist_ = !getenv_flag("STG_GRAM_NOPERSIST");  // development A/B
   const bool gram_rs_ = !getenv_flag("STG_GRAM_NORS");  // development A/B
+  // tests: the persistent kernels also for products with fewer tiles than CTAs (small graphs)
+  const bool persist_always_ = getenv_flag("STG_PERSIST_ALWAYS");
   const bool gram_order_ = !getenv_flag("STG_GRAM_NOORDER");  // development A/B
   const char* gram_partial_tag_ = "gram_partial";  // the side stream's Grams use their own split-K buffer
   // K = X_out'X_out and its Cholesky computed on st_eig_ right after P's marks,

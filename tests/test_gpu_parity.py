@@ -369,3 +369,33 @@ def test_config5_shape_parity_rmat17():
         orc.step(upd)
         ve, sa = check_state(gpu, orc, tag=f"cfg5-s17 step {t}")
         print(f"cfg5-s17 step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", ["sbm-k64", "rmat-k32"])
+def test_persistent_dmma_kernels_on_small_shapes(cfg, monkeypatch):
+    """The persistent Gram / row-local GEMM kernels (device tile counter, producer
+    warp, row-split warp layout, one-box diagonal tiles) take over from the
+    static-grid kernels only when a product has more tiles than CTAs, i.e. at
+    the BASELINE sizes. STG_PERSIST_ALWAYS routes every product of a small
+    graph through them: ragged and diagonal tiles, symmetric products with two
+    different operands (Z'(AZ), k = 64), in-place updates, fewer tiles than
+    CTAs. Parity as everywhere: CSR bit-exact, Ritz 1e-10, sin 1e-8."""
+    from paper_2603_19439_b200 import TrackerSession, init_eig, streams
+
+    monkeypatch.setenv("STG_PERSIST_ALWAYS", "1")  # read when a session is created
+    if cfg == "sbm-k64":
+        s, k = streams.config4(n=1 << 15, steps=2), 64
+    else:
+        s, k = streams.config3(scale=14, steps=2), 32
+    rp, col, val = s.csr0()
+    vals, vecs = init_eig.leading_eigenpairs(rp, col, val, k, "abs_desc", device="cuda:0")
+    n = len(rp) - 1
+    a = po.Csr(n, np.asarray(rp, np.int32), np.asarray(col, np.int32), np.asarray(val, np.float64))
+    orc = po.Session(a, kind="grest-rsvd", k=k, seed=5, values=vals, vectors=vecs)
+    gpu = TrackerSession(a.rowptr, a.col, a.val, vals, vecs, kind="grest-rsvd", k=k, seed=5)
+    for t, upd in enumerate(s.updates):
+        gpu.step(upd)
+        orc.step(upd)
+        ve, sa = check_state(gpu, orc, tag=f"persistent {cfg} step {t}")
+        print(f"persistent {cfg} step {t}: value err {ve:.2e}, subspace sin {sa:.2e}")
