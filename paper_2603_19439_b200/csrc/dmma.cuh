@@ -1,15 +1,21 @@
 // FP64 tensor-core (DMMA) kernels for the tall-skinny algebra of the G-REST
 // step. sm_100a has no tcgen05 kind::f64, so FP64 tensor work is mma.sync
-// m8n8k4 (SASS DMMA.8x8x4); operand tiles are staged through shared memory with
-// a cp.async double buffer.
+// m8n8k4 (SASS DMMA.8x8x4) on operand tiles staged in shared memory by TMA.
 //
-//   gram_tn : Out(m1 x m2) = A(N x m1)' B(N x m2), split-K over the N rows with
-//             a deterministic second-pass reduction (fixed split order). With
-//             `sym` (A == B) only tile pairs ti <= tj are computed and the
-//             result is mirrored exactly.
-//   gemm_nn : Out(N x m2) = alpha A(N x m1) C(m1 x m2) + beta B(N x m2), the
-//             row-local update (projections, R^-1 application, rotations).
-//             B may alias Out (each CTA reads its own tile before writing).
+//   gram : Out(m1 x m2) = A(N x m1)' B(N x m2), split-K over the N rows with
+//          a deterministic second-pass reduction (fixed split order). With
+//          `sym` only tile pairs ti <= tj are computed and the result is
+//          mirrored exactly. gram_persist_rs_kernel (64 x 64 tiles) and
+//          gram_persist_kernel (32 x 128 / 128 x 32) are the persistent
+//          kernels: a device tile counter, one TMA ring across tiles, a
+//          producer warp; gram_tma_kernel is the static grid for products
+//          with fewer tiles than CTAs, gram_tn_kernel the cp.async fallback
+//          (unaligned views, row masks), gram_stream_kernel the <= 32-wide case.
+//   gemm : Out(N x m2) = alpha A(N x m1) C(m1 x m2) + beta B(N x m2), the
+//          row-local update (projections, R^-1 application, rotations);
+//          gemm_nn_persist_kernel / gemm_nn_tma_kernel / gemm_nn_kernel /
+//          gemm_nn_stream_kernel in the same roles. B may alias Out (each tile
+//          is read before it is written).
 // All blocks are row-major with even leading dimensions.
 #pragma once
 
@@ -38,9 +44,12 @@ struct GramArgs {
   int sym;
   const int* mask;  // optional: rows with mask[r] == mask_val contribute nothing
   int mask_val;
-  // persistent kernels: item i is (tile order[i / splits], split i % splits) when `ordered` (the host sorts
-  // the tiles by DMMA work, heaviest first, so the light edge tiles fill the tail), else (i % ntiles, i / ntiles)
-  int ordered;
+  // persistent kernels, item i -> (tile, split). Not `ordered`: (i % ntiles, i / ntiles). `ordered` (the host
+  // sorts the tiles by DMMA work, heaviest first): tile major over the last tail_splits splits, every heavy
+  // tile before any light edge tile, which fills the tail; split major over the splits before them.
+  // tail_splits == splits (all tile major) measured best in the step (Gram class 1.46 vs 1.56 ms with a
+  // one-wave tail), although it re-reads the operand from HBM per tile (ncu: 484 MB vs 171 MB for 200 x 200 sym)
+  int ordered, tail_splits;
   unsigned char order[64];
 };
 
@@ -493,6 +502,21 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
       tj = tile % a.tiles_j;
     }
   };
+  auto item_of = [&](int item, int& tile, int& split) {
+    if (!a.ordered) {
+      tile = item % ntiles;
+      split = item / ntiles;
+      return;
+    }
+    const int head = (splits - a.tail_splits) * ntiles;
+    if (item < head) {
+      tile = a.order[item % ntiles];
+      split = item / ntiles;
+    } else {
+      tile = a.order[(item - head) / a.tail_splits];
+      split = splits - a.tail_splits + (item - head) % a.tail_splits;
+    }
+  };
   auto chunks_of = [&](int split) {
     const i64 r0 = static_cast<i64>(split) * a.rows_per_split;
     const i64 r1 = min(a.nrows, r0 + a.rows_per_split);
@@ -516,8 +540,9 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
         return;
       }
       int ti, tj;
-      const int p_split = a.ordered ? item % splits : item / ntiles;
-      tile_of(a.ordered ? a.order[item / splits] : item % ntiles, ti, tj);
+      int p_split, p_tl;
+      item_of(item, p_tl, p_split);
+      tile_of(p_tl, ti, tj);
       p_item = item;
       p_q = 0;
       p_ca = ti * 64;
@@ -551,8 +576,9 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
     const int2 m = meta[st];
     if (m.x < 0) break;
     if (m.y == 0) {  // a new item
-      tile_of(a.ordered ? a.order[m.x / splits] : m.x % ntiles, ti, tj);
-      split = a.ordered ? m.x % splits : m.x / ntiles;
+      int tl;
+      item_of(m.x, tl, split);
+      tile_of(tl, ti, tj);
       nch = chunks_of(split);
       const int R = frags8_left(a.m1, ti * 64);  // live fragment rows / columns of this tile
       F = frags8_left(a.m2, tj * 64);
@@ -601,9 +627,10 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
 }
 
 // Host: a.order = the 64 x 64 tiles sorted by DMMA fragments (heaviest first, ties in tile order).
-inline void gram_tile_order(GramArgs& a, int ntiles) {
+inline void gram_tile_order(GramArgs& a, int ntiles, int splits, int ctas) {
   a.ordered = 0;
   if (ntiles > 64) return;
+  a.tail_splits = ctas > 0 ? splits : std::min(splits, std::max(1, -ctas / ntiles));  // ctas < 0: one-wave tail
   int w[64], idx = 0;
   for (int ti = 0; ti < a.tiles_i; ++ti)
     for (int tj = a.sym ? ti : 0; tj < a.tiles_j; ++tj) {
@@ -625,7 +652,7 @@ inline void gram_tile_order(GramArgs& a, int ntiles) {
 // same partial slot whichever CTA computes it: the reduction order and the
 // result do not depend on the schedule. ctr as in gemm_nn_persist_kernel.
 template <int WM, int WN>
-__global__ void __launch_bounds__(NT, WM == WN ? STG_GRAM_MINB : 2)
+__global__ void __launch_bounds__(kRsThreads, WM == WN ? STG_GRAM_MINB : 2)
     gram_persist_kernel(GramArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         int ntiles, int splits, int* ctr) {
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -701,12 +728,19 @@ __global__ void __launch_bounds__(NT, WM == WN ? STG_GRAM_MINB : 2)
     tma_load_2d(sa + kBK * SA, &tmB, p_cb, p_row0 + p_q * kBK, &full[st]);
     ++p_q;
   };
-  if (threadIdx.x == 0)
+  if (kGramPW) {  // the fifth warp only issues the loads
+    if (warp == 4) {
+      if (lane == 0)
+        for (int i = 0; !p_done; ++i) produce(i);
+      return;
+    }
+  } else if (threadIdx.x == 0) {
     for (int i = 0; i < kStages - 1 && !p_done; ++i) produce(i);
+  }
   double acc[4][4][2];
   int nx = 0, ny = 0, code = 0, nch = 0, ibase = 0, jbase = 0, split = 0;
   for (int i = 0;; ++i) {
-    if (threadIdx.x == 0 && !p_done) produce(i + kStages - 1);
+    if (!kGramPW && threadIdx.x == 0 && !p_done) produce(i + kStages - 1);
     const int st = i % kStages;
     mbar_wait(&full[st], static_cast<unsigned>((i / kStages) & 1));
     const int2 m = meta[st];

@@ -1330,18 +1330,21 @@ class Session {
       const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, rs ? dm::kRsBK : dm::kBK);
       const dim3 pg(148 * (layout == 0 ? STG_GRAM_MINB : 2));
       const int nsp = static_cast<int>(splits);
-      if (rs && gram_order_) dm::gram_tile_order(a, ntiles);
+      if (rs && gram_order_) dm::gram_tile_order(a, ntiles, nsp, static_cast<int>(pg.x));
       if (layout == 1)
-        launch(dm::gram_persist_kernel<1, 4>, pg, dim3(dm::NT), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb, ntiles, nsp,
+        launch(dm::gram_persist_kernel<1, 4>, pg, dim3(dm::kRsThreads), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb, ntiles,
+               nsp,
                sched_ctr());
       else if (layout == 2)
-        launch(dm::gram_persist_kernel<4, 1>, pg, dim3(dm::NT), dm::gram_tma_smem<4, 1>(), st_, a, ma, mb, ntiles, nsp,
+        launch(dm::gram_persist_kernel<4, 1>, pg, dim3(dm::kRsThreads), dm::gram_tma_smem<4, 1>(), st_, a, ma, mb, ntiles,
+               nsp,
                sched_ctr());
       else if (rs)
         launch(dm::gram_persist_rs_kernel, pg, dim3(dm::kRsThreads), dm::kRsSmem, st_, a, ma, mb, ntiles, nsp,
                sched_ctr());
       else
-        launch(dm::gram_persist_kernel<2, 2>, pg, dim3(dm::NT), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles, nsp,
+        launch(dm::gram_persist_kernel<2, 2>, pg, dim3(dm::kRsThreads), dm::gram_tma_smem<2, 2>(), st_, a, ma, mb, ntiles,
+               nsp,
                sched_ctr());
     }
     else if (bulk) {
@@ -1518,6 +1521,7 @@ class Session {
   const bool spmm_fused_ = !getenv_flag("STG_SPMM_UNFUSED");  // development A/B
   const bool gram_persist_ = !getenv_flag("STG_GRAM_NOPERSIST");  // development A/B
   const bool gram_rs_ = !getenv_flag("STG_GRAM_NORS");  // development A/B
+  const bool eager_plans_ = !getenv_flag("STG_NO_EAGER_PLANS");  // development A/B
   // tests: the persistent kernels also for products with fewer tiles than CTAs (small graphs)
   const bool persist_always_ = getenv_flag("STG_PERSIST_ALWAYS");
   const bool gram_order_ = !getenv_flag("STG_GRAM_NOORDER");  // development A/B
@@ -2252,6 +2256,19 @@ class Session {
       pt.lrp = lrp;
       pt.lcol = lcol;
       unsharded_fields(pt);
+      // the segment plans of this step's Delta products, built here: the main stream would otherwise wait
+      // idle for the K Gram and its Cholesky (early_k, side stream) and build them before the first SpMM
+      if (eager_plans_ && k_ready_ && keep_delta && cfg.kind >= ST_IASC && cfg.kind <= ST_GREST_RSVD) {
+        SpmmArgs pa{};
+        pa.rowptr = lrp;
+        pa.rows = pt.p;
+        spmm_plan(pa, pt.nnz);
+        if (cfg.kind == ST_GREST_RSVD && S > cfg.rsvd_l) {  // Delta_2' M over the appended rows (rsvd_trailing)
+          pa.row_off = pt.p_old;
+          pa.rows = pt.S_loc;
+          spmm_plan(pa, pt.nnz);
+        }
+      }
     }
     return pt;
   }
