@@ -45,11 +45,11 @@ struct GramArgs {
   const int* mask;  // optional: rows with mask[r] == mask_val contribute nothing
   int mask_val;
   // persistent kernels, item i -> (tile, split). Not `ordered`: (i % ntiles, i / ntiles). `ordered` (the host
-  // sorts the tiles by DMMA work, heaviest first): tile major over the last tail_splits splits, every heavy
-  // tile before any light edge tile, which fills the tail; split major over the splits before them.
-  // tail_splits == splits (all tile major) measured best in the step (Gram class 1.46 vs 1.56 ms with a
-  // one-wave tail), although it re-reads the operand from HBM per tile (ncu: 484 MB vs 171 MB for 200 x 200 sym)
-  int ordered, tail_splits;
+  // sorts the tiles by DMMA work, heaviest first): the splits are cut into blocks of block_splits; within a
+  // block the items run tile major, every heavy tile before any light edge tile (which fill each block's and
+  // the kernel's tail), and a block's rows (block_splits row ranges, sized to stay in L2) are read from HBM
+  // once and then from L2 by the other tiles. block_splits == splits is tile major over the whole product.
+  int ordered, block_splits;
   unsigned char order[64];
 };
 
@@ -508,14 +508,11 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
       split = item / ntiles;
       return;
     }
-    const int head = (splits - a.tail_splits) * ntiles;
-    if (item < head) {
-      tile = a.order[item % ntiles];
-      split = item / ntiles;
-    } else {
-      tile = a.order[(item - head) / a.tail_splits];
-      split = splits - a.tail_splits + (item - head) % a.tail_splits;
-    }
+    const int per = a.block_splits * ntiles;  // items of a full block
+    const int blk = item / per, r = item - blk * per;
+    const int tb = min(a.block_splits, splits - blk * a.block_splits);  // the last block may be shorter
+    tile = a.order[r / tb];
+    split = blk * a.block_splits + r % tb;
   };
   auto chunks_of = [&](int split) {
     const i64 r0 = static_cast<i64>(split) * a.rows_per_split;
@@ -627,10 +624,10 @@ __global__ void __launch_bounds__(kRsThreads, STG_GRAM_MINB)
 }
 
 // Host: a.order = the 64 x 64 tiles sorted by DMMA fragments (heaviest first, ties in tile order).
-inline void gram_tile_order(GramArgs& a, int ntiles, int splits, int ctas) {
+inline void gram_tile_order(GramArgs& a, int ntiles, int splits, int block) {
   a.ordered = 0;
   if (ntiles > 64) return;
-  a.tail_splits = ctas > 0 ? splits : std::min(splits, std::max(1, -ctas / ntiles));  // ctas < 0: one-wave tail
+  a.block_splits = block > 0 ? std::min(splits, block) : splits;
   int w[64], idx = 0;
   for (int ti = 0; ti < a.tiles_i; ++ti)
     for (int tj = a.sym ? ti : 0; tj < a.tiles_j; ++tj) {

@@ -1330,7 +1330,11 @@ class Session {
       const CUtensorMap mb = make_tmap_2d(B, rows, m2, ldb, TB + 4, rs ? dm::kRsBK : dm::kBK);
       const dim3 pg(148 * (layout == 0 ? STG_GRAM_MINB : 2));
       const int nsp = static_cast<int>(splits);
-      if (rs && gram_order_) dm::gram_tile_order(a, ntiles, nsp, static_cast<int>(pg.x));
+      if (rs && gram_order_) {
+        // blocks of about gram_block_waves_ waves of items (0: one block, tile major over the whole product)
+        static const int bw = getenv("STG_GRAM_BLOCK_WAVES") ? atoi(getenv("STG_GRAM_BLOCK_WAVES")) : 0;  // development A/B
+        dm::gram_tile_order(a, ntiles, nsp, bw > 0 ? std::max(1, bw * static_cast<int>(pg.x) / ntiles) : 0);
+      }
       if (layout == 1)
         launch(dm::gram_persist_kernel<1, 4>, pg, dim3(dm::kRsThreads), dm::gram_tma_smem<1, 4>(), st_, a, ma, mb, ntiles,
                nsp,

@@ -172,7 +172,7 @@ void real(const double* A, i64 rows, int m1, int m2, bool sym, int waves, double
   cudaEventCreate(&e1);
   const double flops = sym ? 1.0 * rows * m1 * (m1 + 1) : 2.0 * rows * m1 * m2;
   // tiles by DMMA work, heaviest first (as Session::gram)
-  gram_tile_order(a, ntiles, (int)splits, 148 * STG_GRAM_MINB);
+  gram_tile_order(a, ntiles, (int)splits, getenv("BLOCK_WAVES") ? std::max(1, atoi(getenv("BLOCK_WAVES")) * 148 * STG_GRAM_MINB / ntiles) : 0);
   for (int v = 0; v < 4; ++v) {
     if (v == 1 || v == 2) continue;
     a.ordered = v == 3 && ntiles <= 64;
