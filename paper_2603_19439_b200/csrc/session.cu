@@ -1469,9 +1469,7 @@ class Session {
            nullptr, 8.0 * rows * (m1 + m2 + (beta != 0.0 ? m2 : 0)) + 8.0 * m1 * m2);
     if (m2 <= 32)
     {
-      static const bool beta_stream = !getenv_flag("STG_NN_NO_BETA_STREAM");  // development A/B
-      const bool stream = m1 <= 32 && (beta == 0.0 || (beta_stream && B != A)) &&
-                          (reinterpret_cast<uintptr_t>(A) & 15) == 0 && lda % 2 == 0 &&
+      const bool stream = m1 <= 32 && beta == 0.0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 && lda % 2 == 0 &&
                           (reinterpret_cast<uintptr_t>(Out) & 15) == 0 && ldo % 2 == 0;
       if (stream) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::kStreamPitch, dm::kStreamRows);
