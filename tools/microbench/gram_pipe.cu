@@ -198,7 +198,59 @@ void real(const double* A, i64 rows, int m1, int m2, bool sym, int waves, double
   }
 }
 
+// The K Gram of the step: X'X over ~1.08M rows x 32 columns, the rows of P masked (gram_stream_kernel).
+void stream_gram(i64 rows, bool masked) {
+  double *X, *partial;
+  int* mask;
+  cudaMalloc(&X, sizeof(double) * rows * 32);
+  cudaMalloc(&partial, sizeof(double) * 1024 * 148 * 3);
+  cudaMalloc(&mask, sizeof(int) * rows);
+  cudaMemset(X, 0, sizeof(double) * rows * 32);
+  cudaMemset(mask, 0, sizeof(int) * rows);
+  GramArgs a{};
+  a.A = a.B = X;
+  a.lda = a.ldb = 32;
+  a.nrows = rows;
+  a.m1 = a.m2 = 32;
+  a.tiles_i = a.tiles_j = 1;
+  a.sym = 1;
+  a.partial = partial;
+  a.mask = masked ? mask : nullptr;
+  a.mask_val = 7;
+  const CUtensorMap ma = make_tmap_2d(X, rows, 32, 32, kStreamPitch, kGsRows);
+  const int ntl = static_cast<int>(cdiv(rows, kGsRows));
+  STG_CUDA(cudaFuncSetAttribute(gram_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)gram_stream_smem(false)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int G : {148, 296, 444}) {
+    float best = 1e9f;
+    for (int rep = 0; rep < 6; ++rep) {
+      cudaEventRecord(e0);
+      gram_stream_kernel<<<std::min(ntl, G), NT, gram_stream_smem(true)>>>(a, ma, ma, 1, ntl);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0) best = std::min(best, ms);
+    }
+    STG_CUDA(cudaGetLastError());
+    printf("  gram_stream %lld x 32 sym %s grid %d: %6.1f us  %5.2f TB/s\n", rows, masked ? "masked" : "      ", G,
+           best * 1e3, 8.0 * rows * 32 / best / 1e9);
+  }
+  cudaFree(X);
+  cudaFree(partial);
+  cudaFree(mask);
+}
+
 int main() {
+  if (getenv("PROBE_STREAM")) {
+    stream_gram(1080347, true);
+    stream_gram(1080347, false);
+    stream_gram(104049, false);
+    return 0;
+  }
   const i64 rows = 104049;
   const int m = 256;
   double *A, *out;
