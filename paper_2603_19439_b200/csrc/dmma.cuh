@@ -1227,16 +1227,20 @@ __global__ void __launch_bounds__(NT, BETA ? 2 : 3)
 // the output is deterministic. ctr = {next tile, CTAs that saw the end}: the
 // last CTA to see the end re-arms both for the next launch on this stream.
 // (BETA: 176+ registers allow two CTAs per SM, which leaves room for a third stage)
-constexpr int nnp_stages(bool beta) { return beta ? 3 : 2; }
+#ifndef STG_NNP_NB_STAGES
+#define STG_NNP_NB_STAGES 2  // beta == 0: 2 stages x 3 CTAs/SM (3 stages x 2 CTAs/SM measured: see DESIGN 8)
+#endif
+constexpr int nnp_stages(bool beta) { return beta ? 3 : STG_NNP_NB_STAGES; }
+constexpr int nnp_ctas(bool beta) { return beta || STG_NNP_NB_STAGES > 2 ? 2 : 3; }
 constexpr size_t nnp_smem(bool beta) { return 128 + sizeof(double) * nnp_stages(beta) * (BM * SAR2 + BK2 * SST); }
 
 template <bool BETA>
-__global__ void __launch_bounds__(kRsThreads, BETA ? 2 : 3)
+__global__ void __launch_bounds__(kRsThreads, (BETA || STG_NNP_NB_STAGES > 2) ? 2 : 3)
     gemm_nn_persist_kernel(NNArgs a, const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
                            int ntr, int* ctr) {
   if (nn_skipped(a)) return;
   extern __shared__ __align__(128) unsigned char psm[];
-  constexpr int kNNPStages = BETA ? 3 : 2;  // nnp_stages(BETA)
+  constexpr int kNNPStages = BETA ? 3 : STG_NNP_NB_STAGES;  // nnp_stages(BETA)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(psm);
   unsigned long long* empty = full + kNNPStages;
   int2* meta = reinterpret_cast<int2*>(psm + 64);  // per stage: (tile, K chunk); tile < 0 ends the CTA

@@ -1489,7 +1489,7 @@ class Session {
                        lda % 2 == 0 && ldc % 2 == 0;
       static const bool no_persist = getenv_flag("STG_NN_NOPERSIST");  // development A/B
       const i64 ntr = cdiv(rows, dm::BM), tiles_j = cdiv(m2, dm::BN);
-      const int Gp = 148 * (beta != 0.0 ? 2 : 3);
+      const int Gp = 148 * dm::nnp_ctas(beta != 0.0);
       if (tma && !no_persist && m1 > 0 && (persist_always_ || ntr * tiles_j > Gp) && ntr * tiles_j < (1LL << 30)) {
         const CUtensorMap ma = make_tmap_2d(A, rows, m1, lda, dm::SAR2, dm::BM);
         const CUtensorMap mc = make_tmap_2d(C, m1, m2, ldc, dm::SST, dm::BK2);
